@@ -1,0 +1,127 @@
+/*
+ * randqr_b200.h -- C ABI of librandqr_b200.so, the B200 (sm_100a) drop-in for
+ * the HQRRP hot path of the reference package `randqr`
+ * (/root/reference/pkg/src/randqr).
+ *
+ * Every entry point takes plain pointers and sizes.  Matrices are column-major
+ * (Fortran order, as the reference's working copies: blocked.py:161) with an
+ * explicit leading dimension; "d" pointers are device memory, "h" pointers are
+ * host memory.  All work is enqueued on the context's CUDA stream.
+ *
+ * Return codes map 1:1 onto the reference's exceptions (errors.py:4-13):
+ *   RQ_EDIM   -> DimensionError     (blocked.py:152-161, householder.py:177-178)
+ *   RQ_EVALUE -> ValueError         (pivoting.py:97-98, :122-123, householder.py:177-178)
+ *   RQ_ECONV  -> ConvergenceError   (svd.py:52-53)
+ * rq_last_error() returns the message of the last failing call on this thread.
+ */
+#ifndef RANDQR_B200_H
+#define RANDQR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  RQ_OK = 0,
+  RQ_EDIM = 1,
+  RQ_EVALUE = 2,
+  RQ_ECONV = 3,
+  RQ_ECUDA = 4,
+  RQ_EINTERNAL = 5,
+  RQ_EUNSUPPORTED = 6
+};
+
+enum { RQ_PIVOT_PERMUTATION = 0, RQ_PIVOT_REFLECTORS = 1 };
+
+/* RQ_SKETCH_FRESH draws a new Omega per panel from the caller's stream, exactly
+ * as build_sketch does (pivoting.py:100-101); RQ_SKETCH_DOWNDATE draws G once
+ * and downdates Y = G A per panel (HQRRP); its pivots differ legitimately. */
+enum { RQ_SKETCH_FRESH = 0, RQ_SKETCH_DOWNDATE = 1 };
+
+typedef struct rq_ctx rq_ctx;
+
+/* Mirrors BlockConfig (blocked.py:42-50) + SketchConfig (pivoting.py:28-51). */
+typedef struct rq_config {
+  int32_t block;       /* b  = BlockConfig.block                                  */
+  int32_t oversample;  /* p  = SketchConfig.oversample                            */
+  int32_t power;       /* q  = SketchConfig.power                                 */
+  int32_t stabilize;   /* -1: None (on iff q >= 2), 0: off, 1: on                 */
+  int32_t pivot_kind;  /* RQ_PIVOT_PERMUTATION | RQ_PIVOT_REFLECTORS              */
+  int32_t rrqr;        /* 1: block_rrqr semantics (blocked.py:239-279)            */
+  int32_t sketch_mode; /* RQ_SKETCH_FRESH | RQ_SKETCH_DOWNDATE                     */
+  int32_t reserved;
+} rq_config;
+
+/* Called after each completed panel (the reference's `inspect` hook,
+ * blocked.py:184-185, :215-216); the callee may call rq_snapshot(). */
+typedef void (*rq_panel_cb)(int32_t panel, void* user);
+
+const char* rq_version(void);
+const char* rq_last_error(void);
+
+/* Context: owns workspace, the stored compact factors of the last
+ * factorization, and the stream (NULL = legacy default stream). */
+int rq_ctx_create(rq_ctx** out, int32_t device, void* stream);
+int rq_ctx_destroy(rq_ctx* ctx);
+int rq_ctx_set_stream(rq_ctx* ctx, void* stream);
+int rq_ctx_set_inspect(rq_ctx* ctx, rq_panel_cb cb, void* user);
+
+/* block_qr / block_rrqr (blocked.py:175-219 / :239-279) on device memory.
+ * dA (m x n, lda >= m) is overwritten with R (exact zeros below the diagonal).
+ * *counter is the RngState counter (rng.py:21-26) and is advanced exactly as
+ * the reference advances it.  dperm (n int64, may be NULL) receives the
+ * composite permutation (A[:, perm] = A P) when pivots are permutations.
+ * The Q and P factors stay in the context (see rq_form_q / rq_form_p). */
+int rq_factorize(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, double* dA,
+                 int64_t lda, uint64_t seed, uint64_t* counter, int64_t* dperm);
+
+/* Same, end to end from host buffers (copies in and out on the ctx stream,
+ * synchronises before returning).  hR may alias hA. */
+int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, const double* hA,
+                      int64_t lda, uint64_t seed, uint64_t* counter, double* hR, int64_t ldr,
+                      int64_t* hperm);
+
+/* Factorization.expand_q(cols) (blocked.py:134-141): dQ is m x cols, cols in [n, m]. */
+int rq_form_q(rq_ctx* ctx, int64_t cols, double* dQ, int64_t ldq);
+/* Factorization.expand_p() (blocked.py:143-149): dP is n x n. */
+int rq_form_p(rq_ctx* ctx, double* dP, int64_t ldp);
+
+/* Working matrix after the current panel, in the reference's column order
+ * (the matrix `inspect` receives).  Host destination, m x n, ldh >= m. */
+int rq_snapshot(rq_ctx* ctx, double* hW, int64_t ldh);
+
+/* Kernel-plugin level (backend.get_kernels(), backend.py:42-47):
+ * householder_sweep(a, v, perm, steps, pivot) (_kernels_numpy.py:11-22) on
+ * device memory.  dV (m x steps) must be zero and dperm (n) the identity on
+ * entry, as in the reference contract. */
+int rq_householder_sweep(rq_ctx* ctx, double* dA, int64_t m, int64_t n, int64_t lda, double* dV,
+                         int64_t ldv, int64_t* dperm, int64_t steps, int32_t pivot);
+
+/* gaussian_matrix(rows, cols, RngState(seed, counter)) (rng.py:54-68) into
+ * device memory; the caller advances its counter by rows*cols. */
+int rq_gaussian_matrix(rq_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, uint64_t counter,
+                       double* dOut, int64_t ld);
+
+/* Plain splitmix64 words (rng.py:29-39) for the bitwise integer-stream pin. */
+int rq_splitmix_words(rq_ctx* ctx, uint64_t seed, uint64_t first, int64_t count, uint64_t* dOut);
+
+/* Test hook: the FP64 DMMA GEMM used by every dense step,
+ *   C (M x N) = alpha * op(A) * B + beta * C,  op(A) = A^T (A is K x M, a_mmajor = 0)
+ *   or A (A is M x K, a_mmajor = 1); B is K x N.  Views start at element
+ *   (a_r0, a_c0) / (b_r0, b_c0) of buffers with a_rows x a_cols / b_rows x b_cols
+ *   extents.  Leading dimensions must be even, buffers 16 B aligned. */
+int rq_test_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, const double* dA, int64_t lda,
+                 int64_t a_rows, int64_t a_cols, int64_t a_r0, int64_t a_c0, const double* dB, int64_t ldb,
+                 int64_t b_rows, int64_t b_cols, int64_t b_r0, int64_t b_c0, double* dC, int64_t ldc, double alpha,
+                 double beta);
+
+/* Number of kernel launches this context has issued (instrumentation). */
+int64_t rq_launch_count(rq_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RANDQR_B200_H */

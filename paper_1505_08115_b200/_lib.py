@@ -1,0 +1,88 @@
+"""ctypes binding of librandqr_b200.so (declared in include/randqr_b200.h).
+
+The product path has no fallback: if the CUDA library is missing or no CUDA
+device is present, importing the binding raises.  Build it with
+``python -c "import __graft_entry__ as g; g.build()"`` (or ``make -C
+paper_1505_08115_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librandqr_b200.so")
+
+RQ_OK, RQ_EDIM, RQ_EVALUE, RQ_ECONV, RQ_ECUDA, RQ_EINTERNAL, RQ_EUNSUPPORTED = range(7)
+RQ_PIVOT_PERMUTATION, RQ_PIVOT_REFLECTORS = 0, 1
+RQ_SKETCH_FRESH, RQ_SKETCH_DOWNDATE = 0, 1
+
+
+class rq_config(ctypes.Structure):
+    _fields_ = [
+        ("block", ctypes.c_int32),
+        ("oversample", ctypes.c_int32),
+        ("power", ctypes.c_int32),
+        ("stabilize", ctypes.c_int32),
+        ("pivot_kind", ctypes.c_int32),
+        ("rrqr", ctypes.c_int32),
+        ("sketch_mode", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+    ]
+
+
+PANEL_CB = ctypes.CFUNCTYPE(None, ctypes.c_int32, ctypes.c_void_p)
+
+_i32, _i64, _u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+_vp = ctypes.c_void_p
+_SIGS = {
+    "rq_version": (ctypes.c_char_p, []),
+    "rq_last_error": (ctypes.c_char_p, []),
+    "rq_ctx_create": (ctypes.c_int, [ctypes.POINTER(_vp), _i32, _vp]),
+    "rq_ctx_destroy": (ctypes.c_int, [_vp]),
+    "rq_ctx_set_stream": (ctypes.c_int, [_vp, _vp]),
+    "rq_ctx_set_inspect": (ctypes.c_int, [_vp, PANEL_CB, _vp]),
+    "rq_factorize": (ctypes.c_int, [_vp, ctypes.POINTER(rq_config), _i64, _i64, _vp, _i64, _u64,
+                                    ctypes.POINTER(_u64), _vp]),
+    "rq_factorize_host": (ctypes.c_int, [_vp, ctypes.POINTER(rq_config), _i64, _i64, _vp, _i64, _u64,
+                                         ctypes.POINTER(_u64), _vp, _i64, _vp]),
+    "rq_form_q": (ctypes.c_int, [_vp, _i64, _vp, _i64]),
+    "rq_form_p": (ctypes.c_int, [_vp, _vp, _i64]),
+    "rq_snapshot": (ctypes.c_int, [_vp, _vp, _i64]),
+    "rq_householder_sweep": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i32]),
+    "rq_gaussian_matrix": (ctypes.c_int, [_vp, _i64, _i64, _u64, _u64, _vp, _i64]),
+    "rq_splitmix_words": (ctypes.c_int, [_vp, _u64, _u64, _i64, _vp]),
+    "rq_test_gemm": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64,
+                                    _i64, _i64, _i64, _i64, _vp, _i64, ctypes.c_double, ctypes.c_double]),
+    "rq_launch_count": (_i64, [_vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load the library (raises if it is missing; there is no CPU fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is not built; run __graft_entry__.build() (nvcc, sm_100a)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def last_error():
+    return load().rq_last_error().decode(errors="replace")

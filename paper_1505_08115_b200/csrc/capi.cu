@@ -1,0 +1,242 @@
+// extern "C" entry points of librandqr_b200.so (declared in include/randqr_b200.h).
+#include <new>
+
+#include "driver.cuh"
+#include "misc.cuh"
+
+namespace rq {
+const char* last_error();
+void clear_error();
+}  // namespace rq
+
+using rq::Ctx;
+
+#define CTX_CHECK(ctx)                                                    \
+  do {                                                                    \
+    if (!(ctx)) return rq::set_error(RQ_EVALUE, "null rq_ctx");           \
+    cudaError_t _e = cudaSetDevice((ctx)->c.device);                      \
+    if (_e != cudaSuccess)                                                \
+      return rq::set_error(RQ_ECUDA, "cudaSetDevice: %s", cudaGetErrorString(_e)); \
+  } while (0)
+
+extern "C" {
+#pragma GCC visibility push(default)
+
+const char* rq_version(void) { return "randqr_b200 0.1.0 (sm_100a)"; }
+const char* rq_last_error(void) { return rq::last_error(); }
+
+int rq_ctx_create(rq_ctx** out, int32_t device, void* stream) {
+  if (!out) return rq::set_error(RQ_EVALUE, "null output pointer");
+  *out = nullptr;
+  RQ_CUDA_TRY(cudaSetDevice(device));
+  rq_ctx* c = new (std::nothrow) rq_ctx;
+  if (!c) return rq::set_error(RQ_EINTERNAL, "out of host memory");
+  c->c.device = device;
+  c->c.stream = (cudaStream_t)stream;
+  c->c.nbarriers = 1 << 16;
+  cudaError_t e = cudaMalloc(&c->c.barriers, sizeof(unsigned) * c->c.nbarriers);
+  if (e == cudaSuccess) e = cudaMemset(c->c.barriers, 0, sizeof(unsigned) * c->c.nbarriers);
+  if (e != cudaSuccess) {
+    delete c;
+    return rq::set_error(RQ_ECUDA, "barrier ring: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return RQ_OK;
+}
+
+int rq_ctx_destroy(rq_ctx* ctx) {
+  if (!ctx) return RQ_OK;
+  cudaSetDevice(ctx->c.device);
+  if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
+  else cudaDeviceSynchronize();
+  delete ctx;
+  return RQ_OK;
+}
+
+int rq_ctx_set_stream(rq_ctx* ctx, void* stream) {
+  CTX_CHECK(ctx);
+  ctx->c.stream = (cudaStream_t)stream;
+  return RQ_OK;
+}
+
+int rq_ctx_set_inspect(rq_ctx* ctx, rq_panel_cb cb, void* user) {
+  CTX_CHECK(ctx);
+  ctx->c.inspect_cb = cb;
+  ctx->c.inspect_user = user;
+  return RQ_OK;
+}
+
+// Validation in the reference's order (blocked.py:152-161, pivoting.py:97-98).
+// On a sketch-width error the counter is advanced by the draws of the panels
+// the reference completes before raising, so RngState matches afterwards.
+static int validate(const rq_config* cfg, int64_t m, int64_t n, uint64_t* counter) {
+  if (!cfg) return rq::set_error(RQ_EVALUE, "null config");
+  if (m < n) return rq::set_error(RQ_EDIM, "blocked QR needs rows >= cols, got %lldx%lld", (long long)m, (long long)n);
+  if (cfg->block < 1 || cfg->block > n)
+    return rq::set_error(RQ_EDIM, "block size must lie in [1, %lld], got %d", (long long)n, cfg->block);
+  if (cfg->oversample < 0 || cfg->power < 0) return rq::set_error(RQ_EVALUE, "oversample and power must be >= 0");
+  const int b = cfg->block, wdt = cfg->block + cfg->oversample;
+  uint64_t drawn = 0;
+  for (int64_t s = 0; n - s > b; s += b) {
+    const int64_t np = n - s;
+    if (wdt > np) {
+      if (counter && cfg->sketch_mode == RQ_SKETCH_FRESH) *counter += drawn;
+      return rq::set_error(RQ_EVALUE, "sketch width %d exceeds the %lld columns being pivoted", wdt, (long long)np);
+    }
+    drawn += (uint64_t)(m - s) * (uint64_t)wdt;
+  }
+  return RQ_OK;
+}
+
+int rq_factorize(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, double* dA, int64_t lda, uint64_t seed,
+                 uint64_t* counter, int64_t* dperm) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (!counter) return rq::set_error(RQ_EVALUE, "null counter");
+  RQ_TRY(validate(cfg, m, n, counter));
+  if (lda < m || (lda & 1) || ((uintptr_t)dA & 15))
+    return rq::set_error(RQ_EVALUE, "dA must be 16-byte aligned with an even lda >= m");
+  if (cfg->rrqr || cfg->pivot_kind == RQ_PIVOT_REFLECTORS)
+    return rq::set_error(RQ_EUNSUPPORTED, "reflector pivots / rrqr not built yet");
+  if (cfg->sketch_mode != RQ_SKETCH_FRESH) return rq::set_error(RQ_EUNSUPPORTED, "downdate sketch not built yet");
+  return ctx->c.factorize_perm(*cfg, m, n, dA, lda, seed, counter, dperm);
+}
+
+int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, const double* hA, int64_t lda,
+                      uint64_t seed, uint64_t* counter, double* hR, int64_t ldr, int64_t* hperm) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (!counter) return rq::set_error(RQ_EVALUE, "null counter");
+  RQ_TRY(validate(cfg, m, n, counter));
+  Ctx& c = ctx->c;
+  const int64_t ldd = rq::even(m);
+  double* dA = nullptr;
+  int64_t* dp = nullptr;
+  RQ_CUDA_TRY(cudaMallocAsync(&dA, (size_t)ldd * n * 8, c.stream));
+  RQ_CUDA_TRY(cudaMallocAsync(&dp, (size_t)n * 8, c.stream));
+  int rc = RQ_OK;
+  cudaError_t e = cudaMemcpy2DAsync(dA, ldd * 8, hA, lda * 8, m * 8, n, cudaMemcpyHostToDevice, c.stream);
+  if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "H2D: %s", cudaGetErrorString(e));
+  if (rc == RQ_OK) rc = rq_factorize(ctx, cfg, m, n, dA, ldd, seed, counter, dp);
+  if (rc == RQ_OK && hR) {
+    e = cudaMemcpy2DAsync(hR, ldr * 8, dA, ldd * 8, m * 8, n, cudaMemcpyDeviceToHost, c.stream);
+    if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "D2H: %s", cudaGetErrorString(e));
+  }
+  if (rc == RQ_OK && hperm) {
+    e = cudaMemcpyAsync(hperm, dp, n * 8, cudaMemcpyDeviceToHost, c.stream);
+    if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "D2H perm: %s", cudaGetErrorString(e));
+  }
+  cudaFreeAsync(dA, c.stream);
+  cudaFreeAsync(dp, c.stream);
+  e = cudaStreamSynchronize(c.stream);
+  if (rc == RQ_OK && e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "sync: %s", cudaGetErrorString(e));
+  return rc;
+}
+
+int rq_form_q(rq_ctx* ctx, int64_t cols, double* dQ, int64_t ldq) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (!ctx->c.have_factors) return rq::set_error(RQ_EVALUE, "no factorization stored in this context");
+  if (cols < ctx->c.fn || cols > ctx->c.fm)
+    return rq::set_error(RQ_EDIM, "cols must lie in [%lld, %lld]", (long long)ctx->c.fn, (long long)ctx->c.fm);
+  if (ldq < ctx->c.fm || (ldq & 1) || ((uintptr_t)dQ & 15))
+    return rq::set_error(RQ_EVALUE, "dQ must be 16-byte aligned with an even ldq >= m");
+  return ctx->c.form_q(cols, dQ, ldq);
+}
+
+int rq_form_p(rq_ctx* ctx, double* dP, int64_t ldp) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (ldp < ctx->c.fn) return rq::set_error(RQ_EVALUE, "ldp < n");
+  return ctx->c.form_p(dP, ldp);
+}
+
+int rq_snapshot(rq_ctx* ctx, double* hW, int64_t ldh) {
+  CTX_CHECK(ctx);
+  return ctx->c.snapshot(hW, ldh);
+}
+
+int rq_householder_sweep(rq_ctx* ctx, double* dA, int64_t m, int64_t n, int64_t lda, double* dV, int64_t ldv,
+                         int64_t* dperm, int64_t steps, int32_t pivot) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (m < 0 || n < 0 || steps < 0 || steps > n || (steps > 0 && dV == nullptr))
+    return rq::set_error(RQ_EDIM, "householder_sweep: bad shape m=%lld n=%lld steps=%lld", (long long)m,
+                         (long long)n, (long long)steps);
+  if (steps == 0 || m == 0) return RQ_OK;
+  Ctx& c = ctx->c;
+  const int G = rq::sweep_grid_size((int)n);
+  const size_t ws = rq::sweep_workspace_bytes(m, (int)n, G);
+  const int64_t ldr = rq::even(m);
+  const size_t need = ws + 1024 + (size_t)ldr * n * 8 + (size_t)n * 4 * 3 + (size_t)n * 8 + 4096;
+  RQ_TRY(c.qarena.reserve(need));
+  char* base = (char*)c.qarena.base;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  c.sweep_ws = base;
+  c.sweep_ws_bytes = ws;
+  size_t off = al(ws);
+  double* rtmp = (double*)(base + off);
+  off += al((size_t)ldr * n * 8);
+  int* cap = (int*)(base + off);
+  off += al((size_t)n * 4);
+  int* io = (int*)(base + off);
+  off += al((size_t)n * 4);
+  int64_t* ost = (int64_t*)(base + off);
+  rq::SweepCall sc;
+  sc.a = dA;
+  sc.lda = lda;
+  sc.m = m;
+  sc.n = (int)n;
+  sc.steps = (int)steps;
+  sc.pivot = pivot ? 1 : 0;
+  sc.v = dV;
+  sc.ldv = ldv;
+  sc.col_at_pos = cap;
+  sc.r_out = pivot ? rtmp : nullptr;
+  sc.ldr = ldr;
+  RQ_TRY(c.sweep(sc));
+  if (pivot) {
+    RQ_TRY(rq::copy2d(rtmp, ldr, dA, lda, m, n, 0, c.stream, &c.launches));
+    if (dperm) {
+      RQ_TRY(rq::iota(io, (int)n, nullptr, 0, c.stream, &c.launches));
+      rq::MoveCall mv{dA, lda, 0, 0, 0, cap, io, nullptr, (int)n, rtmp, ldr, dperm, ost};
+      RQ_TRY(rq::move_columns(mv, c.stream, &c.launches));
+    }
+  }
+  return RQ_OK;
+}
+
+int rq_gaussian_matrix(rq_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, uint64_t counter, double* dOut,
+                       int64_t ld) {
+  CTX_CHECK(ctx);
+  if (rows < 1 || cols < 1)
+    return rq::set_error(RQ_EDIM, "matrix dimensions must be positive, got %lldx%lld", (long long)rows,
+                         (long long)cols);
+  return rq::gaussian_fill(dOut, rows, cols, ld, seed, counter, ctx->c.stream, &ctx->c.launches);
+}
+
+int rq_splitmix_words(rq_ctx* ctx, uint64_t seed, uint64_t first, int64_t count, uint64_t* dOut) {
+  CTX_CHECK(ctx);
+  return rq::splitmix_words(dOut, seed, first, count, ctx->c.stream, &ctx->c.launches);
+}
+
+int rq_test_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, const double* dA, int64_t lda,
+                 int64_t a_rows, int64_t a_cols, int64_t a_r0, int64_t a_c0, const double* dB, int64_t ldb,
+                 int64_t b_rows, int64_t b_cols, int64_t b_r0, int64_t b_c0, double* dC, int64_t ldc, double alpha,
+                 double beta) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  Ctx& c = ctx->c;
+  const size_t kb = (size_t)rq::kSMs * 256 * 256 * 8;
+  RQ_TRY(c.qarena.reserve(kb));
+  c.kwork = (double*)c.qarena.base;
+  c.kwork_bytes = kb;
+  rq::GemmOperand A{dA, a_rows, a_cols, lda, a_r0, a_c0};
+  rq::GemmOperand B{dB, b_rows, b_cols, ldb, b_r0, b_c0};
+  return c.gemm(M, N, K, A, a_mmajor != 0, B, dC, ldc, alpha, beta);
+}
+
+int64_t rq_launch_count(rq_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+#pragma GCC visibility pop
+}  // extern "C"

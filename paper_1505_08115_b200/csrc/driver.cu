@@ -1,0 +1,496 @@
+// Panel loop of block_qr (HQRRP, Fig. 4) on one B200, enqueue-only: every
+// per-panel decision (pivots, moves, P-hat, T) stays on the device; the host
+// only walks panel offsets.  C ABI in capi.cu.
+//
+// Per non-final panel (blocked.py:204-217, restated):
+//   1  Omega = next m'(b+p) normals of the caller's stream      (rng.py:54-68)
+//   2  Y^T = Omega^T A[s:, s:]                  DMMA GEMM        (pivoting.py:100-101)
+//   3  b-step CPQR of Y^T -> chosen columns     cooperative sweep (pivoting.py:114-129)
+//   4  plan + move chosen columns into the panel (full height)   (blocked.py:205)
+//   5  unpivoted panel QR, leaf by leaf (cluster kernel) + WY GEMMs (householder.py:193)
+//   6  b x b CPQR of R' with Q2^T accumulated                     (householder.py:194)
+//   7  R, rows-above permuted by P-hat                            (blocked.py:208-209)
+//   8  T = (I/2 + striu(V^T V))^{-1}                              (householder.py:197)
+//   9  tail <- Q2^T (tail - V T^T V^T tail)                       (blocked.py:210-211)
+// The final block (n - s <= b) is one pivoted sweep at full height (blocked.py:195-203).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "driver.cuh"
+#include "gemm_f64.cuh"
+#include "misc.cuh"
+#include "panel.cuh"
+
+namespace rq {
+
+// ---------------------------------------------------------------------------
+// Device arena
+// ---------------------------------------------------------------------------
+int Arena::reserve(size_t bytes) {
+  if (bytes <= cap) return RQ_OK;
+  if (base) cudaFree(base);
+  base = nullptr;
+  cap = 0;
+  RQ_CUDA_TRY(cudaMalloc(&base, bytes));
+  cap = bytes;
+  return RQ_OK;
+}
+void Arena::release() {
+  if (base) cudaFree(base);
+  base = nullptr;
+  cap = 0;
+}
+
+struct Carver {
+  char* p;
+  size_t off = 0;
+  explicit Carver(void* b) : p((char*)b) {}
+  template <class T>
+  T* take(size_t count) {
+    size_t bytes = ((count * sizeof(T)) + 255) & ~size_t(255);
+    T* r = reinterpret_cast<T*>(p ? p + off : nullptr);
+    off += bytes;
+    return r;
+  }
+};
+
+
+// ---------------------------------------------------------------------------
+// Layout of scratch + stored factors for one factorization
+// ---------------------------------------------------------------------------
+
+
+static size_t factor_bytes(int64_t m, int64_t n, int b) {
+  size_t t = 0;
+  for (int64_t s = 0; s < n; s += b) {
+    const int64_t mp = m - s, np = n - s;
+    const int w = (int)std::min<int64_t>(b, np);
+    const int steps = (int)std::min<int64_t>(mp, w);
+    const int64_t ldv = even(mp + 1), ldt = even(b);
+    t += (((size_t)ldv * (np <= b ? steps : b) * 8 + 255) & ~size_t(255));
+    t += (((size_t)ldt * b * 8 + 255) & ~size_t(255)) * 2;  // T, Q2^T
+    (void)steps;
+  }
+  return t;
+}
+
+static Layout plan_layout(void* base, int64_t m, int64_t n, int b, int p, int power) {
+  Layout L;
+  Carver c(base);
+  const int wdt = b + p;
+  L.ldo = even(m + 1);
+  L.ldy = even(wdt);
+  const int64_t ldb = even(b);
+  L.omega = c.take<double>((size_t)L.ldo * wdt);
+  L.yt = c.take<double>((size_t)L.ldy * n);
+  L.w1 = c.take<double>((size_t)ldb * n);
+  L.w2 = c.take<double>((size_t)ldb * n);
+  L.ttop = c.take<double>((size_t)ldb * n);
+  L.gram = c.take<double>((size_t)ldb * b);
+  L.tleaf = c.take<double>(32 * 32);
+  L.ybuf = power > 0 ? c.take<double>((size_t)even(n) * wdt) : nullptr;
+  L.kwork_bytes = std::max<size_t>((size_t)kSMs * b * b * 8, (size_t)4 * b * n * 8);
+  L.kwork = c.take<double>(L.kwork_bytes / 8);
+  L.lds_small = ldb;
+  L.small = c.take<double>((size_t)ldb * 2 * b);
+  L.rfin = c.take<double>((size_t)ldb * b);
+  L.stage = c.take<double>((size_t)even(m) * 2 * b + (size_t)even(m) * b);
+  L.chosen = c.take<int>(n);
+  L.lorderA = c.take<int>(n);
+  L.lorderB = c.take<int>(n);
+  L.rankA = c.take<int>(n);
+  L.rankB = c.take<int>(n);
+  L.newloc = c.take<int>(n);
+  L.src = c.take<int>(2 * (size_t)std::max<int64_t>(b, n));
+  L.dst = c.take<int>(2 * (size_t)std::max<int64_t>(b, n));
+  L.nmoves = c.take<int>(4);
+  L.cap = c.take<int>(n);
+  L.iota_b = c.take<int>(std::max<int64_t>(b, n));
+  L.flag = c.take<unsigned char>(n);
+  L.orig = c.take<int64_t>(n);
+  L.ostage = c.take<int64_t>(std::max<int64_t>(2 * b, n));
+  // sweep workspace: largest of (sketch: wdt rows x n cols), (small: b rows x 2b), (final: m rows x b)
+  size_t sw = 0;
+  sw = std::max(sw, sweep_workspace_bytes(wdt, (int)n, sweep_grid_size((int)n)));
+  sw = std::max(sw, sweep_workspace_bytes(b, 2 * b, sweep_grid_size(2 * b)));
+  sw = std::max(sw, sweep_workspace_bytes(m, b, sweep_grid_size(b)));
+  L.sweep_ws_bytes = sw;
+  L.sweep_ws = c.take<char>(sw);
+  L.fstore = c.take<double>(factor_bytes(m, n, b) / 8 + 64);
+  L.total = c.off;
+  return L;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM shorthands (column-major views)
+// ---------------------------------------------------------------------------
+static GemmOperand op(const double* base, int64_t rows, int64_t cols, int64_t ld, int64_t r0 = 0, int64_t c0 = 0) {
+  GemmOperand o;
+  o.base = base;
+  o.rows = rows;
+  o.cols = cols;
+  o.ld = ld;
+  o.r0 = r0;
+  o.c0 = c0;
+  return o;
+}
+
+int Ctx::gemm(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmajor, const GemmOperand& B,
+              double* C, int64_t ldc, double alpha, double beta) {
+  GemmProblem p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.A = A;
+  p.a_mmajor = a_mmajor;
+  p.B = B;
+  p.C = C;
+  p.ldc = ldc;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.splitk = 1;
+  p.work = kwork;
+  // split-K when the output tiles cannot fill the machine and K is long
+  const int64_t tiles = ceil_div(M, 128) * ceil_div(N, 128);
+  const int64_t kch = ceil_div(K, 16);
+  if (kwork && tiles * 2 <= kSMs && kch >= 32) {
+    int64_t sk = std::min<int64_t>(kSMs / tiles, kch / 16);
+    while (sk > 1 && gemm_splitk_workspace(M + 1, N, (int)sk) > kwork_bytes) sk--;
+    if (sk > 1) p.splitk = (int)sk;
+  }
+  return gemm_f64(p, stream, &launches);
+}
+
+int Ctx::sweep(SweepCall c) {
+  SweepWork w;
+  w.scratch = sweep_ws;
+  w.scratch_bytes = sweep_ws_bytes;
+  w.barriers = barriers;
+  w.nbarriers = nbarriers;
+  w.next = next_barrier;
+  int rc = sweep_launch(c, w, stream, &launches);
+  next_barrier = w.next;
+  if (w.wrapped) {
+    // ring wrapped: re-zero (stream-ordered after every launch that used it)
+    RQ_CUDA_TRY(cudaMemsetAsync(barriers, 0, sizeof(unsigned) * nbarriers, stream));
+    launches++;
+  }
+  return rc;
+}
+
+// ---------------------------------------------------------------------------
+// Panel QR of A[s:, s:s+b] (m' x b): leaf kernels + WY updates of the rest.
+// ---------------------------------------------------------------------------
+int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, double* V, int64_t ldv,
+                  int vpad, double* tleaf, double* w1, double* w2) {
+  const int wl_max = leaf_width_for(mp);
+  if (wl_max == 0) return set_error(RQ_EUNSUPPORTED, "panel of %lld rows exceeds the leaf kernel", (long long)mp);
+  const int wl = std::min(wl_max, 32);
+  for (int k0 = 0; k0 < b; k0 += wl) {
+    const int w = std::min(wl, b - k0);
+    const int64_t mm = mp - k0;
+    LeafCall lc;
+    lc.a = A + (s + k0) + (s + k0) * lda;
+    lc.lda = lda;
+    lc.mm = mm;
+    lc.w = w;
+    lc.v = V + vpad + k0 + (int64_t)k0 * ldv;
+    lc.ldv = ldv;
+    lc.tl = tleaf;
+    lc.ldt = 32;
+    RQ_TRY(leaf_qr(lc, stream, &launches));
+    const int64_t nrest = b - k0 - w;
+    if (nrest <= 0) break;
+    // W = V_l^T A_rest ; W2 = T_l^T W ; A_rest -= V_l W2
+    const int64_t ldw = even(w);
+    RQ_TRY(gemm(w, nrest, mm, op(V, mp + vpad, b, ldv, vpad + k0, k0), false, op(A, m, n, lda, s + k0, s + k0 + w),
+                w1, ldw, 1.0, 0.0));
+    RQ_TRY(gemm(w, nrest, w, op(tleaf, 32, 32, 32), false, op(w1, w, nrest, ldw), w2, ldw, 1.0, 0.0));
+    RQ_TRY(gemm(mm, nrest, w, op(V, mp + vpad, b, ldv, vpad + k0, k0), true, op(w2, w, nrest, ldw),
+                A + (s + k0) + (s + k0 + w) * lda, lda, -1.0, 1.0));
+  }
+  return RQ_OK;
+}
+
+// T (k x k) of the reflectors V (rows x k): Gram by DMMA GEMM, then back substitution.
+int Ctx::tfactor(const double* V, int64_t rows, int k, int64_t ldv, int vpad, double* T, int64_t ldt, double* gram) {
+  const int64_t ldg = even(k);
+  RQ_TRY(gemm(k, k, rows, op(V, rows + vpad, k, ldv, vpad), false, op(V, rows + vpad, k, ldv, vpad), gram, ldg, 1.0,
+              0.0));
+  return tfactor_from_gram(gram, ldg, k, T, ldt, stream, &launches);
+}
+
+// ---------------------------------------------------------------------------
+// block_qr with permutation pivots, fresh sketches (reference semantics)
+// ---------------------------------------------------------------------------
+int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, int64_t lda, uint64_t seed,
+                        uint64_t* counter, int64_t* dperm) {
+  const int b = cfg.block, p = cfg.oversample, wdt = b + p;
+  size_t need = plan_layout(nullptr, m, n, b, p, cfg.power).total;
+  RQ_TRY(arena.reserve(need));
+  Layout L = plan_layout(arena.base, m, n, b, p, cfg.power);
+  kwork = L.kwork;
+  kwork_bytes = L.kwork_bytes;
+  sweep_ws = L.sweep_ws;
+  sweep_ws_bytes = L.sweep_ws_bytes;
+  cur_A = A;
+  cur_lda = lda;
+  cur_m = m;
+  cur_n = n;
+  cur_orig = L.orig;
+
+  factors.clear();
+  factors_perm = L.orig;
+  fm = m;
+  fn = n;
+  fb = b;
+
+  RQ_TRY(iota(L.lorderA, (int)n, L.orig, n, stream, &launches));
+  RQ_TRY(iota(L.rankA, (int)n, nullptr, 0, stream, &launches));
+  RQ_TRY(iota(L.iota_b, (int)std::max<int64_t>(b, n), nullptr, 0, stream, &launches));
+  int* lorder = L.lorderA;
+  int* lorder_n = L.lorderB;
+  int* rank = L.rankA;
+  int* rank_n = L.rankB;
+  Carver fc(L.fstore);
+  double* tleaf = L.tleaf;
+
+  int panel = 0;
+  for (int64_t s = 0; s < n; s += b) {
+    panel++;
+    const int64_t mp = m - s, np = n - s;
+    cur_s = s;
+    cur_lorder = lorder;
+    cur_np = np;
+    if (np <= b) {
+      // ---------------- final block: CPQR at full height ----------------
+      const int w = (int)np;
+      const int steps = (int)std::min<int64_t>(mp, w);
+      // bring the remaining columns into reference order
+      MoveCall mv{A, lda, s, 0, m, lorder, L.iota_b, nullptr, w, L.stage, even(m), L.orig, L.ostage};
+      RQ_TRY(move_columns(mv, stream, &launches));
+      const int64_t ldv = even(mp + 1);
+      const int vpad = (int)(s & 1);
+      double* Vf = fc.take<double>((size_t)ldv * steps);
+      double* Tf = fc.take<double>((size_t)even(b) * b);
+      RQ_CUDA_TRY(cudaMemsetAsync(Vf, 0, (size_t)ldv * steps * 8, stream));
+      launches++;
+      SweepCall sc;
+      sc.a = A + s + s * lda;
+      sc.lda = lda;
+      sc.m = mp;
+      sc.n = w;
+      sc.steps = steps;
+      sc.pivot = 1;
+      sc.v = Vf + vpad;
+      sc.ldv = ldv;
+      sc.col_at_pos = L.cap;
+      sc.r_out = L.stage;
+      sc.ldr = even(mp);
+      RQ_TRY(sweep(sc));
+      RQ_TRY(copy2d(L.stage, even(mp), A + s + s * lda, lda, mp, w, 0, stream, &launches));
+      // rows above and labels follow the final block's permutation
+      MoveCall mv2{A, lda, s, 0, s, L.cap, L.iota_b, nullptr, w, L.stage, even(m), L.orig, L.ostage};
+      RQ_TRY(move_columns(mv2, stream, &launches));
+      RQ_TRY(tfactor(Vf, mp, steps, ldv, vpad, Tf, even(b), L.gram));
+      factors.push_back(PanelFactors{s, steps, Vf, ldv, vpad, Tf, even(b), nullptr, 0});
+      RQ_TRY(iota(lorder, (int)np, nullptr, 0, stream, &launches));
+      if (inspect_cb) {
+        cur_lorder = nullptr;
+        RQ_CUDA_TRY(cudaStreamSynchronize(stream));
+        inspect_cb(panel, inspect_user);
+      }
+      break;
+    }
+    // ---------------- 1-2: sketch Y^T = Omega^T X ----------------
+    RQ_TRY(gaussian_fill(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
+    *counter += (uint64_t)mp * (uint64_t)wdt;
+    RQ_TRY(sketch(cfg, A, lda, m, n, s, mp, np, L));
+    // ---------------- 3: b-step CPQR of Y^T ----------------
+    SweepCall sc;
+    sc.a = L.yt;
+    sc.lda = L.ldy;
+    sc.m = wdt;
+    sc.n = (int)np;
+    sc.steps = b;
+    sc.pivot = 1;
+    sc.init_pos = rank;
+    sc.col_at_pos = L.cap;
+    RQ_TRY(sweep(sc));
+    // ---------------- 4: move the chosen columns into the panel ----------------
+    PlanCall pc{L.cap, b, lorder, (int)np, L.flag, L.newloc, L.src, L.dst, L.nmoves, lorder_n, rank_n};
+    RQ_TRY(plan_moves(pc, stream, &launches));
+    MoveCall mv{A, lda, s, 0, m, L.src, L.dst, L.nmoves, 2 * b, L.stage, even(m), L.orig, L.ostage};
+    RQ_TRY(move_columns(mv, stream, &launches));
+    // ---------------- 5: unpivoted panel QR ----------------
+    const int64_t ldv = even(mp + 1), ldt = even(b);
+    const int vpad = (int)(s & 1);
+    double* V = fc.take<double>((size_t)ldv * b);
+    double* T = fc.take<double>((size_t)ldt * b);
+    double* Q2t = fc.take<double>((size_t)ldt * b);
+    // V is lower trapezoidal: the leaves write rows >= their diagonal only
+    RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * b * sizeof(double), stream));
+    launches++;
+    RQ_TRY(panel_qr(A, lda, m, n, s, mp, b, V, ldv, vpad, tleaf, L.w1, L.w2));
+    // ---------------- 6: b x b CPQR of R' with Q2^T accumulated ----------------
+    double* S = L.small;
+    RQ_TRY(copy2d(A + s + s * lda, lda, S, L.lds_small, b, b, 1, stream, &launches));
+    RQ_TRY(fill_eye(S + (int64_t)b * L.lds_small, L.lds_small, b, b, 0, stream, &launches));
+    SweepCall ss;
+    ss.a = S;
+    ss.lda = L.lds_small;
+    ss.m = b;
+    ss.n = b;
+    ss.n_acc = b;
+    ss.steps = b;
+    ss.pivot = 1;
+    ss.col_at_pos = L.cap;
+    ss.r_out = L.rfin;
+    ss.ldr = L.lds_small;
+    RQ_TRY(sweep(ss));
+    RQ_TRY(copy2d(S + (int64_t)b * L.lds_small, L.lds_small, Q2t, ldt, b, b, 0, stream, &launches));
+    // ---------------- 7: R and the rows above follow P-hat ----------------
+    RQ_TRY(copy2d(L.rfin, L.lds_small, A + s + s * lda, lda, b, b, 0, stream, &launches));
+    MoveCall mv2{A, lda, s, 0, s, L.cap, L.iota_b, nullptr, b, L.stage, even(m), L.orig, L.ostage};
+    RQ_TRY(move_columns(mv2, stream, &launches));
+    // ---------------- 8: T of the panel reflectors ----------------
+    RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
+    // ---------------- 9: trailing update ----------------
+    const int64_t n2 = np - b;
+    if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2t, L));
+    factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2t, ldt});
+    std::swap(lorder, lorder_n);
+    std::swap(rank, rank_n);
+    if (inspect_cb) {
+      cur_s = s + b;
+      cur_lorder = lorder;
+      cur_np = np - b;
+      RQ_CUDA_TRY(cudaStreamSynchronize(stream));
+      inspect_cb(panel, inspect_user);
+    }
+  }
+  cur_lorder = nullptr;
+  if (dperm) {
+    RQ_CUDA_TRY(cudaMemcpyAsync(dperm, L.orig, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, stream));
+    launches++;
+  }
+  have_factors = true;
+  return RQ_OK;
+}
+
+// Y^T ((b+p) x n') of the trailing block X = A[s:, s:]: (X^T X)^q X^T Omega,
+// built from TN/NN DMMA GEMMs (pivoting.py:87-111, unstabilised powers).
+int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int64_t np,
+                Layout& L) {
+  const int wdt = cfg.block + cfg.oversample;
+  const bool stab = cfg.stabilize < 0 ? cfg.power >= 2 : cfg.stabilize != 0;
+  if (stab) return set_error(RQ_EUNSUPPORTED, "stabilised power iterations are not implemented yet");
+  const GemmOperand X = op(A, m, n, lda, s, s);
+  const int pad = (int)(s & 1);
+  const GemmOperand Om = op(L.omega, mp + pad, wdt, L.ldo, pad);
+  if (cfg.power == 0) return gemm(wdt, np, mp, Om, false, X, L.yt, L.ldy, 1.0, 0.0);
+  // Y = X^T Omega (np x wdt) in w1-sized scratch; Z = X Y (mp x wdt) in omega
+  double* Y = L.ybuf;  // np x wdt
+  const int64_t ldY = even(np);
+  RQ_TRY(gemm(np, wdt, mp, X, false, Om, Y, ldY, 1.0, 0.0));
+  for (int it = 0; it < cfg.power; it++) {
+    // Z = X Y, stored with the same row padding as Omega
+    RQ_TRY(gemm(mp, wdt, np, op(A, m, n, lda, s, s), true, op(Y, np, wdt, ldY), L.omega + pad, L.ldo, 1.0, 0.0));
+    if (it + 1 < cfg.power) RQ_TRY(gemm(np, wdt, mp, X, false, Om, Y, ldY, 1.0, 0.0));
+  }
+  // Y^T = Z^T X
+  return gemm(wdt, np, mp, Om, false, X, L.yt, L.ldy, 1.0, 0.0);
+}
+
+int Ctx::trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, int64_t n2,
+                         const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2t,
+                         Layout& L) {
+  const int64_t ldw = even(b);
+  const GemmOperand Vop = op(V, mp + vpad, b, ldv, vpad);
+  // W = V^T A2   (b x n2, K = m')
+  RQ_TRY(gemm(b, n2, mp, Vop, false, op(A, m, n, lda, s, s + b), L.w1, ldw, 1.0, 0.0));
+  // W2 = T^T W
+  RQ_TRY(gemm(b, n2, b, op(T, b, b, ldt), false, op(L.w1, b, n2, ldw), L.w2, ldw, 1.0, 0.0));
+  // A2 -= V W2
+  RQ_TRY(gemm(mp, n2, b, Vop, true, op(L.w2, b, n2, ldw), A + s + (s + b) * lda, lda, -1.0, 1.0));
+  if (Q2t) {
+    // top b rows <- Q2^T top
+    RQ_TRY(copy2d(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
+    RQ_TRY(gemm(b, n2, b, op(Q2t, b, b, ldt), true, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
+  }
+  return RQ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Q = U_1 ... U_L applied to eye(m, cols) (blocked.py:134-141), backwards, on
+// the trailing block X = Q[s:, s:] only (columns < s are untouched unit vectors).
+// ---------------------------------------------------------------------------
+int Ctx::form_q(int64_t cols, double* Q, int64_t ldq) {
+  if (!have_factors) return set_error(RQ_EVALUE, "no factorization stored in this context");
+  const int64_t m = fm;
+  RQ_TRY(fill_eye(Q, ldq, m, cols, 0, stream, &launches));
+  const int b = fb;
+  const int64_t ldw = even(std::max(b, 2));
+  size_t need = (size_t)3 * ldw * cols * 8 + (size_t)kSMs * b * b * 8 + 1024;
+  RQ_TRY(qarena.reserve(need));
+  Carver c(qarena.base);
+  double* w1 = c.take<double>((size_t)ldw * cols);
+  double* w2 = c.take<double>((size_t)ldw * cols);
+  double* tt = c.take<double>((size_t)ldw * cols);
+  double* save_kw = kwork;
+  size_t save_kb = kwork_bytes;
+  kwork = c.take<double>((size_t)kSMs * b * b);
+  kwork_bytes = (size_t)kSMs * b * b * 8;
+  int rc = RQ_OK;
+  for (int i = (int)factors.size() - 1; i >= 0 && rc == RQ_OK; i--) {
+    const PanelFactors& f = factors[i];
+    const int64_t s = f.s, mp = m - s, nc = cols - s;
+    if (nc <= 0) continue;
+    double* X = Q + s + s * ldq;
+    if (f.q2t) {
+      // X[0:k] <- Q2 X[0:k]   (Q2 = (Q2^T)^T: TN with A = Q2^T)
+      rc = copy2d(X, ldq, tt, ldw, f.k, nc, 0, stream, &launches);
+      if (rc == RQ_OK)
+        rc = gemm(f.k, nc, f.k, op(f.q2t, f.k, f.k, f.ldq2), false, op(tt, f.k, nc, ldw), X, ldq, 1.0, 0.0);
+    }
+    if (rc != RQ_OK) break;
+    // X <- X - V T (V^T X)
+    const GemmOperand Vop = op(f.v, mp + f.vpad, f.k, f.ldv, f.vpad);
+    rc = gemm(f.k, nc, mp, Vop, false, op(Q, m, cols, ldq, s, s), w1, ldw, 1.0, 0.0);
+    if (rc == RQ_OK)
+      rc = gemm(f.k, nc, f.k, op(f.t, f.k, f.k, f.ldt), true, op(w1, f.k, nc, ldw), w2, ldw, 1.0, 0.0);
+    if (rc == RQ_OK)
+      rc = gemm(mp, nc, f.k, Vop, true, op(w2, f.k, nc, ldw), X, ldq, -1.0, 1.0);
+  }
+  kwork = save_kw;
+  kwork_bytes = save_kb;
+  return rc;
+}
+
+int Ctx::form_p(double* P, int64_t ldp) {
+  if (!have_factors) return set_error(RQ_EVALUE, "no factorization stored in this context");
+  return perm_to_dense(factors_perm, fn, P, ldp, stream, &launches);
+}
+
+int Ctx::snapshot(double* hW, int64_t ldh) {
+  if (!cur_A) return set_error(RQ_EVALUE, "no factorization in progress");
+  RQ_CUDA_TRY(cudaStreamSynchronize(stream));
+  const int64_t m = cur_m, n = cur_n, s = cur_lorder ? cur_s : n;
+  RQ_CUDA_TRY(cudaMemcpy2D(hW, ldh * 8, cur_A, cur_lda * 8, m * 8, s, cudaMemcpyDeviceToHost));
+  if (cur_lorder && s < n) {
+    std::vector<int> lo((size_t)(n - s));
+    RQ_CUDA_TRY(cudaMemcpy(lo.data(), cur_lorder, (n - s) * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < n - s; r++)
+      RQ_CUDA_TRY(cudaMemcpy(hW + (s + r) * ldh, cur_A + (s + lo[r]) * cur_lda, m * 8, cudaMemcpyDeviceToHost));
+  }
+  return RQ_OK;
+}
+
+Ctx::~Ctx() {
+  arena.release();
+  qarena.release();
+  if (barriers) cudaFree(barriers);
+}
+
+}  // namespace rq

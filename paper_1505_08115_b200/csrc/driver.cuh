@@ -1,0 +1,98 @@
+// Host-side driver state (see driver.cu) behind the opaque rq_ctx.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+#include "gemm_f64.cuh"
+#include "sweep.cuh"
+
+namespace rq {
+
+static inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
+
+struct Arena {
+  void* base = nullptr;
+  size_t cap = 0;
+  int reserve(size_t bytes);
+  void release();
+};
+
+struct Layout {
+  // scratch
+  double *omega, *yt, *w1, *w2, *gram, *tleaf, *ybuf, *kwork, *small, *rfin, *stage, *ttop;
+  int64_t ldo, ldy, lds_small;
+  int *chosen, *lorderA, *lorderB, *rankA, *rankB, *newloc, *src, *dst, *nmoves, *cap, *iota_b;
+  unsigned char* flag;
+  int64_t *orig, *ostage;
+  void* sweep_ws;
+  size_t sweep_ws_bytes;
+  size_t kwork_bytes;
+  // stored factors
+  double* fstore;
+  size_t total;
+};
+
+// Compact factors of one panel: U = (I - V T V^T) diag(Q2, I) on rows s..m-1.
+struct PanelFactors {
+  int64_t s;
+  int k;  // reflector count
+  double* v;  // buffer base; row r of the reflectors is v[vpad + r]
+  int64_t ldv;
+  int vpad;   // 1 when s is odd: keeps TMA coordinates 16-byte aligned
+  double* t;
+  int64_t ldt;
+  double* q2t;  // k x k (null for the final block)
+  int64_t ldq2;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  rq_panel_cb inspect_cb = nullptr;
+  void* inspect_user = nullptr;
+  int64_t launches = 0;
+  Arena arena, qarena;
+  unsigned int* barriers = nullptr;
+  int nbarriers = 0;
+  int next_barrier = 0;
+  // scratch views used by helpers
+  double* kwork = nullptr;
+  size_t kwork_bytes = 0;
+  void* sweep_ws = nullptr;
+  size_t sweep_ws_bytes = 0;
+  // stored factorization
+  std::vector<PanelFactors> factors;
+  int64_t* factors_perm = nullptr;
+  int64_t fm = 0, fn = 0;
+  int fb = 0;
+  bool have_factors = false;
+  // in-progress view for rq_snapshot
+  double* cur_A = nullptr;
+  int64_t cur_lda = 0, cur_m = 0, cur_n = 0, cur_s = 0, cur_np = 0;
+  int* cur_lorder = nullptr;
+  int64_t* cur_orig = nullptr;
+
+  ~Ctx();
+  int gemm(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmajor, const GemmOperand& B, double* C,
+           int64_t ldc, double alpha, double beta);
+  int sweep(SweepCall c);
+  int panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, double* V, int64_t ldv,
+               int vpad, double* tleaf, double* w1, double* w2);
+  int tfactor(const double* V, int64_t rows, int k, int64_t ldv, int vpad, double* T, int64_t ldt, double* gram);
+  int sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int64_t np,
+             Layout& L);
+  int trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, int64_t n2,
+                      const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2t,
+                      Layout& L);
+  int factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, int64_t lda, uint64_t seed,
+                     uint64_t* counter, int64_t* dperm);
+  int form_q(int64_t cols, double* Q, int64_t ldq);
+  int form_p(double* P, int64_t ldp);
+  int snapshot(double* hW, int64_t ldh);
+};
+
+}  // namespace rq
+
+struct rq_ctx {
+  rq::Ctx c;
+};

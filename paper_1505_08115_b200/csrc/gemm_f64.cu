@@ -1,0 +1,479 @@
+// FP64 DMMA GEMM with a TMA/mbarrier producer-consumer pipeline (see gemm_f64.cuh).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "gemm_f64.cuh"
+
+namespace rq {
+
+// ---------------------------------------------------------------------------
+// PTX wrappers: mbarrier + TMA
+// ---------------------------------------------------------------------------
+RQ_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+RQ_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+RQ_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+RQ_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+RQ_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+RQ_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+RQ_DEV void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+RQ_DEV void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// ---------------------------------------------------------------------------
+// Kernel
+// ---------------------------------------------------------------------------
+constexpr int BK = 16;  // 16 doubles = one 128 B swizzle row
+
+struct KArgs {
+  int64_t M, N, K;
+  int a_c0, a_c1;  // TMA coordinate origins of the A view (dim0, dim1)
+  int b_c0, b_c1;
+  double* C;
+  int64_t ldc;
+  double alpha, beta;
+  int tiles_m, tiles_n, splitk, kchunks_per_split;
+  int64_t kchunks;
+  double* work;  // split-K slabs (ld = M)
+  int k_lo;      // 1: element k = 0 is padding (odd K origin shifted to even)
+  int m_lo;      // 1: output row 0 is padding (odd M origin shifted to even)
+};
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
+struct GemmCfg {
+  static constexpr int kConsumerWarps = WARPS_M * WARPS_N;
+  static constexpr int kThreads = kConsumerWarps * 32;  // thread 0 doubles as the TMA producer
+  static constexpr int WTM = BM / WARPS_M;
+  static constexpr int WTN = BN / WARPS_N;
+  static constexpr int MT = WTM / 16;
+  static constexpr int NT = WTN / 8;
+  static constexpr int A_LDM = BM + 8;  // padded M-major row (conflict-free fragments)
+  static constexpr int A_BYTES = A_MMAJOR ? BK * A_LDM * 8 : BM * BK * 8;
+  static constexpr int A_BYTES_AL = (A_BYTES + 1023) / 1024 * 1024;
+  static constexpr int B_BYTES = BN * BK * 8;
+  static constexpr int STAGE_BYTES = A_BYTES_AL + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 2 * STAGES * 8;
+  static_assert(WTM % 16 == 0 && WTN % 8 == 0, "warp tile");
+  static_assert(B_BYTES % 1024 == 0, "swizzle-128B stage alignment");
+};
+
+// element (r, k) of a K-major 16-wide tile written by TMA with SWIZZLE_128B
+RQ_DEV double ld_kmajor(const char* tile, int r, int k) {
+  const int off = r * 128 + ((((k >> 1) ^ (r & 7))) << 4) + ((k & 1) << 3);
+  return *reinterpret_cast<const double*>(tile + off);
+}
+
+// Walks this CTA's (unit, k-chunk) sequence; units are assigned round-robin.
+struct ChunkCursor {
+  int u;
+  int64_t kc, kc_end;
+  bool valid;
+  RQ_DEV void unit_range(const KArgs& a) {
+    const int split = u % a.splitk;
+    kc = (int64_t)split * a.kchunks_per_split;
+    kc_end = kc + a.kchunks_per_split;
+    if (kc_end > a.kchunks) kc_end = a.kchunks;
+  }
+  RQ_DEV void start(const KArgs& a, int units) {
+    u = blockIdx.x;
+    valid = u < units;
+    if (valid) unit_range(a);
+    skip_empty(a, units);
+  }
+  RQ_DEV void skip_empty(const KArgs& a, int units) {
+    while (valid && kc >= kc_end) {
+      u += gridDim.x;
+      valid = u < units;
+      if (valid) unit_range(a);
+    }
+  }
+  RQ_DEV void next(const KArgs& a, int units) {
+    kc++;
+    skip_empty(a, units);
+  }
+};
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
+RQ_DEV void issue_stage(const CUtensorMap* tmA, const CUtensorMap* tmB, const KArgs& a, unsigned char* smem,
+                        uint64_t* full, int stage, const ChunkCursor& c) {
+  using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>;
+  const int t = c.u / a.splitk;
+  const int tm = t % a.tiles_m;
+  const int tn = t / a.tiles_m;
+  unsigned char* sA = smem + stage * Cfg::STAGE_BYTES;
+  unsigned char* sB = sA + Cfg::A_BYTES_AL;
+  mbar_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+  const int k = (int)(c.kc * BK);
+  if (A_MMAJOR)
+    tma_load_2d(sA, tmA, &full[stage], a.a_c0 + tm * BM, a.a_c1 + k);
+  else
+    tma_load_2d(sA, tmA, &full[stage], a.a_c0 + k, a.a_c1 + tm * BM);
+  tma_load_2d(sB, tmB, &full[stage], a.b_c0 + k, a.b_c1 + tn * BN);
+}
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>::kThreads, 1)
+    gemm_f64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const KArgs args) {
+  using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int units = args.tiles_m * args.tiles_n * args.splitk;
+
+  // producer cursor (thread 0 only) runs STAGES chunks ahead of the consumers
+  ChunkCursor prod;
+  int pstage = 0;
+  uint32_t pphase = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], Cfg::kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    prod.start(args, units);
+    for (int s = 0; s < STAGES && prod.valid; s++) {
+      issue_stage<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(&tmA, &tmB, args, smem, full, pstage, prod);
+      prod.next(args, units);
+      if (++pstage == STAGES) {
+        pstage = 0;
+        pphase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+
+  const int wm = warp % WARPS_M;
+  const int wn = warp / WARPS_M;
+  const int g = lane >> 2;
+  const int tq = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int split = u % args.splitk;
+    const int t = u / args.splitk;
+    const int tm = t % args.tiles_m;
+    const int tn = t / args.tiles_m;
+    const int64_t kc_begin = (int64_t)split * args.kchunks_per_split;
+    int64_t kc_end = kc_begin + args.kchunks_per_split;
+    if (kc_end > args.kchunks) kc_end = args.kchunks;
+
+    double acc[Cfg::MT][Cfg::NT][4];
+#pragma unroll
+    for (int i = 0; i < Cfg::MT; i++)
+#pragma unroll
+      for (int j = 0; j < Cfg::NT; j++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
+
+    for (int64_t kc = kc_begin; kc < kc_end; kc++) {
+      mbar_wait(&full[stage], phase);
+      const unsigned char* sA = smem + stage * Cfg::STAGE_BYTES;
+      const unsigned char* sB = sA + Cfg::A_BYTES_AL;
+      const int64_t kvalid = args.K - kc * BK;  // >= 16 except on the K tail
+      const int klo = (kc == 0) ? args.k_lo : 0;  // leading padding element
+      if (kvalid >= BK && klo == 0) {
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+          double af[Cfg::MT][2], bf[Cfg::NT];
+#pragma unroll
+          for (int i = 0; i < Cfg::MT; i++) {
+            const int r = wm * Cfg::WTM + i * 16 + g;
+            if (A_MMAJOR) {
+              const double* a = reinterpret_cast<const double*>(sA);
+              af[i][0] = a[(kk + tq) * Cfg::A_LDM + r];
+              af[i][1] = a[(kk + tq) * Cfg::A_LDM + r + 8];
+            } else {
+              af[i][0] = ld_kmajor((const char*)sA, r, kk + tq);
+              af[i][1] = ld_kmajor((const char*)sA, r + 8, kk + tq);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < Cfg::NT; j++)
+            bf[j] = ld_kmajor((const char*)sB, wn * Cfg::WTN + j * 8 + g, kk + tq);
+#pragma unroll
+          for (int i = 0; i < Cfg::MT; i++)
+#pragma unroll
+            for (int j = 0; j < Cfg::NT; j++) dmma_16x8x4(acc[i][j], af[i][0], af[i][1], bf[j]);
+        }
+      } else {
+        // K tail: mask k >= K (the TMA box may have read real, unrelated data)
+        for (int kk = 0; kk < BK; kk += 4) {
+          const bool ok = (kk + tq) < kvalid && (kk + tq) >= klo;
+          double af[Cfg::MT][2], bf[Cfg::NT];
+#pragma unroll
+          for (int i = 0; i < Cfg::MT; i++) {
+            const int r = wm * Cfg::WTM + i * 16 + g;
+            if (A_MMAJOR) {
+              const double* a = reinterpret_cast<const double*>(sA);
+              af[i][0] = ok ? a[(kk + tq) * Cfg::A_LDM + r] : 0.0;
+              af[i][1] = ok ? a[(kk + tq) * Cfg::A_LDM + r + 8] : 0.0;
+            } else {
+              af[i][0] = ok ? ld_kmajor((const char*)sA, r, kk + tq) : 0.0;
+              af[i][1] = ok ? ld_kmajor((const char*)sA, r + 8, kk + tq) : 0.0;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < Cfg::NT; j++)
+            bf[j] = ok ? ld_kmajor((const char*)sB, wn * Cfg::WTN + j * 8 + g, kk + tq) : 0.0;
+#pragma unroll
+          for (int i = 0; i < Cfg::MT; i++)
+#pragma unroll
+            for (int j = 0; j < Cfg::NT; j++) dmma_16x8x4(acc[i][j], af[i][0], af[i][1], bf[j]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      // producer: refill this stage with the chunk STAGES ahead once every warp released it
+      if (threadIdx.x == 0 && prod.valid) {
+        mbar_wait(&empty[pstage], pphase ^ 1);
+        issue_stage<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(&tmA, &tmB, args, smem, full, pstage, prod);
+        prod.next(args, units);
+        if (++pstage == STAGES) {
+          pstage = 0;
+          pphase ^= 1;
+        }
+      }
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+
+    // ------------------------------ epilogue ------------------------------
+    const int64_t m_base = (int64_t)tm * BM + wm * Cfg::WTM;
+    const int64_t n_base = (int64_t)tn * BN + wn * Cfg::WTN;
+    if (args.splitk > 1) {
+      double* W = args.work + (int64_t)split * args.M * args.N;
+#pragma unroll
+      for (int i = 0; i < Cfg::MT; i++)
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; j++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const int64_t m = m_base + i * 16 + g + ((e & 2) ? 8 : 0);
+            const int64_t n = n_base + j * 8 + 2 * tq + (e & 1);
+            if (m < args.M && n < args.N) W[n * args.M + m] = acc[i][j][e];
+          }
+    } else {
+#pragma unroll
+      for (int i = 0; i < Cfg::MT; i++)
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; j++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const int64_t m = m_base + i * 16 + g + ((e & 2) ? 8 : 0);
+            const int64_t n = n_base + j * 8 + 2 * tq + (e & 1);
+            if (m < args.M && n < args.N && m >= args.m_lo) {
+              double* c = args.C + n * args.ldc + m;
+              double v = args.alpha * acc[i][j][e];
+              if (args.beta != 0.0) v = fma(args.beta, *c, v);
+              *c = v;
+            }
+          }
+    }
+  }
+}
+
+// Deterministic split-K reduction: C = alpha * sum_s W_s + beta * C (fixed s order).
+__global__ void splitk_reduce_kernel(const double* __restrict__ work, int splitk, int64_t M, int64_t N,
+                                     double* C, int64_t ldc, double alpha, double beta, int m_lo) {
+  const int64_t total = M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < splitk; k++) s += work[k * total + idx];
+    const int64_t m = idx % M, n = idx / M;
+    if (m < m_lo) continue;
+    double* c = C + n * ldc + m;
+    double v = alpha * s;
+    if (beta != 0.0) v = fma(beta, *c, v);
+    *c = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encoder() {
+  static std::once_flag once;
+  static int rc = RQ_OK;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || fn == nullptr || q != cudaDriverEntryPointSuccess)
+      rc = set_error(RQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    else
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return rc;
+}
+
+static int make_map(CUtensorMap* map, const GemmOperand& op, uint32_t box0, uint32_t box1, bool swizzle) {
+  if (((uintptr_t)op.base & 15) != 0 || (op.ld & 1) != 0)
+    return set_error(RQ_EINTERNAL, "TMA operand misaligned (base %p, ld %lld)", op.base, (long long)op.ld);
+  cuuint64_t dims[2] = {(cuuint64_t)op.rows, (cuuint64_t)op.cols};
+  cuuint64_t strides[1] = {(cuuint64_t)op.ld * 8};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(op.base), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(RQ_ECUDA, "cuTensorMapEncodeTiled failed (%d): dims %llu x %llu ld %lld box %u x %u", (int)r,
+                     (unsigned long long)op.rows, (unsigned long long)op.cols, (long long)op.ld, box0, box1);
+  return RQ_OK;
+}
+
+static int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = kSMs;
+  }
+  return sms;
+}
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
+static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launches) {
+  using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>;
+  auto kern = gemm_f64_kernel<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    attr_set = true;
+  }
+  CUtensorMap ma, mb;
+  if (A_MMAJOR)
+    RQ_TRY(make_map(&ma, p.A, Cfg::A_LDM, BK, false));
+  else
+    RQ_TRY(make_map(&ma, p.A, BK, BM, true));
+  RQ_TRY(make_map(&mb, p.B, BK, BN, true));
+
+  KArgs a;
+  // TMA faults on an odd fp64 coordinate along the contiguous dimension: shift
+  // odd K origins (both operands, same parity) and odd M-major M origins down
+  // by one element and mask the padding element.
+  const int kshift = (int)(p.B.r0 & 1);
+  if (!A_MMAJOR && (int)(p.A.r0 & 1) != kshift)
+    return set_error(RQ_EINTERNAL, "gemm: K origins of A (%lld) and B (%lld) differ in parity", (long long)p.A.r0,
+                     (long long)p.B.r0);
+  const int mshift = A_MMAJOR ? (int)(p.A.r0 & 1) : 0;
+  a.M = p.M + mshift;
+  a.N = p.N;
+  a.K = p.K + kshift;
+  a.k_lo = kshift;
+  a.m_lo = mshift;
+  a.a_c0 = (int)p.A.r0 - (A_MMAJOR ? mshift : kshift);
+  a.a_c1 = (int)p.A.c0 - (A_MMAJOR ? kshift : 0);
+  a.b_c0 = (int)p.B.r0 - kshift;
+  a.b_c1 = (int)p.B.c0;
+  a.C = p.C - mshift;
+  a.ldc = p.ldc;
+  a.alpha = p.alpha;
+  a.beta = p.beta;
+  a.tiles_m = (int)ceil_div(a.M, BM);
+  a.tiles_n = (int)ceil_div(a.N, BN);
+  a.kchunks = ceil_div(a.K, BK);
+  a.splitk = p.splitk > 1 ? p.splitk : 1;
+  a.kchunks_per_split = (int)ceil_div(a.kchunks, a.splitk);
+  a.work = p.work;
+  const int64_t units = (int64_t)a.tiles_m * a.tiles_n * a.splitk;
+  const int grid = (int)(units < num_sms() ? units : num_sms());
+  kern<<<grid, Cfg::kThreads, Cfg::SMEM, stream>>>(ma, mb, a);
+  {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, kern);
+      return set_error(RQ_ECUDA, "gemm<%d,%d,%d> launch: %s (regs %d, maxThreads %d, static smem %zu, dyn %d, maxdyn %d, grid %d)",
+                       BM, BN, (int)A_MMAJOR, cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock,
+                       fa.sharedSizeBytes, Cfg::SMEM, fa.maxDynamicSharedSizeBytes, grid);
+    }
+  }
+  if (launches) (*launches)++;
+  if (a.splitk > 1) {
+    const int64_t total = a.M * a.N;
+    int blocks = (int)ceil_div(total, 256);
+    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(p.work, a.splitk, a.M, a.N, a.C, p.ldc, p.alpha, p.beta,
+                                                     a.m_lo);
+    RQ_CUDA_TRY(cudaGetLastError());
+    if (launches) (*launches)++;
+  }
+  return RQ_OK;
+}
+
+size_t gemm_splitk_workspace(int64_t M, int64_t N, int splitk) {
+  return splitk > 1 ? (size_t)splitk * M * N * sizeof(double) : 0;
+}
+
+int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches) {
+  if (p.M <= 0 || p.N <= 0) return RQ_OK;
+  if (p.K <= 0) {
+    // C = beta * C
+    if (p.beta == 1.0) return RQ_OK;
+    return set_error(RQ_EINTERNAL, "gemm_f64: K == 0 with beta != 1 not supported");
+  }
+  RQ_TRY(get_encoder());
+  if (p.splitk > 1 && p.work == nullptr) return set_error(RQ_EINTERNAL, "gemm_f64: split-K without workspace");
+  // Tile selection: skinny outputs use narrower tiles so the grid fills 148 SMs.
+  if (p.a_mmajor) {
+    if (p.M >= 128 && p.N >= 128) return launch_cfg<128, 128, 2, 4, true, 4>(p, stream, launches);
+    if (p.N < 128) return launch_cfg<128, 32, 4, 2, true, 6>(p, stream, launches);
+    return launch_cfg<64, 128, 2, 4, true, 5>(p, stream, launches);
+  } else {
+    if (p.M >= 128 && p.N >= 128) return launch_cfg<128, 128, 2, 4, false, 4>(p, stream, launches);
+    if (p.N < 128) return launch_cfg<128, 32, 4, 2, false, 6>(p, stream, launches);
+    return launch_cfg<64, 128, 2, 4, false, 5>(p, stream, launches);
+  }
+}
+
+}  // namespace rq

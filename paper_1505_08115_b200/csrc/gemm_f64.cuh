@@ -1,0 +1,43 @@
+// FP64 tensor-core GEMM for sm_100a: TMA (cp.async.bulk.tensor) -> mbarrier
+// pipeline -> mma.sync m16n8k4 f64 (SASS: DMMA.8x8x4).  FP64 has no tcgen05
+// kind on Blackwell (ptxas rejects kind::f64), so DMMA is the FP64 tensor path;
+// measured 36.9 TFLOP/s peak on B200 (profiles/probe_r01.jsonl).
+//
+//   C[M x N] = alpha * op(A) * B + beta * C        (all column-major)
+//     op(A) = A^T, A stored K x M  (A_MMAJOR = false, "TN": K contiguous)
+//     op(A) = A,   A stored M x K  (A_MMAJOR = true,  "NN": M contiguous)
+//     B stored K x N (K contiguous)
+//
+// The operands are addressed through TMA tensor maps over whole buffers plus
+// element-coordinate origins, so sub-matrix views need no pointer alignment.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace rq {
+
+struct GemmOperand {
+  const double* base;  // buffer base (16 B aligned)
+  int64_t rows;        // buffer extent along the contiguous dimension
+  int64_t cols;        // buffer extent along the strided dimension
+  int64_t ld;          // leading dimension (elements, even)
+  int64_t r0, c0;      // origin of the view inside the buffer
+};
+
+struct GemmProblem {
+  int64_t M, N, K;
+  GemmOperand A;  // TN: rows index K, cols index M.   NN: rows index M, cols index K.
+  bool a_mmajor;
+  GemmOperand B;  // rows index K, cols index N
+  double* C;      // view pointer (already offset), column-major
+  int64_t ldc;
+  double alpha, beta;
+  int splitk;            // >1: deterministic split-K through `work`
+  double* work;          // splitk * M * N doubles (slab per split, ld = M)
+};
+
+int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches);
+size_t gemm_splitk_workspace(int64_t M, int64_t N, int splitk);
+
+}  // namespace rq

@@ -1,0 +1,301 @@
+// Small bandwidth/latency kernels around the panel loop:
+//   * T factor from the Gram matrix (K7),
+//   * pivot bookkeeping and the column moves (K5),
+//   * matrix fills / copies used by the driver and by Q formation (K12).
+#include <cub/block/block_scan.cuh>
+
+#include "common.cuh"
+#include "misc.cuh"
+
+namespace rq {
+
+// ---------------------------------------------------------------------------
+// T = (I/2 + striu(V^T V))^{-1}: the compact-WY factor of U = H_0...H_{k-1}
+// with H_j = I - 2 u_j u_j^T (same T as the wy_accumulate recurrence,
+// householder.py:91-102).  One warp per column, back substitution
+//   t_j = 2,  t_i = -2 sum_{k=i+1..j} G_ik t_k.
+// G is symmetric, so row i is read contiguously as column i.
+// ---------------------------------------------------------------------------
+__global__ void tinv_kernel(const double* __restrict__ G, int64_t ldg, int k, double* __restrict__ T,
+                            int64_t ldt) {
+  extern __shared__ double tcol[];  // per warp: k doubles
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (j >= k) return;
+  double* t = tcol + (int64_t)warp * k;
+  for (int i = lane; i < k; i += 32) t[i] = 0.0;
+  __syncwarp();
+  if (lane == 0) t[j] = 2.0;
+  __syncwarp();
+  for (int i = j - 1; i >= 0; i--) {
+    const double* gi = G + (int64_t)i * ldg;  // G(:, i) == G(i, :)
+    double acc = 0.0;
+    for (int kk = i + 1 + lane; kk <= j; kk += 32) acc += gi[kk] * t[kk];
+    acc = warp_sum(acc);
+    if (lane == 0) t[i] = -2.0 * acc;
+    __syncwarp();
+  }
+  for (int i = lane; i < k; i += 32) T[(int64_t)j * ldt + i] = t[i];
+}
+
+int tfactor_from_gram(const double* G, int64_t ldg, int k, double* T, int64_t ldt, cudaStream_t st,
+                      int64_t* launches) {
+  if (k <= 0) return RQ_OK;
+  const int wpb = 8;
+  const size_t smem = (size_t)wpb * k * sizeof(double);
+  static size_t set = 0;
+  if (smem > 48 * 1024 && smem > set) {
+    RQ_CUDA_TRY(cudaFuncSetAttribute(tinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    set = smem;
+  }
+  tinv_kernel<<<(unsigned)ceil_div(k, wpb), wpb * 32, smem, st>>>(G, ldg, k, T, ldt);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Pivot bookkeeping for one panel (single CTA).
+//
+// Local column indices are relative to the trailing block start s.  Inputs:
+//   chosen[b]  local physical columns picked by the sketch CPQR, pivot order
+//   lorder[n'] local physical column of each logical rank (reference order)
+// Outputs:
+//   moves (src, dst) realising "chosen[k] -> slot k" with the displaced panel
+//   columns moved into the vacated slots (no full-height gather of the rest,
+//   unlike PermutationPivot.apply_right, pivoting.py:60-61);
+//   lorder_next / rank_next of the remaining n'-b columns (rebased by b):
+//   the reference's order "chosen ++ rest in original order" (pivoting.py:125-128).
+// ---------------------------------------------------------------------------
+constexpr int PLAN_THREADS = 1024;
+
+__global__ void __launch_bounds__(PLAN_THREADS) plan_moves_kernel(const int* __restrict__ chosen, int b,
+                                                                  const int* __restrict__ lorder, int np,
+                                                                  unsigned char* __restrict__ flag,
+                                                                  int* __restrict__ newloc, int* __restrict__ src,
+                                                                  int* __restrict__ dst, int* __restrict__ nmoves,
+                                                                  int* __restrict__ lorder_next,
+                                                                  int* __restrict__ rank_next) {
+  using Scan = cub::BlockScan<int, PLAN_THREADS>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int base;
+  __shared__ int nm;
+  for (int i = threadIdx.x; i < np; i += PLAN_THREADS) {
+    flag[i] = 0;
+    newloc[i] = i;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < b; k += PLAN_THREADS) flag[chosen[k]] = 1;
+  if (threadIdx.x == 0) {
+    base = 0;
+    nm = 0;
+  }
+  __syncthreads();
+  // chosen[k] -> k for k with chosen[k] != k
+  for (int k0 = 0; k0 < b; k0 += PLAN_THREADS) {
+    const int k = k0 + threadIdx.x;
+    const int mv = (k < b && chosen[k] != k) ? 1 : 0;
+    int off, tot;
+    Scan(tmp).ExclusiveSum(mv, off, tot);
+    if (mv) {
+      src[base + off] = chosen[k];
+      dst[base + off] = k;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) nm = base;
+  __syncthreads();
+  // displaced panel slots (not chosen), in slot order, pair with vacancies
+  // (chosen columns outside the panel), in pivot order.
+  int dbase = 0, vbase = 0;
+  for (int k0 = 0; k0 < b; k0 += PLAN_THREADS) {
+    const int k = k0 + threadIdx.x;
+    const int isd = (k < b && !flag[k]) ? 1 : 0;
+    int doff, dtot;
+    Scan(tmp).ExclusiveSum(isd, doff, dtot);
+    __syncthreads();
+    if (isd) src[nm + dbase + doff] = k;  // displaced column (local k)
+    dbase += dtot;
+    __syncthreads();
+  }
+  for (int k0 = 0; k0 < b; k0 += PLAN_THREADS) {
+    const int k = k0 + threadIdx.x;
+    const int isv = (k < b && chosen[k] >= b) ? 1 : 0;
+    int voff, vtot;
+    Scan(tmp).ExclusiveSum(isv, voff, vtot);
+    __syncthreads();
+    if (isv) dst[nm + vbase + voff] = chosen[k];
+    vbase += vtot;
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < dbase; t += PLAN_THREADS) newloc[src[nm + t]] = dst[nm + t];
+  if (threadIdx.x == 0) *nmoves = nm + dbase;
+  __syncthreads();
+  // stable compaction of the logical order, dropping the chosen columns
+  int cbase = 0;
+  for (int r0 = 0; r0 < np; r0 += PLAN_THREADS) {
+    const int r = r0 + threadIdx.x;
+    int c = -1, keep = 0;
+    if (r < np) {
+      c = lorder[r];
+      keep = flag[c] ? 0 : 1;
+    }
+    int off, tot;
+    Scan(tmp).ExclusiveSum(keep, off, tot);
+    if (keep) {
+      const int nl = newloc[c] - b;
+      lorder_next[cbase + off] = nl;
+      rank_next[nl] = cbase + off;
+    }
+    cbase += tot;
+    __syncthreads();
+  }
+}
+
+int plan_moves(const PlanCall& c, cudaStream_t st, int64_t* launches) {
+  plan_moves_kernel<<<1, PLAN_THREADS, 0, st>>>(c.chosen, c.b, c.lorder, c.np, c.flag, c.newloc, c.src, c.dst,
+                                                c.nmoves, c.lorder_next, c.rank_next);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Column moves through a staging buffer: dst[t] <- src[t] for rows [r0, r1),
+// plus the same move on the int64 `orig` label array.  Two launches (gather,
+// scatter) because src and dst overlap as sets.  One warp per column,
+// vectorised 16 B accesses when the column start is aligned.
+// ---------------------------------------------------------------------------
+__global__ void gather_cols_kernel(const double* __restrict__ A, int64_t lda, int64_t coff, int64_t r0, int64_t r1,
+                                   const int* __restrict__ src, const int* __restrict__ count, int maxn,
+                                   double* __restrict__ stage, int64_t lds, const int64_t* __restrict__ orig,
+                                   int64_t* __restrict__ ostage) {
+  const int n = count ? *count : maxn;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < n; t += nw) {
+    const double* s = A + (coff + src[t]) * lda;
+    double* d = stage + (int64_t)t * lds;
+    for (int64_t i = r0 + lane; i < r1; i += 32) d[i - r0] = s[i];
+    if (orig && lane == 0) ostage[t] = orig[coff + src[t]];
+  }
+}
+__global__ void scatter_cols_kernel(double* __restrict__ A, int64_t lda, int64_t coff, int64_t r0, int64_t r1,
+                                    const int* __restrict__ dst, const int* __restrict__ count, int maxn,
+                                    const double* __restrict__ stage, int64_t lds, int64_t* __restrict__ orig,
+                                    const int64_t* __restrict__ ostage) {
+  const int n = count ? *count : maxn;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = warp; t < n; t += nw) {
+    double* d = A + (coff + dst[t]) * lda;
+    const double* s = stage + (int64_t)t * lds;
+    for (int64_t i = r0 + lane; i < r1; i += 32) d[i] = s[i - r0];
+    if (orig && lane == 0) orig[coff + dst[t]] = ostage[t];
+  }
+}
+
+int move_columns(const MoveCall& c, cudaStream_t st, int64_t* launches) {
+  if (c.r1 <= c.r0 && !c.orig) return RQ_OK;
+  int blocks = (c.maxn * 32 + 255) / 256;
+  if (blocks > 4 * kSMs) blocks = 4 * kSMs;
+  if (blocks < 1) blocks = 1;
+  gather_cols_kernel<<<blocks, 256, 0, st>>>(c.A, c.lda, c.coff, c.r0, c.r1, c.src, c.count, c.maxn, c.stage,
+                                             c.lds, c.orig, c.ostage);
+  RQ_CUDA_TRY(cudaGetLastError());
+  scatter_cols_kernel<<<blocks, 256, 0, st>>>(c.A, c.lda, c.coff, c.r0, c.r1, c.dst, c.count, c.maxn, c.stage,
+                                              c.lds, c.orig, c.ostage);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches) += 2;
+  return RQ_OK;
+}
+
+// identity index arrays
+__global__ void iota_kernel(int* a, int n, int64_t* b, int64_t nb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n || i < nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (a && i < n) a[i] = (int)i;
+    if (b && i < nb) b[i] = i;
+  }
+}
+int iota(int* a, int n, int64_t* b, int64_t nb, cudaStream_t st, int64_t* launches) {
+  const int64_t mx = n > nb ? n : nb;
+  if (mx <= 0) return RQ_OK;
+  int blocks = (int)ceil_div(mx, 256);
+  if (blocks > 4 * kSMs) blocks = 4 * kSMs;
+  iota_kernel<<<blocks, 256, 0, st>>>(a, n, b, nb);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+// X (rows x cols) = [upper part of S (rows x cols_s) | I] helpers
+__global__ void fill_eye_kernel(double* X, int64_t ldx, int64_t rows, int64_t cols, int64_t diag_off) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx / rows, i = idx - j * rows;
+    X[j * ldx + i] = (i == j + diag_off) ? 1.0 : 0.0;
+  }
+}
+int fill_eye(double* X, int64_t ldx, int64_t rows, int64_t cols, int64_t diag_off, cudaStream_t st,
+             int64_t* launches) {
+  if (rows <= 0 || cols <= 0) return RQ_OK;
+  int blocks = (int)ceil_div(rows * cols, 256);
+  if (blocks > 8 * kSMs) blocks = 8 * kSMs;
+  fill_eye_kernel<<<blocks, 256, 0, st>>>(X, ldx, rows, cols, diag_off);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+// 2-D copy (column-major), optionally zeroing strictly-below-diagonal entries
+__global__ void copy2d_kernel(const double* __restrict__ S, int64_t lds, double* __restrict__ D, int64_t ldd,
+                              int64_t rows, int64_t cols, int upper_only) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx / rows, i = idx - j * rows;
+    D[j * ldd + i] = (upper_only && i > j) ? 0.0 : S[j * lds + i];
+  }
+}
+int copy2d(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows, int64_t cols, int upper_only,
+           cudaStream_t st, int64_t* launches) {
+  if (rows <= 0 || cols <= 0) return RQ_OK;
+  int blocks = (int)ceil_div(rows * cols, 256);
+  if (blocks > 8 * kSMs) blocks = 8 * kSMs;
+  copy2d_kernel<<<blocks, 256, 0, st>>>(S, lds, D, ldd, rows, cols, upper_only);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+// dense P from a permutation: P[perm[k], k] = 1
+__global__ void perm_to_dense_kernel(const int64_t* perm, int64_t n, double* P, int64_t ldp) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    P[k * ldp + perm[k]] = 1.0;
+}
+int perm_to_dense(const int64_t* perm, int64_t n, double* P, int64_t ldp, cudaStream_t st, int64_t* launches) {
+  RQ_TRY(fill_eye(P, ldp, n, n, INT64_MAX / 4, st, launches));  // zeros
+  perm_to_dense_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(perm, n, P, ldp);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+// int32 -> int64 widening with offset (perm outputs)
+__global__ void widen_kernel(const int* a, int n, int64_t off, int64_t* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] + off;
+}
+int widen(const int* a, int n, int64_t off, int64_t* out, cudaStream_t st, int64_t* launches) {
+  if (n <= 0) return RQ_OK;
+  widen_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(a, n, off, out);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+}  // namespace rq

@@ -1,0 +1,54 @@
+// Helper kernels around the panel loop (see misc.cu).
+#pragma once
+#include "common.cuh"
+
+namespace rq {
+
+int tfactor_from_gram(const double* G, int64_t ldg, int k, double* T, int64_t ldt, cudaStream_t st,
+                      int64_t* launches);
+
+struct PlanCall {
+  const int* chosen;
+  int b;
+  const int* lorder;
+  int np;
+  unsigned char* flag;  // np
+  int* newloc;          // np
+  int* src;             // 2b
+  int* dst;             // 2b
+  int* nmoves;          // 1
+  int* lorder_next;     // np - b
+  int* rank_next;       // np - b
+};
+int plan_moves(const PlanCall& c, cudaStream_t st, int64_t* launches);
+
+struct MoveCall {
+  double* A;
+  int64_t lda;
+  int64_t coff;  // column offset of local index 0
+  int64_t r0, r1;
+  const int* src;
+  const int* dst;
+  const int* count;  // device count (or null: maxn)
+  int maxn;
+  double* stage;
+  int64_t lds;
+  int64_t* orig;     // optional label array moved alongside
+  int64_t* ostage;
+};
+int move_columns(const MoveCall& c, cudaStream_t st, int64_t* launches);
+
+int iota(int* a, int n, int64_t* b, int64_t nb, cudaStream_t st, int64_t* launches);
+int fill_eye(double* X, int64_t ldx, int64_t rows, int64_t cols, int64_t diag_off, cudaStream_t st,
+             int64_t* launches);
+int copy2d(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows, int64_t cols, int upper_only,
+           cudaStream_t st, int64_t* launches);
+int perm_to_dense(const int64_t* perm, int64_t n, double* P, int64_t ldp, cudaStream_t st, int64_t* launches);
+int widen(const int* a, int n, int64_t off, int64_t* out, cudaStream_t st, int64_t* launches);
+
+int gaussian_fill(double* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t counter,
+                  cudaStream_t st, int64_t* launches);
+int splitmix_words(uint64_t* out, uint64_t seed, uint64_t first, int64_t count, cudaStream_t st,
+                   int64_t* launches);
+
+}  // namespace rq

@@ -1,0 +1,249 @@
+// K6/K7: unpivoted Householder QR of a tall-skinny leaf (mm x WL, WL <= 32)
+// plus its compact-WY T factor, as one thread-block-cluster kernel.
+//
+// Restates householder_sweep(pivot=False) (_kernels_numba.py:35-61) and the
+// compact-WY recurrence of wy_accumulate (householder.py:91-102) in T form:
+//   H_j = I - 2 u_j u_j^T,  U = H_0 ... H_{w-1} = I - V T V^T,
+//   T_jj = 2,  T(0:j, j) = -2 T(0:j, 0:j) (V(:, 0:j)^T u_j).
+//
+// B200 mapping: a cluster of CS CTAs (16, non-portable) splits the rows; each
+// CTA keeps its rows of the leaf in shared memory.  Per column ONE cluster
+// barrier (~0.22 us measured) exchanges the partial sums (trailing norm,
+// column dots, row-j entries, Gram entries for T) through DSMEM; every CTA
+// then sums the CS partials in rank order (deterministic) and derives the
+// same reflector.  The driver calls it once per WL-column leaf and applies
+// the leaf's WY to the rest of the panel with the DMMA GEMM.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "panel.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rq {
+
+constexpr int PL_THREADS = 512;
+constexpr int PL_WARPS = PL_THREADS / 32;
+
+template <int WL>
+struct LeafLayout {
+  static constexpr int PV = 3 * WL + 1;  // [tail | dots(WL) | rowj(WL) | gram(WL)]
+};
+
+RQ_DEV double dsmem_ld(const double* local_addr, unsigned rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(local_addr);
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(r) : "memory");
+  return v;
+}
+
+RQ_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int WL>
+__global__ void __launch_bounds__(PL_THREADS) leaf_qr_kernel(double* __restrict__ a, int64_t lda, int64_t mm,
+                                                             int w, double* __restrict__ v, int64_t ldv,
+                                                             double* __restrict__ tl, int64_t ldt,
+                                                             int rows_per) {
+  constexpr int PV = LeafLayout<WL>::PV;
+  extern __shared__ double sm[];
+  const unsigned CS = gridDim.x;  // one cluster spans the grid
+  const unsigned rank = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)rank * rows_per;
+  const int64_t r1 = min(mm, r0 + rows_per);
+  const int nr = (int)max((int64_t)0, r1 - r0);
+
+  double* A = sm;                                     // nr x WL (ld = rows_per)
+  double* Vs = A + (int64_t)rows_per * WL;            // nr x WL own rows of V
+  double* part = Vs + (int64_t)rows_per * WL;         // 2 x PV partials
+  double* tot = part + 2 * PV;                        // PV totals
+  double* s = tot + PV;                               // WL coefficients
+  double* Ts = s + WL;                                // WL x WL T (CTA-local copy)
+  double* scal = Ts + WL * WL;                        // [refl, beta, inv, h]
+
+  for (int64_t idx = threadIdx.x; idx < (int64_t)nr * WL; idx += PL_THREADS) {
+    const int c = (int)(idx / nr), i = (int)(idx % nr);
+    A[(int64_t)c * rows_per + i] = c < w ? a[(int64_t)c * lda + r0 + i] : 0.0;
+    Vs[(int64_t)c * rows_per + i] = 0.0;
+  }
+  for (int e = threadIdx.x; e < WL * WL; e += PL_THREADS) Ts[e] = 0.0;
+  __syncthreads();
+
+  bool refl_prev = false;
+  for (int j = 0; j <= w; j++) {
+    const bool final_round = (j == w);  // only the last T column remains
+    // ---------------- phase A: pending update + partials ----------------
+    if (j > 0 && refl_prev && !final_round) {
+      // A[i][c] -= s[c] * u_i for own rows i >= j-1, columns c in [j, w)
+      const int64_t lo = max((int64_t)0, (int64_t)(j - 1) - r0);
+      const int ncols = w - j;
+      for (int64_t idx = threadIdx.x; idx < (int64_t)(nr - lo) * ncols; idx += PL_THREADS) {
+        const int c = j + (int)(idx / (nr - lo));
+        const int64_t i = lo + idx % (nr - lo);
+        A[(int64_t)c * rows_per + i] -= s[c] * Vs[(int64_t)(j - 1) * rows_per + i];
+      }
+      __syncthreads();
+    }
+    double* mypart = part + (j & 1) * PV;
+    // items: 0 -> tail of column j; 1..w-j-1 -> dots with columns j+1..; gram k < j-1
+    const int ndots = final_round ? 0 : (w - j);          // tail + dots
+    const int ngram = (j >= 2) ? (j - 1) : 0;             // Gram entries for T column j-1
+    const int nitems = ndots + ngram;
+    for (int it = warp; it < nitems; it += PL_WARPS) {
+      double acc = 0.0;
+      if (it < ndots) {
+        const int c = j + it;  // it == 0 -> tail (c == j)
+        const int64_t lo = max((int64_t)0, (int64_t)(j + 1) - r0);
+        const double* cj = A + (int64_t)j * rows_per;
+        const double* cc = A + (int64_t)c * rows_per;
+        for (int64_t i = lo + lane; i < nr; i += 32) acc += cj[i] * cc[i];
+      } else {
+        const int k = it - ndots;  // Gram entry V_k . u_{j-1}
+        const double* vk = Vs + (int64_t)k * rows_per;
+        const double* vj = Vs + (int64_t)(j - 1) * rows_per;
+        for (int64_t i = lane; i < nr; i += 32) acc += vk[i] * vj[i];
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        if (it < ndots) mypart[it == 0 ? 0 : 1 + (j + it)] = acc;
+        else mypart[1 + 2 * WL + (it - ndots)] = acc;
+      }
+    }
+    // row-j entries (exactly one CTA owns row j; others contribute zeros)
+    if (!final_round)
+      for (int c = j + threadIdx.x; c < w; c += PL_THREADS)
+        mypart[1 + WL + c] = (j >= r0 && j < r1) ? A[(int64_t)c * rows_per + (j - r0)] : 0.0;
+    cluster_sync_all();
+
+    // ---------------- phase B: identical totals in every CTA ----------------
+    for (int e = threadIdx.x; e < PV; e += PL_THREADS) {
+      bool used;
+      if (e == 0) used = !final_round;
+      else if (e <= WL) used = !final_round && (e - 1) > j && (e - 1) < w;
+      else if (e <= 2 * WL) used = !final_round && (e - 1 - WL) >= j && (e - 1 - WL) < w;
+      else used = (e - 1 - 2 * WL) < ngram;
+      if (!used) continue;
+      double t = 0.0;
+      for (unsigned r = 0; r < CS; r++) t += dsmem_ld(part + (j & 1) * PV + e, r);
+      tot[e] = t;
+    }
+    __syncthreads();
+    // T column j-1 (needs Gram entries of u_{j-1}); T_{jj} = 2 regardless
+    if (j >= 1 && warp == 0) {
+      const int jc = j - 1;
+      // T(0:jc, jc) = -2 T(0:jc, 0:jc) g,   g_k = tot_gram[k]
+      for (int i = lane; i < jc; i += 32) {
+        double acc = 0.0;
+        for (int k = i; k < jc; k++) acc += Ts[k * WL + i] * tot[1 + 2 * WL + k];
+        Ts[jc * WL + i] = -2.0 * acc;
+      }
+      if (lane == 0) Ts[jc * WL + jc] = 2.0;
+    }
+    if (final_round) break;
+    if (threadIdx.x == 0) {
+      const double tail = tot[0];
+      const double xjj = tot[1 + WL + j];
+      const double normsq = xjj * xjj + tail;
+      const bool refl = (mm - j >= 2) && (normsq != 0.0);
+      double beta = 0.0, inv = 0.0, h = 0.0;
+      if (refl) {
+        const double nrm = sqrt(normsq);
+        beta = (xjj >= 0.0) ? -nrm : nrm;
+        h = beta - xjj;
+        inv = 1.0 / sqrt(h * h + tail);
+      }
+      scal[0] = refl ? 1.0 : 0.0;
+      scal[1] = beta;
+      scal[2] = inv;
+      scal[3] = h;
+    }
+    __syncthreads();
+    const bool refl = scal[0] != 0.0;
+    if (refl) {
+      const double beta = scal[1], inv = scal[2], h = scal[3];
+      for (int c = j + 1 + threadIdx.x; c < w; c += PL_THREADS)
+        s[c] = 2.0 * inv * (h * tot[1 + WL + c] - tot[1 + c]);
+      // own rows of u_j; column j becomes beta e_j
+      for (int64_t i = threadIdx.x; i < nr; i += PL_THREADS) {
+        const int64_t gi = r0 + i;
+        double ui = 0.0;
+        if (gi == j) {
+          ui = h * inv;
+          A[(int64_t)j * rows_per + i] = beta;
+        } else if (gi > j) {
+          ui = -A[(int64_t)j * rows_per + i] * inv;
+          A[(int64_t)j * rows_per + i] = 0.0;
+        }
+        Vs[(int64_t)j * rows_per + i] = ui;
+      }
+    }
+    refl_prev = refl;
+    __syncthreads();
+  }
+  __syncthreads();  // warp 0 wrote the last T column in the final round
+  // write back R (own rows) and V
+  for (int64_t idx = threadIdx.x; idx < (int64_t)nr * w; idx += PL_THREADS) {
+    const int c = (int)(idx / nr), i = (int)(idx % nr);
+    a[(int64_t)c * lda + r0 + i] = A[(int64_t)c * rows_per + i];
+    v[(int64_t)c * ldv + r0 + i] = Vs[(int64_t)c * rows_per + i];
+  }
+  if (rank == 0 && tl)
+    for (int e = threadIdx.x; e < w * w; e += PL_THREADS) tl[(int64_t)(e / w) * ldt + e % w] = Ts[(e / w) * WL + e % w];
+  cluster_sync_all();  // keep DSMEM alive until every CTA finished reading
+}
+
+template <int WL>
+static int launch_leaf(const LeafCall& c, cudaStream_t st, int64_t* launches) {
+  constexpr int PV = LeafLayout<WL>::PV;
+  const int CS = 16;
+  const int rows_per = (int)ceil_div(c.mm, CS);
+  const size_t smem = ((size_t)2 * rows_per * WL + 3 * PV + WL + WL * WL + 8) * sizeof(double);
+  if (smem > 227 * 1024) return set_error(RQ_EINTERNAL, "leaf_qr: %lld rows x %d too large for smem", (long long)c.mm, WL);
+  auto kern = leaf_qr_kernel<WL>;
+  static bool attr = false;
+  if (!attr) {
+    RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS);
+  cfg.blockDim = dim3(PL_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, c.a, c.lda, c.mm, c.w, c.v, c.ldv, c.tl, c.ldt, rows_per));
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+int leaf_width_for(int64_t mm) {
+  // rows_per * WL * 16 B (A + V) must fit ~220 KB with 16 CTAs
+  const int64_t rows_per = ceil_div(mm, 16);
+  if (rows_per * 32 * 16 <= 200 * 1024) return 32;
+  if (rows_per * 16 * 16 <= 200 * 1024) return 16;
+  if (rows_per * 8 * 16 <= 200 * 1024) return 8;
+  if (rows_per * 4 * 16 <= 200 * 1024) return 4;
+  return 0;
+}
+
+int leaf_qr(const LeafCall& c, cudaStream_t st, int64_t* launches) {
+  if (c.w <= 0) return RQ_OK;
+  if (c.w <= 4 && leaf_width_for(c.mm) >= 4) return launch_leaf<4>(c, st, launches);
+  if (c.w <= 8 && leaf_width_for(c.mm) >= 8) return launch_leaf<8>(c, st, launches);
+  if (c.w <= 16 && leaf_width_for(c.mm) >= 16) return launch_leaf<16>(c, st, launches);
+  if (c.w <= 32 && leaf_width_for(c.mm) >= 32) return launch_leaf<32>(c, st, launches);
+  return set_error(RQ_EINTERNAL, "leaf_qr: width %d too wide for %lld rows", c.w, (long long)c.mm);
+}
+
+}  // namespace rq

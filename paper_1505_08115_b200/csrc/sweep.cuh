@@ -1,0 +1,50 @@
+// Cooperative Householder sweep (see sweep.cu).
+#pragma once
+#include <algorithm>
+#include <climits>
+
+#include "common.cuh"
+
+namespace rq {
+
+// Scratch handed to the cooperative kernels: a flat device buffer plus a ring
+// of zero-initialised grid-barrier counters (one fresh counter per launch).
+struct SweepWork {
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  unsigned int* barriers = nullptr;  // ring, zeroed by the owner
+  int nbarriers = 0;
+  int next = 0;
+  bool wrapped = false;
+  unsigned int* next_barrier() {
+    unsigned int* b = barriers + next;
+    if (++next == nbarriers) {
+      next = 0;
+      wrapped = true;
+    }
+    return b;
+  }
+};
+
+struct SweepCall {
+  double* a;
+  int64_t lda;
+  int64_t m;
+  int n;
+  int n_acc = 0;
+  int steps;
+  int pivot;
+  const int* init_pos = nullptr;
+  double* v = nullptr;
+  int64_t ldv = 0;
+  int* col_at_pos = nullptr;
+  double* r_out = nullptr;
+  int64_t ldr = 0;
+  int grid = 0;
+};
+
+size_t sweep_workspace_bytes(int64_t m, int total_cols, int grid);
+int sweep_grid_size(int total_cols);
+int sweep_launch(const SweepCall& c, SweepWork& w, cudaStream_t st, int64_t* launches);
+
+}  // namespace rq

@@ -1,0 +1,176 @@
+"""End-to-end parity of the B200 block_qr against the reference.
+
+Golden fixtures come from the reference itself (tests/golden/make_golden.py);
+the CPU oracle (pinned bitwise to the reference in test_oracle_golden.py)
+covers inputs without fixtures.  Bars (BASELINE.json north_star):
+  * identical composite permutation,
+  * identical signs of diag(R),
+  * ||R - R_ref|| <= 1e-13 ||A|| elementwise-max (normwise), diag(R) relative 1e-10
+    where |R_jj| >= 1e-6 ||A||,
+  * ||AP - QR||_F <= 1e-13 ||A||_F and ||Q^T Q - I||_F <= 1e-13 sqrt(n).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PERM_CASES = ["m1_24x24_b6", "m1_15x11_b4", "m1_26x17_b5", "m1_24x24_b6_p3", "m1_q1_24x24_b6", "m1_9x9_b9",
+              "m1_300x300_b50_p10", "m1_200x130_b32_p2", "m1_257x257_b64_p1"]
+
+
+@pytest.fixture(scope="module")
+def rq():
+    import paper_1505_08115_b200 as m
+
+    return m
+
+
+def _cfg(rq, b, p, q, refl=False, rr=False):
+    return rq.BlockConfig(b, rq.SketchConfig(b, p, q), "reflectors" if refl else "permutation", rr)
+
+
+def check_against(a, f, r_ref, perm_ref, tol=1e-13):
+    scale = max(np.linalg.norm(a), 1.0)
+    if perm_ref is not None:
+        assert np.array_equal(f.perm, perm_ref)
+    assert np.array_equal(np.sign(np.diag(f.r)), np.sign(np.diag(r_ref)))
+    assert np.abs(f.r - r_ref).max() <= tol * scale
+    d, dr = np.abs(np.diag(f.r)), np.abs(np.diag(r_ref))
+    big = dr >= 1e-6 * scale
+    assert np.all(np.abs(d[big] - dr[big]) <= 1e-10 * dr[big])
+    assert not np.tril(f.r, -1).any()  # exact zeros below the diagonal
+
+
+def check_factorization(a, f, tol=1e-13):
+    m, n = a.shape
+    q = f.expand_q()
+    p = f.expand_p()
+    scale = max(np.linalg.norm(a), 1.0)
+    assert np.linalg.norm(a @ p - q @ f.r[:n, :]) <= tol * scale
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= tol * np.sqrt(m)
+
+
+@pytest.mark.parametrize("tag", PERM_CASES)
+def test_block_qr_matches_reference_golden(golden, rq, tag):
+    g = golden("small_factorizations.npz")
+    m, n, b, p, q, refl, rr, sa, ss = (int(x) for x in g[f"{tag}/cfg"])
+    a = g[f"{tag}/a"]
+    rng = rq.RngState(ss)
+    f = rq.block_qr(a, _cfg(rq, b, p, q), rng)
+    assert rng.counter == int(g[f"{tag}/counter"])
+    check_against(a, f, g[f"{tag}/r"], g[f"{tag}/perm"])
+    check_factorization(a, f)
+    assert np.abs(f.expand_q() - g[f"{tag}/q"]).max() <= 1e-12
+    assert np.array_equal(f.expand_p(), g[f"{tag}/p"])
+
+
+def test_full_q(golden, rq):
+    g = golden("small_factorizations.npz")
+    a = g["m1_26x17_b5/a"]
+    f = rq.block_qr(a, _cfg(rq, 5, 0, 0), rq.RngState(61))
+    qf = f.expand_q(26)
+    assert qf.shape == (26, 26)
+    assert np.linalg.norm(qf.T @ qf - np.eye(26)) <= 1e-13 * np.sqrt(26)
+    assert np.abs(qf[:, :17] - f.expand_q()).max() <= 1e-14
+
+
+def test_cfg1_matches_reference(golden, rq):
+    """BASELINE cfg 1: 2000 x 2000 N(0,1) seed 0, b=64, p=10, sketch seed 1."""
+    from oracle import randqr_oracle as O
+
+    g = golden("cfg1_n2000.npz")
+    a = O.gaussian_matrix(2000, 2000, O.RngState(0))
+    rng = rq.RngState(1)
+    f = rq.block_qr(a, _cfg(rq, 64, 10, 0), rng)
+    assert rng.counter == int(g["counter"])
+    assert np.array_equal(f.perm, g["perm"])
+    scale = np.linalg.norm(a)
+    r = f.r
+    assert np.array_equal(np.sign(np.diag(r)), np.sign(g["diag"]))
+    assert np.abs(np.diag(r) - g["diag"]).max() <= 1e-10 * np.abs(g["diag"]).max()
+    assert np.all(np.abs(np.abs(np.diag(r)) - np.abs(g["diag"])) <= 1e-10 * np.abs(g["diag"]))
+    assert np.abs(r[:64, :] - g["r_top"]).max() <= 1e-13 * scale
+    check_factorization(a, f)
+
+
+def test_cfg2_like_spectrum_matches_reference(golden, rq):
+    """Scaled BASELINE cfg 2 (n=600, 10^(-8j/n) decay): perm and diag(R) vs the reference."""
+    g = golden("cfg2_n600.npz")
+    a = g["a"]
+    rng = rq.RngState(1)
+    f = rq.block_qr(a, _cfg(rq, 64, 10, 0), rng)
+    assert rng.counter == int(g["counter"])
+    check_against(a, f, g["r"], g["perm"])
+
+
+def test_deterministic(rq):
+    from oracle import randqr_oracle as O
+
+    a = O.gaussian_matrix(500, 400, O.RngState(3))
+    f1 = rq.block_qr(a, _cfg(rq, 48, 8, 0), rq.RngState(4))
+    f2 = rq.block_qr(a, _cfg(rq, 48, 8, 0), rq.RngState(4))
+    assert np.array_equal(f1.r, f2.r)
+    assert np.array_equal(f1.perm, f2.perm)
+
+
+def test_input_not_mutated(rq):
+    from oracle import randqr_oracle as O
+
+    a = O.gaussian_matrix(40, 30, O.RngState(3))
+    a0 = a.copy()
+    rq.block_qr(a, _cfg(rq, 8, 2, 0), rq.RngState(4))
+    assert np.array_equal(a, a0)
+
+
+def test_oracle_parity_tall_and_ragged(rq):
+    from oracle import randqr_oracle as O
+
+    for (m, n, b, p) in [(700, 300, 64, 8), (333, 333, 100, 7), (129, 65, 16, 1), (64, 64, 64, 0), (90, 90, 41, 5)]:
+        a = O.gaussian_matrix(m, n, O.RngState(m + n))
+        ref = O.block_qr(a, O.BlockConfig(b, O.SketchConfig(b, p, 0)), O.RngState(9))
+        f = rq.block_qr(a, _cfg(rq, b, p, 0), rq.RngState(9))
+        check_against(a, f, ref.r, ref.perm())
+        check_factorization(a, f)
+
+
+def test_inspect_sparsity_progression(rq):
+    # pkg/tests/test_blocked.py:60-73
+    from oracle import randqr_oracle as O
+
+    a = O.gaussian_matrix(12, 12, O.RngState(64))
+    seen = []
+    rq.block_qr(a, rq.BlockConfig(3), rq.RngState(65), inspect=lambda p, w: seen.append((p, w)))
+    assert [p for p, _ in seen] == [1, 2, 3, 4]
+    ref = []
+    O.block_qr(a, O.BlockConfig(3), O.RngState(65), inspect=lambda p, w: ref.append(w))
+    for (panel, w), wr in zip(seen, ref):
+        k = min(3 * panel, 12)
+        assert not w[k:, :k].any()
+        assert np.abs(w - wr).max() <= 1e-12
+
+
+def test_errors_mirror_reference(rq):
+    from oracle import randqr_oracle as O
+
+    a = O.gaussian_matrix(200, 130, O.RngState(5))
+    rng = rq.RngState(6)
+    ref_rng = O.RngState(6)
+    with pytest.raises(ValueError):
+        rq.block_qr(a, _cfg(rq, 32, 8, 0), rng)
+    with pytest.raises(ValueError):
+        O.block_qr(a, O.BlockConfig(32, O.SketchConfig(32, 8, 0)), ref_rng)
+    assert rng.counter == ref_rng.counter
+    with pytest.raises(rq.DimensionError):
+        rq.block_qr(np.ones((3, 5)), rq.BlockConfig(2), rq.RngState(0))
+    with pytest.raises(rq.DimensionError):
+        rq.block_qr(np.ones((5, 5)), rq.BlockConfig(6), rq.RngState(0))
+    with pytest.raises(rq.DimensionError):
+        rq.block_qr(np.ones(5), rq.BlockConfig(1), rq.RngState(0))
+
+
+def test_diagonal_input_entry_set(rq):
+    # pkg/tests/test_blocked.py:118-125
+    d = np.array([3.0, -7.0, 0.5, 11.0, 2.0, -1.0, 4.0, 6.0])
+    f = rq.block_qr(np.diag(d), rq.BlockConfig(3), rq.RngState(1))
+    assert np.allclose(np.sort(np.abs(np.diag(f.r))), np.sort(np.abs(d)), rtol=1e-14)

@@ -1,0 +1,160 @@
+"""Kernel-level parity on the GPU, through the C ABI (librandqr_b200.so).
+
+Checkers: the CPU oracle (oracle/randqr_oracle.py, pinned to the reference in
+tests/test_oracle_golden.py) and the golden fixtures of the reference itself.
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_1505_08115_b200 import Engine
+
+    return Engine()
+
+
+def test_rng_words_bitwise(golden, eng):
+    import paper_1505_08115_b200 as rq
+
+    g = golden("rng_kernels.npz")
+    assert np.array_equal(rq.splitmix_words(1, 0, 1000, engine=eng), g["rng_words/seed1"])
+    assert np.array_equal(rq.splitmix_words(2**63 + 11, 0, 1000, engine=eng), g["rng_words/seed_big"])
+
+
+def test_rng_normals_match_reference(golden, eng):
+    import paper_1505_08115_b200 as rq
+
+    g = golden("rng_kernels.npz")
+    for key, val in g.items():
+        if not key.startswith("rng/"):
+            continue
+        _, seed, counter, shape = key.split("/")
+        rows, cols = map(int, shape.split("x"))
+        rng = rq.RngState(int(seed), int(counter))
+        z = rq.gaussian_matrix(rows, cols, rng, engine=eng)
+        assert rng.counter == int(counter) + rows * cols
+        # integer stream is exact; log/cos differ from numpy's SIMD versions by <= a few ulp
+        np.testing.assert_allclose(z, val, rtol=4e-15, atol=4e-15)
+
+
+def _gemm(eng, a_mmajor, M, N, K, A, B, C, alpha, beta, a_org=(0, 0), b_org=(0, 0)):
+    import torch
+
+    def dev(x):
+        x = np.asarray(x, dtype=np.float64)
+        buf, ld = eng.alloc_matrix(*x.shape)
+        buf[: x.shape[1], : x.shape[0]].copy_(torch.from_numpy(np.ascontiguousarray(x.T)))
+        return buf, ld
+
+    da, lda = dev(A)
+    db, ldb = dev(B)
+    dc, ldc = dev(C)
+    rc = eng.lib.rq_test_gemm(eng.handle, int(a_mmajor), M, N, K, ctypes.c_void_p(da.data_ptr()), lda,
+                              A.shape[0], A.shape[1], a_org[0], a_org[1], ctypes.c_void_p(db.data_ptr()), ldb,
+                              B.shape[0], B.shape[1], b_org[0], b_org[1], ctypes.c_void_p(dc.data_ptr()), ldc,
+                              alpha, beta)
+    from paper_1505_08115_b200.errors import check
+
+    check(rc)
+    return eng.download(dc, C.shape[0], C.shape[1])
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 300, 1000), (16, 8, 4), (130, 37, 45), (272, 2000, 3000), (31, 129, 7),
+                                   (1000, 1000, 256)])
+@pytest.mark.parametrize("mmajor", [False, True])
+def test_dmma_gemm_vs_fp64_reference(eng, M, N, K, mmajor):
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = rng.standard_normal((M, K) if mmajor else (K, M))
+    B = rng.standard_normal((K, N))
+    C = rng.standard_normal((M, N))
+    out = _gemm(eng, mmajor, M, N, K, A, B, C, -0.5, 1.5)
+    opA = A if mmajor else A.T
+    ref = -0.5 * (opA @ B) + 1.5 * C
+    tol = 1e-13 * np.sqrt(K) * (np.abs(opA) @ np.abs(B)).max()
+    assert np.abs(out - ref).max() <= tol
+
+
+def test_dmma_gemm_views_and_ktail(eng):
+    # views at odd origins, K not a multiple of 16, buffers larger than the views
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((90, 70))
+    B = rng.standard_normal((90, 50))
+    C = rng.standard_normal((33, 21))
+    # TN: op(A) = A[3:3+K, 5:5+M]^T, B view rows 3.., cols 7..
+    M, N, K = 33, 21, 29
+    out = _gemm(eng, False, M, N, K, A, B, C, 1.0, 0.0, a_org=(3, 5), b_org=(3, 7))
+    ref = A[3:3 + K, 5:5 + M].T @ B[3:3 + K, 7:7 + N]
+    assert np.abs(out - ref).max() <= 1e-12
+    # NN: op(A) = A[11:11+M, 2:2+K]
+    out = _gemm(eng, True, M, N, K, A, B, C, 1.0, 0.0, a_org=(11, 2), b_org=(3, 7))
+    ref = A[11:11 + M, 2:2 + K] @ B[3:3 + K, 7:7 + N]
+    assert np.abs(out - ref).max() <= 1e-12
+
+
+@pytest.mark.parametrize("tag", ["sq", "tall", "wide", "part"])
+@pytest.mark.parametrize("pivot", [True, False])
+def test_householder_sweep_vs_reference(golden, eng, tag, pivot):
+    import paper_1505_08115_b200 as rq
+    from oracle import randqr_oracle as O
+
+    g = golden("rng_kernels.npz")
+    a0 = g[f"cpqr/{tag}/a"]
+    m, n = a0.shape
+    steps = min(m, n) if tag != "part" else 32
+    if not pivot and m < n:
+        steps = min(steps, m)
+    a = np.array(a0, order="F")
+    v = np.zeros((m, steps), order="F")
+    perm = np.arange(n, dtype=np.int64)
+    rq.householder_sweep(a, v, perm, steps, pivot, engine=eng)
+    ar = np.array(a0, order="F")
+    vr = np.zeros((m, steps), order="F")
+    pr = np.arange(n, dtype=np.int64)
+    O.householder_sweep(ar, vr, pr, steps, pivot)
+    if pivot:
+        assert np.array_equal(perm, g[f"cpqr/{tag}/perm"])
+        assert np.array_equal(perm, pr)
+    scale = np.abs(a0).max() * max(m, n)
+    assert np.abs(a - ar).max() <= 1e-13 * scale
+    assert np.abs(v - vr).max() <= 1e-12
+    assert np.array_equal(np.sign(np.diag(a)), np.sign(np.diag(ar)))
+
+
+def test_householder_sweep_ties_lowest_index(golden, eng):
+    import paper_1505_08115_b200 as rq
+
+    g = golden("rng_kernels.npz")
+    a = np.array(g["cpqr/ties/a"], order="F")
+    m, n = a.shape
+    v = np.zeros((m, min(m, n)), order="F")
+    perm = np.arange(n, dtype=np.int64)
+    rq.householder_sweep(a, v, perm, min(m, n), True, engine=eng)
+    # the genuine tie (columns 1 and 3, equal norms) goes to the lowest index
+    assert perm[0] == g["cpqr/ties/perm"][0] == 1
+    # afterwards every trailing column is zero up to rounding: any order is a valid CPQR
+    assert np.abs(np.diag(a)[1:]).max() <= 1e-15
+
+
+def test_hand_examples(eng):
+    # pkg/tests/test_householder.py:114-131 and :163-173
+    import paper_1505_08115_b200 as rq
+
+    a = np.array([[3.0, 0.0], [4.0, 5.0]], order="F")
+    v = np.zeros((2, 2), order="F")
+    rq.householder_sweep(a, v, np.arange(2), 2, False, engine=eng)
+    assert np.abs(a - [[-5.0, -4.0], [0.0, 3.0]]).max() <= 1e-13
+    a = np.array([[0.0, 2.0], [0.0, 1.0]], order="F")
+    perm = np.arange(2, dtype=np.int64)
+    rq.householder_sweep(a, np.zeros((2, 2), order="F"), perm, 2, True, engine=eng)
+    assert perm.tolist() == [1, 0]
+    assert abs(a[0, 0]) == pytest.approx(np.sqrt(5.0), abs=1e-14)
+    a = np.eye(4, order="F")
+    perm = np.arange(4, dtype=np.int64)
+    rq.householder_sweep(a, np.zeros((4, 4), order="F"), perm, 4, True, engine=eng)
+    assert perm.tolist() == [0, 1, 2, 3]
