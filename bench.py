@@ -1,0 +1,318 @@
+"""Benchmark: HQRRP (block_qr, BASELINE.json cfg 3) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full block_qr factorization of an n x n i.i.d. N(0,1) fp64
+matrix (cfg 3: n=10000, b=256, p=16, q=0), fresh sketches from RngState(1)
+(reference semantics), starting from a pristine copy of A already resident
+in HBM (the copy is part of the step, as blocked.py:161 copies its input).
+Metric: fp64 TFLOP/s on the (4/3) n^3 count.
+
+* value: device time (CUDA events on the library stream), max over ranks.
+* e2e: the public C ABI entry rq_factorize_host from pinned host memory,
+  H2D of A and D2H of R + perm inside the timed region.
+* roofline: the trailing-update DMMA GEMMs (the dominant kernel class),
+  algorithmic flops 4 m' b n2 + 3 b^2 n2 per panel over
+  their CUDA-event time in the timed steps, against the measured FP64 DMMA
+  peak (profiles/probe_r01.jsonl; MEASURED_PEAKS.json has no FP64 entry).
+* cpu_baseline / --impl reference: the CPU oracle (oracle/, a restatement of
+  the reference's numba/numpy path; the reference is pure Python, so there is
+  nothing to compile) on this host's cores, over a bounded sample: the first
+  `--ref-panels` panels of the same factorization, credited with their share
+  of the 4/3 n^3 count (sum of 4 m' b n2 over the sampled panels).
+N > 1: independent replicas (one factorization per rank, weak scaling); the
+1-D block-cyclic NCCL version is not built yet.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 36.96  # measured DMMA m16n8k4 peak on this pool's B200 (profiles/probe_r01.jsonl)
+METRIC = "fp64 TFLOP/s (4/3·n³ count) for HQRRP at n=10k–40k; % of FP64 TC peak"
+
+
+def nominal_panel_flops(m, n, b, panels=None):
+    """4 m' b n2 per non-final panel: sums to ~(4/3) n^3 for square A."""
+    tot, s, k = 0.0, 0, 0
+    while n - s > b and (panels is None or k < panels):
+        mp, n2 = m - s, n - s - b
+        tot += 4.0 * mp * b * n2
+        s += b
+        k += 1
+    return tot
+
+
+def trailing_algorithmic_flops(m, n, b):
+    tot, s = 0.0, 0
+    while n - s > b:
+        mp, n2 = m - s, n - s - b
+        tot += 4.0 * mp * b * n2 + 3.0 * b * b * n2
+        s += b
+    return tot
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, idx):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{idx}.csv")
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(idx),
+                 "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_oracle_sample(n, b, p, panels, threads=None):
+    """Time the CPU oracle on the first `panels` panels of the cfg-3 factorization."""
+    from oracle import randqr_oracle as O
+
+    a = O.gaussian_matrix(n, n, O.RngState(0))
+    cfg = O.BlockConfig(b, O.SketchConfig(b, p, 0))
+    t0 = time.perf_counter()
+    O.block_qr(a, cfg, O.RngState(1), max_panels=panels)
+    dt = time.perf_counter() - t0
+    return nominal_panel_flops(n, n, b, panels) / dt / 1e12, dt
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (oracle restatement) on host cores."""
+    if rank != 0:
+        return
+    from oracle import randqr_oracle as O
+
+    n, b, p = args.n, args.b, args.p
+    a = O.gaussian_matrix(n, n, O.RngState(0))
+    cfg = O.BlockConfig(b, O.SketchConfig(b, p, 0))
+    for _ in range(args.warmup):
+        O.block_qr(a, cfg, O.RngState(1), max_panels=args.ref_panels)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.block_qr(a, cfg, O.RngState(1), max_panels=args.ref_panels)
+    dt = time.perf_counter() - t0
+    flops = nominal_panel_flops(n, n, b, args.ref_panels) * args.steps
+    val = flops / dt / 1e12
+    cores = host_cores()
+    line = {
+        "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"cfg3 HQRRP fp64 n={n} b={b} p={p} q=0, fresh sketch; "
+                               f"bounded sample: first {args.ref_panels} panel(s) per step",
+                   "n": n, "b": b, "p": p},
+        "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"first {args.ref_panels} panel(s) of n={n}, credited 4 m' b n2 per panel"},
+        "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=10000)
+    ap.add_argument("--b", type=int, default=256)
+    ap.add_argument("--p", type=int, default=16)
+    ap.add_argument("--ref-panels", type=int, default=1)
+    ap.add_argument("--cpu-panels", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1505_08115_b200 as rq
+    from paper_1505_08115_b200 import _lib
+    from paper_1505_08115_b200.errors import check
+
+    n, b, p = args.n, args.b, args.p
+    m = n
+    stream = torch.cuda.Stream()
+    eng = rq.Engine(local, stream=stream)
+    lib = eng.lib
+    # A = gaussian_matrix(n, n, RngState(0)): same counter-based stream as the reference
+    with torch.cuda.stream(stream):
+        a0, ld = rq.gaussian_matrix_device(m, n, rq.RngState(0), engine=eng)
+        work, _ = eng.alloc_matrix(m, n)
+        perm = torch.empty(n, dtype=torch.int64, device=eng.device)
+    cfg = _lib.rq_config(b, p, 0, -1, 0, 0, _lib.RQ_SKETCH_FRESH, 0)
+
+    def step():
+        with torch.cuda.stream(stream):
+            work.copy_(a0)
+        ctr = ctypes.c_uint64(0)
+        check(lib.rq_factorize(eng.handle, ctypes.byref(cfg), m, n, ctypes.c_void_p(work.data_ptr()), ld,
+                               ctypes.c_uint64(1), ctypes.byref(ctr), ctypes.c_void_p(perm.data_ptr())))
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    time.sleep(0.3)
+    check(lib.rq_set_profiling(eng.handle, 1))
+    launches0 = eng.launches
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = eng.launches - launches0
+    clk = clocks.stop()
+    cats = {}
+    for c, name in enumerate(["trailing_gemm", "other_gemm", "cpqr_sweep", "panel_leaf", "other"]):
+        t, f, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        check(lib.rq_profile_read(eng.handle, c, ctypes.byref(t), ctypes.byref(f), ctypes.byref(k)))
+        cats[name] = {"ms": t.value / args.steps, "launches": k.value // args.steps}
+    check(lib.rq_set_profiling(eng.handle, 0))
+    ms_max = ms
+    if dist is not None:
+        tt = torch.tensor([ms], device=eng.device, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_max = float(tt.item())
+    flops_step = 4.0 / 3.0 * n ** 3
+    value = world * args.steps * flops_step / (ms_max * 1e-3) / 1e12
+
+    # dominant kernel roofline: the trailing-update DMMA GEMMs
+    t_trail = cats["trailing_gemm"]["ms"]
+    achieved = trailing_algorithmic_flops(m, n, b) / (t_trail * 1e-3) / 1e12 if t_trail > 0 else None
+
+    # e2e through the public C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        ha = torch.empty((n, ld), dtype=torch.float64, pin_memory=True)
+        ha.copy_(a0.cpu())
+        hr = torch.empty((n, ld), dtype=torch.float64, pin_memory=True)
+        hp = torch.empty(n, dtype=torch.int64, pin_memory=True)
+
+        def e2e_step():
+            ctr = ctypes.c_uint64(0)
+            check(lib.rq_factorize_host(eng.handle, ctypes.byref(cfg), m, n, ctypes.c_void_p(ha.data_ptr()), ld,
+                                        ctypes.c_uint64(1), ctypes.byref(ctr), ctypes.c_void_p(hr.data_ptr()), ld,
+                                        ctypes.c_void_p(hp.data_ptr())))
+
+        e2e_step()
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        k_e2e = max(1, min(args.steps, 3))
+        for _ in range(k_e2e):
+            e2e_step()
+        dt = time.perf_counter() - t0
+        if dist is not None:
+            tt = torch.tensor([dt], device=eng.device, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e = {"value": world * k_e2e * flops_step / dt / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": m * n * 8, "d2h_bytes_per_step": m * n * 8 + n * 8}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        val, dt = cpu_oracle_sample(n, b, p, args.cpu_panels)
+        cpu = {"value": val, "unit": "TFLOP/s", "cores": host_cores(), "kind": "port",
+               "sample": f"oracle block_qr, first {args.cpu_panels} panels of n={n} ({dt:.1f} s), "
+                         f"credited 4 m' b n2 per panel"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg3 HQRRP fp64 n={n} b={b} p={p} q=0, fresh sketch (reference semantics)",
+                       "n": n, "b": b, "p": p, "q": 0, "sketch": "fresh",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs (800 MB) larger than L2 (126 MB)"},
+            "fraction_of_fp64_peak": value / FP64_PEAK_TFLOPS,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+                         "kernel": "gemm_f64_kernel (trailing update: V^T A2, T^T W, A2 -= V W2, Q2^T top)",
+                         "peak_source": "measured DMMA peak, profiles/probe_r01.jsonl"},
+            "breakdown_ms_per_step": cats,
+            "clocks": clk,
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -120,6 +120,13 @@ int rq_test_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K,
 /* Number of kernel launches this context has issued (instrumentation). */
 int64_t rq_launch_count(rq_ctx* ctx);
 
+/* Instrumentation: with profiling on, CUDA events bracket every launch of a
+ * kernel class (0 trailing-update GEMMs, 1 other GEMMs, 2 CPQR sweeps,
+ * 3 panel leaves, 4 other); rq_profile_read sums their device time (ms) and
+ * GEMM flops since the last rq_set_profiling call. */
+int rq_set_profiling(rq_ctx* ctx, int32_t on);
+int rq_profile_read(rq_ctx* ctx, int32_t category, double* ms, double* flops, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,9 @@ _SIGS = {
     "rq_test_gemm": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64,
                                     _i64, _i64, _i64, _i64, _vp, _i64, ctypes.c_double, ctypes.c_double]),
     "rq_launch_count": (_i64, [_vp]),
+    "rq_set_profiling": (ctypes.c_int, [_vp, _i32]),
+    "rq_profile_read": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(_i64)]),
 }
 
 _lib = None

@@ -238,5 +238,32 @@ int rq_test_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K,
 
 int64_t rq_launch_count(rq_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
+int rq_set_profiling(rq_ctx* ctx, int32_t on) {
+  CTX_CHECK(ctx);
+  ctx->c.prof = on != 0;
+  ctx->c.prof_recs.clear();
+  ctx->c.ev_next = 0;
+  return RQ_OK;
+}
+
+int rq_profile_read(rq_ctx* ctx, int32_t category, double* ms, double* flops, int64_t* count) {
+  CTX_CHECK(ctx);
+  RQ_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
+  double t = 0.0, f = 0.0;
+  int64_t k = 0;
+  for (const auto& r : ctx->c.prof_recs) {
+    if (r.cat != category) continue;
+    float e = 0.f;
+    RQ_CUDA_TRY(cudaEventElapsedTime(&e, r.e0, r.e1));
+    t += e;
+    f += r.flops;
+    k++;
+  }
+  if (ms) *ms = t;
+  if (flops) *flops = f;
+  if (count) *count = k;
+  return RQ_OK;
+}
+
 #pragma GCC visibility pop
 }  // extern "C"

@@ -136,8 +136,41 @@ static GemmOperand op(const double* base, int64_t rows, int64_t cols, int64_t ld
   return o;
 }
 
+cudaEvent_t Ctx::prof_event() {
+  if (ev_next == ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ev_pool.push_back(e);
+  }
+  return ev_pool[ev_next++];
+}
+void Ctx::prof_begin(cudaEvent_t* e0) {
+  *e0 = nullptr;
+  if (!prof) return;
+  *e0 = prof_event();
+  cudaEventRecord(*e0, stream);
+}
+void Ctx::prof_end(cudaEvent_t e0, double flops) {
+  if (!prof || !e0) return;
+  cudaEvent_t e1 = prof_event();
+  cudaEventRecord(e1, stream);
+  prof_recs.push_back(ProfRec{cat, e0, e1, flops});
+}
+
 int Ctx::gemm(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmajor, const GemmOperand& B,
               double* C, int64_t ldc, double alpha, double beta) {
+  cudaEvent_t e0;
+  const int saved = cat;
+  if (cat != PROF_TRAIL) cat = PROF_GEMM_OTHER;
+  prof_begin(&e0);
+  int rc = gemm_raw(M, N, K, A, a_mmajor, B, C, ldc, alpha, beta);
+  prof_end(e0, 2.0 * (double)M * (double)N * (double)K);
+  cat = saved;
+  return rc;
+}
+
+int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmajor, const GemmOperand& B,
+                  double* C, int64_t ldc, double alpha, double beta) {
   GemmProblem p;
   p.M = M;
   p.N = N;
@@ -163,6 +196,17 @@ int Ctx::gemm(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmaj
 }
 
 int Ctx::sweep(SweepCall c) {
+  cudaEvent_t e0;
+  const int saved = cat;
+  cat = PROF_SWEEP;
+  prof_begin(&e0);
+  int rc = sweep_raw(c);
+  prof_end(e0, 0.0);
+  cat = saved;
+  return rc;
+}
+
+int Ctx::sweep_raw(SweepCall c) {
   SweepWork w;
   w.scratch = sweep_ws;
   w.scratch_bytes = sweep_ws_bytes;
@@ -199,7 +243,16 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
     lc.ldv = ldv;
     lc.tl = tleaf;
     lc.ldt = 32;
-    RQ_TRY(leaf_qr(lc, stream, &launches));
+    {
+      cudaEvent_t e0;
+      const int saved = cat;
+      cat = PROF_LEAF;
+      prof_begin(&e0);
+      const int rc = leaf_qr(lc, stream, &launches);
+      prof_end(e0, 0.0);
+      cat = saved;
+      RQ_TRY(rc);
+    }
     const int64_t nrest = b - k0 - w;
     if (nrest <= 0) break;
     // W = V_l^T A_rest ; W2 = T_l^T W ; A_rest -= V_l W2
@@ -408,6 +461,12 @@ int Ctx::trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s
                          Layout& L) {
   const int64_t ldw = even(b);
   const GemmOperand Vop = op(V, mp + vpad, b, ldv, vpad);
+  struct CatGuard {
+    int& c;
+    int saved;
+    CatGuard(int& c_, int v) : c(c_), saved(c_) { c = v; }
+    ~CatGuard() { c = saved; }
+  } guard(cat, PROF_TRAIL);
   // W = V^T A2   (b x n2, K = m')
   RQ_TRY(gemm(b, n2, mp, Vop, false, op(A, m, n, lda, s, s + b), L.w1, ldw, 1.0, 0.0));
   // W2 = T^T W

@@ -45,8 +45,26 @@ struct PanelFactors {
   int64_t ldq2;
 };
 
+// Kernel classes timed with CUDA events when profiling is on (rq_set_profiling).
+enum ProfCat { PROF_TRAIL = 0, PROF_GEMM_OTHER = 1, PROF_SWEEP = 2, PROF_LEAF = 3, PROF_OTHER = 4, PROF_NCAT = 5 };
+
+struct ProfRec {
+  int cat;
+  cudaEvent_t e0, e1;
+  double flops;
+};
+
 struct Ctx {
   int device = 0;
+  // profiling
+  bool prof = false;
+  int cat = PROF_OTHER;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  cudaEvent_t prof_event();
+  void prof_begin(cudaEvent_t* e0);
+  void prof_end(cudaEvent_t e0, double flops);
   cudaStream_t stream = nullptr;
   rq_panel_cb inspect_cb = nullptr;
   void* inspect_user = nullptr;
@@ -75,7 +93,10 @@ struct Ctx {
   ~Ctx();
   int gemm(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmajor, const GemmOperand& B, double* C,
            int64_t ldc, double alpha, double beta);
+  int gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmajor, const GemmOperand& B, double* C,
+               int64_t ldc, double alpha, double beta);
   int sweep(SweepCall c);
+  int sweep_raw(SweepCall c);
   int panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, double* V, int64_t ldv,
                int vpad, double* tleaf, double* w1, double* w2);
   int tfactor(const double* V, int64_t rows, int k, int64_t ldv, int vpad, double* T, int64_t ldt, double* gram);
