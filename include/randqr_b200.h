@@ -117,6 +117,13 @@ int rq_test_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K,
                  int64_t b_rows, int64_t b_cols, int64_t b_r0, int64_t b_c0, double* dC, int64_t ldc, double alpha,
                  double beta);
 
+/* Test hooks for the serial kernels (microbenchmarks and parity tests):
+ * sketch CPQR pivot selection on dY (m x n, destroyed) -> dChosen[steps];
+ * panel leaf QR of dA (mm x w, w <= 32) -> R in place, dV (mm x w), dT (w x w). */
+int rq_test_sketch_cpqr(rq_ctx* ctx, double* dY, int64_t ld, int32_t m, int32_t n, int32_t steps, int32_t* dChosen);
+int rq_test_leaf_qr(rq_ctx* ctx, double* dA, int64_t lda, int64_t mm, int32_t w, double* dV, int64_t ldv,
+                    double* dT, int64_t ldt);
+
 /* Number of kernel launches this context has issued (instrumentation). */
 int64_t rq_launch_count(rq_ctx* ctx);
 

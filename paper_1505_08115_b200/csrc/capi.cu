@@ -3,6 +3,7 @@
 
 #include "driver.cuh"
 #include "misc.cuh"
+#include "panel.cuh"
 
 namespace rq {
 const char* last_error();
@@ -234,6 +235,33 @@ int rq_test_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K,
   rq::GemmOperand A{dA, a_rows, a_cols, lda, a_r0, a_c0};
   rq::GemmOperand B{dB, b_rows, b_cols, ldb, b_r0, b_c0};
   return c.gemm(M, N, K, A, a_mmajor != 0, B, dC, ldc, alpha, beta);
+}
+
+int rq_test_sketch_cpqr(rq_ctx* ctx, double* dY, int64_t ld, int32_t m, int32_t n, int32_t steps, int32_t* dChosen) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  Ctx& c = ctx->c;
+  const size_t ws = rq::sweep_workspace_bytes(m, n, rq::kSMs) + 4096;
+  RQ_TRY(c.qarena.reserve(ws));
+  c.sweep_ws = c.qarena.base;
+  c.sweep_ws_bytes = ws;
+  return c.sketch_select(dY, ld, m, n, steps, nullptr, dChosen);
+}
+
+int rq_test_leaf_qr(rq_ctx* ctx, double* dA, int64_t lda, int64_t mm, int32_t w, double* dV, int64_t ldv,
+                    double* dT, int64_t ldt) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  rq::LeafCall lc;
+  lc.a = dA;
+  lc.lda = lda;
+  lc.mm = mm;
+  lc.w = w;
+  lc.v = dV;
+  lc.ldv = ldv;
+  lc.tl = dT;
+  lc.ldt = ldt;
+  return rq::leaf_qr(lc, ctx->c.stream, &ctx->c.launches);
 }
 
 int64_t rq_launch_count(rq_ctx* ctx) { return ctx ? ctx->c.launches : 0; }

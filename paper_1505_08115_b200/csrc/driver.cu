@@ -90,7 +90,8 @@ static Layout plan_layout(void* base, int64_t m, int64_t n, int b, int p, int po
   L.gram = c.take<double>((size_t)ldb * b);
   L.tleaf = c.take<double>(32 * 32);
   L.ybuf = power > 0 ? c.take<double>((size_t)even(n) * wdt) : nullptr;
-  L.kwork_bytes = std::max<size_t>((size_t)kSMs * b * b * 8, (size_t)4 * b * n * 8);
+  // split-K slabs: up to 16 splits of the (b+p+1) x n sketch, or 148 of the b x b Gram
+  L.kwork_bytes = std::max<size_t>((size_t)kSMs * (b + 1) * b * 8, (size_t)16 * (wdt + 1) * n * 8);
   L.kwork = c.take<double>(L.kwork_bytes / 8);
   L.lds_small = ldb;
   L.small = c.take<double>((size_t)ldb * 2 * b);
@@ -182,25 +183,49 @@ int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_
   p.ldc = ldc;
   p.alpha = alpha;
   p.beta = beta;
-  p.splitk = 1;
+  p.splitk = 0;  // automatic
   p.work = kwork;
-  // split-K when the output tiles cannot fill the machine and K is long
-  const int64_t tiles = ceil_div(M, 128) * ceil_div(N, 128);
-  const int64_t kch = ceil_div(K, 16);
-  if (kwork && tiles * 2 <= kSMs && kch >= 32) {
-    int64_t sk = std::min<int64_t>(kSMs / tiles, kch / 16);
-    while (sk > 1 && gemm_splitk_workspace(M + 1, N, (int)sk) > kwork_bytes) sk--;
-    if (sk > 1) p.splitk = (int)sk;
-  }
+  p.work_bytes = kwork ? kwork_bytes : 0;
   return gemm_f64(p, stream, &launches);
 }
 
 int Ctx::sweep(SweepCall c) {
   cudaEvent_t e0;
   const int saved = cat;
-  cat = PROF_SWEEP;
+  cat = (c.n_acc > 0 || c.r_out) ? PROF_SMALL : PROF_SWEEP;
   prof_begin(&e0);
   int rc = sweep_raw(c);
+  prof_end(e0, 0.0);
+  cat = saved;
+  return rc;
+}
+
+int Ctx::sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen) {
+  if (m > 1024) {
+    SweepCall sc;
+    sc.a = const_cast<double*>(yt);
+    sc.lda = ldy;
+    sc.m = m;
+    sc.n = n;
+    sc.steps = steps;
+    sc.pivot = 1;
+    sc.init_pos = init_pos;
+    sc.col_at_pos = chosen;
+    return sweep(sc);
+  }
+  cudaEvent_t e0;
+  const int saved = cat;
+  cat = PROF_SWEEP;
+  prof_begin(&e0);
+  SweepWork w;
+  w.scratch = sweep_ws;
+  w.scratch_bytes = sweep_ws_bytes;
+  if (!sk_counter) {
+    RQ_CUDA_TRY(cudaMalloc(&sk_counter, 64));
+    RQ_CUDA_TRY(cudaMemsetAsync(sk_counter, 0, 64, stream));
+  }
+  const int rc =
+      sketch_cpqr_launch(yt, ldy, m, n, steps, init_pos, chosen, w, sk_counter, sk_counter_base, stream, &launches);
   prof_end(e0, 0.0);
   cat = saved;
   return rc;
@@ -263,6 +288,19 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
     RQ_TRY(gemm(mm, nrest, w, op(V, mp + vpad, b, ldv, vpad + k0, k0), true, op(w2, w, nrest, ldw),
                 A + (s + k0) + (s + k0 + w) * lda, lda, -1.0, 1.0));
   }
+  return RQ_OK;
+}
+
+// Q2 = H'_0 ... H'_{k-1} = I - V2 T2 V2^T (k x k), dense, from the b x b CPQR reflectors.
+int Ctx::small_q(const double* V2, int64_t ldv2, int k, double* Q2, int64_t ldq, Layout& L) {
+  double* T2s = L.ttop;  // k x k scratch (free until the trailing update)
+  const int64_t ldk = even(k);
+  RQ_TRY(tfactor(V2, k, k, ldv2, 0, T2s, ldk, L.gram));
+  RQ_TRY(fill_eye(Q2, ldq, k, k, 0, stream, &launches));
+  // W = V2^T I ; W2 = T2 W ; Q2 -= V2 W2
+  RQ_TRY(gemm(k, k, k, op(V2, k, k, ldv2), false, op(Q2, k, k, ldq), L.w1, ldk, 1.0, 0.0));
+  RQ_TRY(gemm(k, k, k, op(T2s, k, k, ldk), true, op(L.w1, k, k, ldk), L.w2, ldk, 1.0, 0.0));
+  RQ_TRY(gemm(k, k, k, op(V2, k, k, ldv2), true, op(L.w2, k, k, ldk), Q2, ldq, -1.0, 1.0));
   return RQ_OK;
 }
 
@@ -361,16 +399,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     *counter += (uint64_t)mp * (uint64_t)wdt;
     RQ_TRY(sketch(cfg, A, lda, m, n, s, mp, np, L));
     // ---------------- 3: b-step CPQR of Y^T ----------------
-    SweepCall sc;
-    sc.a = L.yt;
-    sc.lda = L.ldy;
-    sc.m = wdt;
-    sc.n = (int)np;
-    sc.steps = b;
-    sc.pivot = 1;
-    sc.init_pos = rank;
-    sc.col_at_pos = L.cap;
-    RQ_TRY(sweep(sc));
+    RQ_TRY(sketch_select(L.yt, L.ldy, wdt, (int)np, b, rank, L.cap));
     // ---------------- 4: move the chosen columns into the panel ----------------
     PlanCall pc{L.cap, b, lorder, (int)np, L.flag, L.newloc, L.src, L.dst, L.nmoves, lorder_n, rank_n};
     RQ_TRY(plan_moves(pc, stream, &launches));
@@ -381,28 +410,31 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     const int vpad = (int)(s & 1);
     double* V = fc.take<double>((size_t)ldv * b);
     double* T = fc.take<double>((size_t)ldt * b);
-    double* Q2t = fc.take<double>((size_t)ldt * b);
+    double* Q2 = fc.take<double>((size_t)ldt * b);
     // V is lower trapezoidal: the leaves write rows >= their diagonal only
     RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * b * sizeof(double), stream));
     launches++;
     RQ_TRY(panel_qr(A, lda, m, n, s, mp, b, V, ldv, vpad, tleaf, L.w1, L.w2));
-    // ---------------- 6: b x b CPQR of R' with Q2^T accumulated ----------------
+    // ---------------- 6: b x b CPQR of R' (reflectors V2), then Q2 = I - V2 T2 V2^T ----------------
     double* S = L.small;
+    double* V2 = L.small + (int64_t)b * L.lds_small;
     RQ_TRY(copy2d(A + s + s * lda, lda, S, L.lds_small, b, b, 1, stream, &launches));
-    RQ_TRY(fill_eye(S + (int64_t)b * L.lds_small, L.lds_small, b, b, 0, stream, &launches));
+    RQ_CUDA_TRY(cudaMemsetAsync(V2, 0, (size_t)L.lds_small * b * sizeof(double), stream));
+    launches++;
     SweepCall ss;
     ss.a = S;
     ss.lda = L.lds_small;
     ss.m = b;
     ss.n = b;
-    ss.n_acc = b;
     ss.steps = b;
     ss.pivot = 1;
+    ss.v = V2;
+    ss.ldv = L.lds_small;
     ss.col_at_pos = L.cap;
     ss.r_out = L.rfin;
     ss.ldr = L.lds_small;
     RQ_TRY(sweep(ss));
-    RQ_TRY(copy2d(S + (int64_t)b * L.lds_small, L.lds_small, Q2t, ldt, b, b, 0, stream, &launches));
+    RQ_TRY(small_q(V2, L.lds_small, b, Q2, ldt, L));
     // ---------------- 7: R and the rows above follow P-hat ----------------
     RQ_TRY(copy2d(L.rfin, L.lds_small, A + s + s * lda, lda, b, b, 0, stream, &launches));
     MoveCall mv2{A, lda, s, 0, s, L.cap, L.iota_b, nullptr, b, L.stage, even(m), L.orig, L.ostage};
@@ -411,8 +443,8 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
     // ---------------- 9: trailing update ----------------
     const int64_t n2 = np - b;
-    if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2t, L));
-    factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2t, ldt});
+    if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L));
+    factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2, ldt});
     std::swap(lorder, lorder_n);
     std::swap(rank, rank_n);
     if (inspect_cb) {
@@ -457,7 +489,7 @@ int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t
 }
 
 int Ctx::trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, int64_t n2,
-                         const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2t,
+                         const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2,
                          Layout& L) {
   const int64_t ldw = even(b);
   const GemmOperand Vop = op(V, mp + vpad, b, ldv, vpad);
@@ -473,10 +505,10 @@ int Ctx::trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s
   RQ_TRY(gemm(b, n2, b, op(T, b, b, ldt), false, op(L.w1, b, n2, ldw), L.w2, ldw, 1.0, 0.0));
   // A2 -= V W2
   RQ_TRY(gemm(mp, n2, b, Vop, true, op(L.w2, b, n2, ldw), A + s + (s + b) * lda, lda, -1.0, 1.0));
-  if (Q2t) {
-    // top b rows <- Q2^T top
+  if (Q2) {
+    // top b rows <- Q2^T top   (TN with A = Q2)
     RQ_TRY(copy2d(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
-    RQ_TRY(gemm(b, n2, b, op(Q2t, b, b, ldt), true, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
+    RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldt), false, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
   }
   return RQ_OK;
 }
@@ -507,11 +539,11 @@ int Ctx::form_q(int64_t cols, double* Q, int64_t ldq) {
     const int64_t s = f.s, mp = m - s, nc = cols - s;
     if (nc <= 0) continue;
     double* X = Q + s + s * ldq;
-    if (f.q2t) {
-      // X[0:k] <- Q2 X[0:k]   (Q2 = (Q2^T)^T: TN with A = Q2^T)
+    if (f.q2) {
+      // X[0:k] <- Q2 X[0:k]   (NN with A = Q2)
       rc = copy2d(X, ldq, tt, ldw, f.k, nc, 0, stream, &launches);
       if (rc == RQ_OK)
-        rc = gemm(f.k, nc, f.k, op(f.q2t, f.k, f.k, f.ldq2), false, op(tt, f.k, nc, ldw), X, ldq, 1.0, 0.0);
+        rc = gemm(f.k, nc, f.k, op(f.q2, f.k, f.k, f.ldq2), true, op(tt, f.k, nc, ldw), X, ldq, 1.0, 0.0);
     }
     if (rc != RQ_OK) break;
     // X <- X - V T (V^T X)
@@ -547,6 +579,8 @@ int Ctx::snapshot(double* hW, int64_t ldh) {
 }
 
 Ctx::~Ctx() {
+  if (sk_counter) cudaFree(sk_counter);
+  for (auto e : ev_pool) cudaEventDestroy(e);
   arena.release();
   qarena.release();
   if (barriers) cudaFree(barriers);

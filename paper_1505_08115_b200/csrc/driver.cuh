@@ -41,12 +41,20 @@ struct PanelFactors {
   int vpad;   // 1 when s is odd: keeps TMA coordinates 16-byte aligned
   double* t;
   int64_t ldt;
-  double* q2t;  // k x k (null for the final block)
+  double* q2;   // k x k Q2 of the b x b CPQR (null for the final block)
   int64_t ldq2;
 };
 
 // Kernel classes timed with CUDA events when profiling is on (rq_set_profiling).
-enum ProfCat { PROF_TRAIL = 0, PROF_GEMM_OTHER = 1, PROF_SWEEP = 2, PROF_LEAF = 3, PROF_OTHER = 4, PROF_NCAT = 5 };
+enum ProfCat {
+  PROF_TRAIL = 0,       // trailing-update GEMMs
+  PROF_GEMM_OTHER = 1,  // sketch, Gram, intra-panel GEMMs
+  PROF_SWEEP = 2,       // sketch CPQR (pivot selection)
+  PROF_LEAF = 3,        // panel leaf QR
+  PROF_OTHER = 4,
+  PROF_SMALL = 5,       // b x b CPQR of R' and the final block
+  PROF_NCAT = 6
+};
 
 struct ProfRec {
   int cat;
@@ -97,16 +105,20 @@ struct Ctx {
                int64_t ldc, double alpha, double beta);
   int sweep(SweepCall c);
   int sweep_raw(SweepCall c);
+  unsigned long long* sk_counter = nullptr;  // device: monotone arrival counter of the sketch CPQR
+  unsigned long long sk_counter_base = 0;    // host mirror of its value
+  int sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen);
   int panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, double* V, int64_t ldv,
                int vpad, double* tleaf, double* w1, double* w2);
   int tfactor(const double* V, int64_t rows, int k, int64_t ldv, int vpad, double* T, int64_t ldt, double* gram);
   int sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int64_t np,
              Layout& L);
   int trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, int64_t n2,
-                      const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2t,
+                      const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2,
                       Layout& L);
   int factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, int64_t lda, uint64_t seed,
                      uint64_t* counter, int64_t* dperm);
+  int small_q(const double* V2, int64_t ldv2, int k, double* Q2, int64_t ldq, Layout& L);
   int form_q(int64_t cols, double* Q, int64_t ldq);
   int form_p(double* P, int64_t ldp);
   int snapshot(double* hW, int64_t ldh);

@@ -455,6 +455,39 @@ size_t gemm_splitk_workspace(int64_t M, int64_t N, int splitk) {
   return splitk > 1 ? (size_t)splitk * M * N * sizeof(double) : 0;
 }
 
+// Split-K factor that best fills the machine (wave efficiency), deterministic
+// reduction afterwards; only when K is long enough to amortise it.
+static int choose_splitk(const GemmProblem& p, int BM, int BN) {
+  if (p.splitk > 0) return p.splitk;
+  if (!p.work) return 1;
+  const int sms = num_sms();
+  const int64_t tiles = ceil_div(p.M + 1, BM) * ceil_div(p.N, BN);
+  const int64_t kch = ceil_div(p.K + 1, 16);
+  auto eff = [&](int64_t units) {
+    const int64_t waves = ceil_div(units, sms);
+    return (double)units / (double)(waves * sms);
+  };
+  int best = 1;
+  double best_eff = eff(tiles);
+  if (best_eff >= 0.9 || tiles >= 8 * sms) return 1;
+  for (int s = 2; s <= 32; s++) {
+    if (kch / s < 8) break;
+    if (gemm_splitk_workspace(p.M + 1, p.N, s) > p.work_bytes) break;
+    const double e = eff(tiles * s) * (1.0 - 0.01 * s);  // mild penalty for the reduction traffic
+    if (e > best_eff + 0.03) {
+      best = s;
+      best_eff = e;
+    }
+  }
+  return best;
+}
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
+static int launch_auto(GemmProblem p, cudaStream_t stream, int64_t* launches) {
+  p.splitk = choose_splitk(p, BM, BN);
+  return launch_cfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(p, stream, launches);
+}
+
 int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches) {
   if (p.M <= 0 || p.N <= 0) return RQ_OK;
   if (p.K <= 0) {
@@ -464,15 +497,18 @@ int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches) {
   }
   RQ_TRY(get_encoder());
   if (p.splitk > 1 && p.work == nullptr) return set_error(RQ_EINTERNAL, "gemm_f64: split-K without workspace");
-  // Tile selection: skinny outputs use narrower tiles so the grid fills 148 SMs.
+  // Tile selection: skinny outputs use narrower tiles so the grid fills 148 SMs;
+  // M in (128, 144] or (256, 288] (the b+p sketch rows) uses 144-row tiles.
+  const bool m144 = (p.M > 128 && p.M <= 144) || (p.M > 256 && p.M <= 288);
   if (p.a_mmajor) {
-    if (p.M >= 128 && p.N >= 128) return launch_cfg<128, 128, 2, 4, true, 4>(p, stream, launches);
-    if (p.N < 128) return launch_cfg<128, 32, 4, 2, true, 6>(p, stream, launches);
-    return launch_cfg<64, 128, 2, 4, true, 5>(p, stream, launches);
+    if (p.M >= 128 && p.N >= 128) return launch_auto<128, 128, 2, 4, true, 4>(p, stream, launches);
+    if (p.N < 128) return launch_auto<128, 32, 4, 2, true, 6>(p, stream, launches);
+    return launch_auto<64, 128, 2, 4, true, 5>(p, stream, launches);
   } else {
-    if (p.M >= 128 && p.N >= 128) return launch_cfg<128, 128, 2, 4, false, 4>(p, stream, launches);
-    if (p.N < 128) return launch_cfg<128, 32, 4, 2, false, 6>(p, stream, launches);
-    return launch_cfg<64, 128, 2, 4, false, 5>(p, stream, launches);
+    if (m144 && p.N >= 128) return launch_auto<144, 128, 3, 4, false, 4>(p, stream, launches);
+    if (p.M >= 128 && p.N >= 128) return launch_auto<128, 128, 2, 4, false, 4>(p, stream, launches);
+    if (p.N < 128) return launch_auto<128, 32, 4, 2, false, 6>(p, stream, launches);
+    return launch_auto<64, 128, 2, 4, false, 5>(p, stream, launches);
   }
 }
 

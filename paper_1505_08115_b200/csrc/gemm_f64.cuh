@@ -33,8 +33,9 @@ struct GemmProblem {
   double* C;      // view pointer (already offset), column-major
   int64_t ldc;
   double alpha, beta;
-  int splitk;            // >1: deterministic split-K through `work`
-  double* work;          // splitk * M * N doubles (slab per split, ld = M)
+  int splitk;            // 0: choose automatically; >1: deterministic split-K through `work`
+  double* work;          // splitk * (M+1) * N doubles (slab per split)
+  size_t work_bytes;
 };
 
 int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches);

@@ -30,13 +30,22 @@ struct LeafLayout {
   static constexpr int PV = 3 * WL + 1;  // [tail | dots(WL) | rowj(WL) | gram(WL)]
 };
 
+// DSMEM load without a memory clobber so consecutive loads can be in flight
+// together (ordering w.r.t. the producers comes from the cluster barrier).
 RQ_DEV double dsmem_ld(const double* local_addr, unsigned rank) {
   uint32_t a = (uint32_t)__cvta_generic_to_shared(local_addr);
   uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
   double v;
-  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(r) : "memory");
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(r));
   return v;
+}
+
+RQ_DEV void dsmem_st(double* local_addr, unsigned rank, double v) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(local_addr);
+  uint32_t r;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(r), "d"(v) : "memory");
 }
 
 RQ_DEV void cluster_sync_all() {
@@ -59,19 +68,21 @@ __global__ void __launch_bounds__(PL_THREADS) leaf_qr_kernel(double* __restrict_
 
   double* A = sm;                                     // nr x WL (ld = rows_per)
   double* Vs = A + (int64_t)rows_per * WL;            // nr x WL own rows of V
-  double* part = Vs + (int64_t)rows_per * WL;         // 2 x PV partials
-  double* tot = part + 2 * PV;                        // PV totals
+  double* part = Vs + (int64_t)rows_per * WL;         // PV own partials
+  double* pin = part + PV;                            // 2 x 16 x PV partials pushed by every CTA
+  double* tot = pin + 2 * 16 * PV;                    // PV totals
   double* s = tot + PV;                               // WL coefficients
   double* Ts = s + WL;                                // WL x WL T (CTA-local copy)
   double* scal = Ts + WL * WL;                        // [refl, beta, inv, h]
 
-  for (int64_t idx = threadIdx.x; idx < (int64_t)nr * WL; idx += PL_THREADS) {
-    const int c = (int)(idx / nr), i = (int)(idx % nr);
-    A[(int64_t)c * rows_per + i] = c < w ? a[(int64_t)c * lda + r0 + i] : 0.0;
-    Vs[(int64_t)c * rows_per + i] = 0.0;
-  }
+  for (int c = warp; c < WL; c += PL_WARPS)
+    for (int i = lane; i < nr; i += 32) {
+      A[c * rows_per + i] = c < w ? a[(int64_t)c * lda + r0 + i] : 0.0;
+      Vs[c * rows_per + i] = 0.0;
+    }
   for (int e = threadIdx.x; e < WL * WL; e += PL_THREADS) Ts[e] = 0.0;
   __syncthreads();
+  cluster_sync_all();  // all CTAs initialised before anyone pushes into them
 
   bool refl_prev = false;
   for (int j = 0; j <= w; j++) {
@@ -79,16 +90,18 @@ __global__ void __launch_bounds__(PL_THREADS) leaf_qr_kernel(double* __restrict_
     // ---------------- phase A: pending update + partials ----------------
     if (j > 0 && refl_prev && !final_round) {
       // A[i][c] -= s[c] * u_i for own rows i >= j-1, columns c in [j, w)
-      const int64_t lo = max((int64_t)0, (int64_t)(j - 1) - r0);
-      const int ncols = w - j;
-      for (int64_t idx = threadIdx.x; idx < (int64_t)(nr - lo) * ncols; idx += PL_THREADS) {
-        const int c = j + (int)(idx / (nr - lo));
-        const int64_t i = lo + idx % (nr - lo);
-        A[(int64_t)c * rows_per + i] -= s[c] * Vs[(int64_t)(j - 1) * rows_per + i];
+      const int lo = (int)max((int64_t)0, (int64_t)(j - 1) - r0);
+      const double* uj = Vs + (j - 1) * rows_per;
+      // 2-D work split: warp-strided columns, lanes over rows (no integer division)
+      for (int c = j + warp; c < w; c += PL_WARPS) {
+        const double sc = s[c];
+        double* col = A + c * rows_per;
+        for (int i = lo + lane; i < nr; i += 32) col[i] -= sc * uj[i];
       }
       __syncthreads();
     }
-    double* mypart = part + (j & 1) * PV;
+    double* mypart = part;
+    const int par = j & 1;
     // items: 0 -> tail of column j; 1..w-j-1 -> dots with columns j+1..; gram k < j-1
     const int ndots = final_round ? 0 : (w - j);          // tail + dots
     const int ngram = (j >= 2) ? (j - 1) : 0;             // Gram entries for T column j-1
@@ -117,6 +130,10 @@ __global__ void __launch_bounds__(PL_THREADS) leaf_qr_kernel(double* __restrict_
     if (!final_round)
       for (int c = j + threadIdx.x; c < w; c += PL_THREADS)
         mypart[1 + WL + c] = (j >= r0 && j < r1) ? A[(int64_t)c * rows_per + (j - r0)] : 0.0;
+    __syncthreads();
+    // push the partial vector into every CTA (fire-and-forget DSMEM stores)
+    for (int dst = warp; dst < (int)CS; dst += PL_WARPS)
+      for (int e = lane; e < PV; e += 32) dsmem_st(pin + (par * 16 + rank) * PV + e, (unsigned)dst, mypart[e]);
     cluster_sync_all();
 
     // ---------------- phase B: identical totals in every CTA ----------------
@@ -128,7 +145,7 @@ __global__ void __launch_bounds__(PL_THREADS) leaf_qr_kernel(double* __restrict_
       else used = (e - 1 - 2 * WL) < ngram;
       if (!used) continue;
       double t = 0.0;
-      for (unsigned r = 0; r < CS; r++) t += dsmem_ld(part + (j & 1) * PV + e, r);
+      for (unsigned r = 0; r < CS; r++) t += pin[(par * 16 + r) * PV + e];  // rank order: deterministic
       tot[e] = t;
     }
     __syncthreads();
@@ -186,11 +203,11 @@ __global__ void __launch_bounds__(PL_THREADS) leaf_qr_kernel(double* __restrict_
   }
   __syncthreads();  // warp 0 wrote the last T column in the final round
   // write back R (own rows) and V
-  for (int64_t idx = threadIdx.x; idx < (int64_t)nr * w; idx += PL_THREADS) {
-    const int c = (int)(idx / nr), i = (int)(idx % nr);
-    a[(int64_t)c * lda + r0 + i] = A[(int64_t)c * rows_per + i];
-    v[(int64_t)c * ldv + r0 + i] = Vs[(int64_t)c * rows_per + i];
-  }
+  for (int c = warp; c < w; c += PL_WARPS)
+    for (int i = lane; i < nr; i += 32) {
+      a[(int64_t)c * lda + r0 + i] = A[c * rows_per + i];
+      v[(int64_t)c * ldv + r0 + i] = Vs[c * rows_per + i];
+    }
   if (rank == 0 && tl)
     for (int e = threadIdx.x; e < w * w; e += PL_THREADS) tl[(int64_t)(e / w) * ldt + e % w] = Ts[(e / w) * WL + e % w];
   cluster_sync_all();  // keep DSMEM alive until every CTA finished reading
@@ -201,7 +218,7 @@ static int launch_leaf(const LeafCall& c, cudaStream_t st, int64_t* launches) {
   constexpr int PV = LeafLayout<WL>::PV;
   const int CS = 16;
   const int rows_per = (int)ceil_div(c.mm, CS);
-  const size_t smem = ((size_t)2 * rows_per * WL + 3 * PV + WL + WL * WL + 8) * sizeof(double);
+  const size_t smem = ((size_t)2 * rows_per * WL + PV + 2 * 16 * PV + PV + WL + WL * WL + 8) * sizeof(double);
   if (smem > 227 * 1024) return set_error(RQ_EINTERNAL, "leaf_qr: %lld rows x %d too large for smem", (long long)c.mm, WL);
   auto kern = leaf_qr_kernel<WL>;
   static bool attr = false;
@@ -227,13 +244,16 @@ static int launch_leaf(const LeafCall& c, cudaStream_t st, int64_t* launches) {
   return RQ_OK;
 }
 
-int leaf_width_for(int64_t mm) {
-  // rows_per * WL * 16 B (A + V) must fit ~220 KB with 16 CTAs
+static size_t leaf_smem(int64_t mm, int WL) {
   const int64_t rows_per = ceil_div(mm, 16);
-  if (rows_per * 32 * 16 <= 200 * 1024) return 32;
-  if (rows_per * 16 * 16 <= 200 * 1024) return 16;
-  if (rows_per * 8 * 16 <= 200 * 1024) return 8;
-  if (rows_per * 4 * 16 <= 200 * 1024) return 4;
+  const int PV = 3 * WL + 1;
+  return ((size_t)2 * rows_per * WL + 34 * PV + WL + WL * WL + 8) * sizeof(double);
+}
+
+int leaf_width_for(int64_t mm) {
+  // own rows of A and V plus the pushed partials must fit one CTA's shared memory
+  for (int wl : {32, 16, 8, 4})
+    if (leaf_smem(mm, wl) <= 220 * 1024) return wl;
   return 0;
 }
 

@@ -47,4 +47,10 @@ size_t sweep_workspace_bytes(int64_t m, int total_cols, int grid);
 int sweep_grid_size(int total_cols);
 int sweep_launch(const SweepCall& c, SweepWork& w, cudaStream_t st, int64_t* launches);
 
+// Pivot selection only (sketch CPQR): chosen[0..steps) = columns in pivot order.
+// y (m x n, ld) is overwritten.  m <= 1024.
+int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, const int* init_pos, int* chosen,
+                       SweepWork& w, unsigned long long* counter, unsigned long long& counter_base, cudaStream_t st,
+                       int64_t* launches);
+
 }  // namespace rq

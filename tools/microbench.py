@@ -1,0 +1,84 @@
+"""Time the serial kernels in isolation through the C-ABI test hooks (debug/perf aid)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.getcwd())
+import torch  # noqa: E402
+
+import paper_1505_08115_b200 as rq  # noqa: E402
+from paper_1505_08115_b200.errors import check  # noqa: E402
+
+eng = rq.Engine()
+lib = eng.lib
+st = eng.stream
+
+
+def timeit(fn, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def dev(x):
+    buf, ld = eng.alloc_matrix(*x.shape)
+    buf[: x.shape[1], : x.shape[0]].copy_(torch.from_numpy(np.ascontiguousarray(x.T)))
+    return buf, ld
+
+
+rng = np.random.default_rng(0)
+which = sys.argv[1:] or ["sweep", "sketch", "leaf"]
+if "sweep" in which:
+    for (m, n, steps) in [(256, 256, 256), (128, 128, 128), (64, 64, 64)]:
+        a0 = rng.standard_normal((m, n))
+        buf, ld = dev(a0)
+        work, _ = eng.alloc_matrix(m, n)
+        v, ldv = eng.alloc_matrix(m, steps)
+        perm = torch.arange(n, dtype=torch.int64, device=eng.device)
+
+        def run():
+            work.copy_(buf)
+            v.zero_()
+            check(lib.rq_householder_sweep(eng.handle, ctypes.c_void_p(work.data_ptr()), m, n, ld,
+                                           ctypes.c_void_p(v.data_ptr()), ldv, ctypes.c_void_p(perm.data_ptr()),
+                                           steps, 1))
+        ms = timeit(run)
+        print(f"cpqr sweep {m}x{n} steps={steps}: {ms*1e3:.0f} us  ({ms*1e3/steps:.2f} us/step)")
+if "sketch" in which:
+    for (m, n, steps) in [(272, 10000, 256), (272, 5000, 256), (272, 1000, 256), (74, 2000, 64)]:
+        y0 = rng.standard_normal((m, n))
+        buf, ld = dev(y0)
+        work, _ = eng.alloc_matrix(m, n)
+        ch = torch.zeros(steps, dtype=torch.int32, device=eng.device)
+
+        def run():
+            work.copy_(buf)
+            check(lib.rq_test_sketch_cpqr(eng.handle, ctypes.c_void_p(work.data_ptr()), ld, m, n, steps,
+                                          ctypes.c_void_p(ch.data_ptr())))
+        ms = timeit(run)
+        print(f"sketch cpqr {m}x{n} steps={steps}: {ms*1e3:.0f} us  ({ms*1e3/steps:.2f} us/step)")
+if "leaf" in which:
+    for (mm, w) in [(10000, 16), (10000, 32), (5000, 32), (2000, 32), (40000, 8)]:
+        a0 = rng.standard_normal((mm, w))
+        buf, ld = dev(a0)
+        work, _ = eng.alloc_matrix(mm, w)
+        v, ldv = eng.alloc_matrix(mm, w)
+        t, ldt = eng.alloc_matrix(32, 32)
+
+        def run():
+            work.copy_(buf)
+            check(lib.rq_test_leaf_qr(eng.handle, ctypes.c_void_p(work.data_ptr()), ld, mm, w,
+                                      ctypes.c_void_p(v.data_ptr()), ldv, ctypes.c_void_p(t.data_ptr()), ldt))
+        try:
+            ms = timeit(run)
+            print(f"leaf {mm}x{w}: {ms*1e3:.0f} us  ({ms*1e3/w:.2f} us/column)")
+        except Exception as e:  # width not supported at this height
+            print(f"leaf {mm}x{w}: {e}")
