@@ -124,6 +124,9 @@ int rq_test_sketch_cpqr(rq_ctx* ctx, double* dY, int64_t ld, int32_t m, int32_t 
 int rq_test_leaf_qr(rq_ctx* ctx, double* dA, int64_t lda, int64_t mm, int32_t w, double* dV, int64_t ldv,
                     double* dT, int64_t ldt);
 
+/* Test hook: per-phase clock64 stamps of the cluster sweep (first 64 steps, 8 per step). */
+int rq_test_debug_timing(int32_t on, uint64_t* host, int32_t count);
+
 /* Number of kernel launches this context has issued (instrumentation). */
 int64_t rq_launch_count(rq_ctx* ctx);
 

@@ -264,6 +264,10 @@ int rq_test_leaf_qr(rq_ctx* ctx, double* dA, int64_t lda, int64_t mm, int32_t w,
   return rq::leaf_qr(lc, ctx->c.stream, &ctx->c.launches);
 }
 
+int rq_test_debug_timing(int32_t on, uint64_t* host, int32_t count) {
+  return rq::sweep_debug_timing(on, (unsigned long long*)host, count);
+}
+
 int64_t rq_launch_count(rq_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
 int rq_set_profiling(rq_ctx* ctx, int32_t on) {

@@ -220,9 +220,9 @@ int Ctx::sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, c
   SweepWork w;
   w.scratch = sweep_ws;
   w.scratch_bytes = sweep_ws_bytes;
-  if (!sk_counter) {
-    RQ_CUDA_TRY(cudaMalloc(&sk_counter, 64));
-    RQ_CUDA_TRY(cudaMemsetAsync(sk_counter, 0, 64, stream));
+  if (!sk_counter) {  // counter (offset 0) + two winner records (offset 64)
+    RQ_CUDA_TRY(cudaMalloc(&sk_counter, 256));
+    RQ_CUDA_TRY(cudaMemsetAsync(sk_counter, 0, 256, stream));
   }
   const int rc =
       sketch_cpqr_launch(yt, ldy, m, n, steps, init_pos, chosen, w, sk_counter, sk_counter_base, stream, &launches);

@@ -273,6 +273,17 @@ RQ_DEV void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Optional phase timestamps (rank 0, thread 0, first 64 steps) for tuning.
+__device__ unsigned long long g_sweep_dbg[64 * 8];
+__device__ int g_sweep_dbg_on;
+RQ_DEV void dbg_stamp(int j, int k) {
+  if (g_sweep_dbg_on && j < 64 && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    g_sweep_dbg[j * 8 + k] = c;
+  }
+}
+
 RQ_DEV void dsmem_st_f64(double* local, unsigned rank, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dsmem_addr(local, rank)), "d"(v) : "memory");
 }
@@ -322,6 +333,7 @@ __global__ void __launch_bounds__(SC_THREADS) sweep_cluster_kernel(const SweepAr
   for (int j = 0; j <= p.steps; j++) {
     const bool last = (j == p.steps);
     const int par = j & 1;
+    dbg_stamp(j, 0);
     double best_key = -1.0, best_tail = 0.0;
     int best_pos = INT_MAX, best_lc = -1;
     for (int lc = warp; lc < ncols; lc += SC_WARPS) {
@@ -375,6 +387,7 @@ __global__ void __launch_bounds__(SC_THREADS) sweep_cluster_kernel(const SweepAr
     // CTA-local argmax across warps (warp 0 reduces the per-warp candidates)
     if (lane == 0) red[warp] = SweepSlot{best_key, best_tail, best_pos, best_lc};
     __syncthreads();
+    dbg_stamp(j, 1);
     if (warp == 0) {
       SweepSlot b = (lane < SC_WARPS) ? red[lane] : SweepSlot{-1.0, 0.0, INT_MAX, -1};
 #pragma unroll
@@ -395,7 +408,9 @@ __global__ void __launch_bounds__(SC_THREADS) sweep_cluster_kernel(const SweepAr
       }
       if (lane == 0) red[SC_WARPS] = b;
     }
+    dbg_stamp(j, 2);
     cluster_barrier();
+    dbg_stamp(j, 3);
     // every CTA picks the same winner from its local table (ranks in order)
     if (warp == 0) {
       SweepSlot b{-1.0, 0.0, INT_MAX, -1};
@@ -422,6 +437,7 @@ __global__ void __launch_bounds__(SC_THREADS) sweep_cluster_kernel(const SweepAr
       }
     }
     __syncthreads();
+    dbg_stamp(j, 4);
     const SweepSlot win = red[SC_WARPS + 1];
     const unsigned wrank = (unsigned)reinterpret_cast<int*>(&red[SC_WARPS])[2];
     double* xs = xin + (int64_t)par * m;
@@ -431,7 +447,9 @@ __global__ void __launch_bounds__(SC_THREADS) sweep_cluster_kernel(const SweepAr
       for (int dstr = warp; dstr < (int)CS; dstr += SC_WARPS)
         for (int64_t i = j + lane; i < m; i += 32) dsmem_st_f64(xs + i, (unsigned)dstr, src[i]);
     }
+    dbg_stamp(j, 5);
     cluster_barrier();
+    dbg_stamp(j, 6);
     const double xj = xs[j];
     const bool refl = (m - j >= 2) && (win.key != 0.0);
     double beta = 0.0;
@@ -464,6 +482,7 @@ __global__ void __launch_bounds__(SC_THREADS) sweep_cluster_kernel(const SweepAr
     have_refl = refl;
     rj = j;
     __syncthreads();
+    dbg_stamp(j, 7);
   }
   // outputs: accumulate columns in place, pivot columns scattered by final position
   for (int lc = warp; lc < ncols; lc += SC_WARPS) {
@@ -479,6 +498,228 @@ __global__ void __launch_bounds__(SC_THREADS) sweep_cluster_kernel(const SweepAr
     for (int lc = threadIdx.x; lc < ncols; lc += SC_THREADS)
       if (c0 + lc < p.n && active[lc]) p.col_at_pos[pos[lc]] = c0 + lc;
   cluster_barrier();  // no CTA exits while others may still push into it
+}
+
+// ---------------------------------------------------------------------------
+// Register-resident cluster sweep for m <= 32*RPL rows and <= 16 columns per
+// CTA (the b x b CPQR of R' and small final blocks): warp w of CTA r owns
+// column r*16 + w, lane l holds rows l, l+32, ... in registers.  Per step:
+// apply the pending reflector and score (registers + one smem broadcast of u),
+// CTA argmax with __reduce_*_sync, stage the candidate column in local smem,
+// ONE cluster barrier, pull the 16 keys and then the winning column over DSMEM.
+// ---------------------------------------------------------------------------
+struct RegKey {
+  unsigned hi, lo;  // bits of the non-negative key (monotone as integers)
+  int pos;
+  int col;          // global column id, -1 = none
+  double tail;      // trailing norm^2 below row j
+  double xj;        // the candidate's entry in row j
+};
+
+// Winner among 32 lanes: max key, then min position.  Returns the lane, or -1.
+RQ_DEV int warp_argmax(unsigned hi, unsigned lo, int pos, bool valid) {
+  const unsigned all = 0xffffffffu;
+  const unsigned h = __reduce_max_sync(all, valid ? hi : 0u);
+  const bool c1 = valid && hi == h;
+  const unsigned l = __reduce_max_sync(all, c1 ? lo : 0u);
+  const bool c2 = c1 && lo == l;
+  const int pm = (int)__reduce_min_sync(all, c2 ? (unsigned)pos : 0xffffffffu);
+  const unsigned ball = __ballot_sync(all, c2 && pos == pm);
+  return ball ? __ffs(ball) - 1 : -1;
+}
+
+RQ_DEV void push_key(RegKey* local_slot, unsigned rank, const RegKey& k) {
+  const uint32_t a = dsmem_addr(local_slot, rank);
+  asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(k.hi), "r"(k.lo) : "memory");
+  asm volatile("st.shared::cluster.v2.s32 [%0], {%1, %2};" ::"r"(a + 8), "r"(k.pos), "r"(k.col) : "memory");
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a + 16), "d"(k.tail), "d"(k.xj) : "memory");
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(512) sweep_reg_kernel(const SweepArgs p) {
+  __shared__ double u[32 * RPL];
+  __shared__ double cand[2][32 * RPL];          // this CTA's candidate column, by step parity
+  __shared__ __align__(16) RegKey keys[2][16];  // candidates pushed by every CTA, by parity
+  __shared__ RegKey wk[16];
+  __shared__ int wsel;
+  const unsigned CS = gridDim.x;
+  const unsigned rank = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = (int)p.m;
+  const int c = (int)rank * 16 + warp;  // global column owned by this warp
+  const bool own = c < p.n;
+  double x[RPL];
+#pragma unroll
+  for (int k = 0; k < RPL; k++) {
+    const int i = lane + 32 * k;
+    x[k] = (own && i < m) ? p.a[(int64_t)c * p.lda + i] : 0.0;
+  }
+  int pos = own ? (p.init_pos ? p.init_pos[c] : c) : INT_MAX;
+  bool active = own;
+  bool have_refl = false;
+  int rj = -1;
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+
+  for (int j = 0; j <= p.steps; j++) {
+    const bool last = (j == p.steps);
+    const int par = j & 1;
+    // ---- A: apply the pending reflector to this warp's column, score it ----
+    dbg_stamp(j, 0);
+    double tail = 0.0;
+    if (active) {
+      if (have_refl) {
+        double uk[RPL], pr[RPL];
+#pragma unroll
+        for (int k = 0; k < RPL; k++) {
+          const int i = lane + 32 * k;
+          uk[k] = (i >= rj && i < m) ? u[i] : 0.0;
+          pr[k] = uk[k] * x[k];
+        }
+#pragma unroll
+        for (int w2 = 1; w2 < RPL; w2 <<= 1)  // pairwise tree: depth log2(RPL)
+#pragma unroll
+          for (int k = 0; k + w2 < RPL; k += 2 * w2) pr[k] += pr[k + w2];
+        const double d = 2.0 * warp_sum(pr[0]);
+#pragma unroll
+        for (int k = 0; k < RPL; k++) x[k] -= d * uk[k];
+      }
+      if (!last) {
+        double sq[RPL];
+#pragma unroll
+        for (int k = 0; k < RPL; k++) {
+          const int i = lane + 32 * k;
+          sq[k] = (i > j && i < m) ? x[k] * x[k] : 0.0;
+        }
+#pragma unroll
+        for (int w2 = 1; w2 < RPL; w2 <<= 1)
+#pragma unroll
+          for (int k = 0; k + w2 < RPL; k += 2 * w2) sq[k] += sq[k + w2];
+        tail = warp_sum(sq[0]);
+      }
+    }
+    if (last) break;
+    double sel = 0.0;
+    const int kj = j >> 5;
+#pragma unroll
+    for (int k = 0; k < RPL; k++) sel = (k == kj) ? x[k] : sel;  // select chain keeps x[] in registers
+    const double xj = __shfl_sync(0xffffffffu, sel, j & 31);
+    const bool elig = active && (p.pivot ? true : pos == j);
+    const double key = xj * xj + tail;
+    // ---- B/C: CTA candidate, pushed into every CTA's key table ----
+    if (lane == 0) {
+      const unsigned long long kb = __double_as_longlong(key);
+      wk[warp] = RegKey{(unsigned)(kb >> 32), (unsigned)kb, pos, elig ? c : -1, tail, xj};
+    }
+    dbg_stamp(j, 1);
+    __syncthreads();
+    dbg_stamp(j, 2);
+    if (warp == 0) {
+      const RegKey r = lane < 16 ? wk[lane] : RegKey{0u, 0u, INT_MAX, -1, 0.0, 0.0};
+      const int wl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);
+      const RegKey best = wl >= 0 ? wk[wl] : RegKey{0u, 0u, INT_MAX, -1, 0.0, 0.0};
+      if (lane < (int)CS) push_key(&keys[par][rank], (unsigned)lane, best);
+      if (lane == 0) wsel = wl;
+    }
+    __syncthreads();
+    dbg_stamp(j, 3);
+    if (wsel == warp) {  // the CTA's best warp stages its column for the cluster
+#pragma unroll
+      for (int k = 0; k < RPL; k++) {
+        const int i = lane + 32 * k;
+        if (i < m) cand[par][i] = x[k];
+      }
+    }
+    dbg_stamp(j, 4);
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    dbg_stamp(j, 5);
+    // ---- F: every warp resolves the cluster winner from the local table ----
+    const RegKey r = lane < (int)CS ? keys[par][lane] : RegKey{0u, 0u, INT_MAX, -1, 0.0, 0.0};
+    const int wl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);
+    const unsigned whi = __shfl_sync(0xffffffffu, r.hi, wl);
+    const unsigned wlo = __shfl_sync(0xffffffffu, r.lo, wl);
+    const int wpos = __shfl_sync(0xffffffffu, r.pos, wl);
+    const int wcol = __shfl_sync(0xffffffffu, r.col, wl);
+    const double wtail = __shfl_sync(0xffffffffu, r.tail, wl);
+    const double wxj = __shfl_sync(0xffffffffu, r.xj, wl);
+    const double wkey = __longlong_as_double(((long long)whi << 32) | (long long)wlo);
+    // ---- G: pull the winning column while computing the reflector scalars ----
+    const bool refl = (m - j >= 2) && (wkey != 0.0);
+    double pulled[(32 * RPL + 511) / 512];
+#pragma unroll
+    for (int t = 0; t < (32 * RPL + 511) / 512; t++) {
+      const int i = j + threadIdx.x + 512 * t;
+      pulled[t] = (refl && i < m) ? dsmem_f64(&cand[par][i], (unsigned)wl) : 0.0;
+    }
+    double beta = 0.0, h = 0.0, inv = 0.0;
+    if (refl) {
+      const double nrm = sqrt(wkey);
+      beta = (wxj >= 0.0) ? -nrm : nrm;
+      h = beta - wxj;
+      inv = 1.0 / sqrt(h * h + wtail);
+    }
+#pragma unroll
+    for (int t = 0; t < (32 * RPL + 511) / 512; t++) {
+      const int i = j + threadIdx.x + 512 * t;
+      if (refl && i < m) u[i] = (i == j) ? h * inv : -pulled[t] * inv;
+    }
+    dbg_stamp(j, 6);
+    // ---- H: positions (registers), winner column finalised ----
+    if (c == wcol) {
+      pos = j;
+      active = false;
+      if (refl) {
+#pragma unroll
+        for (int k = 0; k < RPL; k++) {
+          const int i = lane + 32 * k;
+          if (i >= j) x[k] = (i == j) ? beta : 0.0;
+        }
+      }
+    } else if (own && pos == j) {
+      pos = wpos;
+    }
+    if (rank == 0 && threadIdx.x == 0 && p.col_at_pos) p.col_at_pos[j] = wcol;
+    __syncthreads();  // u complete
+    dbg_stamp(j, 7);
+    if (rank == 0 && p.v && refl)
+      for (int i = j + threadIdx.x; i < m; i += 512) p.v[(int64_t)j * p.ldv + i] = u[i];
+    have_refl = refl;
+    rj = j;
+  }
+  // outputs: pivot columns scattered by final position (or in place)
+  if (own) {
+    double* dst = p.r_out ? p.r_out + (int64_t)pos * p.ldr : p.a + (int64_t)c * p.lda;
+#pragma unroll
+    for (int k = 0; k < RPL; k++) {
+      const int i = lane + 32 * k;
+      if (i < m) dst[i] = x[k];
+    }
+    if (p.col_at_pos && active && lane == 0) p.col_at_pos[pos] = c;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int RPL>
+static int launch_reg(const SweepArgs& a, int CS, cudaStream_t st, int64_t* launches) {
+  static bool attr = false;
+  if (!attr) {
+    RQ_CUDA_TRY(cudaFuncSetAttribute(sweep_reg_kernel<RPL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, sweep_reg_kernel<RPL>, a));
+  if (launches) (*launches)++;
+  return RQ_OK;
 }
 
 static size_t cluster_smem(int64_t m, int per) {
@@ -583,6 +824,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1) sketch_cpqr_kernel(const Sketch
   const int rounds = (ncols + SK_GROUPS - 1) / SK_GROUPS;
   for (int j = 0; j < p.steps; j++) {
     const int par = j & 1;
+    dbg_stamp(j, 0);
     // -------- phase A: apply the pending reflector, score the candidates --------
     double bk = -1.0, bt = 0.0;
     int bp = INT_MAX, bc = -1, bw = 0;
@@ -635,8 +877,10 @@ __global__ void __launch_bounds__(SK_THREADS, 1) sketch_cpqr_kernel(const Sketch
       const int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
       sk_take_better(bk, bt, bp, bc, bw, k2, t2, p2, c2, 0);
     }
+    dbg_stamp(j, 1);
     if (lane == 0) red[warp] = SweepSlot{bk, bt, bp, bc};
     __syncthreads();
+    dbg_stamp(j, 2);
     if (warp == 0) {
       SweepSlot b = red[lane];  // SK_WARPS == 32
       int who = 0;
@@ -668,6 +912,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1) sketch_cpqr_kernel(const Sketch
     }
     // -------- grid barrier: one arrival + one poller per CTA (monotone counter) --------
     __syncthreads();
+    dbg_stamp(j, 3);
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(p.counter, 1ull);
@@ -677,6 +922,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1) sketch_cpqr_kernel(const Sketch
     }
     __syncthreads();
     // -------- every CTA reads the G candidates (one batch of loads) and picks the winner --------
+    dbg_stamp(j, 4);
     if (warp == 0) {
       double k = -1.0, t = 0.0;
       int ps = INT_MAX, cl = -1, who = -1;
@@ -715,6 +961,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1) sketch_cpqr_kernel(const Sketch
       }
     }
     __syncthreads();
+    dbg_stamp(j, 5);
     const SweepSlot win = red[SK_WARPS + 1];
     const int wcta = wbuf[0];
     const double* x = p.slotdata + ((int64_t)par * G + wcta) * m;
@@ -735,11 +982,321 @@ __global__ void __launch_bounds__(SK_THREADS, 1) sketch_cpqr_kernel(const Sketch
         pos[lc] = win.pos;
       }
     }
+    dbg_stamp(j, 6);
     if (blockIdx.x == 0 && threadIdx.x == 0) p.chosen[j] = win.col;
     have_refl = refl;
     rj = j;
     __syncthreads();
+    dbg_stamp(j, 7);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Register-resident sketch CPQR (n' <= G * 16 * CPW columns, m <= 32 * RPL rows).
+// 512 threads; warp w of CTA g owns columns g*16*CPW + w*CPW + q (q < CPW),
+// lane l holds rows l, l+32, ... of each in registers.
+// ---------------------------------------------------------------------------
+struct alignas(16) SkSlot2 {
+  double key;
+  double tail;
+  double xj;
+  int pos;
+  int col;
+};
+
+// Winner record published by the last CTA to arrive in each step.
+struct alignas(16) SkWin {
+  double key;
+  double tail;
+  double xj;
+  int pos;
+  int col;
+  int cta;
+  int pad;
+  unsigned long long flag;  // launch-unique step stamp, written last (release)
+};
+
+template <int RPL, int CPW, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchArgs p, SkSlot2* slots, SkWin* wins,
+                                                                   unsigned long long stamp_base) {
+  constexpr int NT = WARPS * 32;
+  __shared__ double u[32 * RPL];
+  __shared__ RegKey wk[WARPS];
+  __shared__ RegKey win_s;
+  __shared__ int wsel[3];
+  const int G = gridDim.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = p.m;
+  const int cbase = blockIdx.x * WARPS * CPW + warp * CPW;
+  double x[CPW][RPL];
+  int pos[CPW];
+  bool act[CPW];
+#pragma unroll
+  for (int q = 0; q < CPW; q++) {
+    const int c = cbase + q;
+    act[q] = c < p.n;
+    pos[q] = act[q] ? (p.init_pos ? p.init_pos[c] : c) : INT_MAX;
+#pragma unroll
+    for (int k = 0; k < RPL; k++) {
+      const int i = lane + 32 * k;
+      x[q][k] = (act[q] && i < m) ? p.y[(int64_t)c * p.ld + i] : 0.0;
+    }
+  }
+  bool have_refl = false;
+  int rj = -1;
+  for (int j = 0; j < p.steps; j++) {
+    const int par = j & 1;
+    dbg_stamp(j, 0);
+    // -------- A: apply the pending reflector to the warp's columns and score them --------
+    double d[CPW];
+    if (have_refl) {
+      double uk[RPL];
+#pragma unroll
+      for (int k = 0; k < RPL; k++) {
+        const int i = lane + 32 * k;
+        uk[k] = (i >= rj && i < m) ? u[i] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < CPW; q++) {
+        double pr[RPL];
+#pragma unroll
+        for (int k = 0; k < RPL; k++) pr[k] = uk[k] * x[q][k];
+#pragma unroll
+        for (int w2 = 1; w2 < RPL; w2 <<= 1)
+#pragma unroll
+          for (int k = 0; k + w2 < RPL; k += 2 * w2) pr[k] += pr[k + w2];
+        d[q] = pr[0];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < CPW; q++) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+#pragma unroll
+      for (int q = 0; q < CPW; q++) {
+        const double dd = act[q] ? 2.0 * d[q] : 0.0;
+#pragma unroll
+        for (int k = 0; k < RPL; k++) x[q][k] -= dd * uk[k];
+      }
+    }
+    double t[CPW];
+#pragma unroll
+    for (int q = 0; q < CPW; q++) {
+      double sq[RPL];
+#pragma unroll
+      for (int k = 0; k < RPL; k++) {
+        const int i = lane + 32 * k;
+        sq[k] = (i > j && i < m) ? x[q][k] * x[q][k] : 0.0;
+      }
+#pragma unroll
+      for (int w2 = 1; w2 < RPL; w2 <<= 1)
+#pragma unroll
+        for (int k = 0; k + w2 < RPL; k += 2 * w2) sq[k] += sq[k + w2];
+      t[q] = sq[0];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < CPW; q++) t[q] += __shfl_xor_sync(0xffffffffu, t[q], o);
+    const int kj = j >> 5;
+    double bkey = -1.0, btail = 0.0, bxj = 0.0;
+    int bpos = INT_MAX, bq = -1;
+#pragma unroll
+    for (int q = 0; q < CPW; q++) {
+      double sel = 0.0;
+#pragma unroll
+      for (int k = 0; k < RPL; k++) sel = (k == kj) ? x[q][k] : sel;
+      const double xj = __shfl_sync(0xffffffffu, sel, j & 31);
+      const double key = xj * xj + t[q];
+      if (act[q] && (bq < 0 || piv_better(key, pos[q], bkey, bpos))) {
+        bkey = key;
+        btail = t[q];
+        bxj = xj;
+        bpos = pos[q];
+        bq = q;
+      }
+    }
+    if (lane == 0) {
+      const unsigned long long kb = __double_as_longlong(bkey < 0.0 ? 0.0 : bkey);
+      wk[warp] = RegKey{(unsigned)(kb >> 32), (unsigned)kb, bpos, bq >= 0 ? cbase + bq : -1, btail, bxj};
+    }
+    dbg_stamp(j, 1);
+    __syncthreads();
+    dbg_stamp(j, 2);
+    // -------- B: CTA candidate -> global slot; its warp writes the column --------
+    SkSlot2* slot = slots + (int64_t)par * G;
+    if (warp == 0) {
+      const RegKey r = lane < WARPS ? wk[lane] : RegKey{0u, 0u, INT_MAX, -1, 0.0, 0.0};
+      const int wl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);
+      if (lane == 0) {
+        wsel[0] = wl;
+        SkSlot2* me = slot + blockIdx.x;
+        if (wl >= 0) {
+          const RegKey b = wk[wl];
+          me->key = __longlong_as_double(((long long)b.hi << 32) | (long long)b.lo);
+          me->tail = b.tail;
+          me->xj = b.xj;
+          me->pos = b.pos;
+          me->col = b.col;
+        } else {
+          me->key = -1.0;
+          me->col = -1;
+          me->pos = INT_MAX;
+        }
+      }
+    }
+    __syncthreads();
+    if (wsel[0] == warp) {
+      const int bqw = wk[warp].col - cbase;
+      double* sd = p.slotdata + ((int64_t)par * G + blockIdx.x) * m;
+#pragma unroll
+      for (int q = 0; q < CPW; q++)
+        if (q == bqw)
+#pragma unroll
+          for (int k = 0; k < RPL; k++) {
+            const int i = lane + 32 * k;
+            if (i >= j && i < m) sd[i] = x[q][k];
+          }
+    }
+    __syncthreads();
+    dbg_stamp(j, 3);
+    // -------- C: arrive; the last CTA to arrive picks the winner and publishes it --------
+    SkWin* wrec = wins + par;
+    const unsigned long long stamp = stamp_base + (unsigned long long)j + 1ull;
+    if (warp == 0) {
+      unsigned long long old = 0;
+      if (lane == 0) {
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.counter) : "memory");
+      }
+      old = __shfl_sync(0xffffffffu, old, 0);
+      const unsigned long long target = p.counter_base + (unsigned long long)(j + 1) * G;
+      if (old + 1 == target) {
+        // last arriver: every slot of this step is visible (acq_rel atomic).
+        // Issue all slot loads first (independent), then reduce.
+        constexpr int kMaxK = (kSMs + 31) / 32;
+        double kv[kMaxK], tv[kMaxK], xv[kMaxK];
+        int pv[kMaxK], cv[kMaxK];
+#pragma unroll
+        for (int kk = 0; kk < kMaxK; kk++) {
+          const int c = kk * 32 + lane;
+          const bool ok = c < G;
+          const SkSlot2* sp = &slot[ok ? c : 0];
+          kv[kk] = __ldcg(&sp->key);
+          tv[kk] = __ldcg(&sp->tail);
+          xv[kk] = __ldcg(&sp->xj);
+          pv[kk] = __ldcg(&sp->pos);
+          cv[kk] = __ldcg(&sp->col);
+          if (!ok) {
+            kv[kk] = -1.0;
+            cv[kk] = -1;
+          }
+        }
+        double bk = -1.0, bt = 0.0, bx = 0.0;
+        int bp = INT_MAX, bc = -1, bw = -1;
+#pragma unroll
+        for (int kk = 0; kk < kMaxK; kk++)
+          if (kv[kk] >= 0.0 && cv[kk] >= 0 && (bc < 0 || piv_better(kv[kk], pv[kk], bk, bp))) {
+            bk = kv[kk];
+            bt = tv[kk];
+            bx = xv[kk];
+            bp = pv[kk];
+            bc = cv[kk];
+            bw = kk * 32 + lane;
+          }
+        const unsigned long long kb = __double_as_longlong(bk < 0.0 ? 0.0 : bk);
+        const int wl = warp_argmax((unsigned)(kb >> 32), (unsigned)kb, bp, bc >= 0);
+        if (lane == wl) {
+          wrec->key = bk;
+          wrec->tail = bt;
+          wrec->xj = bx;
+          wrec->pos = bp;
+          wrec->col = bc;
+          wrec->cta = bw;
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&wrec->flag), "l"(stamp) : "memory");
+        }
+      } else if (lane == 0) {
+        while (ld_acquire_u64(&wrec->flag) != stamp) {
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        RegKey w;
+        const double kv = __ldcg(&wrec->key);
+        const unsigned long long kb = __double_as_longlong(kv);
+        w.hi = (unsigned)(kb >> 32);
+        w.lo = (unsigned)kb;
+        w.tail = __ldcg(&wrec->tail);
+        w.xj = __ldcg(&wrec->xj);
+        w.pos = __ldcg(&wrec->pos);
+        w.col = __ldcg(&wrec->col);
+        win_s = w;
+        wsel[1] = __ldcg(&wrec->cta);
+      }
+    }
+    __syncthreads();
+    dbg_stamp(j, 4);
+    // -------- E: reflector from the winning column (L2) --------
+    const RegKey win = win_s;
+    const int wcta = wsel[1];
+    const double wkey = __longlong_as_double(((long long)win.hi << 32) | (long long)win.lo);
+    const bool refl = (m - j >= 2) && (wkey != 0.0);
+    if (refl) {
+      const double* xs = p.slotdata + ((int64_t)par * G + wcta) * m;
+      const int i = j + threadIdx.x;
+      const double xv = (i < m) ? __ldcg(&xs[i]) : 0.0;
+      const double nrm = sqrt(wkey);
+      const double beta = (win.xj >= 0.0) ? -nrm : nrm;
+      const double h = beta - win.xj;
+      const double inv = 1.0 / sqrt(h * h + win.tail);
+      if (i < m) u[i] = (i == j) ? h * inv : -xv * inv;
+      for (int i2 = i + NT; i2 < m; i2 += NT) u[i2] = -__ldcg(&xs[i2]) * inv;
+    }
+#pragma unroll
+    for (int q = 0; q < CPW; q++) {
+      if (cbase + q == win.col) {
+        pos[q] = j;
+        act[q] = false;
+      } else if (act[q] && pos[q] == j) {
+        pos[q] = win.pos;
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.chosen[j] = win.col;
+    have_refl = refl;
+    rj = j;
+    __syncthreads();
+    dbg_stamp(j, 5);
+  }
+}
+
+template <int RPL, int CPW, int WARPS>
+static int launch_sketch_reg(const SketchArgs& a, int G, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
+                             cudaStream_t st, int64_t* launches) {
+  void* args[] = {(void*)&a, (void*)&slots, (void*)&wins, (void*)&stamp_base};
+  RQ_CUDA_TRY(cudaLaunchCooperativeKernel((void*)sketch_reg_kernel<RPL, CPW, WARPS>, dim3(G), dim3(WARPS * 32), args,
+                                          0, st));
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+// (warps, columns per warp) options in order of preference; registers: CPW*RPL doubles
+template <int RPL>
+static int dispatch_sketch_reg(const SketchArgs& a, int n, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
+                               cudaStream_t st, int64_t* launches, int* grid) {
+  struct Opt {
+    int warps, cpw;
+  };
+  const Opt opts[] = {{16, 1}, {16, 2}, {16, 3}, {8, 6}, {8, 10}};
+  for (const Opt& o : opts) {
+    if (RPL * o.cpw > (o.warps == 16 ? 30 : 92)) continue;  // register budget
+    const int G = (n + o.warps * o.cpw - 1) / (o.warps * o.cpw);
+    if (G > kSMs) continue;
+    *grid = G;
+    if (o.warps == 16 && o.cpw == 1) return launch_sketch_reg<RPL, 1, 16>(a, G, slots, wins, stamp_base, st, launches);
+    if (o.warps == 16 && o.cpw == 2) return launch_sketch_reg<RPL, 2, 16>(a, G, slots, wins, stamp_base, st, launches);
+    if (o.warps == 16 && o.cpw == 3) return launch_sketch_reg<RPL, 3, 16>(a, G, slots, wins, stamp_base, st, launches);
+    if (o.cpw == 6) return launch_sketch_reg<RPL, 6, 8>(a, G, slots, wins, stamp_base, st, launches);
+    return launch_sketch_reg<RPL, 10, 8>(a, G, slots, wins, stamp_base, st, launches);
+  }
+  return -1;  // does not fit: caller falls back
 }
 
 static size_t sketch_fixed_smem(int m, int per) {
@@ -750,6 +1307,37 @@ int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, con
                        SweepWork& w, unsigned long long* counter, unsigned long long& counter_base, cudaStream_t st,
                        int64_t* launches) {
   if (steps <= 0) return RQ_OK;
+  if (m <= 288) {
+    SketchArgs a{};
+    a.y = y;
+    a.ywork = const_cast<double*>(y);
+    a.ld = ld;
+    a.m = m;
+    a.n = n;
+    a.steps = steps;
+    a.init_pos = init_pos;
+    a.chosen = chosen;
+    SkSlot2* slots = reinterpret_cast<SkSlot2*>(w.scratch);
+    const size_t slot_bytes = ((2 * (size_t)kSMs * sizeof(SkSlot2) + 255) & ~size_t(255));
+    // dedicated, zero-initialised records next to the counter: only older stamps can be stale there
+    SkWin* wins = reinterpret_cast<SkWin*>(reinterpret_cast<char*>(counter) + 64);
+    a.slotdata = reinterpret_cast<double*>(reinterpret_cast<char*>(w.scratch) + slot_bytes + 256);
+    a.counter = counter;
+    a.counter_base = counter_base;
+    const size_t need = slot_bytes + 256 + 2 * (size_t)kSMs * m * 8;
+    if (w.scratch_bytes >= need) {
+      // step stamps are unique across launches: derived from the monotone counter base
+      const unsigned long long stamp_base = counter_base;
+      int rc, G = 0;
+      if (m <= 96) rc = dispatch_sketch_reg<3>(a, n, slots, wins, stamp_base, st, launches, &G);
+      else if (m <= 160) rc = dispatch_sketch_reg<5>(a, n, slots, wins, stamp_base, st, launches, &G);
+      else rc = dispatch_sketch_reg<9>(a, n, slots, wins, stamp_base, st, launches, &G);
+      if (rc >= 0) {
+        counter_base += (unsigned long long)steps * G;  // every CTA arrives once per step
+        return rc;
+      }
+    }
+  }
   int G = (n + 15) / 16;  // >= 16 columns per CTA
   if (G > kSMs) G = kSMs;
   if (G < 1) G = 1;
@@ -794,6 +1382,12 @@ size_t sweep_workspace_bytes(int64_t m, int total_cols, int grid) {
   b += 2 * (size_t)grid * m * sizeof(double) + 256;
   b += (size_t)grid * m * sizeof(double) + 256;  // u fallback
   return b;
+}
+
+int sweep_debug_timing(int on, unsigned long long* host, int count) {
+  RQ_CUDA_TRY(cudaMemcpyToSymbol(g_sweep_dbg_on, &on, sizeof(int)));
+  if (host) RQ_CUDA_TRY(cudaMemcpyFromSymbol(host, g_sweep_dbg, sizeof(unsigned long long) * std::min(count, 512)));
+  return RQ_OK;
 }
 
 int sweep_grid_size(int total_cols) {
@@ -844,6 +1438,27 @@ static int sweep_launch_cluster(const SweepCall& c, int CS, size_t smem, cudaStr
 int sweep_launch(const SweepCall& c, SweepWork& w, cudaStream_t st, int64_t* launches) {
   if (c.steps <= 0) return RQ_OK;
   const int total = c.n + c.n_acc;
+  // register-resident cluster path: one warp per column, rows in registers
+  if (c.n_acc == 0 && c.n <= 256 && c.m <= 512) {
+    SweepArgs a{};
+    a.a = c.a;
+    a.lda = c.lda;
+    a.m = c.m;
+    a.n = c.n;
+    a.steps = c.steps;
+    a.pivot = c.pivot;
+    a.init_pos = c.init_pos;
+    a.v = c.v;
+    a.ldv = c.ldv;
+    a.col_at_pos = c.col_at_pos;
+    a.r_out = c.r_out;
+    a.ldr = c.ldr;
+    const int CS = std::max(1, (c.n + 15) / 16);
+    if (c.m <= 64) return launch_reg<2>(a, CS, st, launches);
+    if (c.m <= 128) return launch_reg<4>(a, CS, st, launches);
+    if (c.m <= 256) return launch_reg<8>(a, CS, st, launches);
+    return launch_reg<16>(a, CS, st, launches);
+  }
   // cluster path when the whole matrix fits in one 16-CTA cluster's shared memory
   if (c.m <= 4096) {
     for (int CS : {4, 8, 16}) {

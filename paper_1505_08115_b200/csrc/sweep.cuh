@@ -45,6 +45,7 @@ struct SweepCall {
 
 size_t sweep_workspace_bytes(int64_t m, int total_cols, int grid);
 int sweep_grid_size(int total_cols);
+int sweep_debug_timing(int on, unsigned long long* host, int count);
 int sweep_launch(const SweepCall& c, SweepWork& w, cudaStream_t st, int64_t* launches);
 
 // Pivot selection only (sketch CPQR): chosen[0..steps) = columns in pivot order.

@@ -82,3 +82,42 @@ if "leaf" in which:
             print(f"leaf {mm}x{w}: {ms*1e3:.0f} us  ({ms*1e3/w:.2f} us/column)")
         except Exception as e:  # width not supported at this height
             print(f"leaf {mm}x{w}: {e}")
+if "stamps" in which:
+    m = n = 256
+    a0 = rng.standard_normal((m, n))
+    buf, ld = dev(a0)
+    v, ldv = eng.alloc_matrix(m, n)
+    perm = torch.arange(n, dtype=torch.int64, device=eng.device)
+    check(lib.rq_test_debug_timing(1, None, 0))
+    check(lib.rq_householder_sweep(eng.handle, ctypes.c_void_p(buf.data_ptr()), m, n, ld,
+                                   ctypes.c_void_p(v.data_ptr()), ldv, ctypes.c_void_p(perm.data_ptr()), n, 1))
+    torch.cuda.synchronize()
+    h = np.zeros(512, dtype=np.uint64)
+    check(lib.rq_test_debug_timing(0, h.ctypes.data_as(ctypes.c_void_p), 512))
+    h = h.reshape(64, 8).astype(np.int64)
+    d = np.diff(h[5:60], axis=1)
+    print("cluster sweep phase cycles (median over steps 5..60):")
+    names = ["A:update+score", "sync1", "argmax+pushkey+sync2", "stage", "cluster barrier", "F+G: winner, pull, u",
+             "H + sync3"]
+    for k, nm in enumerate(names):
+        print(f"  {nm:18s} {int(np.median(d[:, k])):6d}")
+    print("  step total        ", int(np.median(h[6:60, 0] - h[5:59, 0])))
+
+if "skstamps" in which:
+    m, n, steps = 272, int(os.environ.get("SKN", "10000")), 256
+    y0 = rng.standard_normal((m, n))
+    buf, ld = dev(y0)
+    ch = torch.zeros(steps, dtype=torch.int32, device=eng.device)
+    check(lib.rq_test_debug_timing(1, None, 0))
+    check(lib.rq_test_sketch_cpqr(eng.handle, ctypes.c_void_p(buf.data_ptr()), ld, m, n, steps,
+                                  ctypes.c_void_p(ch.data_ptr())))
+    torch.cuda.synchronize()
+    h = np.zeros(512, dtype=np.uint64)
+    check(lib.rq_test_debug_timing(0, h.ctypes.data_as(ctypes.c_void_p), 512))
+    h = h.reshape(64, 8).astype(np.int64)
+    d = np.diff(h[5:60, :6], axis=1)
+    print(f"sketch cpqr phase cycles n={n} (median over steps 5..60):")
+    names = ["phaseA", "sync", "cta argmax+publish", "arrive/last-reduces/poll", "u+pos"]
+    for k, nm in enumerate(names):
+        print(f"  {nm:20s} {int(np.median(d[:, k])):6d}")
+    print("  step total          ", int(np.median(h[6:60, 0] - h[5:59, 0])))
