@@ -1,6 +1,7 @@
 // FP64 DMMA GEMM with a TMA/mbarrier producer-consumer pipeline (see gemm_f64.cuh).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm_f64.cuh"
@@ -80,7 +81,7 @@ struct GemmCfg {
   static constexpr int WTN = BN / WARPS_N;
   static constexpr int MT = WTM / 16;
   static constexpr int NT = WTN / 8;
-  static constexpr int A_LDM = BM + 8;  // padded M-major row (conflict-free fragments)
+  static constexpr int A_LDM = BM + 4;  // padded M-major row: 4 k-rows of a half-warp hit 4 distinct 32 B bank groups
   static constexpr int A_BYTES = A_MMAJOR ? BK * A_LDM * 8 : BM * BK * 8;
   static constexpr int A_BYTES_AL = (A_BYTES + 1023) / 1024 * 1024;
   static constexpr int B_BYTES = BN * BK * 8;
@@ -89,6 +90,11 @@ struct GemmCfg {
   static_assert(WTM % 16 == 0 && WTN % 8 == 0, "warp tile");
   static_assert(B_BYTES % 1024 == 0, "swizzle-128B stage alignment");
 };
+
+// MMA row/column index g -> shared-memory row, so that the 16 lanes of a
+// half-warp (g = 0..3 x 4 k) hit 8 distinct 16-byte chunks of the 128B-swizzled
+// K-major tile (rows 0,2,4,6 then 1,3,5,7).  Undone in the epilogue.
+RQ_DEV int perm8(int g) { return ((g & 3) << 1) | (g >> 2); }
 
 // element (r, k) of a K-major 16-wide tile written by TMA with SWIZZLE_128B
 RQ_DEV double ld_kmajor(const char* tile, int r, int k) {
@@ -145,7 +151,8 @@ RQ_DEV void issue_stage(const CUtensorMap* tmA, const CUtensorMap* tmB, const KA
 }
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>::kThreads, 1)
+__global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>::kThreads,
+                                  (GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>::kThreads <= 128) ? 2 : 1)
     gemm_f64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const KArgs args) {
   using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>;
@@ -187,6 +194,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
   const int wn = warp / WARPS_M;
   const int g = lane >> 2;
   const int tq = lane & 3;
+  const int pg = perm8(g);
   int stage = 0;
   uint32_t phase = 0;
 
@@ -206,6 +214,18 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
       for (int j = 0; j < Cfg::NT; j++)
 #pragma unroll
         for (int e = 0; e < 4; e++) acc[i][j][e] = 0.0;
+    if (args.splitk == 1 && args.beta != 0.0) {
+      // pull this warp's C sub-tile (WTM x WTN) towards L2 while the mainloop runs
+      const int64_t pm0 = (int64_t)tm * BM + wm * Cfg::WTM;
+      const int64_t pn0 = (int64_t)tn * BN + wn * Cfg::WTN;
+      constexpr int kLinesPerCol = (Cfg::WTM * 8 + 127) / 128;
+      for (int q = lane; q < Cfg::WTN * kLinesPerCol; q += 32) {
+        const int64_t n = pn0 + q / kLinesPerCol;
+        const int64_t m = pm0 + (q % kLinesPerCol) * 16;
+        if (n < args.N && m < args.M && m >= 0)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(args.C + n * args.ldc + m));
+      }
+    }
 
     for (int64_t kc = kc_begin; kc < kc_end; kc++) {
       mbar_wait(&full[stage], phase);
@@ -219,19 +239,20 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
           double af[Cfg::MT][2], bf[Cfg::NT];
 #pragma unroll
           for (int i = 0; i < Cfg::MT; i++) {
-            const int r = wm * Cfg::WTM + i * 16 + g;
             if (A_MMAJOR) {
+              const int r = wm * Cfg::WTM + i * 16 + g;
               const double* a = reinterpret_cast<const double*>(sA);
               af[i][0] = a[(kk + tq) * Cfg::A_LDM + r];
               af[i][1] = a[(kk + tq) * Cfg::A_LDM + r + 8];
             } else {
+              const int r = wm * Cfg::WTM + i * 16 + pg;
               af[i][0] = ld_kmajor((const char*)sA, r, kk + tq);
               af[i][1] = ld_kmajor((const char*)sA, r + 8, kk + tq);
             }
           }
 #pragma unroll
           for (int j = 0; j < Cfg::NT; j++)
-            bf[j] = ld_kmajor((const char*)sB, wn * Cfg::WTN + j * 8 + g, kk + tq);
+            bf[j] = ld_kmajor((const char*)sB, wn * Cfg::WTN + j * 8 + pg, kk + tq);
 #pragma unroll
           for (int i = 0; i < Cfg::MT; i++)
 #pragma unroll
@@ -244,19 +265,20 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
           double af[Cfg::MT][2], bf[Cfg::NT];
 #pragma unroll
           for (int i = 0; i < Cfg::MT; i++) {
-            const int r = wm * Cfg::WTM + i * 16 + g;
             if (A_MMAJOR) {
+              const int r = wm * Cfg::WTM + i * 16 + g;
               const double* a = reinterpret_cast<const double*>(sA);
               af[i][0] = ok ? a[(kk + tq) * Cfg::A_LDM + r] : 0.0;
               af[i][1] = ok ? a[(kk + tq) * Cfg::A_LDM + r + 8] : 0.0;
             } else {
+              const int r = wm * Cfg::WTM + i * 16 + pg;
               af[i][0] = ok ? ld_kmajor((const char*)sA, r, kk + tq) : 0.0;
               af[i][1] = ok ? ld_kmajor((const char*)sA, r + 8, kk + tq) : 0.0;
             }
           }
 #pragma unroll
           for (int j = 0; j < Cfg::NT; j++)
-            bf[j] = ok ? ld_kmajor((const char*)sB, wn * Cfg::WTN + j * 8 + g, kk + tq) : 0.0;
+            bf[j] = ok ? ld_kmajor((const char*)sB, wn * Cfg::WTN + j * 8 + pg, kk + tq) : 0.0;
 #pragma unroll
           for (int i = 0; i < Cfg::MT; i++)
 #pragma unroll
@@ -292,26 +314,37 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
         for (int j = 0; j < Cfg::NT; j++)
 #pragma unroll
           for (int e = 0; e < 4; e++) {
-            const int64_t m = m_base + i * 16 + g + ((e & 2) ? 8 : 0);
-            const int64_t n = n_base + j * 8 + 2 * tq + (e & 1);
+            const int64_t m = m_base + i * 16 + (A_MMAJOR ? g : pg) + ((e & 2) ? 8 : 0);
+            const int64_t n = n_base + j * 8 + perm8(2 * tq + (e & 1));
             if (m < args.M && n < args.N) W[n * args.M + m] = acc[i][j][e];
           }
     } else {
+      // one m16 row block at a time: issue its (NT x 4) C loads together, then store
 #pragma unroll
-      for (int i = 0; i < Cfg::MT; i++)
+      for (int i = 0; i < Cfg::MT; i++) {
+        double cv[Cfg::NT][4];
+        bool okv[Cfg::NT][4];
 #pragma unroll
         for (int j = 0; j < Cfg::NT; j++)
 #pragma unroll
           for (int e = 0; e < 4; e++) {
-            const int64_t m = m_base + i * 16 + g + ((e & 2) ? 8 : 0);
-            const int64_t n = n_base + j * 8 + 2 * tq + (e & 1);
-            if (m < args.M && n < args.N && m >= args.m_lo) {
-              double* c = args.C + n * args.ldc + m;
-              double v = args.alpha * acc[i][j][e];
-              if (args.beta != 0.0) v = fma(args.beta, *c, v);
-              *c = v;
-            }
+            const int64_t m = m_base + i * 16 + (A_MMAJOR ? g : pg) + ((e & 2) ? 8 : 0);
+            const int64_t n = n_base + j * 8 + perm8(2 * tq + (e & 1));
+            okv[j][e] = m < args.M && n < args.N && m >= args.m_lo;
+            cv[j][e] = (okv[j][e] && args.beta != 0.0) ? __ldcg(args.C + n * args.ldc + m) : 0.0;
           }
+#pragma unroll
+        for (int j = 0; j < Cfg::NT; j++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            if (!okv[j][e]) continue;
+            const int64_t m = m_base + i * 16 + (A_MMAJOR ? g : pg) + ((e & 2) ? 8 : 0);
+            const int64_t n = n_base + j * 8 + perm8(2 * tq + (e & 1));
+            double v = args.alpha * acc[i][j][e];
+            if (args.beta != 0.0) v = fma(args.beta, cv[j][e], v);
+            args.C[n * args.ldc + m] = v;
+          }
+      }
     }
   }
 }
@@ -426,7 +459,13 @@ static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launch
   a.kchunks_per_split = (int)ceil_div(a.kchunks, a.splitk);
   a.work = p.work;
   const int64_t units = (int64_t)a.tiles_m * a.tiles_n * a.splitk;
-  const int grid = (int)(units < num_sms() ? units : num_sms());
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    RQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::SMEM));
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t slots = (int64_t)num_sms() * per_sm;
+  const int grid = (int)(units < slots ? units : slots);
   kern<<<grid, Cfg::kThreads, Cfg::SMEM, stream>>>(ma, mb, a);
   {
     cudaError_t e = cudaGetLastError();
@@ -500,6 +539,15 @@ int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches) {
   // Tile selection: skinny outputs use narrower tiles so the grid fills 148 SMs;
   // M in (128, 144] or (256, 288] (the b+p sketch rows) uses 144-row tiles.
   const bool m144 = (p.M > 128 && p.M <= 144) || (p.M > 256 && p.M <= 288);
+  static int big = -1;  // RQ_GEMM_BIG=1: 128x64 tiles, 2 CTAs/SM, for large outputs (tuning switch)
+  if (big < 0) {
+    const char* e = getenv("RQ_GEMM_BIG");
+    big = e ? atoi(e) : 0;
+  }
+  if (big == 1 && p.M >= 128 && p.N >= 128) {
+    if (p.a_mmajor) return launch_auto<128, 64, 2, 2, true, 4>(p, stream, launches);
+    if (!m144) return launch_auto<128, 64, 2, 2, false, 4>(p, stream, launches);
+  }
   if (p.a_mmajor) {
     if (p.M >= 128 && p.N >= 128) return launch_auto<128, 128, 2, 4, true, 4>(p, stream, launches);
     if (p.N < 128) return launch_auto<128, 32, 4, 2, true, 6>(p, stream, launches);

@@ -12,43 +12,69 @@ namespace rq {
 // ---------------------------------------------------------------------------
 // T = (I/2 + striu(V^T V))^{-1}: the compact-WY factor of U = H_0...H_{k-1}
 // with H_j = I - 2 u_j u_j^T (same T as the wy_accumulate recurrence,
-// householder.py:91-102).  One warp per column, back substitution
-//   t_j = 2,  t_i = -2 sum_{k=i+1..j} G_ik t_k.
-// G is symmetric, so row i is read contiguously as column i.
+// householder.py:91-102).  One warp per column j, right-looking:
+//   for kk = j..0:  t_kk = (kk == j) ? 2 : -2 acc_kk;  acc_i += G(i, kk) t_kk (i < kk)
+// so each step is an axpy with the contiguous column G(:, kk); the loads do not
+// depend on the recurrence and are issued one step ahead.  acc lives in
+// registers (lane l owns rows l, l+32, ...).
 // ---------------------------------------------------------------------------
-__global__ void tinv_kernel(const double* __restrict__ G, int64_t ldg, int k, double* __restrict__ T,
-                            int64_t ldt) {
-  extern __shared__ double tcol[];  // per warp: k doubles
+template <int RPL>
+__global__ void tinv_kernel(const double* __restrict__ G, int64_t ldg, int k, double* __restrict__ T, int64_t ldt) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + warp;
   if (j >= k) return;
-  double* t = tcol + (int64_t)warp * k;
-  for (int i = lane; i < k; i += 32) t[i] = 0.0;
-  __syncwarp();
-  if (lane == 0) t[j] = 2.0;
-  __syncwarp();
-  for (int i = j - 1; i >= 0; i--) {
-    const double* gi = G + (int64_t)i * ldg;  // G(:, i) == G(i, :)
-    double acc = 0.0;
-    for (int kk = i + 1 + lane; kk <= j; kk += 32) acc += gi[kk] * t[kk];
-    acc = warp_sum(acc);
-    if (lane == 0) t[i] = -2.0 * acc;
-    __syncwarp();
+  double acc[RPL], t[RPL];
+#pragma unroll
+  for (int r = 0; r < RPL; r++) {
+    acc[r] = 0.0;
+    t[r] = 0.0;
   }
-  for (int i = lane; i < k; i += 32) T[(int64_t)j * ldt + i] = t[i];
+  double g[RPL];
+#pragma unroll
+  for (int r = 0; r < RPL; r++) {
+    const int i = lane + 32 * r;
+    g[r] = (i < j) ? __ldg(G + (int64_t)j * ldg + i) : 0.0;
+  }
+  for (int kk = j; kk >= 0; kk--) {
+    // prefetch column kk-1 while this step completes
+    double gn[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; r++) {
+      const int i = lane + 32 * r;
+      gn[r] = (kk > 0 && i < kk - 1) ? __ldg(G + (int64_t)(kk - 1) * ldg + i) : 0.0;
+    }
+    // t_kk from acc_kk (held by lane kk % 32, slot kk / 32)
+    double sel = 0.0;
+    const int rk = kk >> 5;
+#pragma unroll
+    for (int r = 0; r < RPL; r++) sel = (r == rk) ? acc[r] : sel;
+    const double a = __shfl_sync(0xffffffffu, sel, kk & 31);
+    const double tk = (kk == j) ? 2.0 : -2.0 * a;
+#pragma unroll
+    for (int r = 0; r < RPL; r++) {
+      const int i = lane + 32 * r;
+      if (i == kk) t[r] = tk;
+      acc[r] = fma(g[r], tk, acc[r]);  // g is zero for i >= kk
+      g[r] = gn[r];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPL; r++) {
+    const int i = lane + 32 * r;
+    if (i < k) T[(int64_t)j * ldt + i] = (i <= j) ? t[r] : 0.0;
+  }
 }
 
 int tfactor_from_gram(const double* G, int64_t ldg, int k, double* T, int64_t ldt, cudaStream_t st,
                       int64_t* launches) {
   if (k <= 0) return RQ_OK;
-  const int wpb = 8;
-  const size_t smem = (size_t)wpb * k * sizeof(double);
-  static size_t set = 0;
-  if (smem > 48 * 1024 && smem > set) {
-    RQ_CUDA_TRY(cudaFuncSetAttribute(tinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    set = smem;
-  }
-  tinv_kernel<<<(unsigned)ceil_div(k, wpb), wpb * 32, smem, st>>>(G, ldg, k, T, ldt);
+  const int wpb = 4;
+  const unsigned blocks = (unsigned)ceil_div(k, wpb);
+  if (k <= 64) tinv_kernel<2><<<blocks, wpb * 32, 0, st>>>(G, ldg, k, T, ldt);
+  else if (k <= 128) tinv_kernel<4><<<blocks, wpb * 32, 0, st>>>(G, ldg, k, T, ldt);
+  else if (k <= 256) tinv_kernel<8><<<blocks, wpb * 32, 0, st>>>(G, ldg, k, T, ldt);
+  else if (k <= 512) tinv_kernel<16><<<blocks, wpb * 32, 0, st>>>(G, ldg, k, T, ldt);
+  else return set_error(RQ_EUNSUPPORTED, "T factor for more than 512 reflectors");
   RQ_CUDA_TRY(cudaGetLastError());
   if (launches) (*launches)++;
   return RQ_OK;

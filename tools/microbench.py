@@ -121,3 +121,40 @@ if "skstamps" in which:
     for k, nm in enumerate(names):
         print(f"  {nm:20s} {int(np.median(d[:, k])):6d}")
     print("  step total          ", int(np.median(h[6:60, 0] - h[5:59, 0])))
+
+if "gemm" in which:
+    def gemm_case(mm, M, N, K, label):
+        A = torch.randn((K, M) if not mm else (M, K), dtype=torch.float64, device=eng.device)
+        B = torch.randn((K, N), dtype=torch.float64, device=eng.device)
+        C = torch.randn((M, N), dtype=torch.float64, device=eng.device)
+        # column-major views: storage (cols, rows)
+        As = A.T.contiguous() if False else A  # storage as (cols, ld)
+        a_rows, a_cols = (M, K) if mm else (K, M)
+        abuf, lda = eng.alloc_matrix(a_rows, a_cols)
+        bbuf, ldb = eng.alloc_matrix(K, N)
+        cbuf, ldc = eng.alloc_matrix(M, N)
+        abuf.normal_(); bbuf.normal_(); cbuf.normal_()
+
+        def run():
+            check(lib.rq_test_gemm(eng.handle, int(mm), M, N, K, ctypes.c_void_p(abuf.data_ptr()), lda, a_rows, a_cols,
+                                   0, 0, ctypes.c_void_p(bbuf.data_ptr()), ldb, K, N, 0, 0,
+                                   ctypes.c_void_p(cbuf.data_ptr()), ldc, -1.0, 1.0))
+        ms = timeit(run, reps=5)
+        print(f"gemm {label:28s} M={M} N={N} K={K}: {ms*1e3:8.0f} us  {2*M*N*K/ms/1e9:6.2f} TF/s")
+    gemm_case(1, 10000, 10000, 256, "NN  A2 -= V W2")
+    gemm_case(0, 256, 10000, 10000, "TN  W = V^T A2")
+    gemm_case(0, 272, 10000, 10000, "TN  Yt = Om^T X (sketch)")
+    gemm_case(0, 256, 256, 10000, "TN  Gram V^T V")
+    gemm_case(1, 5000, 5000, 256, "NN  half size")
+    gemm_case(0, 4096, 4096, 4096, "TN  square 4096")
+if "gemm_nn" in which:
+    M, N, K = 10000, 10000, 256
+    abuf, lda = eng.alloc_matrix(M, K)
+    bbuf, ldb = eng.alloc_matrix(K, N)
+    cbuf, ldc = eng.alloc_matrix(M, N)
+    abuf.normal_(); bbuf.normal_(); cbuf.normal_()
+    for _ in range(2):
+        check(lib.rq_test_gemm(eng.handle, 1, M, N, K, ctypes.c_void_p(abuf.data_ptr()), lda, M, K, 0, 0,
+                               ctypes.c_void_p(bbuf.data_ptr()), ldb, K, N, 0, 0, ctypes.c_void_p(cbuf.data_ptr()),
+                               ldc, -1.0, 1.0))
+    torch.cuda.synchronize()
