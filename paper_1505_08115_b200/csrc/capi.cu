@@ -265,6 +265,9 @@ int rq_test_leaf_qr(rq_ctx* ctx, double* dA, int64_t lda, int64_t mm, int32_t w,
 }
 
 int rq_test_debug_timing(int32_t on, uint64_t* host, int32_t count) {
+  // on: 1 = cluster/sketch sweeps, 2 = panel leaf
+  if (on == 2 || (on == 0 && count < 0)) return rq::leaf_debug_timing(on == 2, (unsigned long long*)host, -count);
+  RQ_TRY(rq::leaf_debug_timing(0, nullptr, 0));
   return rq::sweep_debug_timing(on, (unsigned long long*)host, count);
 }
 

@@ -253,7 +253,8 @@ int Ctx::sweep_raw(SweepCall c) {
 // ---------------------------------------------------------------------------
 int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, double* V, int64_t ldv,
                   int vpad, double* tleaf, double* w1, double* w2) {
-  const int wl_max = leaf_width_for(mp);
+  int wl_max = leaf_reg_width_for(mp);
+  if (wl_max == 0) wl_max = leaf_width_for(mp);
   if (wl_max == 0) return set_error(RQ_EUNSUPPORTED, "panel of %lld rows exceeds the leaf kernel", (long long)mp);
   const int wl = std::min(wl_max, 32);
   for (int k0 = 0; k0 < b; k0 += wl) {

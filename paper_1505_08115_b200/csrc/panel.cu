@@ -213,6 +213,260 @@ __global__ void __launch_bounds__(PL_THREADS) leaf_qr_kernel(double* __restrict_
   cluster_sync_all();  // keep DSMEM alive until every CTA finished reading
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident leaf: thread t of CTA r owns leaf rows r*rows_per + t + 256*q
+// (q < RPT) for all WL (<= 16) columns in registers.  Per column j the CTA
+// reduces 32 partial sums [tail, dots(c = j+o), gram(k < j-1)] (two 16-value
+// warp reduce-scatters + one smem pass), pushes them into every cluster peer,
+// and after ONE cluster barrier warp 0 derives the reflector coefficients from
+// the 16 pushed vectors (summed in rank order: deterministic) into smem.
+// ---------------------------------------------------------------------------
+__device__ unsigned long long g_leaf_dbg[64 * 8];
+__device__ int g_leaf_dbg_on;
+RQ_DEV void leaf_stamp(int j, int k) {
+  if (g_leaf_dbg_on && j < 64 && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    g_leaf_dbg[j * 8 + k] = c;
+  }
+}
+int leaf_debug_timing(int on, unsigned long long* host, int count) {
+  RQ_CUDA_TRY(cudaMemcpyToSymbol(g_leaf_dbg_on, &on, sizeof(int)));
+  if (host) RQ_CUDA_TRY(cudaMemcpyFromSymbol(host, g_leaf_dbg, sizeof(unsigned long long) * (count < 512 ? count : 512)));
+  return RQ_OK;
+}
+
+constexpr int LR_THREADS = 256;
+constexpr int LR_WARPS = LR_THREADS / 32;
+
+// 16 values per lane -> lane l holds the warp sum of value (l & 15).
+RQ_DEV double warp_reduce_scatter16(double (&v)[16], int lane) {
+#pragma unroll
+  for (int half = 8; half >= 1; half >>= 1) {
+    const bool upper = (lane & half) != 0;
+#pragma unroll
+    for (int k = 0; k < half; k++) {
+      const double send = upper ? v[k] : v[k + half];
+      const double recv = __shfl_xor_sync(0xffffffffu, send, half);
+      v[k] = (upper ? v[k + half] : v[k]) + recv;
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
+template <int WL, int RPT>
+__global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restrict__ a, int64_t lda, int64_t mm, int w,
+                                                                 double* __restrict__ v, int64_t ldv,
+                                                                 double* __restrict__ tl, int64_t ldt, int rows_per) {
+  static_assert(WL <= 16, "leaf width");
+  extern __shared__ double Vs[];                  // [WL][RPT*LR_THREADS] own rows of V (lane-contiguous)
+  constexpr int VLD = RPT * LR_THREADS;
+  __shared__ double wpart[LR_WARPS][32];
+  __shared__ double pin[2][16][32];               // pushed CTA partials, by step parity
+  __shared__ double rowj[16];                     // row j of this CTA (if it owns it), window order
+  __shared__ double sc[16];                       // reflector coefficients, window order (o = c - j)
+  __shared__ double scal[4];                      // refl, beta, h*inv, inv
+  __shared__ double Ts[16][17];
+  const unsigned CS = gridDim.x;
+  const unsigned rank = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)rank * rows_per;
+
+  // register window: x[q][o] holds column j + o of own row q (active column at o = 0)
+  double x[RPT][WL];
+  int64_t grow[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; q++) {
+    const int lr = threadIdx.x + LR_THREADS * q;
+    grow[q] = (lr < rows_per) ? r0 + lr : mm;  // rows beyond mm are inert
+#pragma unroll
+    for (int c = 0; c < WL; c++) {
+      x[q][c] = (grow[q] < mm && c < w) ? a[(int64_t)c * lda + grow[q]] : 0.0;
+      Vs[c * VLD + lr] = 0.0;
+    }
+  }
+  for (int e = threadIdx.x; e < 16 * 17; e += LR_THREADS) (&Ts[0][0])[e] = 0.0;
+  double uprev[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; q++) uprev[q] = 0.0;
+  bool refl_prev = false;
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+
+  for (int j = 0; j <= w; j++) {
+    const bool final_round = (j == w);
+    const int par = j & 1;
+    leaf_stamp(j, 0);
+    // ---- apply the pending reflector j-1 to the window (columns j..) ----
+    if (refl_prev && !final_round) {
+      double s[WL];
+#pragma unroll
+      for (int o = 0; o < WL; o++) s[o] = sc[o];
+#pragma unroll
+      for (int q = 0; q < RPT; q++)
+#pragma unroll
+        for (int o = 0; o < WL; o++) x[q][o] -= s[o] * uprev[q];
+    }
+    // ---- partials: dv[o] = sum x_j x_{j+o} (o = 0: tail), gv[k] = V_k . u_{j-1} ----
+    double dv[16], gv[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+      dv[e] = 0.0;
+      gv[e] = 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; q++) {
+      if (grow[q] > j && grow[q] < mm && !final_round) {
+#pragma unroll
+        for (int o = 0; o < WL; o++) dv[o] += x[q][0] * x[q][o];
+      }
+      if (j >= 2) {
+        const int lr = threadIdx.x + LR_THREADS * q;
+#pragma unroll
+        for (int k = 0; k < WL; k++)
+          if (k < j - 1) gv[k] += Vs[k * VLD + lr] * uprev[q];
+      }
+      if (grow[q] == j && !final_round)
+#pragma unroll
+        for (int o = 0; o < WL; o++) rowj[o] = x[q][o];
+    }
+    leaf_stamp(j, 1);
+    const double dsum = warp_reduce_scatter16(dv, lane);
+    const double gsum = warp_reduce_scatter16(gv, lane);
+    if (lane < 16) {
+      wpart[warp][lane] = dsum;
+      wpart[warp][16 + lane] = gsum;
+    }
+    leaf_stamp(j, 2);
+    __syncthreads();
+    leaf_stamp(j, 3);
+    {
+      // every warp forms the CTA sum of slot `lane` (same order: identical values) and
+      // pushes it to destinations warp, warp + 8: the remote stores are spread over all threads
+      double sum = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < LR_WARPS; ww++) sum += wpart[ww][lane];
+      for (unsigned dst = warp; dst < CS; dst += LR_WARPS) dsmem_st(&pin[par][rank][lane], dst, sum);
+    }
+    leaf_stamp(j, 4);
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    leaf_stamp(j, 5);
+    if (warp == 0) {
+      double t = 0.0;
+      for (unsigned r = 0; r < CS; r++) t += pin[par][r][lane];  // rank order
+      // T column j-1 from the Gram totals (lanes 16.. hold gram k = lane - 16)
+      if (j >= 1) {
+        const int jc = j - 1;
+        double tcol = 0.0;
+        for (int k = jc - 1; k >= 0; k--) {
+          const double g = __shfl_sync(0xffffffffu, t, 16 + k);
+          if (lane <= k) tcol += Ts[lane][k] * g;
+        }
+        if (lane < jc) Ts[lane][jc] = -2.0 * tcol;
+        if (lane == 0) Ts[jc][jc] = 2.0;
+      }
+      if (!final_round) {
+        // row j entries (window order) from the CTA that owns row j
+        const unsigned jrank = (unsigned)(j / rows_per);
+        const double rj = (lane < 16 && j + lane < w) ? dsmem_ld(&rowj[lane], jrank) : 0.0;
+        const double tail = __shfl_sync(0xffffffffu, t, 0);
+        const double xjj = __shfl_sync(0xffffffffu, rj, 0);
+        const double normsq = xjj * xjj + tail;
+        const bool refl = (mm - j >= 2) && (normsq != 0.0);
+        double beta = 0.0, inv = 0.0, h = 0.0;
+        if (refl) {
+          const double nrm = sqrt(normsq);
+          beta = (xjj >= 0.0) ? -nrm : nrm;
+          h = beta - xjj;
+          inv = 1.0 / sqrt(h * h + tail);
+        }
+        // coefficient for window slot o = lane (column j + o), dot_o on lane o
+        if (lane < 16)
+          sc[lane] = (refl && lane > 0 && j + lane < w) ? 2.0 * inv * (h * rj - t) : 0.0;
+        if (lane == 0) {
+          scal[0] = refl ? 1.0 : 0.0;
+          scal[1] = beta;
+          scal[2] = h * inv;
+          scal[3] = inv;
+        }
+      }
+    }
+    if (final_round) break;
+    leaf_stamp(j, 6);
+    __syncthreads();
+    leaf_stamp(j, 7);
+    const bool refl = scal[0] != 0.0;
+    const double beta = scal[1], hinv = scal[2], inv = scal[3];
+#pragma unroll
+    for (int q = 0; q < RPT; q++) {
+      const int lr = threadIdx.x + LR_THREADS * q;
+      double ui = 0.0;
+      if (refl && grow[q] < mm) ui = (grow[q] == j) ? hinv : (grow[q] > j ? -x[q][0] * inv : 0.0);
+      uprev[q] = ui;
+      Vs[j * VLD + lr] = ui;
+      // column j is final: write it out and shift the window
+      if (grow[q] < mm) {
+        const double rjv = (refl && grow[q] >= j) ? ((grow[q] == j) ? beta : 0.0) : x[q][0];
+        a[(int64_t)j * lda + grow[q]] = rjv;
+      }
+#pragma unroll
+      for (int o = 0; o + 1 < WL; o++) x[q][o] = x[q][o + 1];
+      x[q][WL - 1] = 0.0;
+    }
+    // the coefficient window shifts with the columns (sc is rewritten next step)
+    refl_prev = refl;
+    if (refl) {
+      __syncthreads();
+      if (threadIdx.x < 16) {
+        const double nxt = (threadIdx.x + 1 < 16) ? sc[threadIdx.x + 1] : 0.0;
+        __syncwarp(0xffffu);
+        sc[threadIdx.x] = nxt;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // write back V (R columns were written as they left the window)
+#pragma unroll
+  for (int q = 0; q < RPT; q++) {
+    const int lr = threadIdx.x + LR_THREADS * q;
+    if (grow[q] < mm)
+      for (int c = 0; c < w; c++) v[(int64_t)c * ldv + grow[q]] = Vs[c * VLD + lr];
+  }
+  if (rank == 0 && tl)
+    for (int e = threadIdx.x; e < w * w; e += LR_THREADS) tl[(int64_t)(e / w) * ldt + e % w] = Ts[e % w][e / w];
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int WL, int RPT>
+static int launch_leaf_reg(const LeafCall& c, cudaStream_t st, int64_t* launches) {
+  const int CS = 16;
+  const int rows_per = (int)ceil_div(c.mm, CS);
+  auto kern = leaf_reg_kernel<WL, RPT>;
+  const size_t dsm = (size_t)RPT * LR_THREADS * WL * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS);
+  cfg.blockDim = dim3(LR_THREADS);
+  cfg.dynamicSmemBytes = dsm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, c.a, c.lda, c.mm, c.w, c.v, c.ldv, c.tl, c.ldt, rows_per));
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
 template <int WL>
 static int launch_leaf(const LeafCall& c, cudaStream_t st, int64_t* launches) {
   constexpr int PV = LeafLayout<WL>::PV;
@@ -257,8 +511,25 @@ int leaf_width_for(int64_t mm) {
   return 0;
 }
 
+// Register-resident leaf width for mm rows (16 CTAs x 256 threads x RPT rows).
+int leaf_reg_width_for(int64_t mm) {
+  const int64_t rows_per = ceil_div(mm, 16);
+  if (rows_per <= 4 * LR_THREADS) return 16;
+  if (rows_per <= 8 * LR_THREADS) return 8;
+  if (rows_per <= 16 * LR_THREADS) return 4;
+  return 0;
+}
+
 int leaf_qr(const LeafCall& c, cudaStream_t st, int64_t* launches) {
   if (c.w <= 0) return RQ_OK;
+  {
+    const int64_t rows_per = ceil_div(c.mm, 16);
+    if (rows_per <= 1 * LR_THREADS && c.w <= 16) return launch_leaf_reg<16, 1>(c, st, launches);
+    if (rows_per <= 2 * LR_THREADS && c.w <= 16) return launch_leaf_reg<16, 2>(c, st, launches);
+    if (rows_per <= 4 * LR_THREADS && c.w <= 16) return launch_leaf_reg<16, 4>(c, st, launches);
+    if (rows_per <= 8 * LR_THREADS && c.w <= 8) return launch_leaf_reg<8, 8>(c, st, launches);
+    if (rows_per <= 16 * LR_THREADS && c.w <= 4) return launch_leaf_reg<4, 16>(c, st, launches);
+  }
   if (c.w <= 4 && leaf_width_for(c.mm) >= 4) return launch_leaf<4>(c, st, launches);
   if (c.w <= 8 && leaf_width_for(c.mm) >= 8) return launch_leaf<8>(c, st, launches);
   if (c.w <= 16 && leaf_width_for(c.mm) >= 16) return launch_leaf<16>(c, st, launches);

@@ -16,6 +16,8 @@ struct LeafCall {
 };
 
 int leaf_width_for(int64_t mm);
+int leaf_reg_width_for(int64_t mm);
+int leaf_debug_timing(int on, unsigned long long* host, int count);
 int leaf_qr(const LeafCall& c, cudaStream_t st, int64_t* launches);
 
 }  // namespace rq

@@ -158,3 +158,33 @@ if "gemm_nn" in which:
                                ctypes.c_void_p(bbuf.data_ptr()), ldb, K, N, 0, 0, ctypes.c_void_p(cbuf.data_ptr()),
                                ldc, -1.0, 1.0))
     torch.cuda.synchronize()
+
+if "leafstamps" in which:
+    mm, w = int(os.environ.get("LEAFM", "10000")), 16
+    a0 = rng.standard_normal((mm, w))
+    buf, ld = dev(a0)
+    v, ldv = eng.alloc_matrix(mm, w)
+    t, ldt = eng.alloc_matrix(32, 32)
+    check(lib.rq_test_debug_timing(2, None, 0))
+    check(lib.rq_test_leaf_qr(eng.handle, ctypes.c_void_p(buf.data_ptr()), ld, mm, w,
+                              ctypes.c_void_p(v.data_ptr()), ldv, ctypes.c_void_p(t.data_ptr()), ldt))
+    torch.cuda.synchronize()
+    h = np.zeros(512, dtype=np.uint64)
+    check(lib.rq_test_debug_timing(0, h.ctypes.data_as(ctypes.c_void_p), -512))
+    h = h.reshape(64, 8).astype(np.int64)
+    d = np.diff(h[2:14], axis=1)
+    names = ["apply+partials", "reduce-scatter", "sync", "cta sum+push", "cluster barrier", "T+reflector(w0)", "sync"]
+    print(f"leaf phase cycles mm={mm} w={w} (median over columns 2..13):")
+    for k, nm in enumerate(names):
+        print(f"  {nm:18s} {int(np.median(d[:, k])):6d}")
+    print("  column total      ", int(np.median(h[3:14, 0] - h[2:13, 0])))
+if "leaf1" in which:
+    mm, w = int(os.environ.get("LEAFM", "10000")), 16
+    a0 = rng.standard_normal((mm, w))
+    buf, ld = dev(a0)
+    v, ldv = eng.alloc_matrix(mm, w)
+    t, ldt = eng.alloc_matrix(32, 32)
+    for _ in range(2):
+        check(lib.rq_test_leaf_qr(eng.handle, ctypes.c_void_p(buf.data_ptr()), ld, mm, w,
+                                  ctypes.c_void_p(v.data_ptr()), ldv, ctypes.c_void_p(t.data_ptr()), ldt))
+    torch.cuda.synchronize()
