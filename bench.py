@@ -171,6 +171,9 @@ def main():
     ap.add_argument("--cpu-panels", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sketch", default="fresh", choices=["fresh", "downdate"],
+                    help="headline sketch mode (fresh = reference semantics)")
+    ap.add_argument("--no-variant", action="store_true", help="skip timing the other sketch mode")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -204,7 +207,8 @@ def main():
         a0, ld = rq.gaussian_matrix_device(m, n, rq.RngState(0), engine=eng)
         work, _ = eng.alloc_matrix(m, n)
         perm = torch.empty(n, dtype=torch.int64, device=eng.device)
-    cfg = _lib.rq_config(b, p, 0, -1, 0, 0, _lib.RQ_SKETCH_FRESH, 0)
+    mode = _lib.RQ_SKETCH_FRESH if args.sketch == "fresh" else _lib.RQ_SKETCH_DOWNDATE
+    cfg = _lib.rq_config(b, p, 0, -1, 0, 0, mode, 0)
 
     def step():
         with torch.cuda.stream(stream):
@@ -248,6 +252,23 @@ def main():
         ms_max = float(tt.item())
     flops_step = 4.0 / 3.0 * n ** 3
     value = world * args.steps * flops_step / (ms_max * 1e-3) / 1e12
+
+    # the other sketch mode, same workload (reported beside the headline)
+    variant = None
+    if not args.no_variant:
+        other = "downdate" if args.sketch == "fresh" else "fresh"
+        cfg.sketch_mode = _lib.RQ_SKETCH_DOWNDATE if other == "downdate" else _lib.RQ_SKETCH_FRESH
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        vms = ev0.elapsed_time(ev1) / args.steps
+        variant = {"sketch": other, "value": flops_step / (vms * 1e-3) / 1e12, "ms_per_step": vms}
+        cfg.sketch_mode = mode
 
     # dominant kernel roofline: the trailing-update DMMA GEMMs
     t_trail = cats["trailing_gemm"]["ms"]
@@ -294,8 +315,9 @@ def main():
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg3 HQRRP fp64 n={n} b={b} p={p} q=0, fresh sketch (reference semantics)",
-                       "n": n, "b": b, "p": p, "q": 0, "sketch": "fresh",
+            "config": {"workload": f"cfg3 HQRRP fp64 n={n} b={b} p={p} q=0, {args.sketch} sketch"
+                                   + (" (reference semantics)" if args.sketch == "fresh" else " (HQRRP downdate)"),
+                       "n": n, "b": b, "p": p, "q": 0, "sketch": args.sketch,
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "inputs (800 MB) larger than L2 (126 MB)"},
             "fraction_of_fp64_peak": value / FP64_PEAK_TFLOPS,
@@ -304,6 +326,7 @@ def main():
                          "kernel": "gemm_f64_kernel (trailing update: V^T A2, T^T W, A2 -= V W2, Q2^T top)",
                          "peak_source": "measured DMMA peak, profiles/probe_r01.jsonl"},
             "breakdown_ms_per_step": cats,
+            "variant": variant,
             "clocks": clk,
             "gpu_launches": launches,
             "e2e": e2e,

@@ -536,6 +536,59 @@ def block_qr(a, cfg, rng, inspect=None, max_panels=None):
     return f
 
 
+def block_qr_downdate(a, cfg, rng):
+    """HQRRP downdated-sketch variant of block_qr (NOT in the reference package).
+
+    Oracle for the B200 ``sketch="downdate"`` mode, restating the HQRRP
+    downdate (Martinsson et al., SURVEY §8 "Two sketch modes"): G = Omega^T
+    is drawn once (gaussian_matrix(m, b+p), counter += m(b+p)), Y = G A, and
+    after each panel Y2 <- Y2 - G1 R12 with G1 = Y1 R11^{-1}, the sketch
+    columns following every column move.  Pivot selection, the two-stage panel
+    and the trailing update are those of block_qr (blocked.py:175-219).
+    """
+    from scipy.linalg import solve_triangular
+
+    work = _check_input(a, cfg)
+    m, n = work.shape
+    b = cfg.block
+    s_cfg = cfg.resolved_sketch()
+    wdt = b + s_cfg.oversample
+    f = Factorization(m, n, b, "perm_pivot")
+    yt = None
+    if n > b:
+        omega = gaussian_matrix(m, wdt, rng)
+        yt = omega.T @ work
+    start = 0
+    while start < n:
+        if n - start <= b:
+            res = qr_column_pivoted(work[start:, start:])
+            work[:start, start:] = work[:start, start:][:, res.perm]
+            work[start:, start:] = res.r
+            f.q_transforms.append((start, res.q, None))
+            f.p_transforms.append((start, PermPivot(res.perm)))
+            break
+        if wdt > n - start:
+            raise ValueError(f"sketch width {wdt} exceeds the {n - start} columns being pivoted")
+        pivot = select_pivot_permutation(yt[:, start:].T, b)
+        work[:, start:] = pivot.apply_right(work[:, start:])
+        yt[:, start:] = yt[:, start:][:, pivot.order]
+        res = qr_tall_pivoted(work[start:, start: start + b])
+        work[:start, start: start + b] = work[:start, start: start + b][:, res.perm]
+        yt[:, start: start + b] = yt[:, start: start + b][:, res.perm]
+        work[start:, start: start + b] = res.r
+        work[start:, start + b:] = apply_wy_left(res.q, work[start:, start + b:], transposed=True)
+        r11 = work[start: start + b, start: start + b]
+        r12 = work[start: start + b, start + b:]
+        g1 = solve_triangular(r11.T, yt[:, start: start + b].T, lower=True).T  # Y1 R11^{-1}
+        yt[:, start + b:] -= g1 @ r12
+        f.q_transforms.append((start, res.q, None))
+        f.p_transforms.append((start, pivot))
+        f.p_transforms.append((start, PermPivot(res.perm)))
+        start += b
+    f.r = work
+    return f
+
+
 def panel_svd(panel):
     """Unpivoted QR then Jacobi SVD of the triangle (blocked.py:222-236); returns (wy, u', d, v)."""
     panel = np.asarray(panel, dtype=np.float64)

@@ -89,7 +89,9 @@ static Layout plan_layout(void* base, int64_t m, int64_t n, int b, int p, int po
   L.ttop = c.take<double>((size_t)ldb * n);
   L.gram = c.take<double>((size_t)ldb * b);
   L.tleaf = c.take<double>(32 * 32);
-  L.ybuf = power > 0 ? c.take<double>((size_t)even(n) * wdt) : nullptr;
+  L.rinv = c.take<double>((size_t)ldb * b);
+  L.g1 = c.take<double>((size_t)even(wdt) * b);
+  L.ybuf = c.take<double>((size_t)std::max<int64_t>(even(n) * wdt, (int64_t)L.ldy * n));
   // split-K slabs: up to 16 splits of the (b+p+1) x n sketch, or 148 of the b x b Gram
   L.kwork_bytes = std::max<size_t>((size_t)kSMs * (b + 1) * b * 8, (size_t)16 * (wdt + 1) * n * 8);
   L.kwork = c.take<double>(L.kwork_bytes / 8);
@@ -348,6 +350,13 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
   Carver fc(L.fstore);
   double* tleaf = L.tleaf;
 
+  const bool downdate = cfg.sketch_mode == RQ_SKETCH_DOWNDATE;
+  if (downdate && n > b) {
+    // HQRRP: G = Omega^T drawn once (m(b+p) normals), Y = G A; downdated per panel
+    RQ_TRY(gaussian_fill(L.omega, m, wdt, L.ldo, seed, *counter, stream, &launches));
+    *counter += (uint64_t)m * (uint64_t)wdt;
+    RQ_TRY(gemm(wdt, n, m, op(L.omega, m, wdt, L.ldo), false, op(A, m, n, lda, 0, 0), L.yt, L.ldy, 1.0, 0.0));
+  }
   int panel = 0;
   for (int64_t s = 0; s < n; s += b) {
     panel++;
@@ -395,17 +404,28 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       }
       break;
     }
-    // ---------------- 1-2: sketch Y^T = Omega^T X ----------------
-    RQ_TRY(gaussian_fill(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
-    *counter += (uint64_t)mp * (uint64_t)wdt;
-    RQ_TRY(sketch(cfg, A, lda, m, n, s, mp, np, L));
+    // ---------------- 1-2: sketch Y^T = Omega^T X (fresh) or the downdated Y (HQRRP) ----------------
+    double* ycur = L.yt;
+    if (!downdate) {
+      RQ_TRY(gaussian_fill(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
+      *counter += (uint64_t)mp * (uint64_t)wdt;
+      RQ_TRY(sketch(cfg, A, lda, m, n, s, mp, np, L));
+    } else {
+      ycur = L.yt + s * L.ldy;
+      // the CPQR overwrites its input: work on a copy of the trailing sketch columns
+      RQ_TRY(copy2d(ycur, L.ldy, L.ybuf, L.ldy, wdt, np, 0, stream, &launches));
+    }
     // ---------------- 3: b-step CPQR of Y^T ----------------
-    RQ_TRY(sketch_select(L.yt, L.ldy, wdt, (int)np, b, rank, L.cap));
+    RQ_TRY(sketch_select(downdate ? L.ybuf : L.yt, L.ldy, wdt, (int)np, b, rank, L.cap));
     // ---------------- 4: move the chosen columns into the panel ----------------
     PlanCall pc{L.cap, b, lorder, (int)np, L.flag, L.newloc, L.src, L.dst, L.nmoves, lorder_n, rank_n};
     RQ_TRY(plan_moves(pc, stream, &launches));
     MoveCall mv{A, lda, s, 0, m, L.src, L.dst, L.nmoves, 2 * b, L.stage, even(m), L.orig, L.ostage};
     RQ_TRY(move_columns(mv, stream, &launches));
+    if (downdate) {  // the sketch columns follow their matrix columns
+      MoveCall my{L.yt, L.ldy, s, 0, wdt, L.src, L.dst, L.nmoves, 2 * b, L.stage, L.ldy, nullptr, nullptr};
+      RQ_TRY(move_columns(my, stream, &launches));
+    }
     // ---------------- 5: unpivoted panel QR ----------------
     const int64_t ldv = even(mp + 1), ldt = even(b);
     const int vpad = (int)(s & 1);
@@ -440,11 +460,23 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     RQ_TRY(copy2d(L.rfin, L.lds_small, A + s + s * lda, lda, b, b, 0, stream, &launches));
     MoveCall mv2{A, lda, s, 0, s, L.cap, L.iota_b, nullptr, b, L.stage, even(m), L.orig, L.ostage};
     RQ_TRY(move_columns(mv2, stream, &launches));
+    if (downdate) {  // P-hat on the sketch's panel columns
+      MoveCall my2{L.yt, L.ldy, s, 0, wdt, L.cap, L.iota_b, nullptr, b, L.stage, L.ldy, nullptr, nullptr};
+      RQ_TRY(move_columns(my2, stream, &launches));
+    }
     // ---------------- 8: T of the panel reflectors ----------------
     RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
     // ---------------- 9: trailing update ----------------
     const int64_t n2 = np - b;
     if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L));
+    if (downdate && n2 > 0) {
+      // Y2 <- Y2 - G1 R12 with G1 = Y1 R11^{-1}: the sketch of the new trailing block
+      const int64_t ldb2 = even(b), ldg = even(wdt);
+      RQ_TRY(trinv_upper(A + s + s * lda, lda, b, L.rinv, ldb2, stream, &launches));
+      RQ_TRY(gemm(wdt, b, b, op(L.yt, wdt, n, L.ldy, 0, s), true, op(L.rinv, b, b, ldb2), L.g1, ldg, 1.0, 0.0));
+      RQ_TRY(gemm(wdt, n2, b, op(L.g1, wdt, b, ldg), true, op(A, m, n, lda, s, s + b), L.yt + (s + b) * L.ldy,
+                  L.ldy, -1.0, 1.0));
+    }
     factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2, ldt});
     std::swap(lorder, lorder_n);
     std::swap(rank, rank_n);

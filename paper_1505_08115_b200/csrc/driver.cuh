@@ -19,7 +19,7 @@ struct Arena {
 
 struct Layout {
   // scratch
-  double *omega, *yt, *w1, *w2, *gram, *tleaf, *ybuf, *kwork, *small, *rfin, *stage, *ttop;
+  double *omega, *yt, *w1, *w2, *gram, *tleaf, *ybuf, *kwork, *small, *rfin, *stage, *ttop, *rinv, *g1;
   int64_t ldo, ldy, lds_small;
   int *chosen, *lorderA, *lorderB, *rankA, *rankB, *newloc, *src, *dst, *nmoves, *cap, *iota_b;
   unsigned char* flag;

@@ -65,6 +65,75 @@ __global__ void tinv_kernel(const double* __restrict__ G, int64_t ldg, int k, do
   }
 }
 
+// Inverse of an upper-triangular k x k matrix R (column-major), one warp per
+// column, right-looking back substitution (same structure as tinv_kernel).
+// Exactly-zero pivots (exactly rank-deficient input) give zero rows/columns,
+// i.e. a generalised inverse, so the downdated sketch stays finite.
+template <int RPL>
+__global__ void trinv_upper_kernel(const double* __restrict__ R, int64_t ldr, int k, double* __restrict__ X,
+                                   int64_t ldx) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (j >= k) return;
+  double acc[RPL], xv[RPL], g[RPL];
+#pragma unroll
+  for (int r = 0; r < RPL; r++) {
+    acc[r] = 0.0;
+    xv[r] = 0.0;
+  }
+  // x_kk = (delta_kj - acc_kk) / R_kk ;  acc_i += R(i, kk) x_kk  (i < kk)
+#pragma unroll
+  for (int r = 0; r < RPL; r++) {
+    const int i = lane + 32 * r;
+    g[r] = (i <= j) ? __ldg(R + (int64_t)j * ldr + i) : 0.0;
+  }
+  for (int kk = j; kk >= 0; kk--) {
+    double gn[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; r++) {
+      const int i = lane + 32 * r;
+      gn[r] = (kk > 0 && i <= kk - 1) ? __ldg(R + (int64_t)(kk - 1) * ldr + i) : 0.0;
+    }
+    double sa = 0.0, sd = 0.0;
+    const int rk = kk >> 5;
+#pragma unroll
+    for (int r = 0; r < RPL; r++) {
+      sa = (r == rk) ? acc[r] : sa;
+      sd = (r == rk) ? g[r] : sd;  // diagonal R_kk sits in column kk at row kk
+    }
+    const double a = __shfl_sync(0xffffffffu, sa, kk & 31);
+    const double d = __shfl_sync(0xffffffffu, sd, kk & 31);
+    const double rhs = ((kk == j) ? 1.0 : 0.0) - a;
+    const double xk = (d != 0.0) ? rhs / d : 0.0;
+#pragma unroll
+    for (int r = 0; r < RPL; r++) {
+      const int i = lane + 32 * r;
+      if (i == kk) xv[r] = xk;
+      if (i < kk) acc[r] = fma(g[r], xk, acc[r]);
+      g[r] = gn[r];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPL; r++) {
+    const int i = lane + 32 * r;
+    if (i < k) X[(int64_t)j * ldx + i] = (i <= j) ? xv[r] : 0.0;
+  }
+}
+
+int trinv_upper(const double* R, int64_t ldr, int k, double* X, int64_t ldx, cudaStream_t st, int64_t* launches) {
+  if (k <= 0) return RQ_OK;
+  const int wpb = 4;
+  const unsigned blocks = (unsigned)ceil_div(k, wpb);
+  if (k <= 64) trinv_upper_kernel<2><<<blocks, wpb * 32, 0, st>>>(R, ldr, k, X, ldx);
+  else if (k <= 128) trinv_upper_kernel<4><<<blocks, wpb * 32, 0, st>>>(R, ldr, k, X, ldx);
+  else if (k <= 256) trinv_upper_kernel<8><<<blocks, wpb * 32, 0, st>>>(R, ldr, k, X, ldx);
+  else if (k <= 512) trinv_upper_kernel<16><<<blocks, wpb * 32, 0, st>>>(R, ldr, k, X, ldx);
+  else return set_error(RQ_EUNSUPPORTED, "triangular inverse for more than 512 columns");
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
 int tfactor_from_gram(const double* G, int64_t ldg, int k, double* T, int64_t ldt, cudaStream_t st,
                       int64_t* launches) {
   if (k <= 0) return RQ_OK;

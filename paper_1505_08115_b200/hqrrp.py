@@ -139,7 +139,7 @@ class Engine:
         return np.asfortranarray(buf[:n, :m].cpu().numpy().T)
 
 
-def _make_config(cfg, rrqr):
+def _make_config(cfg, rrqr, sketch="fresh"):
     s = cfg.resolved_sketch()
     c = _lib.rq_config()
     c.block = int(cfg.block)
@@ -148,7 +148,9 @@ def _make_config(cfg, rrqr):
     c.stabilize = -1 if s.orthonormalize_between_powers is None else int(bool(s.orthonormalize_between_powers))
     c.pivot_kind = _lib.RQ_PIVOT_REFLECTORS if (rrqr or cfg.pivot_kind == "reflectors") else _lib.RQ_PIVOT_PERMUTATION
     c.rrqr = int(bool(rrqr))
-    c.sketch_mode = _lib.RQ_SKETCH_FRESH
+    if sketch not in ("fresh", "downdate"):
+        raise ValueError(f"sketch must be 'fresh' or 'downdate', not {sketch!r}")
+    c.sketch_mode = _lib.RQ_SKETCH_FRESH if sketch == "fresh" else _lib.RQ_SKETCH_DOWNDATE
     return c
 
 
@@ -249,12 +251,12 @@ class Factorization:
 # --------------------------------------------------------------------------
 # Entry points
 # --------------------------------------------------------------------------
-def _run(a, cfg, rng, inspect, rrqr, engine):
+def _run(a, cfg, rng, inspect, rrqr, engine, sketch="fresh"):
     torch = _torch()
     a = _check_input(a)
     eng = engine if engine is not None else Engine()
     buf, ld, m, n = eng.upload(a)
-    c = _make_config(cfg, rrqr)
+    c = _make_config(cfg, rrqr, sketch)
     counter = ctypes.c_uint64(int(rng.counter))
     perm = None if (rrqr or cfg.pivot_kind == "reflectors") else torch.empty(max(n, 1), dtype=torch.int64,
                                                                                device=eng.device)
@@ -281,12 +283,16 @@ def _run(a, cfg, rng, inspect, rrqr, engine):
     return Factorization(eng, m, n, cfg.block, method, buf, ld, perm)
 
 
-def block_qr(a, cfg, rng, inspect=None, *, engine=None):
+def block_qr(a, cfg, rng, inspect=None, *, engine=None, sketch="fresh"):
     """Blocked QR with randomized block pivoting (blocked.py:175-219), on the B200.
 
     The input is not modified; ``rng.counter`` advances by the draws consumed.
+    ``sketch="fresh"`` (default) reproduces the reference: a new Omega per panel.
+    ``sketch="downdate"`` is HQRRP proper: G is drawn once (counter += m(b+p)),
+    Y = G A is downdated after every panel (Y2 <- Y2 - G1 R12); its pivots
+    legitimately differ from the reference's.
     """
-    return _run(a, cfg, rng, inspect, False, engine)
+    return _run(a, cfg, rng, inspect, False, engine, sketch)
 
 
 def block_rrqr(a, cfg, rng, inspect=None, *, engine=None):

@@ -174,3 +174,32 @@ def test_diagonal_input_entry_set(rq):
     d = np.array([3.0, -7.0, 0.5, 11.0, 2.0, -1.0, 4.0, 6.0])
     f = rq.block_qr(np.diag(d), rq.BlockConfig(3), rq.RngState(1))
     assert np.allclose(np.sort(np.abs(np.diag(f.r))), np.sort(np.abs(d)), rtol=1e-14)
+
+
+@pytest.mark.parametrize("m,n,b,p", [(300, 300, 50, 10), (257, 200, 32, 8), (500, 500, 64, 6)])
+def test_downdate_sketch_matches_hqrrp_oracle(rq, m, n, b, p):
+    """HQRRP downdated sketch (Y2 <- Y2 - G1 R12) vs the oracle restatement."""
+    from oracle import randqr_oracle as O
+
+    a = O.gaussian_matrix(m, n, O.RngState(m * 3 + n))
+    ref_rng = O.RngState(5)
+    ref = O.block_qr_downdate(a, O.BlockConfig(b, O.SketchConfig(b, p, 0)), ref_rng)
+    rng = rq.RngState(5)
+    f = rq.block_qr(a, _cfg(rq, b, p, 0), rng, sketch="downdate")
+    assert rng.counter == ref_rng.counter == m * (b + p)
+    check_against(a, f, ref.r, ref.perm())
+    check_factorization(a, f)
+
+
+def test_downdate_rank_revealing_on_decaying_spectrum(golden, rq):
+    """Downdate pivots track the spectrum like the fresh ones (cfg 2 shape, n=600)."""
+    g = golden("cfg2_n600.npz")
+    a, s = g["a"], g["s"]
+    fd = rq.block_qr(a, _cfg(rq, 64, 10, 0), rq.RngState(1), sketch="downdate")
+    ff = rq.block_qr(a, _cfg(rq, 64, 10, 0), rq.RngState(1))
+    check_factorization(a, fd)
+    rd = np.abs(np.diag(fd.r)) / s
+    rf = np.abs(np.diag(ff.r)) / s
+    # same quality class as the reference's fresh sketches (SURVEY §6: max ratio 4.74 there)
+    assert np.median(rd) <= 2.0 * np.median(rf) + 0.1
+    assert rd.max() <= 3.0 * rf.max()
