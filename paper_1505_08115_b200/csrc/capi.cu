@@ -97,8 +97,9 @@ int rq_factorize(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, double
   RQ_TRY(validate(cfg, m, n, counter));
   if (lda < m || (lda & 1) || ((uintptr_t)dA & 15))
     return rq::set_error(RQ_EVALUE, "dA must be 16-byte aligned with an even lda >= m");
-  if (cfg->rrqr || cfg->pivot_kind == RQ_PIVOT_REFLECTORS)
-    return rq::set_error(RQ_EUNSUPPORTED, "reflector pivots / rrqr not built yet");
+  if (cfg->rrqr) return rq::set_error(RQ_EUNSUPPORTED, "block_rrqr not built yet");
+  if (cfg->pivot_kind == RQ_PIVOT_REFLECTORS && cfg->sketch_mode == RQ_SKETCH_DOWNDATE)
+    return rq::set_error(RQ_EUNSUPPORTED, "the downdated sketch applies to permutation pivots");
   if (cfg->sketch_mode == RQ_SKETCH_DOWNDATE && cfg->power != 0)
     return rq::set_error(RQ_EUNSUPPORTED, "downdate sketch with power iterations");
   return ctx->c.factorize_perm(*cfg, m, n, dA, lda, seed, counter, dperm);

@@ -61,7 +61,7 @@ struct Carver {
 // ---------------------------------------------------------------------------
 
 
-static size_t factor_bytes(int64_t m, int64_t n, int b) {
+static size_t factor_bytes(int64_t m, int64_t n, int b, bool refl = true) {
   size_t t = 0;
   for (int64_t s = 0; s < n; s += b) {
     const int64_t mp = m - s, np = n - s;
@@ -69,7 +69,12 @@ static size_t factor_bytes(int64_t m, int64_t n, int b) {
     const int steps = (int)std::min<int64_t>(mp, w);
     const int64_t ldv = even(mp + 1), ldt = even(b);
     t += (((size_t)ldv * (np <= b ? steps : b) * 8 + 255) & ~size_t(255));
-    t += (((size_t)ldt * b * 8 + 255) & ~size_t(255)) * 2;  // T, Q2^T
+    t += (((size_t)ldt * b * 8 + 255) & ~size_t(255)) * 2;  // T, Q2
+    if (refl) {                                              // V_S, T_S, P-hat
+      t += (((size_t)even(np) * b * 8 + 255) & ~size_t(255));
+      t += (((size_t)ldt * b * 8 + 255) & ~size_t(255));
+      t += (((size_t)std::max<int64_t>(np, b) * 4 + 255) & ~size_t(255));
+    }
     (void)steps;
   }
   return t;
@@ -83,13 +88,16 @@ static Layout plan_layout(void* base, int64_t m, int64_t n, int b, int p, int po
   L.ldy = even(wdt);
   const int64_t ldb = even(b);
   L.omega = c.take<double>((size_t)L.ldo * wdt);
-  L.yt = c.take<double>((size_t)L.ldy * n);
+  L.yt = c.take<double>((size_t)std::max<int64_t>(L.ldy * n, even(n) * wdt));  // Y^T, or Y scratch
   L.w1 = c.take<double>((size_t)ldb * n);
   L.w2 = c.take<double>((size_t)ldb * n);
   L.ttop = c.take<double>((size_t)ldb * n);
   L.gram = c.take<double>((size_t)ldb * b);
   L.tleaf = c.take<double>(32 * 32);
   L.rinv = c.take<double>((size_t)ldb * b);
+  L.zbuf = c.take<double>((size_t)even(m) * b);
+  L.z2buf = c.take<double>((size_t)even(m) * b);
+  L.vst = c.take<double>((size_t)ldb * n);
   L.g1 = c.take<double>((size_t)even(wdt) * b);
   L.ybuf = c.take<double>((size_t)std::max<int64_t>(even(n) * wdt, (int64_t)L.ldy * n));
   // split-K slabs: up to 16 splits of the (b+p+1) x n sketch, or 148 of the b x b Gram
@@ -315,6 +323,18 @@ int Ctx::tfactor(const double* V, int64_t rows, int k, int64_t ldv, int vpad, do
   return tfactor_from_gram(gram, ldg, k, T, ldt, stream, &launches);
 }
 
+// A[:, s:s+np] <- A[:, s:s+np] (I - V_S T_S V_S^T) on `rows` rows (apply_wy_right,
+// householder.py:117-124, at full height as blocked.py:205/261 do).
+int Ctx::apply_right_wy(double* A, int64_t lda, int64_t rows, int64_t ncols_total, int64_t s, int64_t np, int k,
+                        const double* VS, int64_t ldvs, const double* TS, int64_t ldts, double* vst, double* z,
+                        double* z2, int64_t ldz) {
+  const int64_t ldk = even(k);
+  RQ_TRY(transpose(VS, ldvs, vst, ldk, np, k, stream, &launches));
+  RQ_TRY(gemm(rows, k, np, op(A, rows, ncols_total, lda, 0, s), true, op(VS, np, k, ldvs), z, ldz, 1.0, 0.0));
+  RQ_TRY(gemm(rows, k, k, op(z, rows, k, ldz), true, op(TS, k, k, ldts), z2, ldz, 1.0, 0.0));
+  return gemm(rows, np, k, op(z2, rows, k, ldz), true, op(vst, k, np, ldk), A + s * lda, lda, -1.0, 1.0);
+}
+
 // ---------------------------------------------------------------------------
 // block_qr with permutation pivots, fresh sketches (reference semantics)
 // ---------------------------------------------------------------------------
@@ -335,6 +355,9 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
   cur_orig = L.orig;
 
   factors.clear();
+  rfactors.clear();
+  const bool refl_piv = cfg.pivot_kind == RQ_PIVOT_REFLECTORS;
+  p_is_perm = !refl_piv;
   factors_perm = L.orig;
   fm = m;
   fn = n;
@@ -396,6 +419,11 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       RQ_TRY(move_columns(mv2, stream, &launches));
       RQ_TRY(tfactor(Vf, mp, steps, ldv, vpad, Tf, even(b), L.gram));
       factors.push_back(PanelFactors{s, steps, Vf, ldv, vpad, Tf, even(b), nullptr, 0});
+      if (refl_piv) {
+        int* phat = fc.take<int>((size_t)w);
+        RQ_CUDA_TRY(cudaMemcpyAsync(phat, L.cap, (size_t)w * sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        rfactors.push_back(RightFactors{s, np, 0, nullptr, 0, nullptr, 0, phat, w});
+      }
       RQ_TRY(iota(lorder, (int)np, nullptr, 0, stream, &launches));
       if (inspect_cb) {
         cur_lorder = nullptr;
@@ -404,6 +432,24 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       }
       break;
     }
+    if (refl_piv) {
+      // ---------------- reflector pivots (select_pivot_reflectors, pivoting.py:132-146) ----------------
+      RQ_TRY(gaussian_fill(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
+      *counter += (uint64_t)mp * (uint64_t)wdt;
+      RQ_TRY(sketch(cfg, A, lda, m, n, s, mp, np, L, true));  // Y (np x wdt) in ybuf
+      const int64_t ldvs = even(np), ldt = even(b);
+      double* VS = fc.take<double>((size_t)ldvs * b);
+      double* TS = fc.take<double>((size_t)ldt * b);
+      int* phat = fc.take<int>((size_t)std::max<int64_t>(np, b));
+      RQ_CUDA_TRY(cudaMemsetAsync(VS, 0, (size_t)ldvs * b * sizeof(double), stream));
+      launches++;
+      // first b unpivoted reflectors of Y (the p extra columns never influence them)
+      RQ_TRY(panel_qr(L.ybuf, even(np), np, wdt, 0, np, b, VS, ldvs, 0, tleaf, L.w1, L.w2));
+      RQ_TRY(tfactor(VS, np, b, ldvs, 0, TS, ldt, L.gram));
+      // A[:, s:] <- A[:, s:] S at full height (apply_wy_right, blocked.py:205)
+      RQ_TRY(apply_right_wy(A, lda, m, n, s, np, b, VS, ldvs, TS, ldt, L.vst, L.zbuf, L.z2buf, even(m)));
+      rfactors.push_back(RightFactors{s, np, b, VS, ldvs, TS, ldt, phat, b});
+    } else {
     // ---------------- 1-2: sketch Y^T = Omega^T X (fresh) or the downdated Y (HQRRP) ----------------
     double* ycur = L.yt;
     if (!downdate) {
@@ -426,6 +472,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       MoveCall my{L.yt, L.ldy, s, 0, wdt, L.src, L.dst, L.nmoves, 2 * b, L.stage, L.ldy, nullptr, nullptr};
       RQ_TRY(move_columns(my, stream, &launches));
     }
+    }  // permutation pivots
     // ---------------- 5: unpivoted panel QR ----------------
     const int64_t ldv = even(mp + 1), ldt = even(b);
     const int vpad = (int)(s & 1);
@@ -456,6 +503,9 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     ss.ldr = L.lds_small;
     RQ_TRY(sweep(ss));
     RQ_TRY(small_q(V2, L.lds_small, b, Q2, ldt, L));
+    if (refl_piv)
+      RQ_CUDA_TRY(cudaMemcpyAsync(rfactors.back().phat, L.cap, (size_t)b * sizeof(int), cudaMemcpyDeviceToDevice,
+                                  stream));
     // ---------------- 7: R and the rows above follow P-hat ----------------
     RQ_TRY(copy2d(L.rfin, L.lds_small, A + s + s * lda, lda, b, b, 0, stream, &launches));
     MoveCall mv2{A, lda, s, 0, s, L.cap, L.iota_b, nullptr, b, L.stage, even(m), L.orig, L.ostage};
@@ -478,8 +528,12 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
                   L.ldy, -1.0, 1.0));
     }
     factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2, ldt});
-    std::swap(lorder, lorder_n);
-    std::swap(rank, rank_n);
+    if (!refl_piv) {
+      std::swap(lorder, lorder_n);
+      std::swap(rank, rank_n);
+    } else {
+      RQ_TRY(iota(lorder, (int)(np - b), nullptr, 0, stream, &launches));  // columns stay in place
+    }
     if (inspect_cb) {
       cur_s = s + b;
       cur_lorder = lorder;
@@ -500,16 +554,19 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
 // Y^T ((b+p) x n') of the trailing block X = A[s:, s:]: (X^T X)^q X^T Omega,
 // built from TN/NN DMMA GEMMs (pivoting.py:87-111, unstabilised powers).
 int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int64_t np,
-                Layout& L) {
+                Layout& L, bool want_y) {
   const int wdt = cfg.block + cfg.oversample;
   const bool stab = cfg.stabilize < 0 ? cfg.power >= 2 : cfg.stabilize != 0;
   if (stab) return set_error(RQ_EUNSUPPORTED, "stabilised power iterations are not implemented yet");
   const GemmOperand X = op(A, m, n, lda, s, s);
   const int pad = (int)(s & 1);
   const GemmOperand Om = op(L.omega, mp + pad, wdt, L.ldo, pad);
-  if (cfg.power == 0) return gemm(wdt, np, mp, Om, false, X, L.yt, L.ldy, 1.0, 0.0);
+  if (cfg.power == 0) {
+    if (want_y) return gemm(np, wdt, mp, X, false, Om, L.ybuf, even(np), 1.0, 0.0);  // Y = X^T Omega
+    return gemm(wdt, np, mp, Om, false, X, L.yt, L.ldy, 1.0, 0.0);                   // Y^T = Omega^T X
+  }
   // Y = X^T Omega (np x wdt) in w1-sized scratch; Z = X Y (mp x wdt) in omega
-  double* Y = L.ybuf;  // np x wdt
+  double* Y = want_y ? L.yt : L.ybuf;  // np x wdt intermediate (the output goes to ybuf when want_y)
   const int64_t ldY = even(np);
   RQ_TRY(gemm(np, wdt, mp, X, false, Om, Y, ldY, 1.0, 0.0));
   for (int it = 0; it < cfg.power; it++) {
@@ -517,6 +574,7 @@ int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t
     RQ_TRY(gemm(mp, wdt, np, op(A, m, n, lda, s, s), true, op(Y, np, wdt, ldY), L.omega + pad, L.ldo, 1.0, 0.0));
     if (it + 1 < cfg.power) RQ_TRY(gemm(np, wdt, mp, X, false, Om, Y, ldY, 1.0, 0.0));
   }
+  if (want_y) return gemm(np, wdt, mp, X, false, Om, L.ybuf, even(np), 1.0, 0.0);  // Y = X^T Z
   // Y^T = Z^T X
   return gemm(wdt, np, mp, Om, false, X, L.yt, L.ldy, 1.0, 0.0);
 }
@@ -594,7 +652,28 @@ int Ctx::form_q(int64_t cols, double* Q, int64_t ldq) {
 
 int Ctx::form_p(double* P, int64_t ldp) {
   if (!have_factors) return set_error(RQ_EVALUE, "no factorization stored in this context");
-  return perm_to_dense(factors_perm, fn, P, ldp, stream, &launches);
+  if (p_is_perm) return perm_to_dense(factors_perm, fn, P, ldp, stream, &launches);
+  // P = prod_i (S_i, P-hat_i) applied to I in order (Factorization.expand_p, blocked.py:143-149)
+  const int64_t n = fn;
+  RQ_TRY(fill_eye(P, ldp, n, n, 0, stream, &launches));
+  const int b = fb;
+  const int64_t ldz = even(n), ldk = even(b);
+  const size_t need = (size_t)3 * ldz * b * 8 + (size_t)ldk * n * 8 + (size_t)ldz * b * 8 + (size_t)n * 4 * 2 + 8192;
+  RQ_TRY(qarena.reserve(need));
+  Carver c(qarena.base);
+  double* z = c.take<double>((size_t)ldz * b);
+  double* z2 = c.take<double>((size_t)ldz * b);
+  double* vst = c.take<double>((size_t)ldk * n);
+  double* stage = c.take<double>((size_t)ldz * std::max<int64_t>(b, 1) * 2);
+  int* io = c.take<int>((size_t)n);
+  RQ_TRY(iota(io, (int)n, nullptr, 0, stream, &launches));
+  for (const RightFactors& f : rfactors) {
+    if (f.k > 0)
+      RQ_TRY(apply_right_wy(P, ldp, n, n, f.s, f.np, f.k, f.vs, f.ldvs, f.ts, f.ldts, vst, z, z2, ldz));
+    MoveCall mv{P, ldp, f.s, 0, n, f.phat, io, nullptr, f.nphat, stage, ldz, nullptr, nullptr};
+    RQ_TRY(move_columns(mv, stream, &launches));
+  }
+  return RQ_OK;
 }
 
 int Ctx::snapshot(double* hW, int64_t ldh) {

@@ -20,6 +20,7 @@ struct Arena {
 struct Layout {
   // scratch
   double *omega, *yt, *w1, *w2, *gram, *tleaf, *ybuf, *kwork, *small, *rfin, *stage, *ttop, *rinv, *g1;
+  double *zbuf, *z2buf, *vst;  // reflector pivots: A V_S, (A V_S) T_S, V_S^T
   int64_t ldo, ldy, lds_small;
   int *chosen, *lorderA, *lorderB, *rankA, *rankB, *newloc, *src, *dst, *nmoves, *cap, *iota_b;
   unsigned char* flag;
@@ -62,6 +63,19 @@ struct ProfRec {
   double flops;
 };
 
+// Right factor of one panel with reflector pivots: S = I - V_S T_S V_S^T on
+// columns s.., followed by the panel's inner permutation P-hat.
+struct RightFactors {
+  int64_t s, np;
+  int k;
+  double* vs;  // np x k
+  int64_t ldvs;
+  double* ts;  // k x k
+  int64_t ldts;
+  int* phat;   // k (or np for the final block)
+  int nphat;
+};
+
 struct Ctx {
   int device = 0;
   // profiling
@@ -88,6 +102,8 @@ struct Ctx {
   size_t sweep_ws_bytes = 0;
   // stored factorization
   std::vector<PanelFactors> factors;
+  std::vector<RightFactors> rfactors;  // reflector pivots (P is orthogonal, not a permutation)
+  bool p_is_perm = true;
   int64_t* factors_perm = nullptr;
   int64_t fm = 0, fn = 0;
   int fb = 0;
@@ -112,7 +128,10 @@ struct Ctx {
                int vpad, double* tleaf, double* w1, double* w2);
   int tfactor(const double* V, int64_t rows, int k, int64_t ldv, int vpad, double* T, int64_t ldt, double* gram);
   int sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int64_t np,
-             Layout& L);
+             Layout& L, bool want_y = false);
+  int apply_right_wy(double* A, int64_t lda, int64_t rows, int64_t ncols_total, int64_t s, int64_t np, int k,
+                     const double* VS, int64_t ldvs, const double* TS, int64_t ldts, double* vst, double* z,
+                     double* z2, int64_t ldz);
   int trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, int64_t n2,
                       const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2,
                       Layout& L);

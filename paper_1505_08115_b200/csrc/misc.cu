@@ -381,6 +381,31 @@ int perm_to_dense(const int64_t* perm, int64_t n, double* P, int64_t ldp, cudaSt
   return RQ_OK;
 }
 
+// Out-of-place transpose (column-major rows x cols -> cols x rows), 32x32 smem tiles.
+__global__ void transpose_kernel(const double* __restrict__ S, int64_t lds, double* __restrict__ D, int64_t ldd,
+                                 int64_t rows, int64_t cols) {
+  __shared__ double tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + threadIdx.x, c = c0 + k;
+    tile[k][threadIdx.x] = (r < rows && c < cols) ? S[c * lds + r] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t c = c0 + threadIdx.x, r = r0 + k;  // D(c, r) = S(r, c)
+    if (r < rows && c < cols) D[r * ldd + c] = tile[threadIdx.x][k];
+  }
+}
+int transpose(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows, int64_t cols, cudaStream_t st,
+              int64_t* launches) {
+  if (rows <= 0 || cols <= 0) return RQ_OK;
+  dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(cols, 32));
+  transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(S, lds, D, ldd, rows, cols);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
 // int32 -> int64 widening with offset (perm outputs)
 __global__ void widen_kernel(const int* a, int n, int64_t off, int64_t* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] + off;

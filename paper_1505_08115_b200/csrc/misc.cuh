@@ -45,6 +45,8 @@ int fill_eye(double* X, int64_t ldx, int64_t rows, int64_t cols, int64_t diag_of
 int copy2d(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows, int64_t cols, int upper_only,
            cudaStream_t st, int64_t* launches);
 int perm_to_dense(const int64_t* perm, int64_t n, double* P, int64_t ldp, cudaStream_t st, int64_t* launches);
+int transpose(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows, int64_t cols, cudaStream_t st,
+              int64_t* launches);
 int widen(const int* a, int n, int64_t off, int64_t* out, cudaStream_t st, int64_t* launches);
 
 int gaussian_fill(double* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t counter,

@@ -203,3 +203,31 @@ def test_downdate_rank_revealing_on_decaying_spectrum(golden, rq):
     # same quality class as the reference's fresh sketches (max ratio 4.74 there)
     assert np.median(rd) <= 2.0 * np.median(rf) + 0.1
     assert rd.max() <= 3.0 * rf.max()
+
+
+@pytest.mark.parametrize("tag", ["m2_24x24_b6", "m2_160x160_b32_p8"])
+def test_reflector_pivots_match_reference_golden(golden, rq, tag):
+    """block_qr(pivot_kind="reflectors") (pivoting.py:132-146, blocked.py:175-219) vs the reference."""
+    g = golden("small_factorizations.npz")
+    m, n, b, p, q, refl, rr, sa, ss = (int(x) for x in g[f"{tag}/cfg"])
+    a = g[f"{tag}/a"]
+    rng = rq.RngState(ss)
+    f = rq.block_qr(a, _cfg(rq, b, p, q, refl=True), rng)
+    assert rng.counter == int(g[f"{tag}/counter"])
+    assert f.method == "reflector_pivot"
+    check_against(a, f, g[f"{tag}/r"], None, tol=1e-12)
+    check_factorization(a, f)
+    assert np.abs(f.expand_p() - g[f"{tag}/p"]).max() <= 1e-12
+    assert np.abs(f.expand_q() - g[f"{tag}/q"]).max() <= 1e-11
+
+
+def test_reflector_pivots_vs_oracle_larger(rq):
+    from oracle import randqr_oracle as O
+
+    for (m, n, b, p, q) in [(400, 300, 48, 8, 0), (300, 300, 64, 4, 1)]:
+        a = O.gaussian_matrix(m, n, O.RngState(m + 7))
+        ref = O.block_qr(a, O.BlockConfig(b, O.SketchConfig(b, p, q), "reflectors"), O.RngState(3))
+        f = rq.block_qr(a, _cfg(rq, b, p, q, refl=True), rq.RngState(3))
+        check_against(a, f, ref.r, None, tol=1e-12)
+        check_factorization(a, f)
+        assert np.abs(f.expand_p() - ref.expand_p()).max() <= 1e-11
