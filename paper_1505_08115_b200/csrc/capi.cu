@@ -97,7 +97,11 @@ int rq_factorize(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, double
   RQ_TRY(validate(cfg, m, n, counter));
   if (lda < m || (lda & 1) || ((uintptr_t)dA & 15))
     return rq::set_error(RQ_EVALUE, "dA must be 16-byte aligned with an even lda >= m");
-  if (cfg->rrqr) return rq::set_error(RQ_EUNSUPPORTED, "block_rrqr not built yet");
+  if (cfg->rrqr) {
+    if (cfg->sketch_mode != RQ_SKETCH_FRESH)
+      return rq::set_error(RQ_EUNSUPPORTED, "block_rrqr uses fresh sketches (reference semantics)");
+    return ctx->c.factorize_rrqr(*cfg, m, n, dA, lda, seed, counter);
+  }
   if (cfg->pivot_kind == RQ_PIVOT_REFLECTORS && cfg->sketch_mode == RQ_SKETCH_DOWNDATE)
     return rq::set_error(RQ_EUNSUPPORTED, "the downdated sketch applies to permutation pivots");
   if (cfg->sketch_mode == RQ_SKETCH_DOWNDATE && cfg->power != 0)

@@ -70,9 +70,9 @@ static size_t factor_bytes(int64_t m, int64_t n, int b, bool refl = true) {
     const int64_t ldv = even(mp + 1), ldt = even(b);
     t += (((size_t)ldv * (np <= b ? steps : b) * 8 + 255) & ~size_t(255));
     t += (((size_t)ldt * b * 8 + 255) & ~size_t(255)) * 2;  // T, Q2
-    if (refl) {                                              // V_S, T_S, P-hat
+    if (refl) {                                              // V_S, T_S, P-hat, V~ (rrqr)
       t += (((size_t)even(np) * b * 8 + 255) & ~size_t(255));
-      t += (((size_t)ldt * b * 8 + 255) & ~size_t(255));
+      t += (((size_t)ldt * b * 8 + 255) & ~size_t(255)) * 2;
       t += (((size_t)std::max<int64_t>(np, b) * 4 + 255) & ~size_t(255));
     }
     (void)steps;
@@ -98,6 +98,13 @@ static Layout plan_layout(void* base, int64_t m, int64_t n, int b, int p, int po
   L.zbuf = c.take<double>((size_t)even(m) * b);
   L.z2buf = c.take<double>((size_t)even(m) * b);
   L.vst = c.take<double>((size_t)ldb * n);
+  L.ov = c.take<double>((size_t)even(std::max(m, n) + 1) * wdt);
+  L.ot = c.take<double>((size_t)even(wdt) * wdt);
+  L.oe = c.take<double>((size_t)even(std::max(m, n) + 1) * wdt);
+  L.jw = c.take<double>((size_t)ldb * b);
+  L.jv = c.take<double>((size_t)ldb * b);
+  L.jd = c.take<double>((size_t)ldb);
+  L.jstat = c.take<int>((size_t)n / std::max(b, 1) + 2);
   L.g1 = c.take<double>((size_t)even(wdt) * b);
   L.ybuf = c.take<double>((size_t)std::max<int64_t>(even(n) * wdt, (int64_t)L.ldy * n));
   // split-K slabs: up to 16 splits of the (b+p+1) x n sketch, or 148 of the b x b Gram
@@ -422,7 +429,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       if (refl_piv) {
         int* phat = fc.take<int>((size_t)w);
         RQ_CUDA_TRY(cudaMemcpyAsync(phat, L.cap, (size_t)w * sizeof(int), cudaMemcpyDeviceToDevice, stream));
-        rfactors.push_back(RightFactors{s, np, 0, nullptr, 0, nullptr, 0, phat, w});
+        rfactors.push_back(RightFactors{s, np, 0, nullptr, 0, nullptr, 0, phat, w, nullptr, 0, 0});
       }
       RQ_TRY(iota(lorder, (int)np, nullptr, 0, stream, &launches));
       if (inspect_cb) {
@@ -434,21 +441,8 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     }
     if (refl_piv) {
       // ---------------- reflector pivots (select_pivot_reflectors, pivoting.py:132-146) ----------------
-      RQ_TRY(gaussian_fill(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
-      *counter += (uint64_t)mp * (uint64_t)wdt;
-      RQ_TRY(sketch(cfg, A, lda, m, n, s, mp, np, L, true));  // Y (np x wdt) in ybuf
-      const int64_t ldvs = even(np), ldt = even(b);
-      double* VS = fc.take<double>((size_t)ldvs * b);
-      double* TS = fc.take<double>((size_t)ldt * b);
-      int* phat = fc.take<int>((size_t)std::max<int64_t>(np, b));
-      RQ_CUDA_TRY(cudaMemsetAsync(VS, 0, (size_t)ldvs * b * sizeof(double), stream));
-      launches++;
-      // first b unpivoted reflectors of Y (the p extra columns never influence them)
-      RQ_TRY(panel_qr(L.ybuf, even(np), np, wdt, 0, np, b, VS, ldvs, 0, tleaf, L.w1, L.w2));
-      RQ_TRY(tfactor(VS, np, b, ldvs, 0, TS, ldt, L.gram));
-      // A[:, s:] <- A[:, s:] S at full height (apply_wy_right, blocked.py:205)
-      RQ_TRY(apply_right_wy(A, lda, m, n, s, np, b, VS, ldvs, TS, ldt, L.vst, L.zbuf, L.z2buf, even(m)));
-      rfactors.push_back(RightFactors{s, np, b, VS, ldvs, TS, ldt, phat, b});
+      RQ_TRY(reflector_pivot(cfg, A, lda, m, n, s, L, &fc, seed, counter));
+      rfactors.back().nphat = b;
     } else {
     // ---------------- 1-2: sketch Y^T = Omega^T X (fresh) or the downdated Y (HQRRP) ----------------
     double* ycur = L.yt;
@@ -557,10 +551,24 @@ int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t
                 Layout& L, bool want_y) {
   const int wdt = cfg.block + cfg.oversample;
   const bool stab = cfg.stabilize < 0 ? cfg.power >= 2 : cfg.stabilize != 0;
-  if (stab) return set_error(RQ_EUNSUPPORTED, "stabilised power iterations are not implemented yet");
   const GemmOperand X = op(A, m, n, lda, s, s);
   const int pad = (int)(s & 1);
   const GemmOperand Om = op(L.omega, mp + pad, wdt, L.ldo, pad);
+  if (stab) {
+    // build_sketch with re-orthonormalisation after every application (pivoting.py:102-110)
+    double* Y = L.ybuf;  // np x wdt
+    const int64_t ldY = even(np);
+    RQ_TRY(gemm(np, wdt, mp, X, false, Om, Y, ldY, 1.0, 0.0));
+    RQ_TRY(orth(Y, np, wdt, ldY, L));
+    for (int it = 0; it < cfg.power; it++) {
+      RQ_TRY(gemm(mp, wdt, np, op(A, m, n, lda, s, s), true, op(Y, np, wdt, ldY), L.omega + pad, L.ldo, 1.0, 0.0));
+      RQ_TRY(orth(L.omega + pad, mp, wdt, L.ldo, L));
+      RQ_TRY(gemm(np, wdt, mp, X, false, Om, Y, ldY, 1.0, 0.0));
+      RQ_TRY(orth(Y, np, wdt, ldY, L));
+    }
+    if (want_y) return RQ_OK;
+    return transpose(Y, ldY, L.yt, L.ldy, np, wdt, stream, &launches);
+  }
   if (cfg.power == 0) {
     if (want_y) return gemm(np, wdt, mp, X, false, Om, L.ybuf, even(np), 1.0, 0.0);  // Y = X^T Omega
     return gemm(wdt, np, mp, Om, false, X, L.yt, L.ldy, 1.0, 0.0);                   // Y^T = Omega^T X
@@ -601,6 +609,132 @@ int Ctx::trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s
     RQ_TRY(copy2d(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
     RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldt), false, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
   }
+  return RQ_OK;
+}
+
+// _orth (pivoting.py:80-84): src (rows x cols) <- the first cols columns of Q
+// from its unpivoted Householder QR (panel kernels + DMMA GEMMs).
+int Ctx::orth(double* src, int64_t rows, int cols, int64_t ld, Layout& L) {
+  const int64_t lde = even(rows);
+  double* E = L.oe;
+  double* Vo = L.ov;
+  const int64_t ldc = even(cols);
+  RQ_TRY(copy2d(src, ld, E, lde, rows, cols, 0, stream, &launches));
+  RQ_CUDA_TRY(cudaMemsetAsync(Vo, 0, (size_t)lde * cols * sizeof(double), stream));
+  launches++;
+  RQ_TRY(panel_qr(E, lde, rows, cols, 0, rows, cols, Vo, lde, 0, L.tleaf, L.w1, L.w2));
+  RQ_TRY(tfactor(Vo, rows, cols, lde, 0, L.ot, ldc, L.gram));
+  RQ_TRY(fill_eye(E, lde, rows, cols, 0, stream, &launches));
+  RQ_TRY(gemm(cols, cols, rows, op(Vo, rows, cols, lde), false, op(E, rows, cols, lde), L.w1, ldc, 1.0, 0.0));
+  RQ_TRY(gemm(cols, cols, cols, op(L.ot, cols, cols, ldc), true, op(L.w1, cols, cols, ldc), L.w2, ldc, 1.0, 0.0));
+  RQ_TRY(gemm(rows, cols, cols, op(Vo, rows, cols, lde), true, op(L.w2, cols, cols, ldc), E, lde, -1.0, 1.0));
+  return copy2d(E, lde, src, ld, rows, cols, 0, stream, &launches);
+}
+
+// Reflector pivot of the panel at s: sketch Y, its first b unpivoted reflectors,
+// A[:, s:] <- A[:, s:] S at full height.  Records the right factor.
+int Ctx::reflector_pivot(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, Layout& L,
+                         void* fc_ptr, uint64_t seed, uint64_t* counter) {
+  Carver& fc = *reinterpret_cast<Carver*>(fc_ptr);
+  const int b = cfg.block, wdt = cfg.block + cfg.oversample;
+  const int64_t mp = m - s, np = n - s;
+  RQ_TRY(gaussian_fill(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
+  *counter += (uint64_t)mp * (uint64_t)wdt;
+  RQ_TRY(sketch(cfg, A, lda, m, n, s, mp, np, L, true));  // Y (np x wdt) in ybuf
+  const int64_t ldvs = even(np), ldt = even(b);
+  double* VS = fc.take<double>((size_t)ldvs * b);
+  double* TS = fc.take<double>((size_t)ldt * b);
+  int* phat = fc.take<int>((size_t)std::max<int64_t>(np, b));
+  RQ_CUDA_TRY(cudaMemsetAsync(VS, 0, (size_t)ldvs * b * sizeof(double), stream));
+  launches++;
+  RQ_TRY(panel_qr(L.ybuf, even(np), np, wdt, 0, np, b, VS, ldvs, 0, L.tleaf, L.w1, L.w2));
+  RQ_TRY(tfactor(VS, np, b, ldvs, 0, TS, ldt, L.gram));
+  RQ_TRY(apply_right_wy(A, lda, m, n, s, np, b, VS, ldvs, TS, ldt, L.vst, L.zbuf, L.z2buf, even(m)));
+  rfactors.push_back(RightFactors{s, np, b, VS, ldvs, TS, ldt, phat, 0, nullptr, 0, 0});
+  return RQ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// block_rrqr (blocked.py:239-279): reflector pivots, panel SVD (unpivoted QR +
+// wave-parallel cyclic Jacobi), diag(d) blocks, V~ on the rows above,
+// tail <- U'^T Q~^T tail.
+// ---------------------------------------------------------------------------
+int Ctx::factorize_rrqr(const rq_config& cfg0, int64_t m, int64_t n, double* A, int64_t lda, uint64_t seed,
+                        uint64_t* counter) {
+  rq_config cfg = cfg0;
+  cfg.pivot_kind = RQ_PIVOT_REFLECTORS;  // blocked.py:251
+  const int b = cfg.block, p = cfg.oversample;
+  size_t need = plan_layout(nullptr, m, n, b, p, cfg.power).total;
+  RQ_TRY(arena.reserve(need));
+  Layout L = plan_layout(arena.base, m, n, b, p, cfg.power);
+  kwork = L.kwork;
+  kwork_bytes = L.kwork_bytes;
+  sweep_ws = L.sweep_ws;
+  sweep_ws_bytes = L.sweep_ws_bytes;
+  cur_A = A;
+  cur_lda = lda;
+  cur_m = m;
+  cur_n = n;
+  factors.clear();
+  rfactors.clear();
+  p_is_perm = false;
+  fm = m;
+  fn = n;
+  fb = b;
+  Carver fc(L.fstore);
+  int panel = 0;
+  for (int64_t s = 0; s < n; s += b) {
+    const int w = (int)std::min<int64_t>(b, n - s);
+    const bool final = n - s <= b;
+    const int64_t mp = m - s, np = n - s;
+    cur_s = s;
+    cur_lorder = nullptr;
+    if (!final) RQ_TRY(reflector_pivot(cfg, A, lda, m, n, s, L, &fc, seed, counter));
+    // panel_svd: unpivoted QR of the m' x w panel, then the SVD of its w x w triangle
+    const int64_t ldv = even(mp + 1), ldt = even(b);
+    const int vpad = (int)(s & 1);
+    double* V = fc.take<double>((size_t)ldv * w);
+    double* T = fc.take<double>((size_t)ldt * b);
+    double* U = fc.take<double>((size_t)ldt * b);
+    double* Vt = fc.take<double>((size_t)ldt * b);
+    RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * w * sizeof(double), stream));
+    launches++;
+    RQ_TRY(panel_qr(A, lda, m, n, s, mp, w, V, ldv, vpad, L.tleaf, L.w1, L.w2));
+    {
+      cudaEvent_t e0;
+      const int saved = cat;
+      cat = PROF_SMALL;
+      prof_begin(&e0);
+      const int rc = jacobi_svd(A + s + s * lda, lda, w, L.jw, ldt, L.jv, ldt, L.jd, U, ldt, Vt, ldt, L.jstat + panel,
+                                stream, &launches);
+      prof_end(e0, 0.0);
+      cat = saved;
+      RQ_TRY(rc);
+    }
+    // rows above: A[:s, s:s+w] <- A[:s, s:s+w] V~   (blocked.py:265)
+    if (s > 0) {
+      RQ_TRY(copy2d(A + s * lda, lda, L.stage, even(m), s, w, 0, stream, &launches));
+      RQ_TRY(gemm(s, w, w, op(L.stage, s, w, even(m)), true, op(Vt, w, w, ldt), A + s * lda, lda, 1.0, 0.0));
+    }
+    RQ_TRY(tfactor(V, mp, w, ldv, vpad, T, ldt, L.gram));
+    RQ_TRY(set_diag_block(A + s + s * lda, lda, mp, w, L.jd, stream, &launches));  // blocked.py:266-268
+    if (!final) RQ_TRY(trailing_update(A, lda, m, n, s, mp, w, np - w, V, ldv, vpad, T, ldt, U, L));
+    factors.push_back(PanelFactors{s, w, V, ldv, vpad, T, ldt, U, ldt});
+    rfactors.push_back(RightFactors{s, np, 0, nullptr, 0, nullptr, 0, nullptr, 0, Vt, ldt, w});
+    panel++;
+    if (inspect_cb) {
+      RQ_CUDA_TRY(cudaStreamSynchronize(stream));
+      inspect_cb(panel, inspect_user);
+    }
+  }
+  cur_lorder = nullptr;
+  // ConvergenceError after 60 sweeps (svd.py:52-53)
+  std::vector<int> st((size_t)panel);
+  RQ_CUDA_TRY(cudaMemcpyAsync(st.data(), L.jstat, (size_t)panel * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  RQ_CUDA_TRY(cudaStreamSynchronize(stream));
+  for (int i = 0; i < panel; i++)
+    if (st[i] < 0) return set_error(RQ_ECONV, "Jacobi SVD did not converge in 60 sweeps (panel %d)", i + 1);
+  have_factors = true;
   return RQ_OK;
 }
 
@@ -670,8 +804,15 @@ int Ctx::form_p(double* P, int64_t ldp) {
   for (const RightFactors& f : rfactors) {
     if (f.k > 0)
       RQ_TRY(apply_right_wy(P, ldp, n, n, f.s, f.np, f.k, f.vs, f.ldvs, f.ts, f.ldts, vst, z, z2, ldz));
-    MoveCall mv{P, ldp, f.s, 0, n, f.phat, io, nullptr, f.nphat, stage, ldz, nullptr, nullptr};
-    RQ_TRY(move_columns(mv, stream, &launches));
+    if (f.nphat > 0) {
+      MoveCall mv{P, ldp, f.s, 0, n, f.phat, io, nullptr, f.nphat, stage, ldz, nullptr, nullptr};
+      RQ_TRY(move_columns(mv, stream, &launches));
+    }
+    if (f.dense) {  // DenseOrtho (blocked.py:53-63): P[:, s:s+w] <- P[:, s:s+w] V~
+      RQ_TRY(copy2d(P + f.s * ldp, ldp, z, ldz, n, f.wd, 0, stream, &launches));
+      RQ_TRY(gemm(n, f.wd, f.wd, op(z, n, f.wd, ldz), true, op(f.dense, f.wd, f.wd, f.ldd), P + f.s * ldp, ldp, 1.0,
+                  0.0));
+    }
   }
   return RQ_OK;
 }

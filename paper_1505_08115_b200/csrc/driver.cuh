@@ -21,6 +21,9 @@ struct Layout {
   // scratch
   double *omega, *yt, *w1, *w2, *gram, *tleaf, *ybuf, *kwork, *small, *rfin, *stage, *ttop, *rinv, *g1;
   double *zbuf, *z2buf, *vst;  // reflector pivots: A V_S, (A V_S) T_S, V_S^T
+  double *ov, *ot, *oe;         // _orth scratch: reflectors, T, Q
+  double *jw, *jv, *jd;         // panel SVD scratch
+  int* jstat;                   // per-panel Jacobi sweep counts
   int64_t ldo, ldy, lds_small;
   int *chosen, *lorderA, *lorderB, *rankA, *rankB, *newloc, *src, *dst, *nmoves, *cap, *iota_b;
   unsigned char* flag;
@@ -74,6 +77,9 @@ struct RightFactors {
   int64_t ldts;
   int* phat;   // k (or np for the final block)
   int nphat;
+  double* dense;  // w x w right factor V~ of the panel SVD (block_rrqr), or null
+  int64_t ldd;
+  int wd;
 };
 
 struct Ctx {
@@ -138,6 +144,11 @@ struct Ctx {
   int factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, int64_t lda, uint64_t seed,
                      uint64_t* counter, int64_t* dperm);
   int small_q(const double* V2, int64_t ldv2, int k, double* Q2, int64_t ldq, Layout& L);
+  int factorize_rrqr(const rq_config& cfg, int64_t m, int64_t n, double* A, int64_t lda, uint64_t seed,
+                     uint64_t* counter);
+  int orth(double* src, int64_t rows, int cols, int64_t ld, Layout& L);
+  int reflector_pivot(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, Layout& L,
+                      void* fc_ptr, uint64_t seed, uint64_t* counter);
   int form_q(int64_t cols, double* Q, int64_t ldq);
   int form_p(double* P, int64_t ldp);
   int snapshot(double* hW, int64_t ldh);

@@ -406,6 +406,25 @@ int transpose(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows
   return RQ_OK;
 }
 
+// A (rows x w) = [diag(d); 0]  (block_rrqr's diagonal block, blocked.py:266-268)
+__global__ void set_diag_block_kernel(double* A, int64_t lda, int64_t rows, int w, const double* d) {
+  const int64_t total = rows * w;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx / rows, i = idx - j * rows;
+    A[j * lda + i] = (i == j) ? d[j] : 0.0;
+  }
+}
+int set_diag_block(double* A, int64_t lda, int64_t rows, int w, const double* d, cudaStream_t st, int64_t* launches) {
+  if (rows <= 0 || w <= 0) return RQ_OK;
+  int blocks = (int)ceil_div(rows * w, 256);
+  if (blocks > 8 * kSMs) blocks = 8 * kSMs;
+  set_diag_block_kernel<<<blocks, 256, 0, st>>>(A, lda, rows, w, d);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
 // int32 -> int64 widening with offset (perm outputs)
 __global__ void widen_kernel(const int* a, int n, int64_t off, int64_t* out) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = a[i] + off;

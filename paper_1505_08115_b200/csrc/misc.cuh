@@ -47,6 +47,9 @@ int copy2d(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows, i
 int perm_to_dense(const int64_t* perm, int64_t n, double* P, int64_t ldp, cudaStream_t st, int64_t* launches);
 int transpose(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows, int64_t cols, cudaStream_t st,
               int64_t* launches);
+int jacobi_svd(const double* r, int64_t ldr, int w, double* wbuf, int64_t ldw, double* vbuf, int64_t ldv, double* d,
+               double* u, int64_t ldu, double* vt, int64_t ldvt, int* status, cudaStream_t st, int64_t* launches);
+int set_diag_block(double* A, int64_t lda, int64_t rows, int w, const double* d, cudaStream_t st, int64_t* launches);
 int widen(const int* a, int n, int64_t off, int64_t* out, cudaStream_t st, int64_t* launches);
 
 int gaussian_fill(double* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t counter,
