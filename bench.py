@@ -174,6 +174,11 @@ def main():
     ap.add_argument("--sketch", default="fresh", choices=["fresh", "downdate"],
                     help="headline sketch mode (fresh = reference semantics)")
     ap.add_argument("--no-variant", action="store_true", help="skip timing the other sketch mode")
+    ap.add_argument("--method", default="m1", choices=["m1", "m2", "m3"],
+                    help="m1 block_qr permutation pivots (headline), m2 reflector pivots, m3 block_rrqr")
+    ap.add_argument("--q", type=int, default=0, help="power iterations of the sketch")
+    ap.add_argument("--matrix", default="gauss", choices=["gauss", "cfg4"],
+                    help="gauss: N(0,1) (cfg 3); cfg4: U diag(max(10^(-12j/2000),1e-15)) V^T")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -205,10 +210,25 @@ def main():
     # A = gaussian_matrix(n, n, RngState(0)): same counter-based stream as the reference
     with torch.cuda.stream(stream):
         a0, ld = rq.gaussian_matrix_device(m, n, rq.RngState(0), engine=eng)
+        if args.matrix == "cfg4":
+            # input generation only (outside the timed region): Haar U, V from QR of Gaussians
+            g1, _ = rq.gaussian_matrix_device(n, n, rq.RngState(0, 10**12), engine=eng)
+            qu, ru = torch.linalg.qr(g1[:n, :n].T)
+            qu = qu * torch.sign(torch.diagonal(ru))
+            qv, rv = torch.linalg.qr(a0[:n, :n].T)
+            qv = qv * torch.sign(torch.diagonal(rv))
+            jj = torch.arange(1, n + 1, device=eng.device, dtype=torch.float64)
+            sv = torch.clamp(10.0 ** (-12.0 * jj / 2000.0), min=1e-15)
+            amat = (qu * sv) @ qv.T
+            a0[:n, :n].copy_(amat.T)
+            del g1, qu, ru, qv, rv, amat
         work, _ = eng.alloc_matrix(m, n)
         perm = torch.empty(n, dtype=torch.int64, device=eng.device)
     mode = _lib.RQ_SKETCH_FRESH if args.sketch == "fresh" else _lib.RQ_SKETCH_DOWNDATE
-    cfg = _lib.rq_config(b, p, 0, -1, 0, 0, mode, 0)
+    pk = _lib.RQ_PIVOT_PERMUTATION if args.method == "m1" else _lib.RQ_PIVOT_REFLECTORS
+    cfg = _lib.rq_config(b, p, args.q, -1, pk, 1 if args.method == "m3" else 0, mode, 0)
+    if args.method != "m1":
+        args.no_variant = True  # the downdated sketch applies to permutation pivots only
 
     def step():
         with torch.cuda.stream(stream):
@@ -315,9 +335,13 @@ def main():
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg3 HQRRP fp64 n={n} b={b} p={p} q=0, {args.sketch} sketch"
-                                   + (" (reference semantics)" if args.sketch == "fresh" else " (HQRRP downdate)"),
-                       "n": n, "b": b, "p": p, "q": 0, "sketch": args.sketch,
+            "config": {"workload": (f"cfg3 HQRRP fp64 n={n} b={b} p={p} q={args.q}, {args.sketch} sketch"
+                                    + (" (reference semantics)" if args.sketch == "fresh" else " (HQRRP downdate)"))
+                                   if args.method == "m1" else
+                                   f"{args.method} ({'block_rrqr' if args.method == 'm3' else 'reflector pivots'}) "
+                                   f"fp64 n={n} b={b} p={p} q={args.q}, matrix={args.matrix}",
+                       "n": n, "b": b, "p": p, "q": args.q, "sketch": args.sketch, "method": args.method,
+                       "matrix": args.matrix,
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "inputs (800 MB) larger than L2 (126 MB)"},
             "fraction_of_fp64_peak": value / FP64_PEAK_TFLOPS,
