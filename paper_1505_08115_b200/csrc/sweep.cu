@@ -1050,22 +1050,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
     // -------- A: apply the pending reflector to the warp's columns and score them --------
     double d[CPW];
     if (have_refl) {
+      // row slots entirely above the reflector (32k + 31 < rj) are dead: warp-uniform skip
+      const int kmin = rj >> 5;
       double uk[RPL];
 #pragma unroll
       for (int k = 0; k < RPL; k++) {
         const int i = lane + 32 * k;
-        uk[k] = (i >= rj && i < m) ? u[i] : 0.0;
+        uk[k] = (k >= kmin && i >= rj && i < m) ? u[i] : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < CPW; q++) {
-        double pr[RPL];
+        double acc = 0.0;
 #pragma unroll
-        for (int k = 0; k < RPL; k++) pr[k] = uk[k] * x[q][k];
-#pragma unroll
-        for (int w2 = 1; w2 < RPL; w2 <<= 1)
-#pragma unroll
-          for (int k = 0; k + w2 < RPL; k += 2 * w2) pr[k] += pr[k + w2];
-        d[q] = pr[0];
+        for (int k = 0; k < RPL; k++)
+          if (k >= kmin) acc = fma(uk[k], x[q][k], acc);
+        d[q] = acc;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
@@ -1075,23 +1074,23 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
       for (int q = 0; q < CPW; q++) {
         const double dd = act[q] ? 2.0 * d[q] : 0.0;
 #pragma unroll
-        for (int k = 0; k < RPL; k++) x[q][k] -= dd * uk[k];
+        for (int k = 0; k < RPL; k++)
+          if (k >= kmin) x[q][k] -= dd * uk[k];
       }
     }
     double t[CPW];
+    const int kmin_t = (j + 1) >> 5;
 #pragma unroll
     for (int q = 0; q < CPW; q++) {
-      double sq[RPL];
+      double acc = 0.0;
 #pragma unroll
       for (int k = 0; k < RPL; k++) {
+        if (k < kmin_t) continue;
         const int i = lane + 32 * k;
-        sq[k] = (i > j && i < m) ? x[q][k] * x[q][k] : 0.0;
+        const double xv = (i > j && i < m) ? x[q][k] : 0.0;
+        acc = fma(xv, xv, acc);
       }
-#pragma unroll
-      for (int w2 = 1; w2 < RPL; w2 <<= 1)
-#pragma unroll
-        for (int k = 0; k + w2 < RPL; k += 2 * w2) sq[k] += sq[k + w2];
-      t[q] = sq[0];
+      t[q] = acc;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
