@@ -346,7 +346,11 @@ def main():
                        "l2": "inputs (800 MB) larger than L2 (126 MB)"},
             "fraction_of_fp64_peak": value / FP64_PEAK_TFLOPS,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
+                         # ncu --set full, one A2 -= V W2 launch (n = 10000, K = b = 256):
+                         # dram read + write vs 1.640e9 algorithmic bytes (profiles/ncu_gemm_nn_r01.txt)
+                         "traffic": 1.6466e9 if n == 10000 and b == 256 else None,
+                         "traffic_note": "bytes per launch of A2 -= V W2 at panel 1; algorithmic 1.640e9",
                          "kernel": "gemm_f64_kernel (trailing update: V^T A2, T^T W, A2 -= V W2, Q2^T top)",
                          "peak_source": "measured DMMA peak, profiles/probe_r01.jsonl"},
             "breakdown_ms_per_step": cats,
