@@ -260,7 +260,8 @@ def main():
     launches = eng.launches - launches0
     clk = clocks.stop()
     cats = {}
-    for c, name in enumerate(["trailing_gemm", "other_gemm", "sketch_cpqr", "panel_leaf", "other", "small_cpqr"]):
+    for c, name in enumerate(["trailing_gemm", "other_gemm", "sketch_cpqr", "panel_leaf", "other", "small_cpqr",
+                              "sketch_gemm", "panel_gemm", "tfactor"]):
         t, f, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
         check(lib.rq_profile_read(eng.handle, c, ctypes.byref(t), ctypes.byref(f), ctypes.byref(k)))
         cats[name] = {"ms": t.value / args.steps, "launches": k.value // args.steps}

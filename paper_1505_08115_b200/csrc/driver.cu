@@ -175,11 +175,19 @@ void Ctx::prof_end(cudaEvent_t e0, double flops) {
   prof_recs.push_back(ProfRec{cat, e0, e1, flops});
 }
 
+struct CatGuard {
+  int& c;
+  int saved;
+  CatGuard(int& c_, int v) : c(c_), saved(c_) { c = v; }
+  ~CatGuard() { c = saved; }
+};
+
 int Ctx::gemm(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmajor, const GemmOperand& B,
               double* C, int64_t ldc, double alpha, double beta) {
   cudaEvent_t e0;
   const int saved = cat;
-  if (cat != PROF_TRAIL) cat = PROF_GEMM_OTHER;
+  if (cat != PROF_TRAIL && cat != PROF_SKETCH_GEMM && cat != PROF_PANEL_GEMM && cat != PROF_TFACTOR)
+    cat = PROF_GEMM_OTHER;
   prof_begin(&e0);
   int rc = gemm_raw(M, N, K, A, a_mmajor, B, C, ldc, alpha, beta);
   prof_end(e0, 2.0 * (double)M * (double)N * (double)K);
@@ -270,6 +278,7 @@ int Ctx::sweep_raw(SweepCall c) {
 // ---------------------------------------------------------------------------
 int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, double* V, int64_t ldv,
                   int vpad, double* tleaf, double* w1, double* w2) {
+  CatGuard guard(cat, PROF_PANEL_GEMM);
   int wl_max = leaf_reg_width_for(mp);
   if (wl_max == 0) wl_max = leaf_width_for(mp);
   if (wl_max == 0) return set_error(RQ_EUNSUPPORTED, "panel of %lld rows exceeds the leaf kernel", (long long)mp);
@@ -298,19 +307,40 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
     }
     const int64_t nrest = b - k0 - w;
     if (nrest <= 0) break;
-    // W = V_l^T A_rest ; W2 = T_l^T W ; A_rest -= V_l W2
-    const int64_t ldw = even(w);
-    RQ_TRY(gemm(w, nrest, mm, op(V, mp + vpad, b, ldv, vpad + k0, k0), false, op(A, m, n, lda, s + k0, s + k0 + w),
-                w1, ldw, 1.0, 0.0));
-    RQ_TRY(gemm(w, nrest, w, op(tleaf, 32, 32, 32), false, op(w1, w, nrest, ldw), w2, ldw, 1.0, 0.0));
-    RQ_TRY(gemm(mm, nrest, w, op(V, mp + vpad, b, ldv, vpad + k0, k0), true, op(w2, w, nrest, ldw),
-                A + (s + k0) + (s + k0 + w) * lda, lda, -1.0, 1.0));
+    // A_rest -= V_l T_l^T (V_l^T A_rest)
+    if (w <= 16 && ((ceil_div(mm, std::min<int64_t>(kSMs, ceil_div(mm, 32))) | 1) * (nrest + w) + w * nrest) * 8 <=
+                       200 * 1024) {
+      cudaEvent_t e0;
+      prof_begin(&e0);
+      SweepWork sw;
+      sw.barriers = barriers;
+      sw.nbarriers = nbarriers;
+      sw.next = next_barrier;
+      unsigned int* bar = sw.next_barrier();
+      next_barrier = sw.next;
+      int rc = wy_update(A + (s + k0) + (s + k0 + w) * lda, lda, mm, (int)nrest, V + vpad + k0 + (int64_t)k0 * ldv, ldv,
+                         tleaf, 32, w, kwork, kwork_bytes, bar, stream, &launches);
+      if (sw.wrapped) {
+        RQ_CUDA_TRY(cudaMemsetAsync(barriers, 0, sizeof(unsigned) * nbarriers, stream));
+        launches++;
+      }
+      prof_end(e0, 4.0 * (double)mm * w * nrest);
+      RQ_TRY(rc);
+    } else {
+      const int64_t ldw = even(w);
+      RQ_TRY(gemm(w, nrest, mm, op(V, mp + vpad, b, ldv, vpad + k0, k0), false, op(A, m, n, lda, s + k0, s + k0 + w),
+                  w1, ldw, 1.0, 0.0));
+      RQ_TRY(gemm(w, nrest, w, op(tleaf, 32, 32, 32), false, op(w1, w, nrest, ldw), w2, ldw, 1.0, 0.0));
+      RQ_TRY(gemm(mm, nrest, w, op(V, mp + vpad, b, ldv, vpad + k0, k0), true, op(w2, w, nrest, ldw),
+                  A + (s + k0) + (s + k0 + w) * lda, lda, -1.0, 1.0));
+    }
   }
   return RQ_OK;
 }
 
 // Q2 = H'_0 ... H'_{k-1} = I - V2 T2 V2^T (k x k), dense, from the b x b CPQR reflectors.
 int Ctx::small_q(const double* V2, int64_t ldv2, int k, double* Q2, int64_t ldq, Layout& L) {
+  CatGuard guard(cat, PROF_TFACTOR);
   double* T2s = L.ttop;  // k x k scratch (free until the trailing update)
   const int64_t ldk = even(k);
   RQ_TRY(tfactor(V2, k, k, ldv2, 0, T2s, ldk, L.gram));
@@ -324,10 +354,15 @@ int Ctx::small_q(const double* V2, int64_t ldv2, int k, double* Q2, int64_t ldq,
 
 // T (k x k) of the reflectors V (rows x k): Gram by DMMA GEMM, then back substitution.
 int Ctx::tfactor(const double* V, int64_t rows, int k, int64_t ldv, int vpad, double* T, int64_t ldt, double* gram) {
+  CatGuard guard(cat, PROF_TFACTOR);
+  cudaEvent_t e0;
+  prof_begin(&e0);
   const int64_t ldg = even(k);
   RQ_TRY(gemm(k, k, rows, op(V, rows + vpad, k, ldv, vpad), false, op(V, rows + vpad, k, ldv, vpad), gram, ldg, 1.0,
               0.0));
-  return tfactor_from_gram(gram, ldg, k, T, ldt, stream, &launches);
+  const int rc = tfactor_from_gram(gram, ldg, k, T, ldt, stream, &launches);
+  prof_end(e0, 0.0);
+  return rc;
 }
 
 // A[:, s:s+np] <- A[:, s:s+np] (I - V_S T_S V_S^T) on `rows` rows (apply_wy_right,
@@ -549,6 +584,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
 // built from TN/NN DMMA GEMMs (pivoting.py:87-111, unstabilised powers).
 int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int64_t np,
                 Layout& L, bool want_y) {
+  CatGuard guard(cat, PROF_SKETCH_GEMM);
   const int wdt = cfg.block + cfg.oversample;
   const bool stab = cfg.stabilize < 0 ? cfg.power >= 2 : cfg.stabilize != 0;
   const GemmOperand X = op(A, m, n, lda, s, s);
@@ -592,12 +628,7 @@ int Ctx::trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s
                          Layout& L) {
   const int64_t ldw = even(b);
   const GemmOperand Vop = op(V, mp + vpad, b, ldv, vpad);
-  struct CatGuard {
-    int& c;
-    int saved;
-    CatGuard(int& c_, int v) : c(c_), saved(c_) { c = v; }
-    ~CatGuard() { c = saved; }
-  } guard(cat, PROF_TRAIL);
+  CatGuard guard(cat, PROF_TRAIL);
   // W = V^T A2   (b x n2, K = m')
   RQ_TRY(gemm(b, n2, mp, Vop, false, op(A, m, n, lda, s, s + b), L.w1, ldw, 1.0, 0.0));
   // W2 = T^T W

@@ -57,7 +57,10 @@ enum ProfCat {
   PROF_LEAF = 3,        // panel leaf QR
   PROF_OTHER = 4,
   PROF_SMALL = 5,       // b x b CPQR of R' and the final block
-  PROF_NCAT = 6
+  PROF_SKETCH_GEMM = 6, // Y = Omega^T X (+ power iterations)
+  PROF_PANEL_GEMM = 7,  // WY updates between panel leaves
+  PROF_TFACTOR = 8,     // Gram V^T V + T back substitution, small Q2
+  PROF_NCAT = 9
 };
 
 struct ProfRec {

@@ -467,6 +467,160 @@ static int launch_leaf_reg(const LeafCall& c, cudaStream_t st, int64_t* launches
   return RQ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Fused WY update between panel leaves (one cooperative launch instead of three
+// GEMMs):  A_rest <- (I - V T V^T)^T A_rest = A_rest - V T^T (V^T A_rest)
+//   phase 1: every CTA forms the partial V^T A_rest over its row block
+//   phase 2: column slices of W = sum of partials (CTA order: deterministic),
+//            W2 = T^T W
+//   phase 3: every CTA updates its row block with V W2
+// ---------------------------------------------------------------------------
+constexpr int WU_THREADS = 256;
+
+struct WyUpdateArgs {
+  double* a;  // A_rest top-left (mm x nr), lda
+  int64_t lda;
+  int64_t mm;
+  int nr;
+  const double* v;  // mm x w, ldv
+  int64_t ldv;
+  const double* t;  // w x w, ldt
+  int64_t ldt;
+  int w;
+  int rows_per;
+  double* part;  // G x w x nr partials
+  double* w2;    // w x nr
+  unsigned int* bar;
+};
+
+__global__ void __launch_bounds__(WU_THREADS) wy_update_kernel(const WyUpdateArgs p) {
+  extern __shared__ double sm[];
+  const int G = gridDim.x;
+  const int w = p.w, nr = p.nr;
+  const int64_t r0 = (int64_t)blockIdx.x * p.rows_per;
+  const int64_t r1 = min(p.mm, r0 + p.rows_per);
+  const int nrows = (int)max((int64_t)0, r1 - r0);
+  const int lds = p.rows_per | 1;              // odd stride: conflict-free column access
+  double* As = sm;                             // nr columns x lds (this CTA's rows of A_rest)
+  double* Vs = As + (int64_t)nr * lds;          // w columns x lds
+  double* W2s = Vs + (int64_t)w * lds;          // w x nr
+  // stage the row block (coalesced; every load in flight before any use)
+  for (int j = threadIdx.x / 32; j < nr + w; j += WU_THREADS / 32) {
+    const int lane = threadIdx.x & 31;
+    if (j < nr) {
+      const double* col = p.a + (int64_t)j * p.lda + r0;
+      for (int i = lane; i < nrows; i += 32) As[j * lds + i] = col[i];
+    } else {
+      const double* col = p.v + (int64_t)(j - nr) * p.ldv + r0;
+      for (int i = lane; i < nrows; i += 32) Vs[(j - nr) * lds + i] = col[i];
+    }
+  }
+  __syncthreads();
+  // phase 1: partial[k][j] = sum_{i in block} V(i,k) A(i,j); lanes take different j (same k)
+  double* mypart = p.part + (int64_t)blockIdx.x * w * nr;
+  for (int e = threadIdx.x; e < w * nr; e += WU_THREADS) {
+    const int k = e / nr, j = e - k * nr;
+    const double* ac = As + j * lds;
+    const double* vc = Vs + k * lds;
+    double a0 = 0.0, a1 = 0.0;
+    int i = 0;
+    for (; i + 1 < nrows; i += 2) {
+      a0 = fma(vc[i], ac[i], a0);
+      a1 = fma(vc[i + 1], ac[i + 1], a1);
+    }
+    if (i < nrows) a0 = fma(vc[i], ac[i], a0);
+    mypart[(int64_t)k * nr + j] = a0 + a1;
+  }
+  unsigned int gen = 0;
+  grid_barrier(p.bar, gen);
+  // phase 2: CTA g owns columns j = g, g+G, ...: W(:, j) = sum over CTAs (fixed order), W2(:, j) = T^T W(:, j)
+  __shared__ double wcol[16];
+  __shared__ double wchunk[16][17];
+  for (int j = blockIdx.x; j < nr; j += G) {
+    {
+      // thread (k, chunk): 16 chunks of CTAs summed in parallel, then combined in chunk order
+      const int k = threadIdx.x & 15, ch = threadIdx.x >> 4;
+      const int per = (G + 15) / 16;
+      const int g0 = ch * per, g1 = min(G, g0 + per);
+      double acc = 0.0;
+      if (k < w) {
+        double vals[10];
+        int g = g0;
+        for (; g + 10 <= g1; g += 10) {
+#pragma unroll
+          for (int u = 0; u < 10; u++) vals[u] = __ldcg(p.part + ((int64_t)(g + u) * w + k) * nr + j);
+#pragma unroll
+          for (int u = 0; u < 10; u++) acc += vals[u];
+        }
+        for (; g < g1; g++) acc += __ldcg(p.part + ((int64_t)g * w + k) * nr + j);
+      }
+      wchunk[k][ch] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < w) {
+      double acc = 0.0;
+      for (int ch = 0; ch < 16; ch++) acc += wchunk[threadIdx.x][ch];
+      wcol[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < w) {
+      // (T^T W)_k = sum_{l <= k} T(l, k) W_l   (T upper triangular)
+      double acc = 0.0;
+      for (int l = 0; l <= threadIdx.x; l++) acc += p.t[(int64_t)threadIdx.x * p.ldt + l] * wcol[l];
+      p.w2[(int64_t)j * w + threadIdx.x] = acc;
+    }
+    __syncthreads();
+  }
+  grid_barrier(p.bar, gen);
+  // phase 3: A(i, j) -= sum_k V(i, k) W2(k, j) on this CTA's rows, from the staged block
+  for (int idx = threadIdx.x; idx < w * nr; idx += WU_THREADS) W2s[idx] = __ldcg(p.w2 + idx);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nrows * nr; e += WU_THREADS) {
+    const int j = e / nrows, i = e - j * nrows;
+    const double* w2c = W2s + (int64_t)j * w;
+    double acc = 0.0;
+    for (int k = 0; k < w; k++) acc = fma(Vs[k * lds + i], w2c[k], acc);
+    p.a[(int64_t)j * p.lda + r0 + i] = As[j * lds + i] - acc;
+  }
+}
+
+int wy_update(double* a, int64_t lda, int64_t mm, int nr, const double* v, int64_t ldv, const double* t, int64_t ldt,
+              int w, double* scratch, size_t scratch_bytes, unsigned int* bar, cudaStream_t st, int64_t* launches) {
+  if (nr <= 0 || mm <= 0) return RQ_OK;
+  if (w > 16) return set_error(RQ_EINTERNAL, "wy_update: width %d > 16", w);
+  int G = (int)ceil_div(mm, 32);
+  if (G > kSMs) G = kSMs;
+  if (G < 1) G = 1;
+  const int rows_per = (int)ceil_div(mm, G);
+  const size_t smem = ((size_t)(rows_per | 1) * (nr + w) + (size_t)w * nr) * sizeof(double);
+  if (smem > 200 * 1024) return set_error(RQ_EINTERNAL, "wy_update: %lld rows too many", (long long)mm);
+  const size_t need = ((size_t)G * w * nr + (size_t)w * nr) * sizeof(double);
+  if (need > scratch_bytes) return set_error(RQ_EINTERNAL, "wy_update: scratch too small");
+  WyUpdateArgs p;
+  p.a = a;
+  p.lda = lda;
+  p.mm = mm;
+  p.nr = nr;
+  p.v = v;
+  p.ldv = ldv;
+  p.t = t;
+  p.ldt = ldt;
+  p.w = w;
+  p.rows_per = rows_per;
+  p.part = scratch;
+  p.w2 = scratch + (size_t)G * w * nr;
+  p.bar = bar;
+  static bool attr = false;
+  if (!attr) {
+    RQ_CUDA_TRY(cudaFuncSetAttribute(wy_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  void* args[] = {(void*)&p};
+  RQ_CUDA_TRY(cudaLaunchCooperativeKernel((void*)wy_update_kernel, dim3(G), dim3(WU_THREADS), args, smem, st));
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
 template <int WL>
 static int launch_leaf(const LeafCall& c, cudaStream_t st, int64_t* launches) {
   constexpr int PV = LeafLayout<WL>::PV;
