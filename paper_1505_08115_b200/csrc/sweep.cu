@@ -1016,145 +1016,138 @@ struct alignas(16) SkWin {
   unsigned long long flag;  // launch-unique step stamp, written last (release)
 };
 
-template <int RPL, int CPW, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchArgs p, SkSlot2* slots, SkWin* wins,
-                                                                   unsigned long long stamp_base) {
+// Per-step state shared by the step templates below.
+struct SkKey {
+  unsigned hi, lo;  // bits of the non-negative key (monotone as integers)
+  int pos;
+  int col;          // global column id, -1 = none
+};
+
+struct SkShared {
+  SkKey wk[16];
+  SkKey win;
+  double wtail, wxj;
+  int wsel[2];
+};
+
+// Apply the pending reflector u (rows >= 32*K0 may be non-zero; u is exactly 0
+// above the reflector row and below m) to every column the warp owns.
+template <int K0, int RPL, int CPW>
+RQ_DEV void sk_apply(double (&x)[CPW][RPL], const bool (&act)[CPW], const double* u, int lane) {
+  double uk[RPL];
+#pragma unroll
+  for (int k = K0; k < RPL; k++) uk[k] = u[lane + 32 * k];
+  double d[CPW];
+#pragma unroll
+  for (int q = 0; q < CPW; q++) {
+    double acc = 0.0;
+#pragma unroll
+    for (int k = K0; k < RPL; k++) acc = fma(uk[k], x[q][k], acc);
+    d[q] = acc;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int q = 0; q < CPW; q++) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+#pragma unroll
+  for (int q = 0; q < CPW; q++) {
+    const double dd = act[q] ? 2.0 * d[q] : 0.0;
+#pragma unroll
+    for (int k = K0; k < RPL; k++) x[q][k] -= dd * uk[k];
+  }
+}
+
+// Steps j in [32*KJ, jend): row j lives in register slot KJ (lane j & 31), so
+// every row mask below is a compile-time slot range plus one lane predicate.
+template <int KJ, int RPL, int CPW, int WARPS>
+RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
+                     double (&x)[CPW][RPL], int (&pos)[CPW], bool (&act)[CPW], bool& have_refl, double* u,
+                     SkShared& sh, int cbase, int jend) {
   constexpr int NT = WARPS * 32;
-  __shared__ double u[32 * RPL];
-  __shared__ RegKey wk[WARPS];
-  __shared__ RegKey win_s;
-  __shared__ int wsel[3];
   const int G = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = p.m;
-  const int cbase = blockIdx.x * WARPS * CPW + warp * CPW;
-  double x[CPW][RPL];
-  int pos[CPW];
-  bool act[CPW];
-#pragma unroll
-  for (int q = 0; q < CPW; q++) {
-    const int c = cbase + q;
-    act[q] = c < p.n;
-    pos[q] = act[q] ? (p.init_pos ? p.init_pos[c] : c) : INT_MAX;
-#pragma unroll
-    for (int k = 0; k < RPL; k++) {
-      const int i = lane + 32 * k;
-      x[q][k] = (act[q] && i < m) ? p.y[(int64_t)c * p.ld + i] : 0.0;
-    }
-  }
-  bool have_refl = false;
-  int rj = -1;
-  for (int j = 0; j < p.steps; j++) {
+  for (int j = 32 * KJ; j < jend; j++) {
     const int par = j & 1;
+    const int jl = j & 31;
     dbg_stamp(j, 0);
-    // -------- A: apply the pending reflector to the warp's columns and score them --------
-    double d[CPW];
+    // -------- A: apply the pending reflector (row j-1), score rows >= j --------
     if (have_refl) {
-      // row slots entirely above the reflector (32k + 31 < rj) are dead: warp-uniform skip
-      const int kmin = rj >> 5;
-      double uk[RPL];
-#pragma unroll
-      for (int k = 0; k < RPL; k++) {
-        const int i = lane + 32 * k;
-        uk[k] = (k >= kmin && i >= rj && i < m) ? u[i] : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < CPW; q++) {
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < RPL; k++)
-          if (k >= kmin) acc = fma(uk[k], x[q][k], acc);
-        d[q] = acc;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int q = 0; q < CPW; q++) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
-#pragma unroll
-      for (int q = 0; q < CPW; q++) {
-        const double dd = act[q] ? 2.0 * d[q] : 0.0;
-#pragma unroll
-        for (int k = 0; k < RPL; k++)
-          if (k >= kmin) x[q][k] -= dd * uk[k];
-      }
+      if (KJ > 0 && jl == 0) sk_apply<(KJ > 0 ? KJ - 1 : 0), RPL, CPW>(x, act, u, lane);
+      else sk_apply<KJ, RPL, CPW>(x, act, u, lane);
     }
     double t[CPW];
-    const int kmin_t = (j + 1) >> 5;
+    const bool at_or_below = lane >= jl;
 #pragma unroll
     for (int q = 0; q < CPW; q++) {
-      double acc = 0.0;
+      const double xv = at_or_below ? x[q][KJ] : 0.0;
+      double acc = xv * xv;
 #pragma unroll
-      for (int k = 0; k < RPL; k++) {
-        if (k < kmin_t) continue;
-        const int i = lane + 32 * k;
-        const double xv = (i > j && i < m) ? x[q][k] : 0.0;
-        acc = fma(xv, xv, acc);
-      }
+      for (int k = KJ + 1; k < RPL; k++) acc = fma(x[q][k], x[q][k], acc);
       t[q] = acc;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int q = 0; q < CPW; q++) t[q] += __shfl_xor_sync(0xffffffffu, t[q], o);
-    const int kj = j >> 5;
-    double bkey = -1.0, btail = 0.0, bxj = 0.0;
+    double bkey = -1.0;
     int bpos = INT_MAX, bq = -1;
 #pragma unroll
     for (int q = 0; q < CPW; q++) {
-      double sel = 0.0;
-#pragma unroll
-      for (int k = 0; k < RPL; k++) sel = (k == kj) ? x[q][k] : sel;
-      const double xj = __shfl_sync(0xffffffffu, sel, j & 31);
-      const double key = xj * xj + t[q];
-      if (act[q] && (bq < 0 || piv_better(key, pos[q], bkey, bpos))) {
-        bkey = key;
-        btail = t[q];
-        bxj = xj;
+      if (act[q] && (bq < 0 || piv_better(t[q], pos[q], bkey, bpos))) {
+        bkey = t[q];
         bpos = pos[q];
         bq = q;
       }
     }
     if (lane == 0) {
       const unsigned long long kb = __double_as_longlong(bkey < 0.0 ? 0.0 : bkey);
-      wk[warp] = RegKey{(unsigned)(kb >> 32), (unsigned)kb, bpos, bq >= 0 ? cbase + bq : -1, btail, bxj};
+      sh.wk[warp] = SkKey{(unsigned)(kb >> 32), (unsigned)kb, bpos, bq >= 0 ? cbase + bq : -1};
     }
     dbg_stamp(j, 1);
     __syncthreads();
     dbg_stamp(j, 2);
-    // -------- B: CTA candidate -> global slot; its warp writes the column --------
+    // -------- B: the CTA's best warp publishes its column, x_j and tail --------
     SkSlot2* slot = slots + (int64_t)par * G;
-    if (warp == 0) {
-      const RegKey r = lane < WARPS ? wk[lane] : RegKey{0u, 0u, INT_MAX, -1, 0.0, 0.0};
-      const int wl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);
-      if (lane == 0) {
-        wsel[0] = wl;
-        SkSlot2* me = slot + blockIdx.x;
-        if (wl >= 0) {
-          const RegKey b = wk[wl];
-          me->key = __longlong_as_double(((long long)b.hi << 32) | (long long)b.lo);
-          me->tail = b.tail;
-          me->xj = b.xj;
-          me->pos = b.pos;
-          me->col = b.col;
-        } else {
+    {
+      const SkKey r = lane < WARPS ? sh.wk[lane] : SkKey{0u, 0u, INT_MAX, -1};
+      const int wl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);  // warp-uniform, same in every warp
+      if (wl < 0) {
+        if (warp == 0 && lane == 0) {
+          SkSlot2* me = slot + blockIdx.x;
           me->key = -1.0;
           me->col = -1;
           me->pos = INT_MAX;
         }
-      }
-    }
-    __syncthreads();
-    if (wsel[0] == warp) {
-      const int bqw = wk[warp].col - cbase;
-      double* sd = p.slotdata + ((int64_t)par * G + blockIdx.x) * m;
+      } else if (wl == warp) {
+        const SkKey b = sh.wk[warp];
+        const int bqw = b.col - cbase;
+        double* sd = p.slotdata + ((int64_t)par * G + blockIdx.x) * m;
 #pragma unroll
-      for (int q = 0; q < CPW; q++)
-        if (q == bqw)
+        for (int q = 0; q < CPW; q++)
+          if (q == bqw) {
+            const double xj = __shfl_sync(0xffffffffu, x[q][KJ], jl);
+            const double xv = lane > jl ? x[q][KJ] : 0.0;
+            double tl = xv * xv;
 #pragma unroll
-          for (int k = 0; k < RPL; k++) {
-            const int i = lane + 32 * k;
-            if (i >= j && i < m) sd[i] = x[q][k];
+            for (int k = KJ + 1; k < RPL; k++) tl = fma(x[q][k], x[q][k], tl);
+#pragma unroll
+            for (int k = KJ; k < RPL; k++) {
+              const int i = lane + 32 * k;
+              if (i >= j && i < m) sd[i] = x[q][k];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
+            if (lane == 0) {
+              SkSlot2* me = slot + blockIdx.x;
+              me->key = __longlong_as_double(((long long)b.hi << 32) | (long long)b.lo);
+              me->tail = tl;
+              me->xj = xj;
+              me->pos = b.pos;
+              me->col = b.col;
+            }
           }
+      }
     }
     __syncthreads();
     dbg_stamp(j, 3);
@@ -1170,7 +1163,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
       const unsigned long long target = p.counter_base + (unsigned long long)(j + 1) * G;
       if (old + 1 == target) {
         // last arriver: every slot of this step is visible (acq_rel atomic).
-        // Issue all slot loads first (independent), then reduce.
         constexpr int kMaxK = (kSMs + 31) / 32;
         double kv[kMaxK], tv[kMaxK], xv[kMaxK];
         int pv[kMaxK], cv[kMaxK];
@@ -1218,36 +1210,30 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
       }
       __syncwarp();
       if (lane == 0) {
-        RegKey w;
         const double kv = __ldcg(&wrec->key);
         const unsigned long long kb = __double_as_longlong(kv);
-        w.hi = (unsigned)(kb >> 32);
-        w.lo = (unsigned)kb;
-        w.tail = __ldcg(&wrec->tail);
-        w.xj = __ldcg(&wrec->xj);
-        w.pos = __ldcg(&wrec->pos);
-        w.col = __ldcg(&wrec->col);
-        win_s = w;
-        wsel[1] = __ldcg(&wrec->cta);
+        sh.win = SkKey{(unsigned)(kb >> 32), (unsigned)kb, __ldcg(&wrec->pos), __ldcg(&wrec->col)};
+        sh.wtail = __ldcg(&wrec->tail);
+        sh.wxj = __ldcg(&wrec->xj);
+        sh.wsel[1] = __ldcg(&wrec->cta);
       }
     }
     __syncthreads();
     dbg_stamp(j, 4);
-    // -------- E: reflector from the winning column (L2) --------
-    const RegKey win = win_s;
-    const int wcta = wsel[1];
+    // -------- E: reflector from the winning column (L2); u = 0 outside [j, m) --------
+    const SkKey win = sh.win;
+    const int wcta = sh.wsel[1];
     const double wkey = __longlong_as_double(((long long)win.hi << 32) | (long long)win.lo);
     const bool refl = (m - j >= 2) && (wkey != 0.0);
     if (refl) {
       const double* xs = p.slotdata + ((int64_t)par * G + wcta) * m;
-      const int i = j + threadIdx.x;
-      const double xv = (i < m) ? __ldcg(&xs[i]) : 0.0;
+      const double wxj = sh.wxj;
       const double nrm = sqrt(wkey);
-      const double beta = (win.xj >= 0.0) ? -nrm : nrm;
-      const double h = beta - win.xj;
-      const double inv = 1.0 / sqrt(h * h + win.tail);
-      if (i < m) u[i] = (i == j) ? h * inv : -xv * inv;
-      for (int i2 = i + NT; i2 < m; i2 += NT) u[i2] = -__ldcg(&xs[i2]) * inv;
+      const double beta = (wxj >= 0.0) ? -nrm : nrm;
+      const double h = beta - wxj;
+      const double inv = 1.0 / sqrt(h * h + sh.wtail);
+      for (int i = 32 * KJ + threadIdx.x; i < 32 * RPL; i += NT)
+        u[i] = (i > j && i < m) ? -__ldcg(&xs[i]) * inv : (i == j ? h * inv : 0.0);
     }
 #pragma unroll
     for (int q = 0; q < CPW; q++) {
@@ -1260,9 +1246,49 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) p.chosen[j] = win.col;
     have_refl = refl;
-    rj = j;
     __syncthreads();
     dbg_stamp(j, 5);
+  }
+}
+
+template <int KJ, int RPL, int CPW, int WARPS>
+RQ_DEV void sk_dispatch(int kj, const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
+                        double (&x)[CPW][RPL], int (&pos)[CPW], bool (&act)[CPW], bool& have_refl, double* u,
+                        SkShared& sh, int cbase, int jend) {
+  if constexpr (KJ < RPL) {
+    if (kj == KJ)
+      sk_block<KJ, RPL, CPW, WARPS>(p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh, cbase, jend);
+    else
+      sk_dispatch<KJ + 1, RPL, CPW, WARPS>(kj, p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh, cbase,
+                                           jend);
+  }
+}
+
+template <int RPL, int CPW, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchArgs p, SkSlot2* slots, SkWin* wins,
+                                                                   unsigned long long stamp_base) {
+  __shared__ double u[32 * RPL];
+  __shared__ SkShared sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cbase = blockIdx.x * WARPS * CPW + warp * CPW;
+  double x[CPW][RPL];
+  int pos[CPW];
+  bool act[CPW];
+#pragma unroll
+  for (int q = 0; q < CPW; q++) {
+    const int c = cbase + q;
+    act[q] = c < p.n;
+    pos[q] = act[q] ? (p.init_pos ? p.init_pos[c] : c) : INT_MAX;
+#pragma unroll
+    for (int k = 0; k < RPL; k++) {
+      const int i = lane + 32 * k;
+      x[q][k] = (act[q] && i < p.m) ? p.y[(int64_t)c * p.ld + i] : 0.0;
+    }
+  }
+  bool have_refl = false;
+  for (int kj = 0; 32 * kj < p.steps; kj++) {
+    const int jend = min(p.steps, 32 * kj + 32);
+    sk_dispatch<0, RPL, CPW, WARPS>(kj, p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh, cbase, jend);
   }
 }
 

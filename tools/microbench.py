@@ -53,7 +53,7 @@ if "sweep" in which:
         ms = timeit(run)
         print(f"cpqr sweep {m}x{n} steps={steps}: {ms*1e3:.0f} us  ({ms*1e3/steps:.2f} us/step)")
 if "sketch" in which:
-    for (m, n, steps) in [(272, 10000, 256), (272, 5000, 256), (272, 1000, 256), (74, 2000, 64)]:
+    for (m, n, steps) in [(272, 40000, 256), (272, 20000, 256), (272, 11800, 256), (272, 10000, 256), (272, 5000, 256), (272, 1000, 256), (74, 2000, 64)]:
         y0 = rng.standard_normal((m, n))
         buf, ld = dev(y0)
         work, _ = eng.alloc_matrix(m, n)
