@@ -308,8 +308,7 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
     const int64_t nrest = b - k0 - w;
     if (nrest <= 0) break;
     // A_rest -= V_l T_l^T (V_l^T A_rest)
-    if (w <= 16 && ((ceil_div(mm, std::min<int64_t>(kSMs, ceil_div(mm, 32))) | 1) * (nrest + w) + w * nrest) * 8 <=
-                       200 * 1024) {
+    if (wy_update_fits(mm, (int)nrest, w)) {
       cudaEvent_t e0;
       prof_begin(&e0);
       SweepWork sw;

@@ -493,6 +493,11 @@ struct WyUpdateArgs {
   unsigned int* bar;
 };
 
+RQ_DEV void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
 __global__ void __launch_bounds__(WU_THREADS) wy_update_kernel(const WyUpdateArgs p) {
   extern __shared__ double sm[];
   const int G = gridDim.x;
@@ -501,39 +506,66 @@ __global__ void __launch_bounds__(WU_THREADS) wy_update_kernel(const WyUpdateArg
   const int64_t r1 = min(p.mm, r0 + p.rows_per);
   const int nrows = (int)max((int64_t)0, r1 - r0);
   const int lds = p.rows_per | 1;              // odd stride: conflict-free column access
-  double* As = sm;                             // nr columns x lds (this CTA's rows of A_rest)
-  double* Vs = As + (int64_t)nr * lds;          // w columns x lds
-  double* W2s = Vs + (int64_t)w * lds;          // w x nr
-  // stage the row block (coalesced; every load in flight before any use)
-  for (int j = threadIdx.x / 32; j < nr + w; j += WU_THREADS / 32) {
-    const int lane = threadIdx.x & 31;
-    if (j < nr) {
-      const double* col = p.a + (int64_t)j * p.lda + r0;
-      for (int i = lane; i < nrows; i += 32) As[j * lds + i] = col[i];
-    } else {
-      const double* col = p.v + (int64_t)(j - nr) * p.ldv + r0;
-      for (int i = lane; i < nrows; i += 32) Vs[(j - nr) * lds + i] = col[i];
-    }
+  double* Vr = sm;                             // rows_per x 16, row-major (zero-padded beyond w)
+  double* As = Vr + (int64_t)p.rows_per * 16;  // nr columns x lds (this CTA's rows of A_rest)
+  double* red = As + (int64_t)nr * lds;        // row-group partials (phase 1)
+  // ---- stage the row block: every copy in flight at once (cp.async), V row-major ----
+  for (int e = threadIdx.x; e < nr * nrows; e += WU_THREADS) {
+    const int j = e / nrows, i = e - j * nrows;
+    cp_async8(As + j * lds + i, p.a + (int64_t)j * p.lda + r0 + i);
   }
+  for (int e = threadIdx.x; e < nrows * 16; e += WU_THREADS) {
+    const int i = e >> 4, k = e & 15;
+    if (k < w) cp_async8(Vr + e, p.v + (int64_t)k * p.ldv + r0 + i);
+    else Vr[e] = 0.0;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  // phase 1: partial[k][j] = sum_{i in block} V(i,k) A(i,j); lanes take different j (same k)
-  double* mypart = p.part + (int64_t)blockIdx.x * w * nr;
-  for (int e = threadIdx.x; e < w * nr; e += WU_THREADS) {
-    const int k = e / nr, j = e - k * nr;
-    const double* ac = As + j * lds;
-    const double* vc = Vs + k * lds;
-    double a0 = 0.0, a1 = 0.0;
-    int i = 0;
-    for (; i + 1 < nrows; i += 2) {
-      a0 = fma(vc[i], ac[i], a0);
-      a1 = fma(vc[i + 1], ac[i + 1], a1);
+  // ---- phase 1: partial W(k, j) over this block; thread -> (column j, row group) ----
+  const int ngrp = nr >= WU_THREADS ? 1 : WU_THREADS / nr;
+  double* mypart = p.part + (int64_t)blockIdx.x * nr * 16;  // [j][16]
+  for (int jb = 0; jb < nr; jb += WU_THREADS) {
+    const int j = jb + (threadIdx.x % (nr < WU_THREADS ? nr : WU_THREADS));
+    const int grp = threadIdx.x / (nr < WU_THREADS ? nr : WU_THREADS);
+    const bool live = grp < ngrp && j < nr;
+    double acc[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) acc[k] = 0.0;
+    if (live) {
+      const double* ac = As + j * lds;
+      for (int i = grp; i < nrows; i += ngrp) {
+        const double av = ac[i];
+        const double2* vr = reinterpret_cast<const double2*>(Vr + i * 16);
+#pragma unroll
+        for (int k2 = 0; k2 < 8; k2++) {
+          const double2 vv = vr[k2];
+          acc[2 * k2] = fma(vv.x, av, acc[2 * k2]);
+          acc[2 * k2 + 1] = fma(vv.y, av, acc[2 * k2 + 1]);
+        }
+      }
     }
-    if (i < nrows) a0 = fma(vc[i], ac[i], a0);
-    mypart[(int64_t)k * nr + j] = a0 + a1;
+    if (ngrp > 1) {
+      // combine the row groups in group order (deterministic)
+      if (live && grp > 0)
+#pragma unroll
+        for (int k = 0; k < 16; k++) red[((grp - 1) * nr + j) * 17 + k] = acc[k];
+      __syncthreads();
+      if (live && grp == 0) {
+        for (int g2 = 1; g2 < ngrp; g2++)
+#pragma unroll
+          for (int k = 0; k < 16; k++) acc[k] += red[((g2 - 1) * nr + j) * 17 + k];
+      }
+      __syncthreads();
+    }
+    if (live && grp == 0) {
+      double2* dst = reinterpret_cast<double2*>(mypart + (int64_t)j * 16);
+#pragma unroll
+      for (int k2 = 0; k2 < 8; k2++) __stcg(dst + k2, make_double2(acc[2 * k2], acc[2 * k2 + 1]));
+    }
   }
   unsigned int gen = 0;
   grid_barrier(p.bar, gen);
-  // phase 2: CTA g owns columns j = g, g+G, ...: W(:, j) = sum over CTAs (fixed order), W2(:, j) = T^T W(:, j)
+  // ---- phase 2: CTA g owns columns j = g, g+G, ...: W(:, j) = sum over CTAs (fixed order), W2 = T^T W ----
   __shared__ double wcol[16];
   __shared__ double wchunk[16][17];
   for (int j = blockIdx.x; j < nr; j += G) {
@@ -543,17 +575,15 @@ __global__ void __launch_bounds__(WU_THREADS) wy_update_kernel(const WyUpdateArg
       const int per = (G + 15) / 16;
       const int g0 = ch * per, g1 = min(G, g0 + per);
       double acc = 0.0;
-      if (k < w) {
-        double vals[10];
-        int g = g0;
-        for (; g + 10 <= g1; g += 10) {
+      double vals[10];
+      int g = g0;
+      for (; g + 10 <= g1; g += 10) {
 #pragma unroll
-          for (int u = 0; u < 10; u++) vals[u] = __ldcg(p.part + ((int64_t)(g + u) * w + k) * nr + j);
+        for (int u = 0; u < 10; u++) vals[u] = __ldcg(p.part + ((int64_t)(g + u) * nr + j) * 16 + k);
 #pragma unroll
-          for (int u = 0; u < 10; u++) acc += vals[u];
-        }
-        for (; g < g1; g++) acc += __ldcg(p.part + ((int64_t)g * w + k) * nr + j);
+        for (int u = 0; u < 10; u++) acc += vals[u];
       }
+      for (; g < g1; g++) acc += __ldcg(p.part + ((int64_t)g * nr + j) * 16 + k);
       wchunk[k][ch] = acc;
     }
     __syncthreads();
@@ -563,38 +593,75 @@ __global__ void __launch_bounds__(WU_THREADS) wy_update_kernel(const WyUpdateArg
       wcol[threadIdx.x] = acc;
     }
     __syncthreads();
-    if (threadIdx.x < w) {
-      // (T^T W)_k = sum_{l <= k} T(l, k) W_l   (T upper triangular)
+    if (threadIdx.x < 16) {
+      // (T^T W)_k = sum_{l <= k} T(l, k) W_l   (T upper triangular); zero beyond w
       double acc = 0.0;
-      for (int l = 0; l <= threadIdx.x; l++) acc += p.t[(int64_t)threadIdx.x * p.ldt + l] * wcol[l];
-      p.w2[(int64_t)j * w + threadIdx.x] = acc;
+      if (threadIdx.x < w)
+        for (int l = 0; l <= threadIdx.x; l++) acc += p.t[(int64_t)threadIdx.x * p.ldt + l] * wcol[l];
+      p.w2[(int64_t)j * 16 + threadIdx.x] = acc;
     }
     __syncthreads();
   }
   grid_barrier(p.bar, gen);
-  // phase 3: A(i, j) -= sum_k V(i, k) W2(k, j) on this CTA's rows, from the staged block
-  for (int idx = threadIdx.x; idx < w * nr; idx += WU_THREADS) W2s[idx] = __ldcg(p.w2 + idx);
-  __syncthreads();
-  for (int e = threadIdx.x; e < nrows * nr; e += WU_THREADS) {
-    const int j = e / nrows, i = e - j * nrows;
-    const double* w2c = W2s + (int64_t)j * w;
-    double acc = 0.0;
-    for (int k = 0; k < w; k++) acc = fma(Vs[k * lds + i], w2c[k], acc);
-    p.a[(int64_t)j * p.lda + r0 + i] = As[j * lds + i] - acc;
+  // ---- phase 3: A(i, j) -= V(i, :) W2(:, j); thread -> (column j, row group), result back into As ----
+  for (int jb = 0; jb < nr; jb += WU_THREADS) {
+    const int j = jb + (threadIdx.x % (nr < WU_THREADS ? nr : WU_THREADS));
+    const int grp = threadIdx.x / (nr < WU_THREADS ? nr : WU_THREADS);
+    if (grp < ngrp && j < nr) {
+      double w2[16];
+      const double2* src = reinterpret_cast<const double2*>(p.w2 + (int64_t)j * 16);
+#pragma unroll
+      for (int k2 = 0; k2 < 8; k2++) {
+        const double2 t2 = __ldcg(src + k2);
+        w2[2 * k2] = t2.x;
+        w2[2 * k2 + 1] = t2.y;
+      }
+      double* ac = As + j * lds;
+      for (int i = grp; i < nrows; i += ngrp) {
+        const double2* vr = reinterpret_cast<const double2*>(Vr + i * 16);
+        double acc = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 < 8; k2++) {
+          const double2 vv = vr[k2];
+          acc = fma(vv.x, w2[2 * k2], acc);
+          acc = fma(vv.y, w2[2 * k2 + 1], acc);
+        }
+        ac[i] -= acc;
+      }
+    }
   }
+  __syncthreads();
+  // coalesced write-back
+  for (int e = threadIdx.x; e < nr * nrows; e += WU_THREADS) {
+    const int j = e / nrows, i = e - j * nrows;
+    p.a[(int64_t)j * p.lda + r0 + i] = As[j * lds + i];
+  }
+}
+
+static size_t wy_update_smem(int64_t mm, int nr, int* G_out, int* rows_out) {
+  int G = (int)ceil_div(mm, 32);
+  if (G > kSMs) G = kSMs;
+  if (G < 1) G = 1;
+  const int rows_per = (int)ceil_div(mm, G);
+  const int ngrp = nr >= WU_THREADS ? 1 : WU_THREADS / nr;
+  if (G_out) *G_out = G;
+  if (rows_out) *rows_out = rows_per;
+  return ((size_t)rows_per * 16 + (size_t)(rows_per | 1) * nr + (ngrp > 1 ? (size_t)(ngrp - 1) * nr * 17 : 0)) *
+         sizeof(double);
+}
+
+bool wy_update_fits(int64_t mm, int nr, int w) {
+  return w <= 16 && nr > 0 && mm > 0 && wy_update_smem(mm, nr, nullptr, nullptr) <= 200 * 1024;
 }
 
 int wy_update(double* a, int64_t lda, int64_t mm, int nr, const double* v, int64_t ldv, const double* t, int64_t ldt,
               int w, double* scratch, size_t scratch_bytes, unsigned int* bar, cudaStream_t st, int64_t* launches) {
   if (nr <= 0 || mm <= 0) return RQ_OK;
   if (w > 16) return set_error(RQ_EINTERNAL, "wy_update: width %d > 16", w);
-  int G = (int)ceil_div(mm, 32);
-  if (G > kSMs) G = kSMs;
-  if (G < 1) G = 1;
-  const int rows_per = (int)ceil_div(mm, G);
-  const size_t smem = ((size_t)(rows_per | 1) * (nr + w) + (size_t)w * nr) * sizeof(double);
+  int G = 0, rows_per = 0;
+  const size_t smem = wy_update_smem(mm, nr, &G, &rows_per);
   if (smem > 200 * 1024) return set_error(RQ_EINTERNAL, "wy_update: %lld rows too many", (long long)mm);
-  const size_t need = ((size_t)G * w * nr + (size_t)w * nr) * sizeof(double);
+  const size_t need = ((size_t)G * 16 * nr + (size_t)16 * nr) * sizeof(double);
   if (need > scratch_bytes) return set_error(RQ_EINTERNAL, "wy_update: scratch too small");
   WyUpdateArgs p;
   p.a = a;
@@ -608,7 +675,7 @@ int wy_update(double* a, int64_t lda, int64_t mm, int nr, const double* v, int64
   p.w = w;
   p.rows_per = rows_per;
   p.part = scratch;
-  p.w2 = scratch + (size_t)G * w * nr;
+  p.w2 = scratch + (size_t)G * 16 * nr;
   p.bar = bar;
   static bool attr = false;
   if (!attr) {
