@@ -18,9 +18,18 @@ namespace rq {
 // depend on the recurrence and are issued one step ahead.  acc lives in
 // registers (lane l owns rows l, l+32, ...).
 // ---------------------------------------------------------------------------
+// Columns of G are prefetched TR_DEPTH steps ahead through a register ring: a
+// step is ~100 cycles of dependent work, an L2 load ~600.
 template <int RPL>
-__global__ void tinv_kernel(const double* __restrict__ G, int64_t ldg, int k, double* __restrict__ T, int64_t ldt) {
+struct TrDepth {
+  static constexpr int value = RPL >= 16 ? 3 : 8;  // register budget
+};
+
+template <int RPL>
+__global__ void __launch_bounds__(128) tinv_kernel(const double* __restrict__ G, int64_t ldg, int k,
+                                                   double* __restrict__ T, int64_t ldt) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int TR_DEPTH = TrDepth<RPL>::value;
   const int j = blockIdx.x * (blockDim.x >> 5) + warp;
   if (j >= k) return;
   double acc[RPL], t[RPL];
@@ -29,33 +38,35 @@ __global__ void tinv_kernel(const double* __restrict__ G, int64_t ldg, int k, do
     acc[r] = 0.0;
     t[r] = 0.0;
   }
-  double g[RPL];
+  // ring[d] holds G(i, kk) (i < kk) for the column kk = kb - d of the current group
+  double ring[TR_DEPTH][RPL];
 #pragma unroll
-  for (int r = 0; r < RPL; r++) {
-    const int i = lane + 32 * r;
-    g[r] = (i < j) ? __ldg(G + (int64_t)j * ldg + i) : 0.0;
-  }
-  for (int kk = j; kk >= 0; kk--) {
-    // prefetch column kk-1 while this step completes
-    double gn[RPL];
+  for (int d = 0; d < TR_DEPTH; d++)
 #pragma unroll
     for (int r = 0; r < RPL; r++) {
-      const int i = lane + 32 * r;
-      gn[r] = (kk > 0 && i < kk - 1) ? __ldg(G + (int64_t)(kk - 1) * ldg + i) : 0.0;
+      const int i = lane + 32 * r, kk = j - d;
+      ring[d][r] = (kk >= 0 && i < kk) ? __ldg(G + (int64_t)kk * ldg + i) : 0.0;
     }
-    // t_kk from acc_kk (held by lane kk % 32, slot kk / 32)
-    double sel = 0.0;
-    const int rk = kk >> 5;
+  for (int kb = j; kb >= 0; kb -= TR_DEPTH) {
 #pragma unroll
-    for (int r = 0; r < RPL; r++) sel = (r == rk) ? acc[r] : sel;
-    const double a = __shfl_sync(0xffffffffu, sel, kk & 31);
-    const double tk = (kk == j) ? 2.0 : -2.0 * a;
+    for (int d = 0; d < TR_DEPTH; d++) {
+      const int kk = kb - d;
+      if (kk < 0) break;
+      // t_kk from acc_kk (held by lane kk % 32, slot kk / 32)
+      double sel = 0.0;
+      const int rk = kk >> 5;
 #pragma unroll
-    for (int r = 0; r < RPL; r++) {
-      const int i = lane + 32 * r;
-      if (i == kk) t[r] = tk;
-      acc[r] = fma(g[r], tk, acc[r]);  // g is zero for i >= kk
-      g[r] = gn[r];
+      for (int r = 0; r < RPL; r++) sel = (r == rk) ? acc[r] : sel;
+      const double a = __shfl_sync(0xffffffffu, sel, kk & 31);
+      const double tk = (kk == j) ? 2.0 : -2.0 * a;
+      const int kn = kk - TR_DEPTH;
+#pragma unroll
+      for (int r = 0; r < RPL; r++) {
+        const int i = lane + 32 * r;
+        if (i == kk) t[r] = tk;
+        acc[r] = fma(ring[d][r], tk, acc[r]);  // zero for i >= kk
+        ring[d][r] = (kn >= 0 && i < kn) ? __ldg(G + (int64_t)kn * ldg + i) : 0.0;
+      }
     }
   }
 #pragma unroll
@@ -70,47 +81,51 @@ __global__ void tinv_kernel(const double* __restrict__ G, int64_t ldg, int k, do
 // Exactly-zero pivots (exactly rank-deficient input) give zero rows/columns,
 // i.e. a generalised inverse, so the downdated sketch stays finite.
 template <int RPL>
-__global__ void trinv_upper_kernel(const double* __restrict__ R, int64_t ldr, int k, double* __restrict__ X,
-                                   int64_t ldx) {
+__global__ void __launch_bounds__(128) trinv_upper_kernel(const double* __restrict__ R, int64_t ldr, int k,
+                                                          double* __restrict__ X, int64_t ldx) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int TR_DEPTH = TrDepth<RPL>::value;
   const int j = blockIdx.x * (blockDim.x >> 5) + warp;
   if (j >= k) return;
-  double acc[RPL], xv[RPL], g[RPL];
+  double acc[RPL], xv[RPL];
 #pragma unroll
   for (int r = 0; r < RPL; r++) {
     acc[r] = 0.0;
     xv[r] = 0.0;
   }
   // x_kk = (delta_kj - acc_kk) / R_kk ;  acc_i += R(i, kk) x_kk  (i < kk)
+  double ring[TR_DEPTH][RPL];  // R(i, kk), i <= kk
 #pragma unroll
-  for (int r = 0; r < RPL; r++) {
-    const int i = lane + 32 * r;
-    g[r] = (i <= j) ? __ldg(R + (int64_t)j * ldr + i) : 0.0;
-  }
-  for (int kk = j; kk >= 0; kk--) {
-    double gn[RPL];
+  for (int d = 0; d < TR_DEPTH; d++)
 #pragma unroll
     for (int r = 0; r < RPL; r++) {
-      const int i = lane + 32 * r;
-      gn[r] = (kk > 0 && i <= kk - 1) ? __ldg(R + (int64_t)(kk - 1) * ldr + i) : 0.0;
+      const int i = lane + 32 * r, kk = j - d;
+      ring[d][r] = (kk >= 0 && i <= kk) ? __ldg(R + (int64_t)kk * ldr + i) : 0.0;
     }
-    double sa = 0.0, sd = 0.0;
-    const int rk = kk >> 5;
+  for (int kb = j; kb >= 0; kb -= TR_DEPTH) {
 #pragma unroll
-    for (int r = 0; r < RPL; r++) {
-      sa = (r == rk) ? acc[r] : sa;
-      sd = (r == rk) ? g[r] : sd;  // diagonal R_kk sits in column kk at row kk
-    }
-    const double a = __shfl_sync(0xffffffffu, sa, kk & 31);
-    const double d = __shfl_sync(0xffffffffu, sd, kk & 31);
-    const double rhs = ((kk == j) ? 1.0 : 0.0) - a;
-    const double xk = (d != 0.0) ? rhs / d : 0.0;
+    for (int d = 0; d < TR_DEPTH; d++) {
+      const int kk = kb - d;
+      if (kk < 0) break;
+      double sa = 0.0, sd = 0.0;
+      const int rk = kk >> 5;
 #pragma unroll
-    for (int r = 0; r < RPL; r++) {
-      const int i = lane + 32 * r;
-      if (i == kk) xv[r] = xk;
-      if (i < kk) acc[r] = fma(g[r], xk, acc[r]);
-      g[r] = gn[r];
+      for (int r = 0; r < RPL; r++) {
+        sa = (r == rk) ? acc[r] : sa;
+        sd = (r == rk) ? ring[d][r] : sd;  // diagonal R_kk sits in column kk at row kk
+      }
+      const double a = __shfl_sync(0xffffffffu, sa, kk & 31);
+      const double dg = __shfl_sync(0xffffffffu, sd, kk & 31);
+      const double rhs = ((kk == j) ? 1.0 : 0.0) - a;
+      const double xk = (dg != 0.0) ? rhs / dg : 0.0;
+      const int kn = kk - TR_DEPTH;
+#pragma unroll
+      for (int r = 0; r < RPL; r++) {
+        const int i = lane + 32 * r;
+        if (i == kk) xv[r] = xk;
+        if (i < kk) acc[r] = fma(ring[d][r], xk, acc[r]);
+        ring[d][r] = (kn >= 0 && i <= kn) ? __ldg(R + (int64_t)kn * ldr + i) : 0.0;
+      }
     }
   }
 #pragma unroll

@@ -264,10 +264,11 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
   __shared__ double wpart[LR_WARPS][32];
   __shared__ double pin[2][16][32];               // pushed CTA partials, by step parity
   __shared__ double rowj[16];                     // row j of this CTA (if it owns it), window order
-  __shared__ double sc[16];                       // reflector coefficients, window order (o = c - j)
+  __shared__ double rowp[2][16];                  // row j pushed by its owner, by step parity
+  __shared__ double sc[17];                       // reflector coefficients of step j-1 (o = c - j + 1), sc[16] = 0
   __shared__ double scal[4];                      // refl, beta, h*inv, inv
   __shared__ double Ts[16][17];
-  const unsigned CS = gridDim.x;
+  constexpr unsigned CS = 16;  // launch_leaf_reg: one 16-CTA cluster
   const unsigned rank = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = (int64_t)rank * rows_per;
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
     }
   }
   for (int e = threadIdx.x; e < 16 * 17; e += LR_THREADS) (&Ts[0][0])[e] = 0.0;
+  if (threadIdx.x < 17) sc[threadIdx.x] = 0.0;
   double uprev[RPT];
 #pragma unroll
   for (int q = 0; q < RPT; q++) uprev[q] = 0.0;
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
     if (refl_prev && !final_round) {
       double s[WL];
 #pragma unroll
-      for (int o = 0; o < WL; o++) s[o] = sc[o];
+      for (int o = 0; o < WL; o++) s[o] = sc[o + 1];  // window shifted by one since step j-1
 #pragma unroll
       for (int q = 0; q < RPT; q++)
 #pragma unroll
@@ -346,29 +348,39 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
       double sum = 0.0;
 #pragma unroll
       for (int ww = 0; ww < LR_WARPS; ww++) sum += wpart[ww][lane];
-      for (unsigned dst = warp; dst < CS; dst += LR_WARPS) dsmem_st(&pin[par][rank][lane], dst, sum);
+      const bool owner = !final_round && (unsigned)(j / rows_per) == rank;  // this CTA holds row j
+      const double rv = (owner && lane < 16) ? rowj[lane] : 0.0;
+#pragma unroll
+      for (unsigned dst = warp; dst < CS; dst += LR_WARPS) {
+        dsmem_st(&pin[par][rank][lane], dst, sum);
+        if (owner && lane < 16) dsmem_st(&rowp[par][lane], dst, rv);
+      }
     }
     leaf_stamp(j, 4);
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     leaf_stamp(j, 5);
-    if (warp == 0) {
+    if (warp <= 1) {
       double t = 0.0;
-      for (unsigned r = 0; r < CS; r++) t += pin[par][r][lane];  // rank order
-      // T column j-1 from the Gram totals (lanes 16.. hold gram k = lane - 16)
-      if (j >= 1) {
-        const int jc = j - 1;
-        double tcol = 0.0;
-        for (int k = jc - 1; k >= 0; k--) {
-          const double g = __shfl_sync(0xffffffffu, t, 16 + k);
-          if (lane <= k) tcol += Ts[lane][k] * g;
+      double pv[CS];
+#pragma unroll
+      for (unsigned r = 0; r < CS; r++) pv[r] = pin[par][r][lane];
+#pragma unroll
+      for (unsigned r = 0; r < CS; r++) t += pv[r];  // rank order
+      if (warp == 1) {
+        // T column j-1 from the Gram totals (lanes 16.. hold gram k = lane - 16); off the critical path
+        if (j >= 1) {
+          const int jc = j - 1;
+          double tcol = 0.0;
+          for (int kk = jc - 1; kk >= 0; kk--) {
+            const double g = __shfl_sync(0xffffffffu, t, 16 + kk);
+            if (lane <= kk) tcol += Ts[lane][kk] * g;
+          }
+          if (lane < jc) Ts[lane][jc] = -2.0 * tcol;
+          if (lane == 0) Ts[jc][jc] = 2.0;
         }
-        if (lane < jc) Ts[lane][jc] = -2.0 * tcol;
-        if (lane == 0) Ts[jc][jc] = 2.0;
-      }
-      if (!final_round) {
-        // row j entries (window order) from the CTA that owns row j
-        const unsigned jrank = (unsigned)(j / rows_per);
-        const double rj = (lane < 16 && j + lane < w) ? dsmem_ld(&rowj[lane], jrank) : 0.0;
+      } else if (!final_round) {
+        // row j entries (window order), pushed by the CTA that owns row j
+        const double rj = (lane < 16 && j + lane < w) ? rowp[par][lane] : 0.0;
         const double tail = __shfl_sync(0xffffffffu, t, 0);
         const double xjj = __shfl_sync(0xffffffffu, rj, 0);
         const double normsq = xjj * xjj + tail;
@@ -413,17 +425,7 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
       for (int o = 0; o + 1 < WL; o++) x[q][o] = x[q][o + 1];
       x[q][WL - 1] = 0.0;
     }
-    // the coefficient window shifts with the columns (sc is rewritten next step)
     refl_prev = refl;
-    if (refl) {
-      __syncthreads();
-      if (threadIdx.x < 16) {
-        const double nxt = (threadIdx.x + 1 < 16) ? sc[threadIdx.x + 1] : 0.0;
-        __syncwarp(0xffffu);
-        sc[threadIdx.x] = nxt;
-      }
-      __syncthreads();
-    }
   }
   __syncthreads();
   // write back V (R columns were written as they left the window)
@@ -747,6 +749,7 @@ int leaf_qr(const LeafCall& c, cudaStream_t st, int64_t* launches) {
     const int64_t rows_per = ceil_div(c.mm, 16);
     if (rows_per <= 1 * LR_THREADS && c.w <= 16) return launch_leaf_reg<16, 1>(c, st, launches);
     if (rows_per <= 2 * LR_THREADS && c.w <= 16) return launch_leaf_reg<16, 2>(c, st, launches);
+    if (rows_per <= 3 * LR_THREADS && c.w <= 16) return launch_leaf_reg<16, 3>(c, st, launches);
     if (rows_per <= 4 * LR_THREADS && c.w <= 16) return launch_leaf_reg<16, 4>(c, st, launches);
     if (rows_per <= 8 * LR_THREADS && c.w <= 8) return launch_leaf_reg<8, 8>(c, st, launches);
     if (rows_per <= 16 * LR_THREADS && c.w <= 4) return launch_leaf_reg<4, 16>(c, st, launches);

@@ -53,18 +53,19 @@ if "sweep" in which:
         ms = timeit(run)
         print(f"cpqr sweep {m}x{n} steps={steps}: {ms*1e3:.0f} us  ({ms*1e3/steps:.2f} us/step)")
 if "sketch" in which:
-    for (m, n, steps) in [(272, 40000, 256), (272, 20000, 256), (272, 11800, 256), (272, 10000, 256), (272, 5000, 256), (272, 1000, 256), (74, 2000, 64)]:
-        y0 = rng.standard_normal((m, n))
-        buf, ld = dev(y0)
-        work, _ = eng.alloc_matrix(m, n)
-        ch = torch.zeros(steps, dtype=torch.int32, device=eng.device)
+    for _ in [0]:
+        for (m, n, steps) in [(272, 40000, 256), (272, 20000, 256), (272, 11800, 256), (272, 10000, 256), (272, 5000, 256), (272, 1000, 256), (74, 2000, 64)]:
+            y0 = rng.standard_normal((m, n))
+            buf, ld = dev(y0)
+            work, _ = eng.alloc_matrix(m, n)
+            ch = torch.zeros(steps, dtype=torch.int32, device=eng.device)
 
-        def run():
-            work.copy_(buf)
-            check(lib.rq_test_sketch_cpqr(eng.handle, ctypes.c_void_p(work.data_ptr()), ld, m, n, steps,
-                                          ctypes.c_void_p(ch.data_ptr())))
-        ms = timeit(run)
-        print(f"sketch cpqr {m}x{n} steps={steps}: {ms*1e3:.0f} us  ({ms*1e3/steps:.2f} us/step)")
+            def run():
+                work.copy_(buf)
+                check(lib.rq_test_sketch_cpqr(eng.handle, ctypes.c_void_p(work.data_ptr()), ld, m, n, steps,
+                                              ctypes.c_void_p(ch.data_ptr())))
+            ms = timeit(run)
+            print(f"sketch cpqr {m}x{n} steps={steps}: {ms*1e3:.0f} us  ({ms*1e3/steps:.2f} us/step)")
 if "leaf" in which:
     for (mm, w) in [(10000, 16), (10000, 32), (5000, 32), (2000, 32), (40000, 8)]:
         a0 = rng.standard_normal((mm, w))
@@ -115,9 +116,9 @@ if "skstamps" in which:
     h = np.zeros(512, dtype=np.uint64)
     check(lib.rq_test_debug_timing(0, h.ctypes.data_as(ctypes.c_void_p), 512))
     h = h.reshape(64, 8).astype(np.int64)
-    d = np.diff(h[5:60, :6], axis=1)
+    d = np.diff(h[5:60, :7], axis=1)
     print(f"sketch cpqr phase cycles n={n} (median over steps 5..60):")
-    names = ["phaseA", "sync", "cta argmax+publish", "arrive/last-reduces/poll", "u+pos"]
+    names = ["A: apply+score", "sync", "B: cta best + column", "C: arrive/last-reduces/poll", "E: u+pos", "-"]
     for k, nm in enumerate(names):
         print(f"  {nm:20s} {int(np.median(d[:, k])):6d}")
     print("  step total          ", int(np.median(h[6:60, 0] - h[5:59, 0])))
