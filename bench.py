@@ -20,8 +20,10 @@ Metric: fp64 TFLOP/s on the (4/3) n^3 count.
   nothing to compile) on this host's cores, over a bounded sample: the first
   `--ref-panels` panels of the same factorization, credited with their share
   of the 4/3 n^3 count (sum of 4 m' b n2 over the sampled panels).
-N > 1: independent replicas (one factorization per rank, weak scaling); the
-1-D block-cyclic NCCL version is not built yet.
+N > 1 (torchrun, one rank per GPU, NCCL): the 1-D block-cyclic driver
+(paper_1505_08115_b200/dist.py) factors ONE n x n matrix spread
+over the ranks (strong scaling: value = whole-job (4/3) n^3 / max-over-ranks
+device time).  `--dist` runs that driver at N = 1 as well.
 """
 
 from __future__ import annotations
@@ -158,6 +160,138 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def trailing_flops_rank(m, n, b, world, rank):
+    """Algorithmic trailing-update flops of one rank's columns (block-cyclic)."""
+    from paper_1505_08115_b200.dist import BlockCyclic
+
+    lay = BlockCyclic(n, b, world)
+    tot, s, i = 0.0, 0, 0
+    while n - s > b:
+        mp = m - s
+        n2 = lay.n_local(rank) - lay.local_from(rank, i + 1)
+        tot += 4.0 * mp * b * n2 + 3.0 * b * b * n2
+        s += b
+        i += 1
+    return tot
+
+
+def run_distributed(args, dist, rank, world, local):
+    """One n x n factorization spread over `world` GPUs (dist.py), timed on the device."""
+    import torch
+
+    import paper_1505_08115_b200 as rq
+    from paper_1505_08115_b200 import dist as rqd
+    from paper_1505_08115_b200.errors import check
+
+    n, b, p = args.n, args.b, args.p
+    m = n
+    stream = torch.cuda.Stream()
+    eng = rq.Engine(local, stream=stream)
+    se = rqd.CudaStepEngine(eng)
+    cfg = rq.BlockConfig(b, rq.SketchConfig(b, p, 0))
+    with torch.cuda.stream(stream):
+        a_full, _ = rq.gaussian_matrix_device(m, n, rq.RngState(0), engine=eng)
+        a0_loc, lda = rqd.scatter_columns(a_full, m, n, b, world, rank, se)
+        del a_full
+        work = torch.empty_like(a0_loc)
+    nloc = rqd.BlockCyclic(n, b, world).n_local(rank)
+
+    def step():
+        with torch.cuda.stream(stream):
+            work.copy_(a0_loc)
+            rqd.factorize_local(work, lda, m, n, cfg, rq.RngState(1), engine=se)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    time.sleep(0.3)
+    check(eng.lib.rq_set_profiling(eng.handle, 1))
+    launches0 = eng.launches
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = eng.launches - launches0
+    clk = clocks.stop()
+    cats = {}
+    for c, name in enumerate(["trailing_gemm", "other_gemm", "sketch_cpqr", "panel_leaf", "other", "small_cpqr",
+                              "sketch_gemm", "panel_gemm", "tfactor"]):
+        t, f, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        check(eng.lib.rq_profile_read(eng.handle, c, ctypes.byref(t), ctypes.byref(f), ctypes.byref(k)))
+        cats[name] = {"ms": t.value / args.steps, "launches": k.value // args.steps}
+    check(eng.lib.rq_set_profiling(eng.handle, 0))
+    tt = torch.tensor([ms], device=eng.device, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_max = float(tt.item())
+    flops_step = 4.0 / 3.0 * n ** 3
+    value = args.steps * flops_step / (ms_max * 1e-3) / 1e12
+    t_trail = cats["trailing_gemm"]["ms"]
+    achieved = trailing_flops_rank(m, n, b, world, rank) / (t_trail * 1e-3) / 1e12 if t_trail > 0 else None
+
+    e2e = None
+    if not args.no_e2e:
+        # host (pinned) local columns -> device -> factorize -> local R columns back to the host
+        ha = torch.empty_like(a0_loc, device="cpu").pin_memory()
+        ha.copy_(a0_loc.cpu())
+        hr = torch.empty_like(ha).pin_memory()
+
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                work.copy_(ha, non_blocking=True)
+                rqd.factorize_local(work, lda, m, n, cfg, rq.RngState(1), engine=se)
+                hr.copy_(work, non_blocking=True)
+            stream.synchronize()
+
+        e2e_step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        k_e2e = max(1, min(args.steps, 3))
+        for _ in range(k_e2e):
+            e2e_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dt = ev0.elapsed_time(ev1) * 1e-3
+        tt = torch.tensor([dt], device=eng.device, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        e2e = {"value": k_e2e * flops_step / dt / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": m * n * 8, "d2h_bytes_per_step": m * n * 8,
+               "note": "per rank: its block-cyclic columns in and its R columns out (summed over ranks)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg3 HQRRP fp64 n={n} b={b} p={p} q=0, fresh sketch (reference semantics), "
+                                   f"1-D block-cyclic columns over {world} GPU(s)",
+                       "n": n, "b": b, "p": p, "q": 0, "sketch": "fresh", "method": "m1", "matrix": "gauss",
+                       "parallelism": f"block-cyclic columns x{world} (NCCL all-gather / send-recv / broadcast)",
+                       "l2": "inputs (800 MB) larger than L2 (126 MB)"},
+            "fraction_of_fp64_peak": value / (FP64_PEAK_TFLOPS * world),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None, "traffic": None,
+                         "kernel": "gemm_f64_kernel (rank 0's trailing updates, rq_panel_apply)",
+                         "peak_source": "measured DMMA peak, profiles/probe_r01.jsonl"},
+            "breakdown_ms_per_step": cats,
+            "local_columns_rank0": nloc,
+            "clocks": clk,
+            "gpu_launches": launches,
+            "e2e": e2e,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -177,6 +311,7 @@ def main():
     ap.add_argument("--method", default="m1", choices=["m1", "m2", "m3"],
                     help="m1 block_qr permutation pivots (headline), m2 reflector pivots, m3 block_rrqr")
     ap.add_argument("--q", type=int, default=0, help="power iterations of the sketch")
+    ap.add_argument("--dist", action="store_true", help="use the block-cyclic multi-GPU driver even at N = 1")
     ap.add_argument("--matrix", default="gauss", choices=["gauss", "cfg4"],
                     help="gauss: N(0,1) (cfg 3); cfg4: U diag(max(10^(-12j/2000),1e-15)) V^T")
     args = ap.parse_args()
@@ -193,10 +328,19 @@ def main():
 
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.dist:
         import torch.distributed as dist
 
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
+
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.method == "m1" and args.sketch == "fresh" and args.q == 0 and args.matrix == "gauss":
+            return run_distributed(args, dist, rank, world, local)
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": "multi-GPU runs cover m1 fresh q=0 (dist.py)"}))
+        dist.destroy_process_group()
+        return
 
     import paper_1505_08115_b200 as rq
     from paper_1505_08115_b200 import _lib

@@ -107,6 +107,41 @@ int rq_gaussian_matrix(rq_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, u
 /* Plain splitmix64 words (rng.py:29-39) for the bitwise integer-stream pin. */
 int rq_splitmix_words(rq_ctx* ctx, uint64_t seed, uint64_t first, int64_t count, uint64_t* dOut);
 
+/* ---- Panel-step API: one HQRRP panel at a time on caller-owned device buffers.
+ * Used by a driver that owns the column distribution (paper_1505_08115_b200/dist.py,
+ * 1-D block-cyclic columns over ranks).  The pieces are those of
+ * block_qr's panel loop (blocked.py:175-219): pivot selection (pivoting.py:114-129),
+ * qr_tall_pivoted (householder.py:183-198) and the trailing update
+ * (householder.py:105-114).  Buffers: column-major, even leading dimensions,
+ * 16-byte aligned bases. */
+
+/* C (M x N) = alpha op(A) B + beta C, op(A) = A^T (A is K x M, a_mmajor = 0) or A
+ * (A is M x K, a_mmajor = 1); B is K x N.  Views start at element (r0, c0) of
+ * buffers with rows x cols extents (FP64 DMMA GEMM). */
+int rq_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, const double* dA, int64_t lda,
+            int64_t a_rows, int64_t a_cols, int64_t a_r0, int64_t a_c0, const double* dB, int64_t ldb, int64_t b_rows,
+            int64_t b_cols, int64_t b_r0, int64_t b_c0, double* dC, int64_t ldc, double alpha, double beta);
+
+/* select_pivot_permutation on a sketch Y (m x n, destroyed): the steps columns a
+ * column-pivoted QR of Y picks, in order (dChosen, column indices of Y).  dInitPos
+ * (n, or null = 0..n-1) is each column's logical position: ties go to the lower one. */
+int rq_sketch_select(rq_ctx* ctx, double* dY, int64_t ldy, int32_t m, int32_t n, int32_t steps,
+                     const int32_t* dInitPos, int32_t* dChosen);
+
+/* qr_tall_pivoted of the panel dP (mp x b, mp >= b): unpivoted leaf QR, then a
+ * column-pivoted QR of the b x b R'.  On return dP holds R (b x b upper, columns in
+ * P-hat order; zero below), dV the panel reflectors (mp x b, unit u with
+ * H = I - 2uu^T), dT their compact-WY T (b x b), dQ2 the b x b orthogonal factor of
+ * the second stage and dPhat[t] the panel column now at position t. */
+int rq_panel_factor(rq_ctx* ctx, double* dP, int64_t ldp, int64_t mp, int32_t b, double* dV, int64_t ldv, double* dT,
+                    int64_t ldt, double* dQ2, int64_t ldq2, int32_t* dPhat);
+
+/* Trailing update of an mp x n2 block at (r0, c0) of dA (a_rows x a_cols buffer):
+ * A2 <- (I - V T V^T)^T A2, then its top b rows <- Q2^T (top b rows); dQ2 may be null. */
+int rq_panel_apply(rq_ctx* ctx, const double* dV, int64_t ldv, const double* dT, int64_t ldt, const double* dQ2,
+                   int64_t ldq2, int64_t mp, int32_t b, double* dA, int64_t lda, int64_t a_rows, int64_t a_cols,
+                   int64_t r0, int64_t c0, int64_t n2);
+
 /* Test hook: the FP64 DMMA GEMM used by every dense step,
  *   C (M x N) = alpha * op(A) * B + beta * C,  op(A) = A^T (A is K x M, a_mmajor = 0)
  *   or A (A is M x K, a_mmajor = 1); B is K x N.  Views start at element

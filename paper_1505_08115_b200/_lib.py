@@ -54,6 +54,12 @@ _SIGS = {
     "rq_householder_sweep": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i32]),
     "rq_gaussian_matrix": (ctypes.c_int, [_vp, _i64, _i64, _u64, _u64, _vp, _i64]),
     "rq_splitmix_words": (ctypes.c_int, [_vp, _u64, _u64, _i64, _vp]),
+    "rq_gemm": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64,
+                               _i64, _i64, _i64, _i64, _vp, _i64, ctypes.c_double, ctypes.c_double]),
+    "rq_sketch_select": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "rq_panel_factor": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "rq_panel_apply": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i32, _vp, _i64, _i64, _i64,
+                                      _i64, _i64, _i64]),
     "rq_test_gemm": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64,
                                     _i64, _i64, _i64, _i64, _vp, _i64, ctypes.c_double, ctypes.c_double]),
     "rq_test_sketch_cpqr": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp]),

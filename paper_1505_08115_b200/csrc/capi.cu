@@ -243,6 +243,64 @@ int rq_test_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K,
   return c.gemm(M, N, K, A, a_mmajor != 0, B, dC, ldc, alpha, beta);
 }
 
+// ---------------------------------------------------------------------------
+// Panel-step API (multi-GPU driver, dist.py)
+// ---------------------------------------------------------------------------
+static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int rq_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, const double* dA, int64_t lda,
+            int64_t a_rows, int64_t a_cols, int64_t a_r0, int64_t a_c0, const double* dB, int64_t ldb, int64_t b_rows,
+            int64_t b_cols, int64_t b_r0, int64_t b_c0, double* dC, int64_t ldc, double alpha, double beta) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (M < 0 || N < 0 || K < 0) return rq::set_error(RQ_EDIM, "gemm: negative extent");
+  if ((lda & 1) || (ldb & 1) || !al16(dA) || !al16(dB))
+    return rq::set_error(RQ_EVALUE, "gemm: operands need even leading dimensions and 16-byte aligned bases");
+  if (M == 0 || N == 0) return RQ_OK;
+  Ctx& c = ctx->c;
+  const size_t kb = (size_t)rq::kSMs * 256 * 256 * 8;
+  RQ_TRY(c.sarena.reserve(kb));
+  c.kwork = (double*)c.sarena.base;
+  c.kwork_bytes = kb;
+  rq::GemmOperand A{dA, a_rows, a_cols, lda, a_r0, a_c0};
+  rq::GemmOperand B{dB, b_rows, b_cols, ldb, b_r0, b_c0};
+  return c.gemm(M, N, K, A, a_mmajor != 0, B, dC, ldc, alpha, beta);
+}
+
+int rq_sketch_select(rq_ctx* ctx, double* dY, int64_t ldy, int32_t m, int32_t n, int32_t steps,
+                     const int32_t* dInitPos, int32_t* dChosen) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (m <= 0 || n <= 0 || steps < 0 || steps > n || steps > m || ldy < m)
+    return rq::set_error(RQ_EDIM, "sketch_select: bad shape m=%d n=%d steps=%d", m, n, steps);
+  return ctx->c.step_sketch_select(dY, ldy, m, n, steps, dInitPos, dChosen);
+}
+
+int rq_panel_factor(rq_ctx* ctx, double* dP, int64_t ldp, int64_t mp, int32_t b, double* dV, int64_t ldv, double* dT,
+                    int64_t ldt, double* dQ2, int64_t ldq2, int32_t* dPhat) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (b <= 0 || b > 512 || mp < b || ldp < mp || ldv < mp || ldt < b || ldq2 < b)
+    return rq::set_error(RQ_EDIM, "panel_factor: bad shape mp=%lld b=%d", (long long)mp, b);
+  if ((ldp & 1) || (ldv & 1) || (ldt & 1) || (ldq2 & 1) || !al16(dP) || !al16(dV) || !al16(dT) || !al16(dQ2))
+    return rq::set_error(RQ_EVALUE, "panel_factor: buffers need even leading dimensions and 16-byte alignment");
+  return ctx->c.step_panel_factor(dP, ldp, mp, b, dV, ldv, dT, ldt, dQ2, ldq2, dPhat);
+}
+
+int rq_panel_apply(rq_ctx* ctx, const double* dV, int64_t ldv, const double* dT, int64_t ldt, const double* dQ2,
+                   int64_t ldq2, int64_t mp, int32_t b, double* dA, int64_t lda, int64_t a_rows, int64_t a_cols,
+                   int64_t r0, int64_t c0, int64_t n2) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (b <= 0 || b > 512 || mp < b || n2 < 0 || r0 < 0 || c0 < 0 || r0 + mp > a_rows || c0 + n2 > a_cols ||
+      lda < a_rows)
+    return rq::set_error(RQ_EDIM, "panel_apply: bad shape");
+  if ((ldv & 1) || (ldt & 1) || (ldq2 & 1) || (lda & 1) || !al16(dV) || !al16(dT) || !al16(dA) ||
+      (dQ2 && !al16(dQ2)))
+    return rq::set_error(RQ_EVALUE, "panel_apply: buffers need even leading dimensions and 16-byte alignment");
+  return ctx->c.step_panel_apply(dV, ldv, dT, ldt, dQ2, ldq2, mp, b, dA, lda, a_rows, a_cols, r0, c0, n2);
+}
+
 int rq_test_sketch_cpqr(rq_ctx* ctx, double* dY, int64_t ld, int32_t m, int32_t n, int32_t steps, int32_t* dChosen) {
   CTX_CHECK(ctx);
   rq::clear_error();

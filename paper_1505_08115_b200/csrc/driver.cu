@@ -861,11 +861,130 @@ int Ctx::snapshot(double* hW, int64_t ldh) {
   return RQ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Panel-step API: the pieces of factorize_perm (steps 3, 5-9) on caller-owned
+// buffers, for a driver that distributes the columns itself (dist.py, SURVEY
+// section 8(e)).  Scratch comes from `sarena`.
+// ---------------------------------------------------------------------------
+namespace {
+struct StepScratch {
+  double *w1, *w2, *ttop, *gram, *tleaf, *small, *rfin, *kwork, *vpad;
+  size_t kwork_bytes;
+  void* sweep_ws;
+  size_t sweep_ws_bytes;
+  size_t total;
+};
+
+StepScratch plan_step(void* base, int64_t ncols, int b, int64_t mp = 0) {
+  StepScratch S;
+  Carver c(base);
+  const int64_t ldb = even(b);
+  const int64_t nc = std::max<int64_t>(ncols, b);
+  S.w1 = c.take<double>((size_t)ldb * nc);
+  S.w2 = c.take<double>((size_t)ldb * nc);
+  S.ttop = c.take<double>((size_t)ldb * nc);
+  S.gram = c.take<double>((size_t)ldb * b);
+  S.tleaf = c.take<double>(32 * 32);
+  S.small = c.take<double>((size_t)ldb * 2 * b);
+  S.rfin = c.take<double>((size_t)ldb * b);
+  S.kwork_bytes = std::max<size_t>((size_t)kSMs * (b + 1) * b * 8, (size_t)16 * (b + 1) * nc * 8);
+  S.kwork = c.take<double>(S.kwork_bytes / 8);
+  S.sweep_ws_bytes = sweep_workspace_bytes(b, 2 * b, sweep_grid_size(2 * b));
+  S.sweep_ws = c.take<char>(S.sweep_ws_bytes);
+  S.vpad = c.take<double>((size_t)even(mp + 1) * b);  // V at a one-row offset (operand parity)
+  S.total = c.off;
+  return S;
+}
+}  // namespace
+
+int Ctx::step_sketch_select(double* Y, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen) {
+  const size_t ws = sweep_workspace_bytes(m, n, kSMs) + 4096;
+  RQ_TRY(sarena.reserve(ws));
+  sweep_ws = sarena.base;
+  sweep_ws_bytes = ws;
+  return sketch_select(Y, ldy, m, n, steps, init_pos, chosen);
+}
+
+int Ctx::step_panel_factor(double* P, int64_t ldp, int64_t mp, int b, double* V, int64_t ldv, double* T, int64_t ldt,
+                           double* Q2, int64_t ldq2, int* phat) {
+  RQ_TRY(sarena.reserve(plan_step(nullptr, b, b).total));
+  StepScratch S = plan_step(sarena.base, b, b);
+  kwork = S.kwork;
+  kwork_bytes = S.kwork_bytes;
+  sweep_ws = S.sweep_ws;
+  sweep_ws_bytes = S.sweep_ws_bytes;
+  const int64_t lds = even(b);
+  // 5: unpivoted panel QR (V lower trapezoidal: leaves write rows >= their diagonal)
+  RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * b * sizeof(double), stream));
+  launches++;
+  RQ_TRY(panel_qr(P, ldp, mp, b, 0, mp, b, V, ldv, 0, S.tleaf, S.w1, S.w2));
+  // 6: b x b CPQR of R' (reflectors V2), Q2 = I - V2 T2 V2^T
+  double* Sm = S.small;
+  double* V2 = S.small + (int64_t)b * lds;
+  RQ_TRY(copy2d(P, ldp, Sm, lds, b, b, 1, stream, &launches));
+  RQ_CUDA_TRY(cudaMemsetAsync(V2, 0, (size_t)lds * b * sizeof(double), stream));
+  launches++;
+  SweepCall ss;
+  ss.a = Sm;
+  ss.lda = lds;
+  ss.m = b;
+  ss.n = b;
+  ss.steps = b;
+  ss.pivot = 1;
+  ss.v = V2;
+  ss.ldv = lds;
+  ss.col_at_pos = phat;
+  ss.r_out = S.rfin;
+  ss.ldr = lds;
+  RQ_TRY(sweep(ss));
+  Layout L{};
+  L.ttop = S.ttop;
+  L.gram = S.gram;
+  L.w1 = S.w1;
+  L.w2 = S.w2;
+  RQ_TRY(small_q(V2, lds, b, Q2, ldq2, L));
+  // 7: R of the panel (columns in P-hat order)
+  RQ_TRY(copy2d(S.rfin, lds, P, ldp, b, b, 0, stream, &launches));
+  // 8: T of the panel reflectors
+  return tfactor(V, mp, b, ldv, 0, T, ldt, S.gram);
+}
+
+int Ctx::step_panel_apply(const double* V, int64_t ldv, const double* T, int64_t ldt, const double* Q2, int64_t ldq2,
+                          int64_t mp, int b, double* A, int64_t lda, int64_t a_rows, int64_t a_cols, int64_t r0,
+                          int64_t c0, int64_t n2) {
+  if (n2 <= 0 || mp <= 0) return RQ_OK;
+  const bool odd = (r0 & 1) != 0;
+  RQ_TRY(sarena.reserve(plan_step(nullptr, n2, b, odd ? mp : 0).total));
+  StepScratch S = plan_step(sarena.base, n2, b, odd ? mp : 0);
+  kwork = S.kwork;
+  kwork_bytes = S.kwork_bytes;
+  const int64_t ldw = even(b);
+  // the GEMM's K origins of V and A2 must share parity (16-byte TMA coordinates):
+  // for an odd r0, V is staged one row down, as factorize_perm's vpad does
+  GemmOperand Vop = op(V, mp, b, ldv, 0);
+  if (odd) {
+    const int64_t ldp = even(mp + 1);
+    RQ_TRY(copy2d(V, ldv, S.vpad + 1, ldp, mp, b, 0, stream, &launches));
+    Vop = op(S.vpad, mp + 1, b, ldp, 1);
+  }
+  CatGuard guard(cat, PROF_TRAIL);
+  double* A2 = A + r0 + c0 * lda;
+  RQ_TRY(gemm(b, n2, mp, Vop, false, op(A, a_rows, a_cols, lda, r0, c0), S.w1, ldw, 1.0, 0.0));
+  RQ_TRY(gemm(b, n2, b, op(T, b, b, ldt), false, op(S.w1, b, n2, ldw), S.w2, ldw, 1.0, 0.0));
+  RQ_TRY(gemm(mp, n2, b, Vop, true, op(S.w2, b, n2, ldw), A2, lda, -1.0, 1.0));
+  if (Q2) {
+    RQ_TRY(copy2d(A2, lda, S.ttop, ldw, b, n2, 0, stream, &launches));
+    RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldq2), false, op(S.ttop, b, n2, ldw), A2, lda, 1.0, 0.0));
+  }
+  return RQ_OK;
+}
+
 Ctx::~Ctx() {
   if (sk_counter) cudaFree(sk_counter);
   for (auto e : ev_pool) cudaEventDestroy(e);
   arena.release();
   qarena.release();
+  sarena.release();
   if (barriers) cudaFree(barriers);
 }
 

@@ -100,7 +100,7 @@ struct Ctx {
   rq_panel_cb inspect_cb = nullptr;
   void* inspect_user = nullptr;
   int64_t launches = 0;
-  Arena arena, qarena;
+  Arena arena, qarena, sarena;  // factorization, Q/P formation + test hooks, panel-step API
   unsigned int* barriers = nullptr;
   int nbarriers = 0;
   int next_barrier = 0;
@@ -153,6 +153,13 @@ struct Ctx {
   int reflector_pivot(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, Layout& L,
                       void* fc_ptr, uint64_t seed, uint64_t* counter);
   int form_q(int64_t cols, double* Q, int64_t ldq);
+  // Panel-step API for drivers that own the column distribution (multi-GPU, dist.py)
+  int step_sketch_select(double* Y, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen);
+  int step_panel_factor(double* P, int64_t ldp, int64_t mp, int b, double* V, int64_t ldv, double* T, int64_t ldt,
+                        double* Q2, int64_t ldq2, int* phat);
+  int step_panel_apply(const double* V, int64_t ldv, const double* T, int64_t ldt, const double* Q2, int64_t ldq2,
+                       int64_t mp, int b, double* A, int64_t lda, int64_t a_rows, int64_t a_cols, int64_t r0,
+                       int64_t c0, int64_t n2);
   int form_p(double* P, int64_t ldp);
   int snapshot(double* hW, int64_t ldh);
 };

@@ -1,0 +1,442 @@
+"""Multi-GPU HQRRP: 1-D block-cyclic column panels over torch.distributed ranks.
+
+SURVEY section 8(e).  Physical column *slots* are grouped in blocks of b; slot
+block k lives on rank k % G (as its local block k // G, stored contiguously in
+column-major order).  Per panel i (columns s = i*b ..), with owner o = i % G:
+
+1. every rank sketches its own trailing columns, Y_loc = Omega^T A_loc[s:, trailing]
+   (blocked.py:164-172, pivoting.py:80-111; every rank draws the same Omega from
+   the same counter-based stream, so Omega is never sent);
+2. one all-gather of Y; every rank runs the identical column-pivoted QR of Y
+   (pivoting.py:114-129), so the pivot list agrees everywhere with no second
+   exchange;
+3. the <= 2b moved columns travel at full height between ranks (packed per rank
+   pair, batched send/recv); the rest of the matrix never moves;
+4. the owner factors the panel (qr_tall_pivoted, householder.py:183-198) and
+   broadcasts V, T, Q2 and P-hat in one message;
+5. every rank applies the panel to its own trailing columns
+   (householder.py:105-114).
+
+Host bookkeeping -- which original column sits in each slot, and its logical
+position, which decides the reference's ties and "rest in original order"
+(pivoting.py:125-128) -- is replicated and updated identically on every rank.
+After the last panel the slots hold R's columns in the reference's order, so
+``perm[slot]`` is the reference's composite permutation.
+
+Device work goes through an *engine*; the product engine is ``CudaStepEngine``
+(the C ABI's panel-step entry points).  Collectives are torch.distributed calls
+(NCCL between GPUs).  Fresh sketches, q = 0, permutation pivots and m >= n are
+supported; power iterations, reflector pivots and block_rrqr run on one GPU
+(hqrrp.block_qr / block_rrqr).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import DimensionError, check
+from .hqrrp import BlockConfig, Engine, RngState
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class CudaStepEngine:
+    """Panel steps on the GPU through the C ABI (rq_gemm, rq_sketch_select,
+    rq_panel_factor, rq_panel_apply, rq_householder_sweep, rq_gaussian_matrix)."""
+
+    def __init__(self, engine: Engine | None = None):
+        import torch
+
+        self.torch = torch
+        self.eng = engine if engine is not None else Engine()
+        self.lib = self.eng.lib
+        self.h = self.eng.handle
+        self.device = self.eng.device
+
+    # storage convention: column-major rows x cols, tensor of shape (cols, ld), ld even
+    def alloc(self, rows, cols):
+        buf, ld = self.eng.alloc_matrix(rows, cols)
+        buf.zero_()
+        return buf, ld
+
+    def gaussian(self, rows, cols, seed, counter):
+        buf, ld = self.alloc(rows, cols)
+        check(self.lib.rq_gaussian_matrix(self.h, rows, cols, seed, counter, _ptr(buf), ld))
+        return buf, ld
+
+    def sketch(self, om, ldo, a, lda, a_rows, a_cols, r0, c0, mp, nt, wdt, cols_alloc):
+        y, ldy = self.alloc(wdt, max(cols_alloc, 1))
+        if nt > 0:
+            check(self.lib.rq_gemm(self.h, 0, wdt, nt, mp, _ptr(om), ldo, mp, wdt, 0, 0, _ptr(a), lda, a_rows,
+                                   a_cols, r0, c0, _ptr(y), ldy, 1.0, 0.0))
+        return y, ldy
+
+    def select(self, y, ldy, wdt, n, steps, init_pos):
+        torch = self.torch
+        ip = torch.as_tensor(np.asarray(init_pos, dtype=np.int32), device=self.device)
+        ch = torch.empty(steps, dtype=torch.int32, device=self.device)
+        check(self.lib.rq_sketch_select(self.h, _ptr(y), ldy, wdt, n, steps, _ptr(ip), _ptr(ch)))
+        return ch.cpu().numpy().astype(np.int64)
+
+    def panel_factor(self, p, ldp, mp, b):
+        torch = self.torch
+        v, ldv = self.alloc(mp, b)
+        t, ldt = self.alloc(b, b)
+        q2, ldq = self.alloc(b, b)
+        ph = torch.empty(b, dtype=torch.int32, device=self.device)
+        check(self.lib.rq_panel_factor(self.h, _ptr(p), ldp, mp, b, _ptr(v), ldv, _ptr(t), ldt, _ptr(q2), ldq,
+                                       _ptr(ph)))
+        return (v, ldv, t, ldt, q2, ldq), ph.to(torch.int64)
+
+    def panel_apply(self, fac, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
+        v, ldv, t, ldt, q2, ldq = fac
+        check(self.lib.rq_panel_apply(self.h, _ptr(v), ldv, _ptr(t), ldt, _ptr(q2), ldq, mp, b, _ptr(a), lda,
+                                      a_rows, a_cols, r0, c0, n2))
+
+    def final_block(self, blk, ldb, mp, w):
+        """Column-pivoted sweep of an mp x w block in place; returns perm (position t holds column perm[t])."""
+        torch = self.torch
+        v, ldv = self.alloc(mp, w)
+        perm = torch.arange(w, dtype=torch.int64, device=self.device)
+        check(self.lib.rq_householder_sweep(self.h, _ptr(blk), mp, w, ldb, _ptr(v), ldv, _ptr(perm), min(mp, w), 1))
+        return perm
+
+    def synchronize(self):
+        self.torch.cuda.synchronize(self.device)
+
+
+# --------------------------------------------------------------------------
+# 1-D block-cyclic layout of the column slots
+# --------------------------------------------------------------------------
+@dataclass
+class BlockCyclic:
+    n: int
+    b: int
+    world: int
+
+    @property
+    def nblk(self):
+        return -(-self.n // self.b)
+
+    def size(self, k):
+        return min(self.b, self.n - k * self.b)
+
+    def owner(self, k):
+        return k % self.world
+
+    def local_off(self, k):
+        """Local column offset of slot block k on its owner (every block but the last is full)."""
+        return (k // self.world) * self.b
+
+    def n_local(self, r):
+        return sum(self.size(k) for k in range(r, self.nblk, self.world))
+
+    def first_owned(self, r, k0):
+        """First block index >= k0 owned by rank r, or None."""
+        k = k0 + ((r - k0) % self.world)
+        return k if k < self.nblk else None
+
+    def local_from(self, r, k0):
+        """Local column offset where rank r's blocks k >= k0 start (n_local if none)."""
+        k = self.first_owned(r, k0)
+        return self.n_local(r) if k is None else self.local_off(k)
+
+    def slots_from(self, r, k0):
+        """Physical slots of rank r's blocks k >= k0, in local storage order."""
+        k = self.first_owned(r, k0)
+        if k is None:
+            return np.zeros(0, dtype=np.int64)
+        return np.concatenate([np.arange(kk * self.b, kk * self.b + self.size(kk), dtype=np.int64)
+                               for kk in range(k, self.nblk, self.world)])
+
+    def locate(self, slot):
+        """(owner rank, local column) of a physical slot."""
+        k = slot // self.b
+        return self.owner(k), self.local_off(k) + (slot - k * self.b)
+
+
+def plan_moves(chosen_slots, s, b):
+    """Full-height column moves that put the chosen slots' columns into slots s..s+b-1
+    (in selection order) and the displaced panel columns into the vacated slots.
+    Returns a list of (src_slot, dst_slot)."""
+    chosen = [int(c) for c in chosen_slots]
+    cset = set(chosen)
+    moves = [(c, s + t) for t, c in enumerate(chosen) if c != s + t]
+    displaced = [d for d in range(s, s + b) if d not in cset]
+    vacated = [c for c in chosen if c >= s + b]
+    assert len(displaced) == len(vacated)
+    moves += list(zip(displaced, vacated))
+    return moves
+
+
+def _apply_moves_host(arr, moves):
+    old = arr.copy()
+    for src, dst in moves:
+        arr[dst] = old[src]
+
+
+class _Dist:
+    def __init__(self, group):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def global_rank(self, r):
+        if self.group is None:
+            return r
+        return self.dist.get_global_rank(self.group, r)
+
+
+def _exchange_columns(a_loc, m, lay, rank, moves, d: _Dist, engine):
+    """Execute full-height column moves between ranks: gather every outgoing column
+    first, then write every incoming one (so a slot can be both source and target)."""
+    torch = engine.torch
+    world = d.world
+    send = {q: [] for q in range(world)}  # (move index, local src col) per destination rank
+    recv = {q: [] for q in range(world)}  # (move index, local dst col) per source rank
+    for idx, (src, dst) in enumerate(moves):
+        rs, ls = lay.locate(src)
+        rd, ldst = lay.locate(dst)
+        if rs == rank:
+            send[rd].append((idx, ls))
+        if rd == rank:
+            recv[rs].append((idx, ldst))
+    bufs_out = {}
+    for q, lst in send.items():
+        if lst:
+            cols = torch.as_tensor([c for _, c in lst], dtype=torch.int64, device=a_loc.device)
+            bufs_out[q] = a_loc.index_select(0, cols).contiguous()
+    bufs_in = {}
+    for q, lst in recv.items():
+        if lst:
+            bufs_in[q] = bufs_out[q] if q == rank else torch.empty((len(lst), a_loc.shape[1]), dtype=a_loc.dtype,
+                                                                   device=a_loc.device)
+    ops = []
+    for q in range(world):
+        if q == rank:
+            continue
+        if q in bufs_out:
+            ops.append(d.dist.P2POp(d.dist.isend, bufs_out[q], d.global_rank(q), d.group))
+        if q in bufs_in:
+            ops.append(d.dist.P2POp(d.dist.irecv, bufs_in[q], d.global_rank(q), d.group))
+    if ops:
+        for req in d.dist.batch_isend_irecv(ops):
+            req.wait()
+    for q, lst in recv.items():
+        if lst:
+            cols = torch.as_tensor([c for _, c in lst], dtype=torch.int64, device=a_loc.device)
+            a_loc.index_copy_(0, cols, bufs_in[q])
+
+
+@dataclass
+class DistResult:
+    """Local result of one rank: R's columns in this rank's slots, plus the global perm."""
+
+    a_loc: object      # storage (n_loc, lda): R's columns of the owned slots
+    lda: int
+    m: int
+    n: int
+    layout: BlockCyclic
+    perm: np.ndarray   # perm[j] = original column at position j (A[:, perm] = Q R)
+
+
+def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=None, engine=None):
+    """HQRRP (fresh sketches, permutation pivots) on this rank's block-cyclic columns.
+
+    ``a_loc`` is the (n_local, lda) column-major storage of the slot blocks this rank
+    owns (see ``BlockCyclic``); it is overwritten with the rank's columns of R.
+    ``rng.counter`` advances exactly as in the single-GPU / reference run."""
+    d = _Dist(group)
+    engine = engine if engine is not None else CudaStepEngine()
+    torch = engine.torch
+    b = cfg.block
+    sk = cfg.resolved_sketch()
+    if cfg.pivot_kind != "permutation" or cfg.rrqr:
+        raise NotImplementedError("multi-GPU path: permutation pivots (block_qr) only")
+    if sk.power != 0:
+        raise NotImplementedError("multi-GPU path: power iterations run on one GPU")
+    if m < n:
+        raise DimensionError(f"blocked QR needs rows >= cols, got {m}x{n}")
+    if b < 1 or b > n:
+        raise DimensionError(f"block size must lie in [1, {n}], got {b}")
+    wdt = b + sk.oversample
+    lay = BlockCyclic(n, b, d.world)
+    rank = d.rank
+    nloc = lay.n_local(rank)
+    if a_loc.shape[0] < nloc or lda < m:
+        raise DimensionError("local storage does not hold this rank's columns")
+    # the reference raises before drawing the offending sketch (pivoting.py:97-98)
+    for s in range(0, n, b):
+        if n - s <= b:
+            break
+        if wdt > n - s:
+            bad = s
+            rng.counter += sum((m - t) * wdt for t in range(0, bad, b))
+            raise ValueError(f"sketch width {wdt} exceeds the {n - s} columns being pivoted")
+    slot_orig = np.arange(n, dtype=np.int64)
+    slot_lpos = np.arange(n, dtype=np.int64)
+    counts_cache = {}
+    for i in range(lay.nblk):
+        s = i * b
+        np_ = n - s
+        mp = m - s
+        o = lay.owner(i)
+        if np_ <= b:
+            _final_block(a_loc, lda, m, n, s, i, lay, rank, slot_orig, slot_lpos, d, engine)
+            break
+        # ---- 1: sketch of the local trailing columns (same Omega on every rank) ----
+        om, ldo = engine.gaussian(mp, wdt, rng.seed, rng.counter)
+        rng.counter += mp * wdt
+        counts = counts_cache.get(i)
+        if counts is None:
+            counts = [lay.n_local(q) - lay.local_from(q, i) for q in range(d.world)]
+            counts_cache[i] = counts
+        cmax = max(counts)
+        t0 = lay.local_from(rank, i)
+        y, ldy = engine.sketch(om, ldo, a_loc, lda, m, nloc, s, t0, mp, counts[rank], wdt, cmax)
+        del om
+        # ---- 2: all-gather Y, identical pivot selection everywhere ----
+        if d.world > 1:
+            gathered = torch.empty((d.world * cmax, ldy), dtype=y.dtype, device=y.device)
+            d.dist.all_gather_into_tensor(gathered, y[:cmax].contiguous(), group=d.group)
+            idx = np.concatenate([np.arange(q * cmax, q * cmax + counts[q]) for q in range(d.world)])
+            y_all = gathered.index_select(0, torch.as_tensor(idx, device=y.device)).contiguous()
+            del gathered
+        else:
+            y_all = y[:counts[0]].contiguous()
+        ycol_slot = np.concatenate([lay.slots_from(q, i) for q in range(d.world)])
+        init_pos = slot_lpos[ycol_slot] - s
+        chosen_y = engine.select(y_all, ldy, wdt, np_, b, init_pos)
+        del y, y_all
+        chosen = ycol_slot[chosen_y]
+        # ---- 3: move the chosen columns into the panel slots ----
+        moves = plan_moves(chosen, s, b)
+        _exchange_columns(a_loc, m, lay, rank, moves, d, engine)
+        _apply_moves_host(slot_orig, moves)
+        _apply_moves_host(slot_lpos, moves)
+        rest = np.arange(s + b, n, dtype=np.int64)
+        order = np.argsort(slot_lpos[rest], kind="stable")
+        slot_lpos[rest[order]] = s + b + np.arange(rest.size, dtype=np.int64)
+        slot_lpos[s:s + b] = s + np.arange(b, dtype=np.int64)
+        # ---- 4: panel on the owner; V, T, Q2, P-hat broadcast in one message ----
+        ldv = mp + (mp & 1)
+        ldb = b + (b & 1)
+        nfac = b * ldv + 2 * b * ldb + b
+        pack = torch.empty(nfac, dtype=torch.float64, device=a_loc.device)
+        if rank == o:
+            lo = lay.local_off(i)
+            p, ldp = engine.alloc(mp, b)
+            p[:b, :mp].copy_(a_loc[lo:lo + b, s:m])
+            fac, ph = engine.panel_factor(p, ldp, mp, b)
+            a_loc[lo:lo + b, s:m].copy_(p[:b, :mp])
+            if s > 0:  # rows above follow P-hat
+                a_loc[lo:lo + b, :s] = a_loc[lo:lo + b, :s].index_select(0, ph)
+            v, _, t, _, q2, _ = fac
+            pack[:b * ldv].copy_(v[:b, :ldv].reshape(-1))
+            pack[b * ldv:b * ldv + b * ldb].copy_(t[:b, :ldb].reshape(-1))
+            pack[b * ldv + b * ldb:b * ldv + 2 * b * ldb].copy_(q2[:b, :ldb].reshape(-1))
+            pack[nfac - b:].copy_(ph.to(torch.float64))
+        if d.world > 1:
+            d.dist.broadcast(pack, src=d.global_rank(o), group=d.group)
+        v = pack[:b * ldv].view(b, ldv)
+        t = pack[b * ldv:b * ldv + b * ldb].view(b, ldb)
+        q2 = pack[b * ldv + b * ldb:b * ldv + 2 * b * ldb].view(b, ldb)
+        ph_host = pack[nfac - b:].cpu().numpy().astype(np.int64)
+        slot_orig[s:s + b] = slot_orig[s + ph_host]
+        # ---- 5: trailing update of the local columns ----
+        t1 = lay.local_from(rank, i + 1)
+        n2 = nloc - t1
+        if n2 > 0:
+            engine.panel_apply((v, ldv, t, ldb, q2, ldb), mp, b, a_loc, lda, m, nloc, s, t1, n2)
+        del pack
+    return DistResult(a_loc, lda, m, n, lay, slot_orig)
+
+
+def _final_block(a_loc, lda, m, n, s, i, lay, rank, slot_orig, slot_lpos, d: _Dist, engine):
+    """Last block (n - s <= b columns, one owner): reference order, then a full-height CPQR."""
+    torch = engine.torch
+    w = n - s
+    mp = m - s
+    o = lay.owner(i)
+    order = np.argsort(slot_lpos[s:n], kind="stable")
+    permbuf = torch.empty(w, dtype=torch.float64, device=a_loc.device)
+    if rank == o:
+        lo = lay.local_off(i)
+        idx = torch.as_tensor(lo + order, dtype=torch.int64, device=a_loc.device)
+        a_loc[lo:lo + w] = a_loc.index_select(0, idx)
+        blk, ldb = engine.alloc(mp, w)
+        blk[:w, :mp].copy_(a_loc[lo:lo + w, s:m])
+        perm = engine.final_block(blk, ldb, mp, w)
+        a_loc[lo:lo + w, s:m].copy_(blk[:w, :mp])
+        if s > 0:
+            a_loc[lo:lo + w, :s] = a_loc[lo:lo + w, :s].index_select(0, perm)
+        permbuf.copy_(perm.to(torch.float64))
+    if d.world > 1:
+        d.dist.broadcast(permbuf, src=d.global_rank(o), group=d.group)
+    perm_host = permbuf.cpu().numpy().astype(np.int64)
+    slot_orig[s:n] = slot_orig[s + order]
+    slot_orig[s:n] = slot_orig[s + perm_host]
+    slot_lpos[s:n] = np.arange(s, n)
+
+
+# --------------------------------------------------------------------------
+# Convenience: scatter a full matrix, factorize, gather R on every rank
+# --------------------------------------------------------------------------
+def scatter_columns(a_full_storage, m, n, b, world, rank, engine):
+    """This rank's block-cyclic columns of a full (n, ld) column-major storage."""
+    lay = BlockCyclic(n, b, world)
+    slots = lay.slots_from(rank, 0)
+    buf, lda = engine.alloc(m, max(len(slots), 1))
+    if len(slots):
+        idx = engine.torch.as_tensor(slots, dtype=engine.torch.int64, device=buf.device)
+        buf[:len(slots), :m].copy_(a_full_storage.index_select(0, idx)[:, :m])
+    return buf, lda
+
+
+def gather_r(res: DistResult, engine, group=None):
+    """R (n-column storage (n, lda), reference order) assembled on every rank."""
+    d = _Dist(group)
+    torch = engine.torch
+    lay = res.layout
+    counts = [lay.n_local(q) for q in range(d.world)]
+    cmax = max(counts)
+    local = torch.zeros((cmax, res.lda), dtype=torch.float64, device=res.a_loc.device)
+    local[:counts[d.rank]].copy_(res.a_loc[:counts[d.rank], :res.lda])
+    if d.world > 1:
+        allb = torch.empty((d.world * cmax, res.lda), dtype=torch.float64, device=local.device)
+        d.dist.all_gather_into_tensor(allb, local, group=d.group)
+    else:
+        allb = local
+    full = torch.zeros((res.n, res.lda), dtype=torch.float64, device=local.device)
+    for q in range(d.world):
+        slots = lay.slots_from(q, 0)
+        if len(slots):
+            full.index_copy_(0, torch.as_tensor(slots, device=local.device),
+                             allb[q * cmax:q * cmax + counts[q]])
+    return full
+
+
+def block_qr_distributed(a, cfg: BlockConfig, rng: RngState, *, group=None, engine=None):
+    """``block_qr(a, cfg, rng)`` (blocked.py:175) with the columns spread over the
+    ranks of ``group``; every rank passes the same ``a`` and gets (R, perm) back.
+    R is upper trapezoidal (m x n, numpy), perm as in ``Factorization.perm``."""
+    engine = engine if engine is not None else CudaStepEngine()
+    d = _Dist(group)
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    full, _ = engine.alloc(m, n)
+    full[:n, :m].copy_(engine.torch.from_numpy(np.ascontiguousarray(a.T)))
+    a_loc, lda = scatter_columns(full, m, n, cfg.block, d.world, d.rank, engine)
+    del full
+    res = factorize_local(a_loc, lda, m, n, cfg, rng, group=group, engine=engine)
+    r_full = gather_r(res, engine, group)
+    r = np.asfortranarray(r_full[:n, :m].cpu().numpy().T)
+    return np.triu(r), res.perm
