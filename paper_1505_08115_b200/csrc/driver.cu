@@ -101,6 +101,10 @@ static Layout plan_layout(void* base, int64_t m, int64_t n, int b, int p, int po
   L.ov = c.take<double>((size_t)even(std::max(m, n) + 1) * wdt);
   L.ot = c.take<double>((size_t)even(wdt) * wdt);
   L.oe = c.take<double>((size_t)even(std::max(m, n) + 1) * wdt);
+  L.wside = c.take<double>((size_t)ldb * n);
+  L.gram2 = c.take<double>((size_t)ldb * b);
+  L.kwork2_bytes = std::max<size_t>((size_t)kSMs * (b + 1) * b * 8, (size_t)8 * (b + 1) * n * 8);
+  L.kwork2 = c.take<double>(L.kwork2_bytes / 8);
   L.jw = c.take<double>((size_t)ldb * b);
   L.jv = c.take<double>((size_t)ldb * b);
   L.jd = c.take<double>((size_t)ldb);
@@ -211,7 +215,20 @@ int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_
   p.splitk = 0;  // automatic
   p.work = kwork;
   p.work_bytes = kwork ? kwork_bytes : 0;
+  p.max_ctas = gemm_max_ctas;
   return gemm_f64(p, stream, &launches);
+}
+
+int Ctx::ensure_side() {
+  if (side) return RQ_OK;
+  int lo = 0, hi = 0;
+  RQ_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  RQ_CUDA_TRY(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+  RQ_CUDA_TRY(cudaStreamCreateWithPriority(&hip, cudaStreamNonBlocking, hi));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_v, cudaEventDisableTiming));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_hi, cudaEventDisableTiming));
+  return RQ_OK;
 }
 
 int Ctx::sweep(SweepCall c) {
@@ -511,6 +528,15 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * b * sizeof(double), stream));
     launches++;
     RQ_TRY(panel_qr(A, lda, m, n, s, mp, b, V, ldv, vpad, tleaf, L.w1, L.w2));
+    const int64_t n2 = np - b;
+    // ---- overlap: the b x b CPQR below runs on its 16-SM cluster from a highest-priority
+    //      stream (so it is dispatched first), while W = V^T A2 (half the trailing update)
+    //      and T run on the remaining SMs from a side stream ----
+    static const int env_overlap = [] {
+      const char* e = getenv("RQ_OVERLAP");
+      return e ? atoi(e) : 1;
+    }();
+    const bool overlap = overlap_on && env_overlap != 0 && n2 > 0;
     // ---------------- 6: b x b CPQR of R' (reflectors V2), then Q2 = I - V2 T2 V2^T ----------------
     double* S = L.small;
     double* V2 = L.small + (int64_t)b * L.lds_small;
@@ -529,7 +555,39 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     ss.col_at_pos = L.cap;
     ss.r_out = L.rfin;
     ss.ldr = L.lds_small;
-    RQ_TRY(sweep(ss));
+    if (overlap) {
+      RQ_TRY(ensure_side());
+      RQ_CUDA_TRY(cudaEventRecord(ev_v, stream));
+      RQ_CUDA_TRY(cudaStreamWaitEvent(hip, ev_v, 0));
+      RQ_CUDA_TRY(cudaStreamWaitEvent(side, ev_v, 0));
+      cudaStream_t main_stream = stream;
+      stream = hip;  // the CPQR first: its cluster gets SMs before the side GEMM's CTAs
+      int rc = sweep(ss);
+      if (rc == RQ_OK) rc = cudaEventRecord(ev_hi, hip) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
+      double* kw = kwork;
+      const size_t kwb = kwork_bytes;
+      if (rc == RQ_OK) {
+        stream = side;
+        kwork = L.kwork2;
+        kwork_bytes = L.kwork2_bytes;
+        gemm_max_ctas = kSMs - 16;
+        {
+          CatGuard g(cat, PROF_TRAIL);
+          rc = gemm(b, n2, mp, op(V, mp + vpad, b, ldv, vpad), false, op(A, m, n, lda, s, s + b), L.wside, even(b),
+                    1.0, 0.0);
+        }
+        if (rc == RQ_OK) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
+        if (rc == RQ_OK) rc = cudaEventRecord(ev_side, side) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
+      }
+      gemm_max_ctas = 0;
+      kwork = kw;
+      kwork_bytes = kwb;
+      stream = main_stream;
+      RQ_TRY(rc);
+      RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_hi, 0));
+    } else {
+      RQ_TRY(sweep(ss));
+    }
     RQ_TRY(small_q(V2, L.lds_small, b, Q2, ldt, L));
     if (refl_piv)
       RQ_CUDA_TRY(cudaMemcpyAsync(rfactors.back().phat, L.cap, (size_t)b * sizeof(int), cudaMemcpyDeviceToDevice,
@@ -542,11 +600,12 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       MoveCall my2{L.yt, L.ldy, s, 0, wdt, L.cap, L.iota_b, nullptr, b, L.stage, L.ldy, nullptr, nullptr};
       RQ_TRY(move_columns(my2, stream, &launches));
     }
-    // ---------------- 8: T of the panel reflectors ----------------
-    RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
+    // ---------------- 8: T of the panel reflectors (on the side stream when overlapped) ----------------
+    if (overlap) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_side, 0));
+    else RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
     // ---------------- 9: trailing update ----------------
-    const int64_t n2 = np - b;
-    if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L));
+    if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L,
+                                       overlap ? L.wside : nullptr));
     if (downdate && n2 > 0) {
       // Y2 <- Y2 - G1 R12 with G1 = Y1 R11^{-1}: the sketch of the new trailing block
       const int64_t ldb2 = even(b), ldg = even(wdt);
@@ -624,14 +683,15 @@ int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t
 
 int Ctx::trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, int64_t n2,
                          const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2,
-                         Layout& L) {
+                         Layout& L, const double* Wpre) {
   const int64_t ldw = even(b);
   const GemmOperand Vop = op(V, mp + vpad, b, ldv, vpad);
   CatGuard guard(cat, PROF_TRAIL);
-  // W = V^T A2   (b x n2, K = m')
-  RQ_TRY(gemm(b, n2, mp, Vop, false, op(A, m, n, lda, s, s + b), L.w1, ldw, 1.0, 0.0));
+  // W = V^T A2   (b x n2, K = m'), unless the side stream already formed it
+  const double* W = Wpre ? Wpre : L.w1;
+  if (!Wpre) RQ_TRY(gemm(b, n2, mp, Vop, false, op(A, m, n, lda, s, s + b), L.w1, ldw, 1.0, 0.0));
   // W2 = T^T W
-  RQ_TRY(gemm(b, n2, b, op(T, b, b, ldt), false, op(L.w1, b, n2, ldw), L.w2, ldw, 1.0, 0.0));
+  RQ_TRY(gemm(b, n2, b, op(T, b, b, ldt), false, op(W, b, n2, ldw), L.w2, ldw, 1.0, 0.0));
   // A2 -= V W2
   RQ_TRY(gemm(mp, n2, b, Vop, true, op(L.w2, b, n2, ldw), A + s + (s + b) * lda, lda, -1.0, 1.0));
   if (Q2) {
@@ -985,6 +1045,11 @@ Ctx::~Ctx() {
   arena.release();
   qarena.release();
   sarena.release();
+  if (side) cudaStreamDestroy(side);
+  if (hip) cudaStreamDestroy(hip);
+  if (ev_v) cudaEventDestroy(ev_v);
+  if (ev_side) cudaEventDestroy(ev_side);
+  if (ev_hi) cudaEventDestroy(ev_hi);
   if (barriers) cudaFree(barriers);
 }
 

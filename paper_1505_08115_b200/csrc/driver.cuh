@@ -22,6 +22,8 @@ struct Layout {
   double *omega, *yt, *w1, *w2, *gram, *tleaf, *ybuf, *kwork, *small, *rfin, *stage, *ttop, *rinv, *g1;
   double *zbuf, *z2buf, *vst;  // reflector pivots: A V_S, (A V_S) T_S, V_S^T
   double *ov, *ot, *oe;         // _orth scratch: reflectors, T, Q
+  double *wside, *gram2, *kwork2;  // side stream: W = V^T A2, Gram, split-K slabs
+  size_t kwork2_bytes;
   double *jw, *jv, *jd;         // panel SVD scratch
   int* jstat;                   // per-panel Jacobi sweep counts
   int64_t ldo, ldy, lds_small;
@@ -104,6 +106,13 @@ struct Ctx {
   unsigned int* barriers = nullptr;
   int nbarriers = 0;
   int next_barrier = 0;
+  // overlap (factorize_perm): the b x b CPQR on a highest-priority stream `hip`,
+  // W = V^T A2 and T on a lowest-priority stream `side`
+  cudaStream_t side = nullptr, hip = nullptr;
+  cudaEvent_t ev_v = nullptr, ev_side = nullptr, ev_hi = nullptr;
+  bool overlap_on = true;
+  int gemm_max_ctas = 0;
+  int ensure_side();
   // scratch views used by helpers
   double* kwork = nullptr;
   size_t kwork_bytes = 0;
@@ -143,7 +152,7 @@ struct Ctx {
                      double* z2, int64_t ldz);
   int trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, int64_t n2,
                       const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2,
-                      Layout& L);
+                      Layout& L, const double* Wpre = nullptr);
   int factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, int64_t lda, uint64_t seed,
                      uint64_t* counter, int64_t* dperm);
   int small_q(const double* V2, int64_t ldv2, int k, double* Q2, int64_t ldq, Layout& L);

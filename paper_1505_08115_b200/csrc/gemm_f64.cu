@@ -464,7 +464,8 @@ static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launch
     RQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::SMEM));
     if (per_sm < 1) per_sm = 1;
   }
-  const int64_t slots = (int64_t)num_sms() * per_sm;
+  const int sm_cap = p.max_ctas > 0 ? std::min(num_sms(), p.max_ctas) : num_sms();
+  const int64_t slots = (int64_t)sm_cap * per_sm;
   const int grid = (int)(units < slots ? units : slots);
   kern<<<grid, Cfg::kThreads, Cfg::SMEM, stream>>>(ma, mb, a);
   {
@@ -499,7 +500,7 @@ size_t gemm_splitk_workspace(int64_t M, int64_t N, int splitk) {
 static int choose_splitk(const GemmProblem& p, int BM, int BN) {
   if (p.splitk > 0) return p.splitk;
   if (!p.work) return 1;
-  const int sms = num_sms();
+  const int sms = p.max_ctas > 0 ? std::min(num_sms(), p.max_ctas) : num_sms();
   const int64_t tiles = ceil_div(p.M + 1, BM) * ceil_div(p.N, BN);
   const int64_t kch = ceil_div(p.K + 1, 16);
   auto eff = [&](int64_t units) {

@@ -36,6 +36,7 @@ struct GemmProblem {
   int splitk;            // 0: choose automatically; >1: deterministic split-K through `work`
   double* work;          // splitk * (M+1) * N doubles (slab per split)
   size_t work_bytes;
+  int max_ctas = 0;      // > 0: cap the persistent grid (leave SMs to a concurrent kernel)
 };
 
 int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches);
