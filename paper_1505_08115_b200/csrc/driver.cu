@@ -216,6 +216,7 @@ int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_
   p.work = kwork;
   p.work_bytes = kwork ? kwork_bytes : 0;
   p.max_ctas = gemm_max_ctas;
+  p.pdl = gemm_pdl;
   return gemm_f64(p, stream, &launches);
 }
 
@@ -556,14 +557,22 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     ss.r_out = L.rfin;
     ss.ldr = L.lds_small;
     if (overlap) {
+      // env_overlap 1: CPQR then the W GEMM in one stream, the GEMM a programmatic dependent launch
+      //   (it starts once every CPQR CTA is resident, so the cluster never waits behind it), with a
+      //   CPQR-done event between them for small_q; 3: the same without that event;
+      // 4: CPQR on a highest-priority stream, W on a lowest-priority one.
       RQ_TRY(ensure_side());
       RQ_CUDA_TRY(cudaEventRecord(ev_v, stream));
-      RQ_CUDA_TRY(cudaStreamWaitEvent(hip, ev_v, 0));
-      RQ_CUDA_TRY(cudaStreamWaitEvent(side, ev_v, 0));
+      const bool pdl = env_overlap != 4;
+      cudaStream_t cpqr_stream = pdl ? side : hip;
+      RQ_CUDA_TRY(cudaStreamWaitEvent(cpqr_stream, ev_v, 0));
+      if (!pdl) RQ_CUDA_TRY(cudaStreamWaitEvent(side, ev_v, 0));
       cudaStream_t main_stream = stream;
-      stream = hip;  // the CPQR first: its cluster gets SMs before the side GEMM's CTAs
+      stream = cpqr_stream;
       int rc = sweep(ss);
-      if (rc == RQ_OK) rc = cudaEventRecord(ev_hi, hip) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
+      const bool hi_event = env_overlap != 3;
+      if (rc == RQ_OK && hi_event)
+        rc = cudaEventRecord(ev_hi, cpqr_stream) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
       double* kw = kwork;
       const size_t kwb = kwork_bytes;
       if (rc == RQ_OK) {
@@ -571,20 +580,23 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
         kwork = L.kwork2;
         kwork_bytes = L.kwork2_bytes;
         gemm_max_ctas = kSMs - 16;
+        gemm_pdl = pdl;
         {
           CatGuard g(cat, PROF_TRAIL);
           rc = gemm(b, n2, mp, op(V, mp + vpad, b, ldv, vpad), false, op(A, m, n, lda, s, s + b), L.wside, even(b),
                     1.0, 0.0);
         }
+        gemm_pdl = false;
         if (rc == RQ_OK) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
         if (rc == RQ_OK) rc = cudaEventRecord(ev_side, side) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
       }
       gemm_max_ctas = 0;
+      gemm_pdl = false;
       kwork = kw;
       kwork_bytes = kwb;
       stream = main_stream;
       RQ_TRY(rc);
-      RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_hi, 0));
+      RQ_CUDA_TRY(cudaStreamWaitEvent(stream, hi_event ? ev_hi : ev_side, 0));
     } else {
       RQ_TRY(sweep(ss));
     }

@@ -112,6 +112,7 @@ struct Ctx {
   cudaEvent_t ev_v = nullptr, ev_side = nullptr, ev_hi = nullptr;
   bool overlap_on = true;
   int gemm_max_ctas = 0;
+  bool gemm_pdl = false;
   int ensure_side();
   // scratch views used by helpers
   double* kwork = nullptr;

@@ -467,7 +467,21 @@ static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launch
   const int sm_cap = p.max_ctas > 0 ? std::min(num_sms(), p.max_ctas) : num_sms();
   const int64_t slots = (int64_t)sm_cap * per_sm;
   const int grid = (int)(units < slots ? units : slots);
-  kern<<<grid, Cfg::kThreads, Cfg::SMEM, stream>>>(ma, mb, a);
+  if (p.pdl) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(Cfg::kThreads);
+    lc.dynamicSmemBytes = Cfg::SMEM;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, kern, ma, mb, a);
+  } else {
+    kern<<<grid, Cfg::kThreads, Cfg::SMEM, stream>>>(ma, mb, a);
+  }
   {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

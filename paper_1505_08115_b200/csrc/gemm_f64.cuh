@@ -37,6 +37,8 @@ struct GemmProblem {
   double* work;          // splitk * (M+1) * N doubles (slab per split)
   size_t work_bytes;
   int max_ctas = 0;      // > 0: cap the persistent grid (leave SMs to a concurrent kernel)
+  bool pdl = false;      // programmatic dependent launch: may start once the previous kernel in the
+                         // stream triggered (the GEMM must not read that kernel's output)
 };
 
 int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches);

@@ -57,6 +57,9 @@ struct SweepArgs {
 // Smem layout: [u (m doubles, if u_in_smem)] [cached columns (cache_cols * m)]
 //              [pos (cols_per_cta ints)] [active (cols_per_cta)] [reduce scratch]
 __global__ void __launch_bounds__(SW_THREADS) sweep_kernel(const SweepArgs p) {
+  // a kernel launched after this one with programmatic stream serialization (the
+  // overlapped W = V^T A2 GEMM, driver.cu) may start once every CTA is resident
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ double sm[];
   const int G = gridDim.x;
   const int total_cols = p.n + p.n_acc;
@@ -296,6 +299,9 @@ RQ_DEV void dsmem_st_i32(int* local, unsigned rank, int v) {
 // barrier every read is local.  Two cluster barriers per step: candidates,
 // then the winning column.
 __global__ void __launch_bounds__(SC_THREADS) sweep_cluster_kernel(const SweepArgs p) {
+  // a kernel launched after this one with programmatic stream serialization (the
+  // overlapped W = V^T A2 GEMM, driver.cu) may start once every CTA is resident
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ double sm[];
   const unsigned CS = gridDim.x;
   const unsigned rank = blockIdx.x;
@@ -537,6 +543,9 @@ RQ_DEV void push_key(RegKey* local_slot, unsigned rank, const RegKey& k) {
 
 template <int RPL>
 __global__ void __launch_bounds__(512) sweep_reg_kernel(const SweepArgs p) {
+  // a kernel launched after this one with programmatic stream serialization (the
+  // overlapped W = V^T A2 GEMM, driver.cu) may start once every CTA is resident
+  asm volatile("griddepcontrol.launch_dependents;");
   __shared__ double u[32 * RPL];
   __shared__ double cand[2][32 * RPL];          // this CTA's candidate column, by step parity
   __shared__ __align__(16) RegKey keys[2][16];  // candidates pushed by every CTA, by parity
