@@ -11,7 +11,6 @@ namespace rq {
 // ---------------------------------------------------------------------------
 // PTX wrappers: mbarrier + TMA
 // ---------------------------------------------------------------------------
-RQ_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 RQ_DEV void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
   __shared__ double sc[17];                       // reflector coefficients of step j-1 (o = c - j + 1), sc[16] = 0
   __shared__ double scal[4];                      // refl, beta, h*inv, inv
   __shared__ double Ts[16][17];
+  __shared__ __align__(8) unsigned long long lmbar[2];  // pushes of step j complete on lmbar[j & 1]
   constexpr unsigned CS = 16;  // launch_leaf_reg: one 16-CTA cluster
   const unsigned rank = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -292,6 +293,11 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
 #pragma unroll
   for (int q = 0; q < RPT; q++) uprev[q] = 0.0;
   bool refl_prev = false;
+  if (threadIdx.x == 0) {
+    mbar_init(&lmbar[0], 1);
+    mbar_init(&lmbar[1], 1);
+    mbar_init_fence();
+  }
   __syncthreads();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 
@@ -299,6 +305,8 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
     const bool final_round = (j == w);
     const int par = j & 1;
     leaf_stamp(j, 0);
+    // this step's pushes: 32 partial sums from every CTA, plus row j from its owner
+    if (threadIdx.x == 0) mbar_expect_tx(&lmbar[par], CS * 32 * 8 + (final_round ? 0 : 16 * 8));
     // ---- apply the pending reflector j-1 to the window (columns j..) ----
     if (refl_prev && !final_round) {
       double s[WL];
@@ -350,14 +358,19 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
       for (int ww = 0; ww < LR_WARPS; ww++) sum += wpart[ww][lane];
       const bool owner = !final_round && (unsigned)(j / rows_per) == rank;  // this CTA holds row j
       const double rv = (owner && lane < 16) ? rowj[lane] : 0.0;
+      const uint32_t pin_l = smem_u32(&pin[par][rank][lane]);
+      const uint32_t row_l = smem_u32(&rowp[par][lane & 15]);
+      const uint32_t mb_l = smem_u32(&lmbar[par]);
 #pragma unroll
       for (unsigned dst = warp; dst < CS; dst += LR_WARPS) {
-        dsmem_st(&pin[par][rank][lane], dst, sum);
-        if (owner && lane < 16) dsmem_st(&rowp[par][lane], dst, rv);
+        const uint32_t mb = cluster_map(mb_l, dst);
+        st_async_f64(cluster_map(pin_l, dst), sum, mb);
+        if (owner && lane < 16) st_async_f64(cluster_map(row_l, dst), rv, mb);
       }
     }
     leaf_stamp(j, 4);
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    // warps 0 and 1 consume the pushed partials; the others meet them at the __syncthreads below
+    if (warp <= 1) mbar_wait_cluster(&lmbar[par], (unsigned)(j >> 1) & 1u);
     leaf_stamp(j, 5);
     if (warp <= 1) {
       double t = 0.0;

@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(512) sweep_reg_kernel(const SweepArgs p) {
   __shared__ __align__(16) RegKey keys[2][16];  // candidates pushed by every CTA, by parity
   __shared__ RegKey wk[16];
   __shared__ int wsel;
+  __shared__ __align__(8) unsigned long long kmbar[2];  // key pushes of step j complete on kmbar[j & 1]
   const unsigned CS = gridDim.x;
   const unsigned rank = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -567,11 +568,18 @@ __global__ void __launch_bounds__(512) sweep_reg_kernel(const SweepArgs p) {
   bool active = own;
   bool have_refl = false;
   int rj = -1;
+  if (threadIdx.x == 0) {
+    mbar_init(&kmbar[0], 1);
+    mbar_init(&kmbar[1], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 
   for (int j = 0; j <= p.steps; j++) {
     const bool last = (j == p.steps);
     const int par = j & 1;
+    if (!last && threadIdx.x == 0) mbar_expect_tx(&kmbar[par], CS * (unsigned)sizeof(RegKey));
     // ---- A: apply the pending reflector to this warp's column, score it ----
     dbg_stamp(j, 0);
     double tail = 0.0;
@@ -622,24 +630,33 @@ __global__ void __launch_bounds__(512) sweep_reg_kernel(const SweepArgs p) {
     dbg_stamp(j, 1);
     __syncthreads();
     dbg_stamp(j, 2);
-    if (warp == 0) {
+    {
+      // the CTA's best warp (same answer in every warp) stages its column for the cluster
       const RegKey r = lane < 16 ? wk[lane] : RegKey{0u, 0u, INT_MAX, -1, 0.0, 0.0};
       const int wl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);
-      const RegKey best = wl >= 0 ? wk[wl] : RegKey{0u, 0u, INT_MAX, -1, 0.0, 0.0};
-      if (lane < (int)CS) push_key(&keys[par][rank], (unsigned)lane, best);
-      if (lane == 0) wsel = wl;
-    }
-    __syncthreads();
-    dbg_stamp(j, 3);
-    if (wsel == warp) {  // the CTA's best warp stages its column for the cluster
+      if (wl == warp) {
 #pragma unroll
-      for (int k = 0; k < RPL; k++) {
-        const int i = lane + 32 * k;
-        if (i < m) cand[par][i] = x[k];
+        for (int k = 0; k < RPL; k++) {
+          const int i = lane + 32 * k;
+          if (i < m) cand[par][i] = x[k];
+        }
+      }
+      __syncthreads();  // cand complete before the key push below releases it to the cluster
+      dbg_stamp(j, 3);
+      if (warp == 0 && lane < (int)CS) {
+        // push this CTA's key into every CTA's table; st.async completes on the receiver's mbarrier
+        // (release at cluster scope: the staged column is visible to whoever acquires that phase)
+        const RegKey best = wl >= 0 ? wk[wl] : RegKey{0u, 0u, INT_MAX, -1, 0.0, 0.0};
+        const uint32_t dst_key = cluster_map(smem_u32(&keys[par][rank]), (unsigned)lane);
+        const uint32_t mb = cluster_map(smem_u32(&kmbar[par]), (unsigned)lane);
+        st_async_u64(dst_key, ((unsigned long long)best.lo << 32) | best.hi, mb);
+        st_async_u64(dst_key + 8, ((unsigned long long)(unsigned)best.col << 32) | (unsigned)best.pos, mb);
+        st_async_u64(dst_key + 16, (unsigned long long)__double_as_longlong(best.tail), mb);
+        st_async_u64(dst_key + 24, (unsigned long long)__double_as_longlong(best.xj), mb);
       }
     }
     dbg_stamp(j, 4);
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    mbar_wait_cluster(&kmbar[par], (unsigned)(j >> 1) & 1u);
     dbg_stamp(j, 5);
     // ---- F: every warp resolves the cluster winner from the local table ----
     const RegKey r = lane < (int)CS ? keys[par][lane] : RegKey{0u, 0u, INT_MAX, -1, 0.0, 0.0};
