@@ -1054,7 +1054,21 @@ struct SkShared {
   SkKey win;
   double wtail, wxj;
   int wsel[2];
+  unsigned long long wbits[16][2];  // last arriver: tail / x_j bits of each warp's best slot
+  int wcta[16];
 };
+
+// LL words: 32-bit payload (high half) + 32-bit step stamp (low half), stored and loaded
+// as 16-byte pairs; each 8-byte word is single-copy atomic, so a stamp match is a data match.
+RQ_DEV unsigned long long ll_word(unsigned data, unsigned stamp) {
+  return ((unsigned long long)data << 32) | stamp;
+}
+RQ_DEV void st_ll2(unsigned long long* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+RQ_DEV void ld_ll2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
 
 // Apply the pending reflector u (rows >= 32*K0 may be non-zero; u is exactly 0
 // above the reflector row and below m) to every column the warp owns.
@@ -1133,22 +1147,28 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
     dbg_stamp(j, 1);
     __syncthreads();
     dbg_stamp(j, 2);
-    // -------- B: the CTA's best warp publishes its column, x_j and tail --------
-    SkSlot2* slot = slots + (int64_t)par * G;
+    // -------- B: the CTA's best warp publishes its key, x_j, tail and column (LL words) --------
+    // Every 8-byte word carries the step stamp in its low half: a reader that sees the stamp
+    // in every word it needs has current data, so no fences sit on the exchange path.
+    const unsigned stamp = (unsigned)(stamp_base + (unsigned long long)j + 1ull);
+    unsigned long long* slw = reinterpret_cast<unsigned long long*>(slots) + ((int64_t)par * G) * 8;
+    unsigned long long* colw = reinterpret_cast<unsigned long long*>(p.slotdata);
+    const int64_t cstride = 2 * (int64_t)(m + 2);
     {
       const SkKey r = lane < WARPS ? sh.wk[lane] : SkKey{0u, 0u, INT_MAX, -1};
       const int wl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);  // warp-uniform, same in every warp
       if (wl < 0) {
         if (warp == 0 && lane == 0) {
-          SkSlot2* me = slot + blockIdx.x;
-          me->key = -1.0;
-          me->col = -1;
-          me->pos = INT_MAX;
+          unsigned long long* me = slw + (int64_t)blockIdx.x * 8;
+          st_ll2(me, ll_word(0u, stamp), ll_word(0u, stamp));
+          st_ll2(me + 2, ll_word((unsigned)INT_MAX, stamp), ll_word(0xffffffffu, stamp));
+          st_ll2(me + 4, ll_word(0u, stamp), ll_word(0u, stamp));
+          st_ll2(me + 6, ll_word(0u, stamp), ll_word(0u, stamp));
         }
       } else if (wl == warp) {
         const SkKey b = sh.wk[warp];
         const int bqw = b.col - cbase;
-        double* sd = p.slotdata + ((int64_t)par * G + blockIdx.x) * m;
+        unsigned long long* cb = colw + ((int64_t)par * G + blockIdx.x) * cstride;
 #pragma unroll
         for (int q = 0; q < CPW; q++)
           if (q == bqw) {
@@ -1160,106 +1180,132 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
 #pragma unroll
             for (int k = KJ; k < RPL; k++) {
               const int i = lane + 32 * k;
-              if (i >= j && i < m) sd[i] = x[q][k];
+              if (i >= j && i < m) {
+                const unsigned long long bits = __double_as_longlong(x[q][k]);
+                st_ll2(cb + 2 * i, ll_word((unsigned)(bits >> 32), stamp), ll_word((unsigned)bits, stamp));
+              }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
             if (lane == 0) {
-              SkSlot2* me = slot + blockIdx.x;
-              me->key = __longlong_as_double(((long long)b.hi << 32) | (long long)b.lo);
-              me->tail = tl;
-              me->xj = xj;
-              me->pos = b.pos;
-              me->col = b.col;
+              unsigned long long* me = slw + (int64_t)blockIdx.x * 8;
+              const unsigned long long tb = __double_as_longlong(tl), xb = __double_as_longlong(xj);
+              st_ll2(me, ll_word(b.hi, stamp), ll_word(b.lo, stamp));
+              st_ll2(me + 2, ll_word((unsigned)b.pos, stamp), ll_word((unsigned)b.col, stamp));
+              st_ll2(me + 4, ll_word((unsigned)(tb >> 32), stamp), ll_word((unsigned)tb, stamp));
+              st_ll2(me + 6, ll_word((unsigned)(xb >> 32), stamp), ll_word((unsigned)xb, stamp));
             }
           }
       }
     }
     __syncthreads();
     dbg_stamp(j, 3);
-    // -------- C: arrive; the last CTA to arrive picks the winner and publishes it --------
-    SkWin* wrec = wins + par;
-    const unsigned long long stamp = stamp_base + (unsigned long long)j + 1ull;
-    if (warp == 0) {
-      unsigned long long old = 0;
-      if (lane == 0) {
-        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.counter) : "memory");
+    // -------- C: arrive (relaxed); the last CTA reduces every slot and publishes the winner --------
+    unsigned long long* wrw = reinterpret_cast<unsigned long long*>(wins) + par * 10;
+    if (threadIdx.x == 0) {
+      unsigned long long old;
+      asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.counter) : "memory");
+      sh.wsel[0] = (old + 1 == p.counter_base + (unsigned long long)(j + 1) * G) ? 1 : 0;
+    }
+    __syncthreads();
+    if (sh.wsel[0]) {
+      // one slot per thread (G <= NT): spin until its four words carry this step's stamp
+      unsigned khi = 0u, klo = 0u;
+      int kpos = INT_MAX, kcol = -1;
+      unsigned long long ktb = 0ull, kxb = 0ull;
+      if ((int)threadIdx.x < G) {
+        const unsigned long long* sp = slw + (int64_t)threadIdx.x * 8;
+        unsigned long long a0, a1, a2, a3, a4, a5, a6, a7;
+        do {
+          ld_ll2(sp, a0, a1);
+          ld_ll2(sp + 2, a2, a3);
+          ld_ll2(sp + 4, a4, a5);
+          ld_ll2(sp + 6, a6, a7);
+        } while ((unsigned)a0 != stamp || (unsigned)a1 != stamp || (unsigned)a2 != stamp || (unsigned)a3 != stamp ||
+                 (unsigned)a4 != stamp || (unsigned)a5 != stamp || (unsigned)a6 != stamp || (unsigned)a7 != stamp);
+        khi = (unsigned)(a0 >> 32);
+        klo = (unsigned)(a1 >> 32);
+        kpos = (int)(a2 >> 32);
+        kcol = (int)(a3 >> 32);
+        ktb = (a4 & 0xffffffff00000000ull) | (a5 >> 32);
+        kxb = (a6 & 0xffffffff00000000ull) | (a7 >> 32);
       }
-      old = __shfl_sync(0xffffffffu, old, 0);
-      const unsigned long long target = p.counter_base + (unsigned long long)(j + 1) * G;
-      if (old + 1 == target) {
-        // last arriver: every slot of this step is visible (acq_rel atomic).
-        constexpr int kMaxK = (kSMs + 31) / 32;
-        double kv[kMaxK], tv[kMaxK], xv[kMaxK];
-        int pv[kMaxK], cv[kMaxK];
-#pragma unroll
-        for (int kk = 0; kk < kMaxK; kk++) {
-          const int c = kk * 32 + lane;
-          const bool ok = c < G;
-          const SkSlot2* sp = &slot[ok ? c : 0];
-          kv[kk] = __ldcg(&sp->key);
-          tv[kk] = __ldcg(&sp->tail);
-          xv[kk] = __ldcg(&sp->xj);
-          pv[kk] = __ldcg(&sp->pos);
-          cv[kk] = __ldcg(&sp->col);
-          if (!ok) {
-            kv[kk] = -1.0;
-            cv[kk] = -1;
-          }
-        }
-        double bk = -1.0, bt = 0.0, bx = 0.0;
-        int bp = INT_MAX, bc = -1, bw = -1;
-#pragma unroll
-        for (int kk = 0; kk < kMaxK; kk++)
-          if (kv[kk] >= 0.0 && cv[kk] >= 0 && (bc < 0 || piv_better(kv[kk], pv[kk], bk, bp))) {
-            bk = kv[kk];
-            bt = tv[kk];
-            bx = xv[kk];
-            bp = pv[kk];
-            bc = cv[kk];
-            bw = kk * 32 + lane;
-          }
-        const unsigned long long kb = __double_as_longlong(bk < 0.0 ? 0.0 : bk);
-        const int wl = warp_argmax((unsigned)(kb >> 32), (unsigned)kb, bp, bc >= 0);
-        if (lane == wl) {
-          wrec->key = bk;
-          wrec->tail = bt;
-          wrec->xj = bx;
-          wrec->pos = bp;
-          wrec->col = bc;
-          wrec->cta = bw;
-          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&wrec->flag), "l"(stamp) : "memory");
-        }
-      } else if (lane == 0) {
-        while (ld_acquire_u64(&wrec->flag) != stamp) {
+      const int wl = warp_argmax(khi, klo, kpos, kcol >= 0);
+      if (lane == (wl < 0 ? 0 : wl)) {
+        sh.wk[warp] = SkKey{khi, klo, kpos, wl < 0 ? -1 : kcol};
+        sh.wbits[warp][0] = ktb;
+        sh.wbits[warp][1] = kxb;
+        sh.wcta[warp] = (int)threadIdx.x;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        const SkKey r = lane < WARPS ? sh.wk[lane] : SkKey{0u, 0u, INT_MAX, -1};
+        const int gl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);
+        if (lane == gl) {
+          const unsigned long long tb = sh.wbits[gl][0], xb = sh.wbits[gl][1];
+          const int cta = sh.wcta[gl];
+          st_ll2(wrw, ll_word(r.hi, stamp), ll_word(r.lo, stamp));
+          st_ll2(wrw + 2, ll_word((unsigned)r.pos, stamp), ll_word((unsigned)r.col, stamp));
+          st_ll2(wrw + 4, ll_word((unsigned)cta, stamp), ll_word(0u, stamp));
+          st_ll2(wrw + 6, ll_word((unsigned)(tb >> 32), stamp), ll_word((unsigned)tb, stamp));
+          st_ll2(wrw + 8, ll_word((unsigned)(xb >> 32), stamp), ll_word((unsigned)xb, stamp));
+          sh.win = r;
+          sh.wtail = __longlong_as_double((long long)tb);
+          sh.wxj = __longlong_as_double((long long)xb);
+          sh.wsel[1] = cta;
         }
       }
-      __syncwarp();
+    } else if (warp == 0) {
+      // lanes 0..4 poll one word pair each of the winner record
+      unsigned long long a = 0ull, b = 0ull;
+      bool ok = lane >= 5;
+      do {
+        if (!ok) {
+          ld_ll2(wrw + 2 * lane, a, b);
+          ok = (unsigned)a == stamp && (unsigned)b == stamp;
+        }
+      } while (!__all_sync(0xffffffffu, ok));
+      const unsigned h0 = (unsigned)(__shfl_sync(0xffffffffu, a, 0) >> 32);
+      const unsigned l0 = (unsigned)(__shfl_sync(0xffffffffu, b, 0) >> 32);
+      const int ps = (int)(__shfl_sync(0xffffffffu, a, 1) >> 32);
+      const int cl = (int)(__shfl_sync(0xffffffffu, b, 1) >> 32);
+      const int ct = (int)(__shfl_sync(0xffffffffu, a, 2) >> 32);
+      const unsigned long long t3a = __shfl_sync(0xffffffffu, a, 3), t3b = __shfl_sync(0xffffffffu, b, 3);
+      const unsigned long long t4a = __shfl_sync(0xffffffffu, a, 4), t4b = __shfl_sync(0xffffffffu, b, 4);
       if (lane == 0) {
-        const double kv = __ldcg(&wrec->key);
-        const unsigned long long kb = __double_as_longlong(kv);
-        sh.win = SkKey{(unsigned)(kb >> 32), (unsigned)kb, __ldcg(&wrec->pos), __ldcg(&wrec->col)};
-        sh.wtail = __ldcg(&wrec->tail);
-        sh.wxj = __ldcg(&wrec->xj);
-        sh.wsel[1] = __ldcg(&wrec->cta);
+        sh.win = SkKey{h0, l0, ps, cl};
+        sh.wsel[1] = ct;
+        sh.wtail = __longlong_as_double((long long)((t3a & 0xffffffff00000000ull) | (t3b >> 32)));
+        sh.wxj = __longlong_as_double((long long)((t4a & 0xffffffff00000000ull) | (t4b >> 32)));
       }
     }
     __syncthreads();
     dbg_stamp(j, 4);
-    // -------- E: reflector from the winning column (L2); u = 0 outside [j, m) --------
+    // -------- E: reflector from the winning column (LL words in L2); u = 0 outside [j, m) --------
     const SkKey win = sh.win;
     const int wcta = sh.wsel[1];
     const double wkey = __longlong_as_double(((long long)win.hi << 32) | (long long)win.lo);
     const bool refl = (m - j >= 2) && (wkey != 0.0);
     if (refl) {
-      const double* xs = p.slotdata + ((int64_t)par * G + wcta) * m;
+      const unsigned long long* cb = colw + ((int64_t)par * G + wcta) * cstride;
       const double wxj = sh.wxj;
       const double nrm = sqrt(wkey);
       const double beta = (wxj >= 0.0) ? -nrm : nrm;
       const double h = beta - wxj;
       const double inv = 1.0 / sqrt(h * h + sh.wtail);
-      for (int i = 32 * KJ + threadIdx.x; i < 32 * RPL; i += NT)
-        u[i] = (i > j && i < m) ? -__ldcg(&xs[i]) * inv : (i == j ? h * inv : 0.0);
+      for (int i = 32 * KJ + threadIdx.x; i < 32 * RPL; i += NT) {
+        double val = 0.0;
+        if (i > j && i < m) {
+          unsigned long long c0, c1;
+          do {
+            ld_ll2(cb + 2 * i, c0, c1);
+          } while ((unsigned)c0 != stamp || (unsigned)c1 != stamp);
+          val = -__longlong_as_double((long long)((c0 & 0xffffffff00000000ull) | (c1 >> 32))) * inv;
+        } else if (i == j) {
+          val = h * inv;
+        }
+        u[i] = val;
+      }
     }
 #pragma unroll
     for (int q = 0; q < CPW; q++) {
@@ -1350,6 +1396,9 @@ static int dispatch_sketch_reg(const SketchArgs& a, int n, SkSlot2* slots, SkWin
   return -1;  // does not fit: caller falls back
 }
 
+size_t sketch_ll_column_bytes(int m) { return 2 * (size_t)kSMs * 2 * ((size_t)m + 2) * 8; }
+size_t sketch_workspace_bytes(int m) { return ((2 * (size_t)kSMs * 64 + 255) & ~size_t(255)) + 256 + sketch_ll_column_bytes(m); }
+
 static size_t sketch_fixed_smem(int m, int per) {
   return (size_t)m * 8 + (size_t)per * 8 + 16 + (SK_WARPS + 2) * sizeof(SweepSlot) + 64;
 }
@@ -1368,14 +1417,14 @@ int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, con
     a.steps = steps;
     a.init_pos = init_pos;
     a.chosen = chosen;
-    SkSlot2* slots = reinterpret_cast<SkSlot2*>(w.scratch);
-    const size_t slot_bytes = ((2 * (size_t)kSMs * sizeof(SkSlot2) + 255) & ~size_t(255));
-    // dedicated, zero-initialised records next to the counter: only older stamps can be stale there
+    SkSlot2* slots = reinterpret_cast<SkSlot2*>(w.scratch);  // [2][G] slots of 8 LL words
+    const size_t slot_bytes = ((2 * (size_t)kSMs * 64 + 255) & ~size_t(255));
+    // dedicated, zero-initialised winner records (2 x 10 LL words) next to the counter
     SkWin* wins = reinterpret_cast<SkWin*>(reinterpret_cast<char*>(counter) + 64);
-    a.slotdata = reinterpret_cast<double*>(reinterpret_cast<char*>(w.scratch) + slot_bytes + 256);
+    a.slotdata = reinterpret_cast<double*>(reinterpret_cast<char*>(w.scratch) + slot_bytes + 256);  // LL columns
     a.counter = counter;
     a.counter_base = counter_base;
-    const size_t need = slot_bytes + 256 + 2 * (size_t)kSMs * m * 8;
+    const size_t need = slot_bytes + 256 + sketch_ll_column_bytes(m);
     if (w.scratch_bytes >= need) {
       // step stamps are unique across launches: derived from the monotone counter base
       const unsigned long long stamp_base = counter_base;
