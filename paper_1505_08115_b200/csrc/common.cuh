@@ -71,12 +71,7 @@ RQ_DEV void mbar_init(unsigned long long* mbar, unsigned count) {
 }
 RQ_DEV void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 RQ_DEV void mbar_expect_tx(unsigned long long* mbar, unsigned bytes) {
-  unsigned long long state;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
-               : "=l"(state)
-               : "r"(smem_u32(mbar)), "r"(bytes)
-               : "memory");
-  (void)state;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
 }
 RQ_DEV void mbar_wait_cluster(unsigned long long* mbar, unsigned parity) {
   const uint32_t a = smem_u32(mbar);

@@ -550,7 +550,6 @@ __global__ void __launch_bounds__(512) sweep_reg_kernel(const SweepArgs p) {
   __shared__ double cand[2][32 * RPL];          // this CTA's candidate column, by step parity
   __shared__ __align__(16) RegKey keys[2][16];  // candidates pushed by every CTA, by parity
   __shared__ RegKey wk[16];
-  __shared__ int wsel;
   __shared__ __align__(8) unsigned long long kmbar[2];  // key pushes of step j complete on kmbar[j & 1]
   const unsigned CS = gridDim.x;
   const unsigned rank = blockIdx.x;
@@ -792,6 +791,7 @@ struct SketchArgs {
   unsigned long long* counter;      // monotone arrival counter (never reset)
   unsigned long long counter_base;  // its value when this launch starts
   int cache_cols;
+  int spw;  // register kernel: shared-memory-resident columns per warp (0 = registers only)
 };
 
 RQ_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -1097,12 +1097,35 @@ RQ_DEV void sk_apply(double (&x)[CPW][RPL], const bool (&act)[CPW], const double
   }
 }
 
+// One shared-memory-resident column (same arithmetic as sk_apply).
+template <int K0, int RPL>
+RQ_DEV void sk_apply1(double (&y)[RPL], const double* u, int lane) {
+  double d = 0.0;
+#pragma unroll
+  for (int k = K0; k < RPL; k++) d = fma(u[lane + 32 * k], y[k], d);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  d *= 2.0;
+#pragma unroll
+  for (int k = K0; k < RPL; k++) y[k] -= d * u[lane + 32 * k];
+}
+
+// Columns beyond the register capacity live in shared memory, [column][slot k][lane].
+struct SkSmem {
+  double* xs;
+  int* spos;
+  int* sact;
+  int spw;      // columns per warp
+  int cbase_s;  // global id of this warp's first shared-memory column
+};
+
 // Steps j in [32*KJ, jend): row j lives in register slot KJ (lane j & 31), so
 // every row mask below is a compile-time slot range plus one lane predicate.
-template <int KJ, int RPL, int CPW, int WARPS>
+template <int KJ, int RPL, int CPW, int WARPS, bool SMEM>
 RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
                      double (&x)[CPW][RPL], int (&pos)[CPW], bool (&act)[CPW], bool& have_refl, double* u,
-                     SkShared& sh, int cbase, int jend) {
+                     SkShared& sh, int cbase, int jend, const SkSmem& sm) {
+  constexpr int KL = KJ > 0 ? KJ - 1 : 0;  // lowest slot the pending reflector can touch
   constexpr int NT = WARPS * 32;
   const int G = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1140,9 +1163,38 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
         bq = q;
       }
     }
+    int bcol = bq >= 0 ? cbase + bq : -1;
+    if constexpr (SMEM) {
+      for (int s2 = 0; s2 < sm.spw; s2++) {
+        const int sc = warp * sm.spw + s2;
+        if (!sm.sact[sc]) continue;  // warp-uniform
+        double* col = sm.xs + (int64_t)sc * RPL * 32 + lane;
+        double y[RPL];
+#pragma unroll
+        for (int k = KL; k < RPL; k++) y[k] = col[k * 32];
+        if (have_refl) {
+          if (KJ > 0 && jl == 0) sk_apply1<KL, RPL>(y, u, lane);
+          else sk_apply1<KJ, RPL>(y, u, lane);
+        }
+        const double yv = at_or_below ? y[KJ] : 0.0;
+        double tt = yv * yv;
+#pragma unroll
+        for (int k = KJ + 1; k < RPL; k++) tt = fma(y[k], y[k], tt);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tt += __shfl_xor_sync(0xffffffffu, tt, o);
+#pragma unroll
+        for (int k = KL; k < RPL; k++) col[k * 32] = y[k];
+        const int ps = sm.spos[sc];
+        if (bcol < 0 || piv_better(tt, ps, bkey, bpos)) {
+          bkey = tt;
+          bpos = ps;
+          bcol = sm.cbase_s + s2;
+        }
+      }
+    }
     if (lane == 0) {
       const unsigned long long kb = __double_as_longlong(bkey < 0.0 ? 0.0 : bkey);
-      sh.wk[warp] = SkKey{(unsigned)(kb >> 32), (unsigned)kb, bpos, bq >= 0 ? cbase + bq : -1};
+      sh.wk[warp] = SkKey{(unsigned)(kb >> 32), (unsigned)kb, bpos, bcol};
     }
     dbg_stamp(j, 1);
     __syncthreads();
@@ -1167,35 +1219,49 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
         }
       } else if (wl == warp) {
         const SkKey b = sh.wk[warp];
-        const int bqw = b.col - cbase;
         unsigned long long* cb = colw + ((int64_t)par * G + blockIdx.x) * cstride;
+        auto publish = [&](const double (&xc)[RPL]) {
+          const double xj = __shfl_sync(0xffffffffu, xc[KJ], jl);
+          const double xv = lane > jl ? xc[KJ] : 0.0;
+          double tl = xv * xv;
 #pragma unroll
-        for (int q = 0; q < CPW; q++)
-          if (q == bqw) {
-            const double xj = __shfl_sync(0xffffffffu, x[q][KJ], jl);
-            const double xv = lane > jl ? x[q][KJ] : 0.0;
-            double tl = xv * xv;
+          for (int k = KJ + 1; k < RPL; k++) tl = fma(xc[k], xc[k], tl);
 #pragma unroll
-            for (int k = KJ + 1; k < RPL; k++) tl = fma(x[q][k], x[q][k], tl);
-#pragma unroll
-            for (int k = KJ; k < RPL; k++) {
-              const int i = lane + 32 * k;
-              if (i >= j && i < m) {
-                const unsigned long long bits = __double_as_longlong(x[q][k]);
-                st_ll2(cb + 2 * i, ll_word((unsigned)(bits >> 32), stamp), ll_word((unsigned)bits, stamp));
-              }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
-            if (lane == 0) {
-              unsigned long long* me = slw + (int64_t)blockIdx.x * 8;
-              const unsigned long long tb = __double_as_longlong(tl), xb = __double_as_longlong(xj);
-              st_ll2(me, ll_word(b.hi, stamp), ll_word(b.lo, stamp));
-              st_ll2(me + 2, ll_word((unsigned)b.pos, stamp), ll_word((unsigned)b.col, stamp));
-              st_ll2(me + 4, ll_word((unsigned)(tb >> 32), stamp), ll_word((unsigned)tb, stamp));
-              st_ll2(me + 6, ll_word((unsigned)(xb >> 32), stamp), ll_word((unsigned)xb, stamp));
+          for (int k = KJ; k < RPL; k++) {
+            const int i = lane + 32 * k;
+            if (i >= j && i < m) {
+              const unsigned long long bits = __double_as_longlong(xc[k]);
+              st_ll2(cb + 2 * i, ll_word((unsigned)(bits >> 32), stamp), ll_word((unsigned)bits, stamp));
             }
           }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
+          if (lane == 0) {
+            unsigned long long* me = slw + (int64_t)blockIdx.x * 8;
+            const unsigned long long tb = __double_as_longlong(tl), xb = __double_as_longlong(xj);
+            st_ll2(me, ll_word(b.hi, stamp), ll_word(b.lo, stamp));
+            st_ll2(me + 2, ll_word((unsigned)b.pos, stamp), ll_word((unsigned)b.col, stamp));
+            st_ll2(me + 4, ll_word((unsigned)(tb >> 32), stamp), ll_word((unsigned)tb, stamp));
+            st_ll2(me + 6, ll_word((unsigned)(xb >> 32), stamp), ll_word((unsigned)xb, stamp));
+          }
+        };
+        bool done = false;
+        if constexpr (SMEM) {
+          if (b.col >= sm.cbase_s && b.col < sm.cbase_s + sm.spw) {
+            const double* col = sm.xs + (int64_t)(warp * sm.spw + (b.col - sm.cbase_s)) * RPL * 32 + lane;
+            double y[RPL];
+#pragma unroll
+            for (int k = 0; k < RPL; k++) y[k] = k >= KJ ? col[k * 32] : 0.0;
+            publish(y);
+            done = true;
+          }
+        }
+        if (!done) {
+          const int bqw = b.col - cbase;
+#pragma unroll
+          for (int q = 0; q < CPW; q++)
+            if (q == bqw) publish(x[q]);
+        }
       }
     }
     __syncthreads();
@@ -1316,6 +1382,17 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
         pos[q] = win.pos;
       }
     }
+    if constexpr (SMEM) {
+      if (lane < sm.spw) {
+        const int sc = warp * sm.spw + lane;
+        if (sm.cbase_s + lane == win.col) {
+          sm.spos[sc] = j;
+          sm.sact[sc] = 0;
+        } else if (sm.sact[sc] && sm.spos[sc] == j) {
+          sm.spos[sc] = win.pos;
+        }
+      }
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) p.chosen[j] = win.col;
     have_refl = refl;
     __syncthreads();
@@ -1323,26 +1400,36 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
   }
 }
 
-template <int KJ, int RPL, int CPW, int WARPS>
+template <int KJ, int RPL, int CPW, int WARPS, bool SMEM>
 RQ_DEV void sk_dispatch(int kj, const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
                         double (&x)[CPW][RPL], int (&pos)[CPW], bool (&act)[CPW], bool& have_refl, double* u,
-                        SkShared& sh, int cbase, int jend) {
+                        SkShared& sh, int cbase, int jend, const SkSmem& sm) {
   if constexpr (KJ < RPL) {
     if (kj == KJ)
-      sk_block<KJ, RPL, CPW, WARPS>(p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh, cbase, jend);
+      sk_block<KJ, RPL, CPW, WARPS, SMEM>(p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh, cbase, jend, sm);
     else
-      sk_dispatch<KJ + 1, RPL, CPW, WARPS>(kj, p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh, cbase,
-                                           jend);
+      sk_dispatch<KJ + 1, RPL, CPW, WARPS, SMEM>(kj, p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh,
+                                                 cbase, jend, sm);
   }
 }
 
-template <int RPL, int CPW, int WARPS>
+// Register-resident sketch CPQR.  CTA g owns columns [g*PER, (g+1)*PER): WARPS*CPW in registers
+// (warp w: g*PER + w*CPW + q) then, with SMEM, WARPS*spw in shared memory (warp w: after the
+// register block, w*spw + s).
+template <int RPL, int CPW, int WARPS, bool SMEM>
 __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchArgs p, SkSlot2* slots, SkWin* wins,
                                                                    unsigned long long stamp_base) {
   __shared__ double u[32 * RPL];
   __shared__ SkShared sh;
+  extern __shared__ double sk_dyn[];
+  constexpr int kMaxSpw = 8;
+  __shared__ int spos_s[SMEM ? WARPS * kMaxSpw : 1];
+  __shared__ int sact_s[SMEM ? WARPS * kMaxSpw : 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cbase = blockIdx.x * WARPS * CPW + warp * CPW;
+  const int spw = SMEM ? p.spw : 0;
+  const int per = WARPS * CPW + WARPS * spw;
+  const int cbase = blockIdx.x * per + warp * CPW;
+  SkSmem sm{sk_dyn, spos_s, sact_s, spw, (int)blockIdx.x * per + WARPS * CPW + warp * spw};
   double x[CPW][RPL];
   int pos[CPW];
   bool act[CPW];
@@ -1357,31 +1444,61 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
       x[q][k] = (act[q] && i < p.m) ? p.y[(int64_t)c * p.ld + i] : 0.0;
     }
   }
+  if constexpr (SMEM) {
+    for (int s2 = 0; s2 < spw; s2++) {
+      const int sc = warp * spw + s2;
+      const int c = sm.cbase_s + s2;
+      const bool a = c < p.n;
+      double* col = sk_dyn + (int64_t)sc * RPL * 32 + lane;
+#pragma unroll
+      for (int k = 0; k < RPL; k++) {
+        const int i = lane + 32 * k;
+        col[k * 32] = (a && i < p.m) ? p.y[(int64_t)c * p.ld + i] : 0.0;
+      }
+      if (lane == 0) {
+        sact_s[sc] = a ? 1 : 0;
+        spos_s[sc] = a ? (p.init_pos ? p.init_pos[c] : c) : INT_MAX;
+      }
+    }
+    __syncthreads();
+  }
   bool have_refl = false;
   for (int kj = 0; 32 * kj < p.steps; kj++) {
     const int jend = min(p.steps, 32 * kj + 32);
-    sk_dispatch<0, RPL, CPW, WARPS>(kj, p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh, cbase, jend);
+    sk_dispatch<0, RPL, CPW, WARPS, SMEM>(kj, p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh, cbase, jend,
+                                          sm);
   }
 }
 
-template <int RPL, int CPW, int WARPS>
+template <int RPL, int CPW, int WARPS, bool SMEM = false>
 static int launch_sketch_reg(const SketchArgs& a, int G, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
                              cudaStream_t st, int64_t* launches) {
   void* args[] = {(void*)&a, (void*)&slots, (void*)&wins, (void*)&stamp_base};
-  RQ_CUDA_TRY(cudaLaunchCooperativeKernel((void*)sketch_reg_kernel<RPL, CPW, WARPS>, dim3(G), dim3(WARPS * 32), args,
-                                          0, st));
+  auto kern = sketch_reg_kernel<RPL, CPW, WARPS, SMEM>;
+  const size_t dyn = SMEM ? (size_t)WARPS * a.spw * RPL * 32 * sizeof(double) : 0;
+  if (SMEM) {
+    static bool attr = false;
+    if (!attr) {
+      RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+  }
+  RQ_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(WARPS * 32), args, dyn, st));
   if (launches) (*launches)++;
   return RQ_OK;
 }
 
-// (warps, columns per warp) options in order of preference; registers: CPW*RPL doubles
+// (warps, columns per warp) options in order of preference; registers: CPW*RPL doubles.
+// Beyond their capacity (RPL = 9, i.e. b+p <= 288): 12 warps x 6 register columns plus up to
+// 7 shared-memory columns per warp (<= 200 KB), 156 columns per CTA.
 template <int RPL>
-static int dispatch_sketch_reg(const SketchArgs& a, int n, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
+static int dispatch_sketch_reg(SketchArgs a, int n, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
                                cudaStream_t st, int64_t* launches, int* grid) {
   struct Opt {
     int warps, cpw;
   };
   const Opt opts[] = {{16, 1}, {16, 2}, {16, 3}, {8, 6}, {8, 10}};
+  a.spw = 0;
   for (const Opt& o : opts) {
     if (RPL * o.cpw > (o.warps == 16 ? 30 : 92)) continue;  // register budget
     const int G = (n + o.warps * o.cpw - 1) / (o.warps * o.cpw);
@@ -1392,6 +1509,18 @@ static int dispatch_sketch_reg(const SketchArgs& a, int n, SkSlot2* slots, SkWin
     if (o.warps == 16 && o.cpw == 3) return launch_sketch_reg<RPL, 3, 16>(a, G, slots, wins, stamp_base, st, launches);
     if (o.cpw == 6) return launch_sketch_reg<RPL, 6, 8>(a, G, slots, wins, stamp_base, st, launches);
     return launch_sketch_reg<RPL, 10, 8>(a, G, slots, wins, stamp_base, st, launches);
+  }
+  if constexpr (RPL == 9) {
+    constexpr int W = 12, C = 6;
+    const int per_needed = (n + kSMs - 1) / kSMs;
+    const int spw = std::max(1, (per_needed - W * C + W - 1) / W);
+    if (spw <= 7 && (size_t)W * spw * RPL * 32 * 8 <= 200 * 1024) {
+      a.spw = spw;
+      const int per = W * C + W * spw;
+      const int G = (n + per - 1) / per;
+      *grid = G;
+      return launch_sketch_reg<RPL, C, W, true>(a, G, slots, wins, stamp_base, st, launches);
+    }
   }
   return -1;  // does not fit: caller falls back
 }

@@ -138,3 +138,21 @@ def test_distributed_world1_nccl_matches_single_gpu(m, n, b, p):
         assert rng.counter == rng1.counter == ref_rng.counter
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,steps", [(900, 256), (9000, 256), (13000, 256), (21500, 96), (24000, 40)])
+def test_sketch_select_every_kernel_tier(n, steps):
+    """The sketch CPQR picks the reference's pivots in every tier: register-resident
+    (n' <= 11840), registers + shared memory (<= ~23k), and the L2-streaming fallback."""
+    import randqr_oracle as orc
+
+    e = _eng()
+    wdt = 272
+    y = np.random.default_rng(n).standard_normal((wdt, n))
+    buf, ld = e.alloc(wdt, n)
+    _put(buf, y)
+    got = e.select(buf, ld, wdt, n, steps, np.arange(n))
+    v = np.zeros((wdt, steps), order="F")
+    perm = np.arange(n, dtype=np.int64)
+    orc.householder_sweep(np.asfortranarray(y), v, perm, steps, True)
+    assert np.array_equal(got, perm[:steps])
