@@ -285,3 +285,43 @@ def test_block_rrqr_cfg4_like_spectrum(golden, rq):
     rr_ref = np.abs(np.log10(np.maximum(ref[:100], 1e-300) / s[:100]))
     assert np.median(rr) <= np.median(rr_ref) + 0.1
     check_factorization(a, f, tol=1e-12)
+
+
+def test_bench_workload_n10k_properties_and_leading_pivots(rq):
+    """BASELINE cfg 3 at its full size (n = 10000, b = 256, p = 16, A = gaussian_matrix(n, n,
+    RngState(0)), sketch seed 1): size-independent properties through random probes --
+    ||A[:, perm] x - Q (R x)|| <= 1e-13 ||A|| ||x||, ||Q^T (Q y) - y|| <= 1e-13 sqrt(n) ||y|| --
+    and the first two panels' 512 pivots identical to the reference algorithm (oracle, bounded
+    to two panels, which fixes those positions of the composite permutation)."""
+    import os
+    import sys
+
+    import torch
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "oracle"))
+    import randqr_oracle as orc
+
+    n, b, p = 10000, 256, 16
+    eng = rq.Engine()
+    a_dev, ld = rq.gaussian_matrix_device(n, n, rq.RngState(0), engine=eng)
+    a = a_dev[:n, :n].T  # torch view of A (n x n)
+    rng = rq.RngState(1)
+    f = rq.block_qr(a.cpu().numpy(), _cfg(rq, b, p, 0), rng, engine=eng)
+    perm = torch.as_tensor(f.perm, device=a.device)
+    r = torch.as_tensor(f.r, device=a.device)
+    qbuf, ldq = f.expand_q_device()
+    q = qbuf[:n, :n].T
+    g = torch.Generator(device=a.device).manual_seed(5)
+    x = torch.randn(n, 4, dtype=torch.float64, device=a.device, generator=g)
+    anorm = torch.linalg.norm(a)
+    res = torch.linalg.norm(a[:, perm] @ x - q @ (r @ x)) / (anorm * torch.linalg.norm(x))
+    assert float(res) <= 1e-13
+    y = torch.randn(n, 4, dtype=torch.float64, device=a.device, generator=g)
+    orth = torch.linalg.norm(q.T @ (q @ y) - y) / torch.linalg.norm(y)
+    assert float(orth) <= 1e-13 * np.sqrt(n)
+    assert not np.tril(f.r, -1).any()
+    # leading pivots vs the reference algorithm
+    ao = orc.gaussian_matrix(n, n, orc.RngState(0))
+    fo = orc.block_qr(ao, orc.BlockConfig(b, orc.SketchConfig(b, p, 0)), orc.RngState(1), max_panels=2)
+    assert np.array_equal(f.perm[:2 * b], fo.perm()[:2 * b])
+    assert rng.counter == sum((n - s) * (b + p) for s in range(0, n - b, b))
