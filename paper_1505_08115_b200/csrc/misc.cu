@@ -2,6 +2,8 @@
 //   * T factor from the Gram matrix (K7),
 //   * pivot bookkeeping and the column moves (K5),
 //   * matrix fills / copies used by the driver and by Q formation (K12).
+#include <algorithm>
+
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -279,45 +281,76 @@ int plan_moves(const PlanCall& c, cudaStream_t st, int64_t* launches) {
 // scatter) because src and dst overlap as sets.  One warp per column,
 // vectorised 16 B accesses when the column start is aligned.
 // ---------------------------------------------------------------------------
-__global__ void gather_cols_kernel(const double* __restrict__ A, int64_t lda, int64_t coff, int64_t r0, int64_t r1,
-                                   const int* __restrict__ src, const int* __restrict__ count, int maxn,
-                                   double* __restrict__ stage, int64_t lds, const int64_t* __restrict__ orig,
-                                   int64_t* __restrict__ ostage) {
+// Full-height column moves, two passes (all sources staged before any target is
+// written, so a slot can be both).  Grid (row chunks, columns): every chunk is
+// 2048 rows, 8 independent loads in flight per thread -> HBM-bound.
+constexpr int MV_THREADS = 256;
+constexpr int MV_PER = 8;
+constexpr int MV_CHUNK = MV_THREADS * MV_PER;
+
+__global__ void __launch_bounds__(MV_THREADS) gather_cols_kernel(const double* __restrict__ A, int64_t lda,
+                                                                 int64_t coff, int64_t r0, int64_t r1,
+                                                                 const int* __restrict__ src,
+                                                                 const int* __restrict__ count, int maxn,
+                                                                 double* __restrict__ stage, int64_t lds,
+                                                                 const int64_t* __restrict__ orig,
+                                                                 int64_t* __restrict__ ostage) {
   const int n = count ? *count : maxn;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int t = warp; t < n; t += nw) {
-    const double* s = A + (coff + src[t]) * lda;
-    double* d = stage + (int64_t)t * lds;
-    for (int64_t i = r0 + lane; i < r1; i += 32) d[i - r0] = s[i];
-    if (orig && lane == 0) ostage[t] = orig[coff + src[t]];
+  const int t = blockIdx.y;
+  if (t >= n) return;
+  const double* s = A + (coff + src[t]) * lda;
+  double* d = stage + (int64_t)t * lds;
+  const int64_t i0 = r0 + (int64_t)blockIdx.x * MV_CHUNK + threadIdx.x;
+  double v[MV_PER];
+#pragma unroll
+  for (int k = 0; k < MV_PER; k++) {
+    const int64_t i = i0 + (int64_t)k * MV_THREADS;
+    v[k] = i < r1 ? __ldcs(&s[i]) : 0.0;
   }
+#pragma unroll
+  for (int k = 0; k < MV_PER; k++) {
+    const int64_t i = i0 + (int64_t)k * MV_THREADS;
+    if (i < r1) d[i - r0] = v[k];
+  }
+  if (orig && blockIdx.x == 0 && threadIdx.x == 0) ostage[t] = orig[coff + src[t]];
 }
-__global__ void scatter_cols_kernel(double* __restrict__ A, int64_t lda, int64_t coff, int64_t r0, int64_t r1,
-                                    const int* __restrict__ dst, const int* __restrict__ count, int maxn,
-                                    const double* __restrict__ stage, int64_t lds, int64_t* __restrict__ orig,
-                                    const int64_t* __restrict__ ostage) {
+__global__ void __launch_bounds__(MV_THREADS) scatter_cols_kernel(double* __restrict__ A, int64_t lda, int64_t coff,
+                                                                  int64_t r0, int64_t r1,
+                                                                  const int* __restrict__ dst,
+                                                                  const int* __restrict__ count, int maxn,
+                                                                  const double* __restrict__ stage, int64_t lds,
+                                                                  int64_t* __restrict__ orig,
+                                                                  const int64_t* __restrict__ ostage) {
   const int n = count ? *count : maxn;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int t = warp; t < n; t += nw) {
-    double* d = A + (coff + dst[t]) * lda;
-    const double* s = stage + (int64_t)t * lds;
-    for (int64_t i = r0 + lane; i < r1; i += 32) d[i] = s[i - r0];
-    if (orig && lane == 0) orig[coff + dst[t]] = ostage[t];
+  const int t = blockIdx.y;
+  if (t >= n) return;
+  double* d = A + (coff + dst[t]) * lda;
+  const double* s = stage + (int64_t)t * lds;
+  const int64_t i0 = r0 + (int64_t)blockIdx.x * MV_CHUNK + threadIdx.x;
+  double v[MV_PER];
+#pragma unroll
+  for (int k = 0; k < MV_PER; k++) {
+    const int64_t i = i0 + (int64_t)k * MV_THREADS;
+    v[k] = i < r1 ? s[i - r0] : 0.0;
   }
+#pragma unroll
+  for (int k = 0; k < MV_PER; k++) {
+    const int64_t i = i0 + (int64_t)k * MV_THREADS;
+    if (i < r1) d[i] = v[k];
+  }
+  if (orig && blockIdx.x == 0 && threadIdx.x == 0) orig[coff + dst[t]] = ostage[t];
 }
 
 int move_columns(const MoveCall& c, cudaStream_t st, int64_t* launches) {
   if (c.r1 <= c.r0 && !c.orig) return RQ_OK;
-  int blocks = (c.maxn * 32 + 255) / 256;
-  if (blocks > 4 * kSMs) blocks = 4 * kSMs;
-  if (blocks < 1) blocks = 1;
-  gather_cols_kernel<<<blocks, 256, 0, st>>>(c.A, c.lda, c.coff, c.r0, c.r1, c.src, c.count, c.maxn, c.stage,
-                                             c.lds, c.orig, c.ostage);
+  if (c.maxn <= 0) return RQ_OK;
+  const int64_t rows = c.r1 > c.r0 ? c.r1 - c.r0 : 0;
+  const dim3 grid((unsigned)std::max<int64_t>(1, ceil_div(rows, MV_CHUNK)), (unsigned)c.maxn);
+  gather_cols_kernel<<<grid, MV_THREADS, 0, st>>>(c.A, c.lda, c.coff, c.r0, c.r1, c.src, c.count, c.maxn, c.stage,
+                                                  c.lds, c.orig, c.ostage);
   RQ_CUDA_TRY(cudaGetLastError());
-  scatter_cols_kernel<<<blocks, 256, 0, st>>>(c.A, c.lda, c.coff, c.r0, c.r1, c.dst, c.count, c.maxn, c.stage,
-                                              c.lds, c.orig, c.ostage);
+  scatter_cols_kernel<<<grid, MV_THREADS, 0, st>>>(c.A, c.lda, c.coff, c.r0, c.r1, c.dst, c.count, c.maxn, c.stage,
+                                                   c.lds, c.orig, c.ostage);
   RQ_CUDA_TRY(cudaGetLastError());
   if (launches) (*launches) += 2;
   return RQ_OK;
