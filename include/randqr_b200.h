@@ -107,6 +107,17 @@ int rq_gaussian_matrix(rq_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, u
 /* Plain splitmix64 words (rng.py:29-39) for the bitwise integer-stream pin. */
 int rq_splitmix_words(rq_ctx* ctx, uint64_t seed, uint64_t first, int64_t count, uint64_t* dOut);
 
+/* Unpivoted blocked Householder QR in place (qr_unpivoted, householder.py:152-161;
+ * reflector convention householder.py:55-69), in blocks of `block` columns; m >= n.
+ * dA becomes R; the factors are kept in the context for rq_form_q (Q) -- the
+ * device-side haar_orthonormal of matrices.py:34-41 is built on it. */
+int rq_qr_unpivoted(rq_ctx* ctx, int64_t m, int64_t n, double* dA, int64_t lda, int32_t block);
+
+/* Frobenius truncation errors at scale (metrics.truncation_errors, metrics.py:37-52, without
+ * dense expansion): A P = Q R gives ||A - Q(:,1:k) R(1:k,:) P^T||_F = ||R(k:, k:)||_F, so for the
+ * n x n upper-triangular block dR this writes dE2[k] = ||R(k:, k:)||_F^2, k = 0..n (n+1 values). */
+int rq_trailing_frobenius(rq_ctx* ctx, const double* dR, int64_t n, int64_t ldr, double* dE2);
+
 /* ---- Panel-step API: one HQRRP panel at a time on caller-owned device buffers.
  * Used by a driver that owns the column distribution (paper_1505_08115_b200/dist.py,
  * 1-D block-cyclic columns over ranks).  The pieces are those of

@@ -243,6 +243,25 @@ int rq_test_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K,
   return c.gemm(M, N, K, A, a_mmajor != 0, B, dC, ldc, alpha, beta);
 }
 
+int rq_qr_unpivoted(rq_ctx* ctx, int64_t m, int64_t n, double* dA, int64_t lda, int32_t block) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (m < n) return rq::set_error(RQ_EDIM, "qr_unpivoted needs rows >= cols, got %lldx%lld", (long long)m, (long long)n);
+  if (n < 1 || block < 1) return rq::set_error(RQ_EDIM, "bad shape n=%lld block=%d", (long long)n, block);
+  if (lda < m || (lda & 1) || ((uintptr_t)dA & 15))
+    return rq::set_error(RQ_EVALUE, "dA must be 16-byte aligned with an even lda >= m");
+  return ctx->c.factorize_unpivoted(m, n, dA, lda, std::min<int64_t>(block, n));
+}
+
+// Frobenius truncation errors from R (metrics.truncation_errors at scale): for an
+// upper-triangular R (n x n block at dR), e2[k] = ||R[k:, k:]||_F^2, k = 0..n (e2[n] = 0).
+int rq_trailing_frobenius(rq_ctx* ctx, const double* dR, int64_t n, int64_t ldr, double* dE2) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (n < 0 || ldr < n) return rq::set_error(RQ_EDIM, "trailing_frobenius: bad shape");
+  return rq::trailing_frobenius(dR, n, ldr, dE2, ctx->c.stream, &ctx->c.launches);
+}
+
 // ---------------------------------------------------------------------------
 // Panel-step API (multi-GPU driver, dist.py)
 // ---------------------------------------------------------------------------

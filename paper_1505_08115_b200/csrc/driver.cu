@@ -651,6 +651,48 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
   return RQ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Unpivoted blocked Householder QR (qr_unpivoted, householder.py:152-161, in
+// blocks of b): the panel kernels + T + trailing update, no sketch, no pivots.
+// Used by the device-side test-matrix generator (haar_orthonormal,
+// matrices.py:34-41).  R overwrites A; the factors are stored for form_q.
+// ---------------------------------------------------------------------------
+int Ctx::factorize_unpivoted(int64_t m, int64_t n, double* A, int64_t lda, int b) {
+  size_t need = plan_layout(nullptr, m, n, b, 0, 0).total;
+  RQ_TRY(arena.reserve(need));
+  Layout L = plan_layout(arena.base, m, n, b, 0, 0);
+  kwork = L.kwork;
+  kwork_bytes = L.kwork_bytes;
+  sweep_ws = L.sweep_ws;
+  sweep_ws_bytes = L.sweep_ws_bytes;
+  factors.clear();
+  rfactors.clear();
+  p_is_perm = true;
+  factors_perm = L.orig;
+  fm = m;
+  fn = n;
+  fb = b;
+  RQ_TRY(iota(nullptr, 0, L.orig, n, stream, &launches));
+  Carver fc(L.fstore);
+  for (int64_t s = 0; s < n; s += b) {
+    const int w = (int)std::min<int64_t>(b, n - s);
+    const int64_t mp = m - s;
+    const int64_t ldv = even(mp + 1), ldt = even(b);
+    const int vpad = (int)(s & 1);
+    double* V = fc.take<double>((size_t)ldv * w);  // as factor_bytes sizes the final panel
+    double* T = fc.take<double>((size_t)ldt * b);
+    RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * w * sizeof(double), stream));
+    launches++;
+    RQ_TRY(panel_qr(A, lda, m, n, s, mp, w, V, ldv, vpad, L.tleaf, L.w1, L.w2));
+    RQ_TRY(tfactor(V, mp, w, ldv, vpad, T, ldt, L.gram));
+    const int64_t n2 = n - s - w;
+    if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, w, n2, V, ldv, vpad, T, ldt, nullptr, L));
+    factors.push_back(PanelFactors{s, w, V, ldv, vpad, T, ldt, nullptr, 0});
+  }
+  have_factors = true;
+  return RQ_OK;
+}
+
 // Y^T ((b+p) x n') of the trailing block X = A[s:, s:]: (X^T X)^q X^T Omega,
 // built from TN/NN DMMA GEMMs (pivoting.py:87-111, unstabilised powers).
 int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int64_t np,

@@ -163,6 +163,7 @@ struct Ctx {
   int reflector_pivot(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, Layout& L,
                       void* fc_ptr, uint64_t seed, uint64_t* counter);
   int form_q(int64_t cols, double* Q, int64_t ldq);
+  int factorize_unpivoted(int64_t m, int64_t n, double* A, int64_t lda, int b);
   // Panel-step API for drivers that own the column distribution (multi-GPU, dist.py)
   int step_sketch_select(double* Y, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen);
   int step_panel_factor(double* P, int64_t ldp, int64_t mp, int b, double* V, int64_t ldv, double* T, int64_t ldt,

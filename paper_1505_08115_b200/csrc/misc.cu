@@ -356,6 +356,41 @@ int move_columns(const MoveCall& c, cudaStream_t st, int64_t* launches) {
   return RQ_OK;
 }
 
+// e2[k] = sum_{i >= k} sum_{j >= i} R(i, j)^2 for upper-triangular R: row sums of squares
+// (thread per row: for a fixed column the warp's loads are contiguous), then a suffix
+// scan in fixed order (one thread; n <= a few 1e4).
+__global__ void row_sq_kernel(const double* __restrict__ R, int64_t n, int64_t ldr, double* __restrict__ rs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t j = i; j < n; j++) {
+      const double v = R[j * ldr + i];
+      acc = fma(v, v, acc);
+    }
+    rs[i] = acc;
+  }
+}
+__global__ void suffix_sum_kernel(double* e, int64_t n) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double acc = 0.0;
+    e[n] = 0.0;
+    for (int64_t k = n - 1; k >= 0; k--) {
+      acc += e[k];
+      e[k] = acc;
+    }
+  }
+}
+int trailing_frobenius(const double* R, int64_t n, int64_t ldr, double* e2, cudaStream_t st, int64_t* launches) {
+  if (n > 0) {
+    const int blocks = (int)std::min<int64_t>(4 * kSMs, ceil_div(n, 256));
+    row_sq_kernel<<<blocks, 256, 0, st>>>(R, n, ldr, e2);
+    RQ_CUDA_TRY(cudaGetLastError());
+  }
+  suffix_sum_kernel<<<1, 32, 0, st>>>(e2, n);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches) += 2;
+  return RQ_OK;
+}
+
 // identity index arrays
 __global__ void iota_kernel(int* a, int n, int64_t* b, int64_t nb) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n || i < nb;
