@@ -357,17 +357,18 @@ def main():
     with torch.cuda.stream(stream):
         a0, ld = rq.gaussian_matrix_device(m, n, rq.RngState(0), engine=eng)
         if args.matrix == "cfg4":
-            # input generation only (outside the timed region): Haar U, V from QR of Gaussians
-            g1, _ = rq.gaussian_matrix_device(n, n, rq.RngState(0, 10**12), engine=eng)
-            qu, ru = torch.linalg.qr(g1[:n, :n].T)
-            qu = qu * torch.sign(torch.diagonal(ru))
-            qv, rv = torch.linalg.qr(a0[:n, :n].T)
-            qv = qv * torch.sign(torch.diagonal(rv))
+            # cfg 4: U diag(s) V^T, U and V = haar_orthonormal(n, RngState(0))
+            # drawn U first (matrices.py:34-41, 67-68), s_j = max(10^(-12 j / 2000), 1e-15); built on
+            # the device with this library's unpivoted QR, outside the timed region
+            from paper_1505_08115_b200.matrices import haar_orthonormal_device
+
+            hr = rq.RngState(0)
+            u, _ = haar_orthonormal_device(n, hr, engine=eng)
+            v, _ = haar_orthonormal_device(n, hr, engine=eng)
             jj = torch.arange(1, n + 1, device=eng.device, dtype=torch.float64)
             sv = torch.clamp(10.0 ** (-12.0 * jj / 2000.0), min=1e-15)
-            amat = (qu * sv) @ qv.T
-            a0[:n, :n].copy_(amat.T)
-            del g1, qu, ru, qv, rv, amat
+            a0[:n, :n] = v[:n, :n].T @ (u[:n, :n] * sv[:, None])  # storage = A^T = V diag(s) U^T
+            del u, v
         work, _ = eng.alloc_matrix(m, n)
         perm = torch.empty(n, dtype=torch.int64, device=eng.device)
     mode = _lib.RQ_SKETCH_FRESH if args.sketch == "fresh" else _lib.RQ_SKETCH_DOWNDATE
