@@ -294,6 +294,64 @@ def run_distributed(args, dist, rank, world, local):
     dist.destroy_process_group()
 
 
+def run_fp32(args, local):
+    """cfg 3 fp32: one factorization per step on one GPU (fp32.py), device-timed."""
+    import torch
+
+    import paper_1505_08115_b200 as rq
+    from paper_1505_08115_b200 import dist as rqd
+    from paper_1505_08115_b200.fp32 import Fp32StepEngine
+
+    torch.cuda.set_device(local)
+    n, b, p = args.n, args.b, args.p
+    m = n
+    stream = torch.cuda.Stream()
+    eng = rq.Engine(local, stream=stream)
+    se = Fp32StepEngine(eng)
+    cfg = rq.BlockConfig(b, rq.SketchConfig(b, p, 0))
+    with torch.cuda.stream(stream):
+        a64, _ = rq.gaussian_matrix_device(m, n, rq.RngState(0), engine=eng)
+        a0, lda = se.alloc(m, n)
+        a0[:n, :m] = a64[:n, :m]
+        del a64
+        work = torch.empty_like(a0)
+
+    def step():
+        with torch.cuda.stream(stream):
+            work.copy_(a0)
+            rqd.factorize_local(work, lda, m, n, cfg, rq.RngState(1), engine=se)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    time.sleep(0.3)
+    launches0 = eng.launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    flops_step = 4.0 / 3.0 * n ** 3
+    value = args.steps * flops_step / (ms * 1e-3) / 1e12
+    line = {
+        "metric": "fp32 TFLOP/s (4/3·n³ count) for HQRRP, cfg 3 fp32 variant", "value": value, "unit": "TFLOP/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (GEMMs) / f64 (serial kernels)",
+        "data": "synthetic",
+        "config": {"workload": f"cfg3 fp32 HQRRP n={n} b={b} p={p} q=0, fresh sketch", "n": n, "b": b, "p": p,
+                   "parallelism": "single", "l2": "inputs (400 MB) larger than L2 (126 MB)"},
+        "note": "fp32 storage; sketch and trailing GEMMs = cuBLAS SGEMM via torch (TF32 off); sketch CPQR, panel "
+                "QR, b x b CPQR, T in this library's fp64 kernels (fp32.py)",
+        "clocks": clk, "gpu_launches": eng.launches - launches0, "e2e": None, "cpu_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -314,6 +372,8 @@ def main():
                     help="m1 block_qr permutation pivots (headline), m2 reflector pivots, m3 block_rrqr")
     ap.add_argument("--q", type=int, default=0, help="power iterations of the sketch")
     ap.add_argument("--dist", action="store_true", help="use the block-cyclic multi-GPU driver even at N = 1")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
+                    help="f32: cfg 3's fp32 variant (fp32 storage and GEMMs, fp64 serial kernels; fp32.py)")
     ap.add_argument("--matrix", default="gauss", choices=["gauss", "cfg4"],
                     help="gauss: N(0,1) (cfg 3); cfg4: U diag(max(10^(-12j/2000),1e-15)) V^T")
     args = ap.parse_args()
@@ -324,6 +384,9 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.dtype == "f32":
+        run_fp32(args, local)
         return
 
     import torch

@@ -186,8 +186,12 @@ class _Dist:
 
         self.dist = dist
         self.group = group
-        self.world = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
+        if dist.is_available() and dist.is_initialized():
+            self.world = dist.get_world_size(group)
+            self.rank = dist.get_rank(group)
+        else:  # single process without a process group (e.g. the fp32 path on one GPU)
+            self.world = 1
+            self.rank = 0
 
     def global_rank(self, r):
         if self.group is None:
@@ -330,7 +334,7 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         ldv = mp + (mp & 1)
         ldb = b + (b & 1)
         nfac = b * ldv + 2 * b * ldb + b
-        pack = torch.empty(nfac, dtype=torch.float64, device=a_loc.device)
+        pack = torch.empty(nfac, dtype=a_loc.dtype, device=a_loc.device)  # P-hat exact in fp32 too (b < 2^24)
         if rank == o:
             lo = lay.local_off(i)
             p, ldp = engine.alloc(mp, b)
@@ -343,7 +347,7 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
             pack[:b * ldv].copy_(v[:b, :ldv].reshape(-1))
             pack[b * ldv:b * ldv + b * ldb].copy_(t[:b, :ldb].reshape(-1))
             pack[b * ldv + b * ldb:b * ldv + 2 * b * ldb].copy_(q2[:b, :ldb].reshape(-1))
-            pack[nfac - b:].copy_(ph.to(torch.float64))
+            pack[nfac - b:].copy_(ph.to(pack.dtype))
         if d.world > 1:
             d.dist.broadcast(pack, src=d.global_rank(o), group=d.group)
         v = pack[:b * ldv].view(b, ldv)
@@ -408,14 +412,14 @@ def gather_r(res: DistResult, engine, group=None):
     lay = res.layout
     counts = [lay.n_local(q) for q in range(d.world)]
     cmax = max(counts)
-    local = torch.zeros((cmax, res.lda), dtype=torch.float64, device=res.a_loc.device)
+    local = torch.zeros((cmax, res.lda), dtype=res.a_loc.dtype, device=res.a_loc.device)
     local[:counts[d.rank]].copy_(res.a_loc[:counts[d.rank], :res.lda])
     if d.world > 1:
-        allb = torch.empty((d.world * cmax, res.lda), dtype=torch.float64, device=local.device)
+        allb = torch.empty((d.world * cmax, res.lda), dtype=local.dtype, device=local.device)
         d.dist.all_gather_into_tensor(allb, local, group=d.group)
     else:
         allb = local
-    full = torch.zeros((res.n, res.lda), dtype=torch.float64, device=local.device)
+    full = torch.zeros((res.n, res.lda), dtype=local.dtype, device=local.device)
     for q in range(d.world):
         slots = lay.slots_from(q, 0)
         if len(slots):
