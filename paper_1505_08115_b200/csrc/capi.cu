@@ -124,14 +124,38 @@ int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, c
   int rc = RQ_OK;
   cudaError_t e = cudaMemcpy2DAsync(dA, ldd * 8, hA, lda * 8, m * 8, n, cudaMemcpyHostToDevice, c.stream);
   if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "H2D: %s", cudaGetErrorString(e));
-  if (rc == RQ_OK) rc = rq_factorize(ctx, cfg, m, n, dA, ldd, seed, counter, dp);
+  // R streams back panel by panel on a copy stream while later panels compute
+  static thread_local cudaStream_t cs = nullptr;
+  static thread_local cudaEvent_t ev = nullptr;
+  if (rc == RQ_OK && hR && !cs) {
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+      rc = rq::set_error(RQ_ECUDA, "copy stream");
+  }
+  int64_t copied = 0;  // columns [0, copied) queued
   if (rc == RQ_OK && hR) {
-    e = cudaMemcpy2DAsync(hR, ldr * 8, dA, ldd * 8, m * 8, n, cudaMemcpyDeviceToHost, c.stream);
+    c.on_cols_final = [&](int64_t s, int64_t w) {
+      if (s != copied) return;  // keep the watermark contiguous; the rest goes at the end
+      cudaEventRecord(ev, c.stream);
+      cudaStreamWaitEvent(cs, ev, 0);
+      cudaMemcpy2DAsync(hR + s * ldr, ldr * 8, dA + s * ldd, ldd * 8, m * 8, w, cudaMemcpyDeviceToHost, cs);
+      copied = s + w;
+    };
+  }
+  if (rc == RQ_OK) rc = rq_factorize(ctx, cfg, m, n, dA, ldd, seed, counter, dp);
+  c.on_cols_final = nullptr;
+  if (rc == RQ_OK && hR && copied < n) {
+    e = cudaMemcpy2DAsync(hR + copied * ldr, ldr * 8, dA + copied * ldd, ldd * 8, m * 8, n - copied,
+                          cudaMemcpyDeviceToHost, c.stream);
     if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "D2H: %s", cudaGetErrorString(e));
   }
   if (rc == RQ_OK && hperm) {
     e = cudaMemcpyAsync(hperm, dp, n * 8, cudaMemcpyDeviceToHost, c.stream);
     if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "D2H perm: %s", cudaGetErrorString(e));
+  }
+  if (cs && copied > 0) {  // dA is freed on the main stream: after the streamed copies
+    cudaEventRecord(ev, cs);
+    cudaStreamWaitEvent(c.stream, ev, 0);
   }
   cudaFreeAsync(dA, c.stream);
   cudaFreeAsync(dp, c.stream);

@@ -485,6 +485,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
         rfactors.push_back(RightFactors{s, np, 0, nullptr, 0, nullptr, 0, phat, w, nullptr, 0, 0});
       }
       RQ_TRY(iota(lorder, (int)np, nullptr, 0, stream, &launches));
+      if (on_cols_final) on_cols_final(s, np);
       if (inspect_cb) {
         cur_lorder = nullptr;
         RQ_CUDA_TRY(cudaStreamSynchronize(stream));
@@ -609,6 +610,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     RQ_TRY(copy2d(L.rfin, L.lds_small, A + s + s * lda, lda, b, b, 0, stream, &launches));
     MoveCall mv2{A, lda, s, 0, s, L.cap, L.iota_b, nullptr, b, L.stage, even(m), L.orig, L.ostage};
     RQ_TRY(move_columns(mv2, stream, &launches));
+    if (on_cols_final) on_cols_final(s, b);  // later steps only touch columns >= s + b
     if (downdate) {  // P-hat on the sketch's panel columns
       MoveCall my2{L.yt, L.ldy, s, 0, wdt, L.cap, L.iota_b, nullptr, b, L.stage, L.ldy, nullptr, nullptr};
       RQ_TRY(move_columns(my2, stream, &launches));

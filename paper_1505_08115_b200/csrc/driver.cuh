@@ -1,5 +1,6 @@
 // Host-side driver state (see driver.cu) behind the opaque rq_ctx.
 #pragma once
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -111,6 +112,9 @@ struct Ctx {
   cudaStream_t side = nullptr, hip = nullptr;
   cudaEvent_t ev_v = nullptr, ev_side = nullptr, ev_hi = nullptr;
   bool overlap_on = true;
+  // called (host side, enqueue order) when columns [s, s + w) of R are final: no later step
+  // writes them (rq_factorize_host streams them to the host while later panels compute)
+  std::function<void(int64_t, int64_t)> on_cols_final;
   int gemm_max_ctas = 0;
   bool gemm_pdl = false;
   int ensure_side();

@@ -325,3 +325,28 @@ def test_bench_workload_n10k_properties_and_leading_pivots(rq):
     fo = orc.block_qr(ao, orc.BlockConfig(b, orc.SketchConfig(b, p, 0)), orc.RngState(1), max_panels=2)
     assert np.array_equal(f.perm[:2 * b], fo.perm()[:2 * b])
     assert rng.counter == sum((n - s) * (b + p) for s in range(0, n - b, b))
+
+
+@pytest.mark.parametrize("m,n,b,p,kind", [(700, 650, 64, 8, "permutation"), (520, 500, 96, 10, "reflectors")])
+def test_host_entry_streams_r_identically(rq, m, n, b, p, kind):
+    """rq_factorize_host (host buffers, R streamed back panel by panel while later panels
+    compute) returns exactly the device path's R and permutation."""
+    import ctypes
+
+    from paper_1505_08115_b200 import _lib
+    from paper_1505_08115_b200.errors import check
+
+    a = np.asfortranarray(np.random.default_rng(m + n).standard_normal((m, n)))
+    f = rq.block_qr(a, _cfg(rq, b, p, 0, refl=(kind == "reflectors")), rq.RngState(3))
+    eng = rq.Engine()
+    pk = _lib.RQ_PIVOT_PERMUTATION if kind == "permutation" else _lib.RQ_PIVOT_REFLECTORS
+    cfg = _lib.rq_config(b, p, 0, -1, pk, 0, _lib.RQ_SKETCH_FRESH, 0)
+    hr = np.zeros((m, n), order="F")
+    hp = np.zeros(n, dtype=np.int64)
+    ctr = ctypes.c_uint64(0)
+    check(eng.lib.rq_factorize_host(eng.handle, ctypes.byref(cfg), m, n, a.ctypes.data_as(ctypes.c_void_p), m,
+                                    ctypes.c_uint64(3), ctypes.byref(ctr), hr.ctypes.data_as(ctypes.c_void_p), m,
+                                    hp.ctypes.data_as(ctypes.c_void_p)))
+    assert np.array_equal(np.triu(hr), f.r)
+    if kind == "permutation":
+        assert np.array_equal(hp, f.perm)
