@@ -288,12 +288,14 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
     slot_orig = np.arange(n, dtype=np.int64)
     slot_lpos = np.arange(n, dtype=np.int64)
     counts_cache = {}
+    ph_pending = []
     for i in range(lay.nblk):
         s = i * b
         np_ = n - s
         mp = m - s
         o = lay.owner(i)
         if np_ <= b:
+            _apply_pending_phat(slot_orig, ph_pending)
             _final_block(a_loc, lda, m, n, s, i, lay, rank, slot_orig, slot_lpos, d, engine)
             break
         # ---- 1: sketch of the local trailing columns (same Omega on every rank) ----
@@ -353,15 +355,29 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         v = pack[:b * ldv].view(b, ldv)
         t = pack[b * ldv:b * ldv + b * ldb].view(b, ldb)
         q2 = pack[b * ldv + b * ldb:b * ldv + 2 * b * ldb].view(b, ldb)
-        ph_host = pack[nfac - b:].cpu().numpy().astype(np.int64)
-        slot_orig[s:s + b] = slot_orig[s + ph_host]
+        # P-hat reorders the panel's slots; those never compete for pivots again, so only
+        # the final perm needs it: keep it on the device (no host sync here), apply at the end
+        ph_pending.append((s, pack[nfac - b:].clone()))
         # ---- 5: trailing update of the local columns ----
         t1 = lay.local_from(rank, i + 1)
         n2 = nloc - t1
         if n2 > 0:
             engine.panel_apply((v, ldv, t, ldb, q2, ldb), mp, b, a_loc, lda, m, nloc, s, t1, n2)
         del pack
+    _apply_pending_phat(slot_orig, ph_pending)
     return DistResult(a_loc, lda, m, n, lay, slot_orig)
+
+
+def _apply_pending_phat(slot_orig, pending):
+    """slot s + t of each finished panel holds what was in slot s + P-hat[t]."""
+    if not pending:
+        return
+    import torch
+
+    allph = torch.stack([p for _, p in pending]).cpu().numpy().astype(np.int64)  # one sync
+    for (s, _), ph in zip(pending, allph):
+        slot_orig[s:s + len(ph)] = slot_orig[s + ph]
+    pending.clear()
 
 
 def _final_block(a_loc, lda, m, n, s, i, lay, rank, slot_orig, slot_lpos, d: _Dist, engine):
