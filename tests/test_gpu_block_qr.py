@@ -350,3 +350,71 @@ def test_host_entry_streams_r_identically(rq, m, n, b, p, kind):
     assert np.array_equal(np.triu(hr), f.r)
     if kind == "permutation":
         assert np.array_equal(hp, f.perm)
+
+
+def test_cfg2_full_size_vs_reference_algorithm(rq):
+    """BASELINE cfg 2 at its full size: A = U diag(s) V^T, U, V = haar_orthonormal(4000,
+    RngState(0)) (built on the device with this library's QR), s_j = 10^(-8 j / n); m1 with
+    b = 128, p = 10, RngState(1).  The same A goes to the reference algorithm (oracle):
+    identical permutation, |R_jj| within 1e-10 relative, and |R_jj| tracks s_j."""
+    import os
+    import sys
+
+    import torch
+
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "oracle"))
+    import randqr_oracle as orc
+    from paper_1505_08115_b200.matrices import haar_orthonormal_device
+
+    n, b, p = 4000, 128, 10
+    eng = rq.Engine()
+    hr = rq.RngState(0)
+    u, _ = haar_orthonormal_device(n, hr, engine=eng)
+    v, _ = haar_orthonormal_device(n, hr, engine=eng)
+    s = 10.0 ** (-8.0 * np.arange(1, n + 1) / n)
+    st = torch.as_tensor(s, device=u.device)
+    a = (v[:n, :n].T @ (u[:n, :n] * st[:, None])).T.cpu().numpy()  # storage is A^T
+    a = np.asfortranarray(a)
+    f = rq.block_qr(a, _cfg(rq, b, p, 0), rq.RngState(1), engine=eng)
+    fo = orc.block_qr(a, orc.BlockConfig(b, orc.SketchConfig(b, p, 0)), orc.RngState(1))
+    assert np.array_equal(f.perm, fo.perm())
+    d, do = np.abs(np.diag(f.r)), np.abs(np.diag(fo.r))
+    assert np.all(np.abs(d - do) <= 1e-10 * do + 1e-13 * np.linalg.norm(a))
+    ratio = d / s  # rank-revealing: |R_jj| ~ s_j within modest factors on this spectrum
+    assert np.all(ratio[: n // 2] > 1e-2) and np.all(ratio[: n // 2] < 1e2)
+
+
+def test_cfg5_size_n40k_properties(rq):
+    """BASELINE cfg 5 size (n = 40000, 12.8 GB, b = 256, p = 16, downdated sketch = the HQRRP
+    throughput mode) on the device: ||A[:, perm] x - Q (R x)|| <= 1e-13 ||A|| ||x|| and
+    ||Q^T Q y - y|| <= 1e-13 sqrt(n) ||y|| through random probes; R upper triangular."""
+    import ctypes
+
+    import torch
+
+    from paper_1505_08115_b200 import _lib
+    from paper_1505_08115_b200.errors import check
+
+    n, b, p = 40000, 256, 16
+    eng = rq.Engine()
+    a0, ld = rq.gaussian_matrix_device(n, n, rq.RngState(0), engine=eng)
+    work = a0.clone()
+    perm = torch.empty(n, dtype=torch.int64, device=a0.device)
+    cfg = _lib.rq_config(b, p, 0, -1, _lib.RQ_PIVOT_PERMUTATION, 0, _lib.RQ_SKETCH_DOWNDATE, 0)
+    ctr = ctypes.c_uint64(0)
+    check(eng.lib.rq_factorize(eng.handle, ctypes.byref(cfg), n, n, ctypes.c_void_p(work.data_ptr()), ld,
+                               ctypes.c_uint64(1), ctypes.byref(ctr), ctypes.c_void_p(perm.data_ptr())))
+    g = torch.Generator(device=a0.device).manual_seed(9)
+    x = torch.randn(n, 2, dtype=torch.float64, device=a0.device, generator=g)
+    ax = (a0[:n, :n].T)[:, perm] @ x
+    r = torch.triu(work[:n, :n].T)
+    assert torch.equal(r, work[:n, :n].T)
+    rx = r @ x
+    del work
+    q, ldq = eng.alloc_matrix(n, n)
+    check(eng.lib.rq_form_q(eng.handle, n, ctypes.c_void_p(q.data_ptr()), ldq))
+    qm = q[:n, :n].T
+    anorm = torch.linalg.norm(a0[:n, :n])
+    assert float(torch.linalg.norm(ax - qm @ rx) / (anorm * torch.linalg.norm(x))) <= 1e-13
+    y = torch.randn(n, 2, dtype=torch.float64, device=a0.device, generator=g)
+    assert float(torch.linalg.norm(qm.T @ (qm @ y) - y) / torch.linalg.norm(y)) <= 1e-13 * np.sqrt(n)
