@@ -584,9 +584,20 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
         gemm_max_ctas = kSMs - 16;
         gemm_pdl = pdl;
         {
+          // the CPQR holds 16 SMs for ~b * 2.7 us: the first n_a columns of W run capped beside
+          // it, the rest (launched once those finish) on the whole GPU
           CatGuard g(cat, PROF_TRAIL);
-          rc = gemm(b, n2, mp, op(V, mp + vpad, b, ldv, vpad), false, op(A, m, n, lda, s, s + b), L.wside, even(b),
+          const double cpqr_s = (double)b * 2.7e-6, rate = 24e12;  // measured CPQR step, capped DMMA rate
+          int64_t n_a = (int64_t)(cpqr_s * rate / (2.0 * b * (double)mp));
+          n_a = std::max<int64_t>(128, (n_a + 127) / 128 * 128);
+          if (n_a >= n2 - 256) n_a = n2;
+          rc = gemm(b, n_a, mp, op(V, mp + vpad, b, ldv, vpad), false, op(A, m, n, lda, s, s + b), L.wside, even(b),
                     1.0, 0.0);
+          gemm_pdl = false;
+          gemm_max_ctas = 0;
+          if (rc == RQ_OK && n_a < n2)
+            rc = gemm(b, n2 - n_a, mp, op(V, mp + vpad, b, ldv, vpad), false, op(A, m, n, lda, s, s + b + n_a),
+                      L.wside + n_a * even(b), even(b), 1.0, 0.0);
         }
         gemm_pdl = false;
         if (rc == RQ_OK) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
