@@ -156,8 +156,10 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
                     const KArgs args) {
   using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment by offsetting the __shared__ array itself (not through uintptr_t),
+  // so fragment loads stay LDS instead of generic LD with 64-bit address arithmetic
+  const uint32_t mis = (uint32_t)__cvta_generic_to_shared(smem_raw) & 1023u;
+  unsigned char* smem = smem_raw + ((1024u - mis) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
 
