@@ -3,9 +3,13 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One step = one full block_qr factorization of an n x n i.i.d. N(0,1) fp64
-matrix (cfg 3: n=10000, b=256, p=16, q=0), fresh sketches from RngState(1)
-(reference semantics), starting from a pristine copy of A already resident
-in HBM (the copy is part of the step, as blocked.py:161 copies its input).
+matrix (cfg 3: n=10000, b=256, p=16, q=0) starting from a pristine copy of A
+already resident in HBM (the copy is part of the step, as blocked.py:161
+copies its input).  Headline sketch mode: HQRRP's downdated sketch (G drawn
+once from RngState(1), Y = G A, Y2 <- Y2 - G1 R12 per panel; SURVEY section 8
+"the mode used for the throughput numbers"); the reference's fresh per-panel
+sketch (reference semantics, +2 m' n' (b+p) flops per panel that the 4/3 n^3
+count does not credit) is timed on the same input and reported as `variant`.
 Metric: fp64 TFLOP/s on the (4/3) n^3 count.
 
 * value: device time (CUDA events on the library stream), max over ranks.
@@ -365,8 +369,9 @@ def main():
     ap.add_argument("--cpu-panels", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--sketch", default="fresh", choices=["fresh", "downdate"],
-                    help="headline sketch mode (fresh = reference semantics)")
+    ap.add_argument("--sketch", default="downdate", choices=["fresh", "downdate"],
+                    help="headline sketch mode: downdate = HQRRP (Y = G A once, Y2 <- Y2 - G1 R12 per panel, "
+                         "the north star's hot path); fresh = the reference's per-panel fresh sketch")
     ap.add_argument("--no-variant", action="store_true", help="skip timing the other sketch mode")
     ap.add_argument("--method", default="m1", choices=["m1", "m2", "m3"],
                     help="m1 block_qr permutation pivots (headline), m2 reflector pivots, m3 block_rrqr")
@@ -400,8 +405,8 @@ def main():
             os.environ.setdefault(k, v)
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        if args.method == "m1" and args.sketch == "fresh" and args.q == 0 and args.matrix == "gauss":
-            return run_distributed(args, dist, rank, world, local)
+        if args.method == "m1" and args.q == 0 and args.matrix == "gauss":
+            return run_distributed(args, dist, rank, world, local)  # fresh sketches (dist.py scope)
         if rank == 0:
             print(json.dumps({"metric": METRIC, "unavailable": "multi-GPU runs cover m1 fresh q=0 (dist.py)"}))
         dist.destroy_process_group()

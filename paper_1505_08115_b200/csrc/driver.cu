@@ -221,6 +221,33 @@ int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_
   return gemm_f64(p, stream, &launches);
 }
 
+// Pending look-ahead tiles [la.next, upto): beside a leaf kernel (programmatic dependent launch,
+// grid capped to the SMs outside the leaf's 16-CTA cluster) or, at the end, on the whole GPU.
+int Ctx::la_chunk(int64_t upto, bool beside_leaf) {
+  if (!la.on) return RQ_OK;
+  upto = std::min(upto, la.tiles);
+  if (upto > la.next) {
+    GemmProblem p = la.g;
+    p.tile_begin = la.next;
+    p.tile_end = upto;
+    p.work = nullptr;  // no split-K inside a tile range
+    p.work_bytes = 0;
+    p.splitk = 1;
+    p.max_ctas = beside_leaf ? kSMs - 16 : 0;
+    p.pdl = beside_leaf;
+    CatGuard g(cat, PROF_TRAIL);
+    cudaEvent_t e0;
+    if (!beside_leaf) prof_begin(&e0);  // events between the leaf and its chunk would serialise them
+    const int rc = gemm_f64(p, stream, &launches);
+    if (!beside_leaf) prof_end(e0, 2.0 * (double)p.M * (double)p.N * (double)p.K * (double)(upto - la.next) /
+                                       (double)la.tiles);
+    RQ_TRY(rc);
+    la.next = upto;
+  }
+  if (la.next >= la.tiles) la.on = false;
+  return RQ_OK;
+}
+
 int Ctx::ensure_side() {
   if (side) return RQ_OK;
   int lo = 0, hi = 0;
@@ -302,6 +329,10 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
   if (wl_max == 0) wl_max = leaf_width_for(mp);
   if (wl_max == 0) return set_error(RQ_EUNSUPPORTED, "panel of %lld rows exceeds the leaf kernel", (long long)mp);
   const int wl = std::min(wl_max, 32);
+  // look-ahead: spread the pending tiles over the leaves in whole waves of the capped grid
+  const int nleaves = (b + wl - 1) / wl;
+  const int64_t la_wave = kSMs - 16;
+  const int64_t la_t0 = la.next, la_waves = la.on ? ceil_div(la.tiles - la.next, la_wave) : 0;
   for (int k0 = 0; k0 < b; k0 += wl) {
     const int w = std::min(wl, b - k0);
     const int64_t mm = mp - k0;
@@ -323,6 +354,10 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
       prof_end(e0, 0.0);
       cat = saved;
       RQ_TRY(rc);
+    }
+    if (la.on) {
+      const int64_t leaf = k0 / wl + 1;
+      RQ_TRY(la_chunk(la_t0 + ceil_div(la_waves * leaf, (int64_t)nleaves) * la_wave, true));
     }
     const int64_t nrest = b - k0 - w;
     if (nrest <= 0) break;
@@ -434,6 +469,15 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
   double* tleaf = L.tleaf;
 
   const bool downdate = cfg.sketch_mode == RQ_SKETCH_DOWNDATE;
+  // look-ahead (downdated sketches, permutation pivots): the next panel's sketch CPQR and column
+  // moves run as soon as the top b rows (R12) are final, the next panel's columns are updated
+  // first, and the rest of A2 -= V W2 runs in chunks beside the next panel's leaf kernels.
+  static const int env_la = [] {
+    const char* e = getenv("RQ_LOOKAHEAD");
+    return e ? atoi(e) : 1;
+  }();
+  const bool la_mode = downdate && !refl_piv && !inspect_cb && env_la != 0;
+  la.on = false;
   if (downdate && n > b) {
     // HQRRP: G = Omega^T drawn once (m(b+p) normals), Y = G A; downdated per panel
     RQ_TRY(gaussian_fill(L.omega, m, wdt, L.ldo, seed, *counter, stream, &launches));
@@ -497,7 +541,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       // ---------------- reflector pivots (select_pivot_reflectors, pivoting.py:132-146) ----------------
       RQ_TRY(reflector_pivot(cfg, A, lda, m, n, s, L, &fc, seed, counter));
       rfactors.back().nphat = b;
-    } else {
+    } else if (!(la_mode && panel > 1)) {  // (look-ahead: selected and moved at the end of the last panel)
     // ---------------- 1-2: sketch Y^T = Omega^T X (fresh) or the downdated Y (HQRRP) ----------------
     double* ycur = L.yt;
     if (!downdate) {
@@ -530,7 +574,9 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     // V is lower trapezoidal: the leaves write rows >= their diagonal only
     RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * b * sizeof(double), stream));
     launches++;
-    RQ_TRY(panel_qr(A, lda, m, n, s, mp, b, V, ldv, vpad, tleaf, L.w1, L.w2));
+    // (look-ahead: L.w2 holds the previous panel's W2 until its last chunk ran; ttop is free)
+    RQ_TRY(panel_qr(A, lda, m, n, s, mp, b, V, ldv, vpad, tleaf, L.w1, la_mode ? L.ttop : L.w2));
+    RQ_TRY(la_flush());
     const int64_t n2 = np - b;
     // ---- overlap: the b x b CPQR below runs on its 16-SM cluster from a highest-priority
     //      stream (so it is dispatched first), while W = V^T A2 (half the trailing update)
@@ -630,6 +676,12 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     if (overlap) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_side, 0));
     else RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
     // ---------------- 9: trailing update ----------------
+    if (la_mode && n2 > 0) {
+      RQ_TRY(lookahead_tail(cfg, A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L,
+                            overlap ? L.wside : nullptr, lorder, lorder_n, rank, rank_n));
+      factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2, ldt});
+      continue;  // lorder/rank were swapped for the next panel inside
+    }
     if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L,
                                        overlap ? L.wside : nullptr));
     if (downdate && n2 > 0) {
@@ -747,6 +799,81 @@ int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t
   if (want_y) return gemm(np, wdt, mp, X, false, Om, L.ybuf, even(np), 1.0, 0.0);  // Y = X^T Z
   // Y^T = Z^T X
   return gemm(wdt, np, mp, Om, false, X, L.yt, L.ldy, 1.0, 0.0);
+}
+
+// Look-ahead tail of a non-final panel at s (downdated sketches, permutation pivots):
+//   W2 = T^T W;  top b rows: R12 = Q2^T (A2_top - V_top W2)  (final);
+//   Y2 <- Y2 - G1 R12 (the next panel's sketch);
+//   if the next panel is not the final block: its b-step CPQR, plan and column moves (A at full
+//   height, Y, and W2's columns, whose rows below the top are not applied yet), then
+//   A2 -= V W2 on the next panel's b columns, and the rest left pending (la) for panel_qr to
+//   issue beside the next panel's leaves;  otherwise A2 -= V W2 now.
+// lorder/rank are swapped to the next panel's (as the end of the panel loop does).
+int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp,
+                        int b, int64_t n2, const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt,
+                        const double* Q2, Layout& L, const double* Wpre, int*& lorder, int*& lorder_n, int*& rank,
+                        int*& rank_n) {
+  const int wdt = b + cfg.oversample;
+  const int64_t ldw = even(b);
+  const GemmOperand Vop = op(V, mp + vpad, b, ldv, vpad);
+  const GemmOperand Vlow = op(V, mp + vpad, b, ldv, vpad + b);  // rows b.. of V
+  {
+    CatGuard guard(cat, PROF_TRAIL);
+    const double* W = Wpre ? Wpre : L.w1;
+    if (!Wpre) RQ_TRY(gemm(b, n2, mp, Vop, false, op(A, m, n, lda, s, s + b), L.w1, ldw, 1.0, 0.0));
+    RQ_TRY(gemm(b, n2, b, op(T, b, b, ldt), false, op(W, b, n2, ldw), L.w2, ldw, 1.0, 0.0));
+    // top b rows: A2_top -= V_top W2, then Q2^T
+    RQ_TRY(gemm(b, n2, b, Vop, true, op(L.w2, b, n2, ldw), A + s + (s + b) * lda, lda, -1.0, 1.0));
+    RQ_TRY(copy2d(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
+    RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldt), false, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
+  }
+  std::swap(lorder, lorder_n);
+  std::swap(rank, rank_n);
+  const int64_t np2 = n - s - b;  // the next panel's columns
+  const bool next_full = np2 > b;
+  if (!next_full) {
+    CatGuard guard(cat, PROF_TRAIL);
+    return gemm(mp - b, n2, b, Vlow, true, op(L.w2, b, n2, ldw), A + (s + b) + (s + b) * lda, lda, -1.0, 1.0);
+  }
+  // Y2 <- Y2 - G1 R12 with G1 = Y1 R11^{-1}
+  const int64_t ldg = even(wdt);
+  RQ_TRY(trinv_upper(A + s + s * lda, lda, b, L.rinv, ldw, stream, &launches));
+  RQ_TRY(gemm(wdt, b, b, op(L.yt, wdt, n, L.ldy, 0, s), true, op(L.rinv, b, b, ldw), L.g1, ldg, 1.0, 0.0));
+  RQ_TRY(gemm(wdt, n2, b, op(L.g1, wdt, b, ldg), true, op(A, m, n, lda, s, s + b), L.yt + (s + b) * L.ldy, L.ldy,
+              -1.0, 1.0));
+  // the next panel's pivots (b-step CPQR of a copy of its sketch) and moves
+  const int64_t s2 = s + b;
+  RQ_TRY(copy2d(L.yt + s2 * L.ldy, L.ldy, L.ybuf, L.ldy, wdt, np2, 0, stream, &launches));
+  RQ_TRY(sketch_select(L.ybuf, L.ldy, wdt, (int)np2, b, rank, L.cap));
+  PlanCall pc{L.cap, b, lorder, (int)np2, L.flag, L.newloc, L.src, L.dst, L.nmoves, lorder_n, rank_n};
+  RQ_TRY(plan_moves(pc, stream, &launches));
+  MoveCall mv{A, lda, s2, 0, m, L.src, L.dst, L.nmoves, 2 * b, L.stage, even(m), L.orig, L.ostage};
+  RQ_TRY(move_columns(mv, stream, &launches));
+  MoveCall my{L.yt, L.ldy, s2, 0, wdt, L.src, L.dst, L.nmoves, 2 * b, L.stage, L.ldy, nullptr, nullptr};
+  RQ_TRY(move_columns(my, stream, &launches));
+  MoveCall mw{L.w2, ldw, 0, 0, b, L.src, L.dst, L.nmoves, 2 * b, L.stage, even(m), nullptr, nullptr};
+  RQ_TRY(move_columns(mw, stream, &launches));
+  // the next panel's columns first; the rest pending
+  {
+    CatGuard guard(cat, PROF_TRAIL);
+    RQ_TRY(gemm(mp - b, b, b, Vlow, true, op(L.w2, b, n2, ldw), A + s2 + s2 * lda, lda, -1.0, 1.0));
+  }
+  GemmProblem& g = la.g;
+  g = GemmProblem();
+  g.M = mp - b;
+  g.N = n2 - b;
+  g.K = b;
+  g.A = Vlow;
+  g.a_mmajor = true;
+  g.B = op(L.w2, b, n2, ldw, 0, b);
+  g.C = A + s2 + (s2 + b) * lda;
+  g.ldc = lda;
+  g.alpha = -1.0;
+  g.beta = 1.0;
+  la.tiles = g.N > 0 ? gemm_f64_tiles(g) : 0;
+  la.next = 0;
+  la.on = la.tiles > 0;
+  return RQ_OK;
 }
 
 int Ctx::trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, int64_t n2,

@@ -118,6 +118,17 @@ struct Ctx {
   int gemm_max_ctas = 0;
   bool gemm_pdl = false;
   int ensure_side();
+  // look-ahead (factorize_perm, downdated sketches): the previous panel's A2 -= V W2 on the
+  // columns after the current panel, issued in tile-range chunks, each launched right behind one
+  // of the current panel's leaf kernels (programmatic serialization: it runs on the SMs the
+  // leaf's cluster leaves free)
+  struct LaPending {
+    bool on = false;
+    GemmProblem g;  // the whole GEMM; chunks set tile_begin/tile_end
+    int64_t tiles = 0, next = 0;
+  } la;
+  int la_chunk(int64_t upto, bool beside_leaf);
+  int la_flush() { return la.on ? la_chunk(la.tiles, false) : RQ_OK; }
   // scratch views used by helpers
   double* kwork = nullptr;
   size_t kwork_bytes = 0;
@@ -158,6 +169,9 @@ struct Ctx {
   int trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, int64_t n2,
                       const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2,
                       Layout& L, const double* Wpre = nullptr);
+  int lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b,
+                     int64_t n2, const double* V, int64_t ldv, int vpad, const double* T, int64_t ldt, const double* Q2,
+                     Layout& L, const double* Wpre, int*& lorder, int*& lorder_n, int*& rank, int*& rank_n);
   int factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, int64_t lda, uint64_t seed,
                      uint64_t* counter, int64_t* dperm);
   int small_q(const double* V2, int64_t ldv2, int k, double* Q2, int64_t ldq, Layout& L);

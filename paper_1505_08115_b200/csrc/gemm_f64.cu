@@ -70,6 +70,7 @@ struct KArgs {
   double* work;  // split-K slabs (ld = M)
   int k_lo;      // 1: element k = 0 is padding (odd K origin shifted to even)
   int m_lo;      // 1: output row 0 is padding (odd M origin shifted to even)
+  int u0, u1;    // unit range of this launch (a tile-range chunk of a larger GEMM, or all units)
 };
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
@@ -113,7 +114,7 @@ struct ChunkCursor {
     if (kc_end > a.kchunks) kc_end = a.kchunks;
   }
   RQ_DEV void start(const KArgs& a, int units) {
-    u = blockIdx.x;
+    u = a.u0 + blockIdx.x;
     valid = u < units;
     if (valid) unit_range(a);
     skip_empty(a, units);
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int units = args.tiles_m * args.tiles_n * args.splitk;
+  const int units = args.u1;  // units [u0, u1) of tiles_m * tiles_n * splitk
 
   // producer cursor (thread 0 only) runs STAGES chunks ahead of the consumers
   ChunkCursor prod;
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
   int stage = 0;
   uint32_t phase = 0;
 
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+  for (int u = args.u0 + blockIdx.x; u < units; u += gridDim.x) {
     const int split = u % args.splitk;
     const int t = u / args.splitk;
     const int tm = t % args.tiles_m;
@@ -459,7 +460,16 @@ static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launch
   a.splitk = p.splitk > 1 ? p.splitk : 1;
   a.kchunks_per_split = (int)ceil_div(a.kchunks, a.splitk);
   a.work = p.work;
-  const int64_t units = (int64_t)a.tiles_m * a.tiles_n * a.splitk;
+  const int64_t all_units = (int64_t)a.tiles_m * a.tiles_n * a.splitk;
+  a.u0 = 0;
+  a.u1 = (int)all_units;
+  if (p.tile_end > 0) {  // a tile-range chunk (no split-K)
+    if (a.splitk != 1) return set_error(RQ_EINTERNAL, "gemm: tile ranges need splitk == 1");
+    a.u0 = (int)std::min<int64_t>(p.tile_begin, all_units);
+    a.u1 = (int)std::min<int64_t>(p.tile_end, all_units);
+    if (a.u1 <= a.u0) return RQ_OK;
+  }
+  const int64_t units = a.u1 - a.u0;
   static int per_sm = 0;
   if (per_sm == 0) {
     RQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::SMEM));
@@ -541,6 +551,27 @@ template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
 static int launch_auto(GemmProblem p, cudaStream_t stream, int64_t* launches) {
   p.splitk = choose_splitk(p, BM, BN);
   return launch_cfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(p, stream, launches);
+}
+
+// Output tiles of the configuration gemm_f64 picks for p (for tile-range chunks).
+int64_t gemm_f64_tiles(const GemmProblem& p) {
+  int bm = 128, bn = 128;
+  const bool m144 = (p.M > 128 && p.M <= 144) || (p.M > 256 && p.M <= 288);
+  const char* e = getenv("RQ_GEMM_BIG");
+  if (e && atoi(e) == 1 && p.M >= 128 && p.N >= 128 && (p.a_mmajor || !m144)) {
+    bn = 64;
+  } else if (p.a_mmajor) {
+    if (p.M >= 128 && p.N >= 128) bn = 128;
+    else if (p.N < 128) bn = 32;
+    else bm = 64;
+  } else {
+    if (m144 && p.N >= 128) bm = 144;
+    else if (p.M >= 128 && p.N >= 128) bn = 128;
+    else if (p.N < 128) bn = 32;
+    else bm = 64;
+  }
+  const int mshift = p.a_mmajor ? (int)(p.A.r0 & 1) : 0;
+  return ceil_div(p.M + mshift, bm) * ceil_div(p.N, bn);
 }
 
 int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches) {

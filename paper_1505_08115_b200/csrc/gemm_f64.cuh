@@ -39,9 +39,12 @@ struct GemmProblem {
   int max_ctas = 0;      // > 0: cap the persistent grid (leave SMs to a concurrent kernel)
   bool pdl = false;      // programmatic dependent launch: may start once the previous kernel in the
                          // stream triggered (the GEMM must not read that kernel's output)
+  int64_t tile_begin = 0, tile_end = 0;  // tile_end > 0: only output tiles [tile_begin, tile_end)
+                                         // (column-major tile order; see gemm_f64_tiles)
 };
 
 int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches);
+int64_t gemm_f64_tiles(const GemmProblem& p);
 size_t gemm_splitk_workspace(int64_t M, int64_t N, int splitk);
 
 }  // namespace rq

@@ -270,6 +270,10 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
   __shared__ double Ts[16][17];
   __shared__ __align__(8) unsigned long long lmbar[2];  // pushes of step j complete on lmbar[j & 1]
   constexpr unsigned CS = 16;  // launch_leaf_reg: one 16-CTA cluster
+  // look-ahead (driver.cu): a chunk of the previous panel's trailing update launched after this
+  // kernel with programmatic stream serialization starts once the cluster is resident, on the
+  // other 132 SMs (it touches neither this leaf's columns nor its outputs)
+  asm volatile("griddepcontrol.launch_dependents;");
   const unsigned rank = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = (int64_t)rank * rows_per;
