@@ -221,6 +221,36 @@ int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_
   return gemm_f64(p, stream, &launches);
 }
 
+void Ctx::phase(int id) {
+  if (!phases_on) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, stream);
+  phase_ev.emplace_back(id, e);
+}
+
+void Ctx::phase_report() {
+  if (!phases_on || phase_ev.empty()) return;
+  static const char* names[] = {"start", "panel_qr", "cpqr||W,T", "wait_T", "W2,top", "downdate",
+                                "sketch_cpqr", "moves,NNc", "final", "fresh_sketch", "trail+dd", "small_q",
+                                "R,moves"};
+  double acc[16] = {0};
+  cudaEventSynchronize(phase_ev.back().second);
+  for (size_t k = 1; k < phase_ev.size(); k++) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, phase_ev[k - 1].second, phase_ev[k].second);
+    acc[phase_ev[k].first] += ms;
+  }
+  float tot = 0.f;
+  cudaEventElapsedTime(&tot, phase_ev.front().second, phase_ev.back().second);
+  fprintf(stderr, "[rq phases] total %.2f ms:", tot);
+  for (int i = 1; i < 13; i++)
+    if (acc[i] > 0) fprintf(stderr, " %s=%.2f", names[i], acc[i]);
+  fprintf(stderr, "\n");
+  for (auto& pe : phase_ev) cudaEventDestroy(pe.second);
+  phase_ev.clear();
+}
+
 // Pending look-ahead tiles [la.next, upto): beside a leaf kernel (programmatic dependent launch,
 // grid capped to the SMs outside the leaf's 16-CTA cluster) or, at the end, on the whole GPU.
 int Ctx::la_chunk(int64_t upto, bool beside_leaf) {
@@ -478,6 +508,9 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
   }();
   const bool la_mode = downdate && !refl_piv && !inspect_cb && env_la != 0;
   la.on = false;
+  static const bool env_phases = getenv("RQ_PHASES") && atoi(getenv("RQ_PHASES")) != 0;
+  phases_on = env_phases && !prof;
+  phase(0);
   if (downdate && n > b) {
     // HQRRP: G = Omega^T drawn once (m(b+p) normals), Y = G A; downdated per panel
     RQ_TRY(gaussian_fill(L.omega, m, wdt, L.ldo, seed, *counter, stream, &launches));
@@ -565,6 +598,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       RQ_TRY(move_columns(my, stream, &launches));
     }
     }  // permutation pivots
+    phase(la_mode ? 7 : 9);
     // ---------------- 5: unpivoted panel QR ----------------
     const int64_t ldv = even(mp + 1), ldt = even(b);
     const int vpad = (int)(s & 1);
@@ -577,6 +611,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     // (look-ahead: L.w2 holds the previous panel's W2 until its last chunk ran; ttop is free)
     RQ_TRY(panel_qr(A, lda, m, n, s, mp, b, V, ldv, vpad, tleaf, L.w1, la_mode ? L.ttop : L.w2));
     RQ_TRY(la_flush());
+    phase(1);
     const int64_t n2 = np - b;
     // ---- overlap: the b x b CPQR below runs on its 16-SM cluster from a highest-priority
     //      stream (so it is dispatched first), while W = V^T A2 (half the trailing update)
@@ -659,7 +694,9 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     } else {
       RQ_TRY(sweep(ss));
     }
+    phase(2);
     RQ_TRY(small_q(V2, L.lds_small, b, Q2, ldt, L));
+    phase(11);
     if (refl_piv)
       RQ_CUDA_TRY(cudaMemcpyAsync(rfactors.back().phat, L.cap, (size_t)b * sizeof(int), cudaMemcpyDeviceToDevice,
                                   stream));
@@ -672,14 +709,17 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       MoveCall my2{L.yt, L.ldy, s, 0, wdt, L.cap, L.iota_b, nullptr, b, L.stage, L.ldy, nullptr, nullptr};
       RQ_TRY(move_columns(my2, stream, &launches));
     }
+    phase(12);
     // ---------------- 8: T of the panel reflectors (on the side stream when overlapped) ----------------
     if (overlap) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_side, 0));
     else RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
+    phase(3);
     // ---------------- 9: trailing update ----------------
     if (la_mode && n2 > 0) {
       RQ_TRY(lookahead_tail(cfg, A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L,
                             overlap ? L.wside : nullptr, lorder, lorder_n, rank, rank_n));
       factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2, ldt});
+      phase(7);
       continue;  // lorder/rank were swapped for the next panel inside
     }
     if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L,
@@ -693,6 +733,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
                   L.ldy, -1.0, 1.0));
     }
     factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2, ldt});
+    phase(10);
     if (!refl_piv) {
       std::swap(lorder, lorder_n);
       std::swap(rank, rank_n);
@@ -712,6 +753,8 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     RQ_CUDA_TRY(cudaMemcpyAsync(dperm, L.orig, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, stream));
     launches++;
   }
+  phase(8);
+  phase_report();
   have_factors = true;
   return RQ_OK;
 }
@@ -827,6 +870,7 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
     RQ_TRY(copy2d(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
     RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldt), false, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
   }
+  phase(4);
   std::swap(lorder, lorder_n);
   std::swap(rank, rank_n);
   const int64_t np2 = n - s - b;  // the next panel's columns
@@ -841,10 +885,12 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
   RQ_TRY(gemm(wdt, b, b, op(L.yt, wdt, n, L.ldy, 0, s), true, op(L.rinv, b, b, ldw), L.g1, ldg, 1.0, 0.0));
   RQ_TRY(gemm(wdt, n2, b, op(L.g1, wdt, b, ldg), true, op(A, m, n, lda, s, s + b), L.yt + (s + b) * L.ldy, L.ldy,
               -1.0, 1.0));
+  phase(5);
   // the next panel's pivots (b-step CPQR of a copy of its sketch) and moves
   const int64_t s2 = s + b;
   RQ_TRY(copy2d(L.yt + s2 * L.ldy, L.ldy, L.ybuf, L.ldy, wdt, np2, 0, stream, &launches));
   RQ_TRY(sketch_select(L.ybuf, L.ldy, wdt, (int)np2, b, rank, L.cap));
+  phase(6);
   PlanCall pc{L.cap, b, lorder, (int)np2, L.flag, L.newloc, L.src, L.dst, L.nmoves, lorder_n, rank_n};
   RQ_TRY(plan_moves(pc, stream, &launches));
   MoveCall mv{A, lda, s2, 0, m, L.src, L.dst, L.nmoves, 2 * b, L.stage, even(m), L.orig, L.ostage};

@@ -128,6 +128,12 @@ struct Ctx {
     int64_t tiles = 0, next = 0;
   } la;
   int la_chunk(int64_t upto, bool beside_leaf);
+  // RQ_PHASES=1: CUDA events at phase boundaries of factorize_perm on the main stream (never
+  // between a leaf and its look-ahead chunk); per-phase totals printed to stderr per call
+  bool phases_on = false;
+  std::vector<std::pair<int, cudaEvent_t>> phase_ev;
+  void phase(int id);
+  void phase_report();
   int la_flush() { return la.on ? la_chunk(la.tiles, false) : RQ_OK; }
   // scratch views used by helpers
   double* kwork = nullptr;
