@@ -526,8 +526,9 @@ static int choose_splitk(const GemmProblem& p, int BM, int BN) {
   if (p.splitk > 0) return p.splitk;
   if (!p.work) return 1;
   const int sms = p.max_ctas > 0 ? std::min(num_sms(), p.max_ctas) : num_sms();
-  const int64_t tiles = ceil_div(p.M + 1, BM) * ceil_div(p.N, BN);
-  const int64_t kch = ceil_div(p.K + 1, 16);
+  const int mshift = p.a_mmajor ? (int)(p.A.r0 & 1) : 0, kshift = (int)(p.B.r0 & 1);
+  const int64_t tiles = ceil_div(p.M + mshift, BM) * ceil_div(p.N, BN);
+  const int64_t kch = ceil_div(p.K + kshift, 16);
   auto eff = [&](int64_t units) {
     const int64_t waves = ceil_div(units, sms);
     return (double)units / (double)(waves * sms);

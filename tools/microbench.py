@@ -160,6 +160,19 @@ if "gemm_nn" in which:
                                ldc, -1.0, 1.0))
     torch.cuda.synchronize()
 
+if "gemm_tn" in which:
+    # W = V^T A2 at n = 10k, as the trailing update issues it (split-K workspace from the engine)
+    M, N, K = 256, 10000, 10000
+    abuf, lda = eng.alloc_matrix(K, M)
+    bbuf, ldb = eng.alloc_matrix(K, N)
+    cbuf, ldc = eng.alloc_matrix(M, N)
+    abuf.normal_(); bbuf.normal_(); cbuf.normal_()
+    for _ in range(2):
+        check(lib.rq_test_gemm(eng.handle, 0, M, N, K, ctypes.c_void_p(abuf.data_ptr()), lda, K, M, 0, 0,
+                               ctypes.c_void_p(bbuf.data_ptr()), ldb, K, N, 0, 0, ctypes.c_void_p(cbuf.data_ptr()),
+                               ldc, 1.0, 0.0))
+    torch.cuda.synchronize()
+
 if "leafstamps" in which:
     mm, w = int(os.environ.get("LEAFM", "10000")), 16
     a0 = rng.standard_normal((mm, w))
