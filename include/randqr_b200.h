@@ -51,8 +51,13 @@ typedef struct rq_config {
   int32_t pivot_kind;  /* RQ_PIVOT_PERMUTATION | RQ_PIVOT_REFLECTORS              */
   int32_t rrqr;        /* 1: block_rrqr semantics (blocked.py:239-279)            */
   int32_t sketch_mode; /* RQ_SKETCH_FRESH | RQ_SKETCH_DOWNDATE                     */
-  int32_t reserved;
+  int32_t flags;       /* RQ_FLAG_* (0: defaults)                                  */
 } rq_config;
+
+/* rq_config.flags: RQ_FLAG_NO_LOOKAHEAD runs the downdated-sketch driver without
+ * look-ahead (each panel's trailing update completes before the next panel's sketch
+ * CPQR); results are identical, only the schedule differs. */
+#define RQ_FLAG_NO_LOOKAHEAD 1
 
 /* Called after each completed panel (the reference's `inspect` hook,
  * blocked.py:184-185, :215-216); the callee may call rq_snapshot(). */

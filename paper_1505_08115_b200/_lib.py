@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "librandqr_b200.so")
 RQ_OK, RQ_EDIM, RQ_EVALUE, RQ_ECONV, RQ_ECUDA, RQ_EINTERNAL, RQ_EUNSUPPORTED = range(7)
 RQ_PIVOT_PERMUTATION, RQ_PIVOT_REFLECTORS = 0, 1
 RQ_SKETCH_FRESH, RQ_SKETCH_DOWNDATE = 0, 1
+RQ_FLAG_NO_LOOKAHEAD = 1
 
 
 class rq_config(ctypes.Structure):
@@ -29,7 +30,7 @@ class rq_config(ctypes.Structure):
         ("pivot_kind", ctypes.c_int32),
         ("rrqr", ctypes.c_int32),
         ("sketch_mode", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
 
 

@@ -117,10 +117,13 @@ int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, c
   RQ_TRY(validate(cfg, m, n, counter));
   Ctx& c = ctx->c;
   const int64_t ldd = rq::even(m);
-  double* dA = nullptr;
-  int64_t* dp = nullptr;
-  RQ_CUDA_TRY(cudaMallocAsync(&dA, (size_t)ldd * n * 8, c.stream));
-  RQ_CUDA_TRY(cudaMallocAsync(&dp, (size_t)n * 8, c.stream));
+  // device copy of A (and the permutation) in a context-owned, grow-only buffer: no per-call
+  // allocation (a freed-and-remapped 800 MB pool block cost tens of ms, erratically)
+  const size_t abytes = ((size_t)ldd * n * 8 + 255) & ~size_t(255);
+  RQ_CUDA_TRY(cudaStreamSynchronize(c.stream));  // the buffer may still feed an earlier call's copies
+  RQ_TRY(c.harena.reserve(abytes + (size_t)n * 8));
+  double* dA = static_cast<double*>(c.harena.base);
+  int64_t* dp = reinterpret_cast<int64_t*>(static_cast<char*>(c.harena.base) + abytes);
   int rc = RQ_OK;
   cudaError_t e = cudaMemcpy2DAsync(dA, ldd * 8, hA, lda * 8, m * 8, n, cudaMemcpyHostToDevice, c.stream);
   if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "H2D: %s", cudaGetErrorString(e));
@@ -157,8 +160,6 @@ int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, c
     cudaEventRecord(ev, cs);
     cudaStreamWaitEvent(c.stream, ev, 0);
   }
-  cudaFreeAsync(dA, c.stream);
-  cudaFreeAsync(dp, c.stream);
   e = cudaStreamSynchronize(c.stream);
   if (rc == RQ_OK && e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "sync: %s", cudaGetErrorString(e));
   return rc;

@@ -263,14 +263,19 @@ int Ctx::la_chunk(int64_t upto, bool beside_leaf) {
     p.work = nullptr;  // no split-K inside a tile range
     p.work_bytes = 0;
     p.splitk = 1;
+    static const int env_pdl = [] {
+      const char* e = getenv("RQ_LA_PDL");
+      return e ? atoi(e) : 1;
+    }();
     p.max_ctas = beside_leaf ? kSMs - 16 : 0;
-    p.pdl = beside_leaf;
+    p.pdl = beside_leaf && env_pdl != 0;
     CatGuard g(cat, PROF_TRAIL);
+    // (in a profiled step the events between the leaf and its chunk serialise them: the per-class
+    //  breakdown is taken from a separate step, never from the timed ones)
     cudaEvent_t e0;
-    if (!beside_leaf) prof_begin(&e0);  // events between the leaf and its chunk would serialise them
+    prof_begin(&e0);
     const int rc = gemm_f64(p, stream, &launches);
-    if (!beside_leaf) prof_end(e0, 2.0 * (double)p.M * (double)p.N * (double)p.K * (double)(upto - la.next) /
-                                       (double)la.tiles);
+    prof_end(e0, 2.0 * (double)p.M * (double)p.N * (double)p.K * (double)(upto - la.next) / (double)la.tiles);
     RQ_TRY(rc);
     la.next = upto;
   }
@@ -424,6 +429,17 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
 // Q2 = H'_0 ... H'_{k-1} = I - V2 T2 V2^T (k x k), dense, from the b x b CPQR reflectors.
 int Ctx::small_q(const double* V2, int64_t ldv2, int k, double* Q2, int64_t ldq, Layout& L) {
   CatGuard guard(cat, PROF_TFACTOR);
+  static const int env_q = [] {
+    const char* e = getenv("RQ_SMALLQ_GEMM");  // 1: the compact-WY path below
+    return e ? atoi(e) : 0;
+  }();
+  if (env_q == 0 && k <= 256) {
+    cudaEvent_t e0;
+    prof_begin(&e0);
+    const int rc = q_from_reflectors(V2, ldv2, k, k, Q2, ldq, stream, &launches);
+    prof_end(e0, 2.0 * k * (double)k * k);
+    return rc;
+  }
   double* T2s = L.ttop;  // k x k scratch (free until the trailing update)
   const int64_t ldk = even(k);
   RQ_TRY(tfactor(V2, k, k, ldv2, 0, T2s, ldk, L.gram));
@@ -506,7 +522,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     const char* e = getenv("RQ_LOOKAHEAD");
     return e ? atoi(e) : 1;
   }();
-  const bool la_mode = downdate && !refl_piv && !inspect_cb && env_la != 0;
+  const bool la_mode = downdate && !refl_piv && !inspect_cb && env_la != 0 && !(cfg.flags & RQ_FLAG_NO_LOOKAHEAD);
   la.on = false;
   static const bool env_phases = getenv("RQ_PHASES") && atoi(getenv("RQ_PHASES")) != 0;
   phases_on = env_phases && !prof;
@@ -1286,6 +1302,7 @@ Ctx::~Ctx() {
   arena.release();
   qarena.release();
   sarena.release();
+  harena.release();
   if (side) cudaStreamDestroy(side);
   if (hip) cudaStreamDestroy(hip);
   if (ev_v) cudaEventDestroy(ev_v);

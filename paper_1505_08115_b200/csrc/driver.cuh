@@ -104,6 +104,7 @@ struct Ctx {
   void* inspect_user = nullptr;
   int64_t launches = 0;
   Arena arena, qarena, sarena;  // factorization, Q/P formation + test hooks, panel-step API
+  Arena harena;                 // rq_factorize_host: device copy of A and the permutation
   unsigned int* barriers = nullptr;
   int nbarriers = 0;
   int next_barrier = 0;

@@ -151,6 +151,75 @@ int trinv_upper(const double* R, int64_t ldr, int k, double* X, int64_t ldx, cud
   return RQ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Q = H_0 H_1 ... H_{k-1} (n x n, n <= 32 RPL), H_j = I - 2 v_j v_j^T with unit reflectors
+// v_j = V(:, j) (zero above row j; a zero column is the identity, as the reference skips
+// it, _kernels_numba.py:35-41).  One warp per column of Q, applied to e_c from the last
+// reflector to the first, 16 columns per CTA, reflectors staged through shared memory in
+// chunks of 16.  Replaces Q2 = I - V2 T2 V2^T (Gram GEMM, triangular inverse, three
+// GEMMs) for the b x b CPQR: columns are independent, so no grid-wide synchronisation.
+// ---------------------------------------------------------------------------
+constexpr int QR_WARPS = 16;
+
+template <int RPL>
+__global__ void __launch_bounds__(QR_WARPS * 32) q_from_reflectors_kernel(const double* __restrict__ V, int64_t ldv,
+                                                                          int k, int n, double* __restrict__ Q,
+                                                                          int64_t ldq) {
+  constexpr int QC = 16;  // reflectors per shared-memory chunk (32 KB at RPL = 8)
+  __shared__ double vs[QC][32 * RPL];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * QR_WARPS + warp;
+  double x[RPL];
+#pragma unroll
+  for (int r = 0; r < RPL; r++) x[r] = (lane + 32 * r == c) ? 1.0 : 0.0;
+  const int nchunks = (k + QC - 1) / QC;
+  for (int ch = nchunks - 1; ch >= 0; ch--) {
+    const int j0 = ch * QC;
+    const int kc = min(QC, k - j0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < QC * 32 * RPL; e += QR_WARPS * 32) {
+      const int jj = e / (32 * RPL), i = e - jj * (32 * RPL);
+      vs[jj][i] = (jj < kc && i < n) ? V[(int64_t)(j0 + jj) * ldv + i] : 0.0;
+    }
+    __syncthreads();
+    if (c < n) {
+      for (int jj = kc - 1; jj >= 0; jj--) {
+        double u[RPL];
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < RPL; r++) {
+          u[r] = vs[jj][lane + 32 * r];
+          if (r & 1) d1 = fma(u[r], x[r], d1);
+          else d0 = fma(u[r], x[r], d0);
+        }
+        double d = d0 + d1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        d *= 2.0;
+#pragma unroll
+        for (int r = 0; r < RPL; r++) x[r] = fma(-d, u[r], x[r]);
+      }
+    }
+  }
+  if (c < n)
+#pragma unroll
+    for (int r = 0; r < RPL; r++)
+      if (lane + 32 * r < n) Q[(int64_t)c * ldq + lane + 32 * r] = x[r];
+}
+
+int q_from_reflectors(const double* V, int64_t ldv, int k, int n, double* Q, int64_t ldq, cudaStream_t st,
+                      int64_t* launches) {
+  if (n <= 0) return RQ_OK;
+  const unsigned blocks = (unsigned)ceil_div(n, QR_WARPS);
+  if (n <= 64) q_from_reflectors_kernel<2><<<blocks, QR_WARPS * 32, 0, st>>>(V, ldv, k, n, Q, ldq);
+  else if (n <= 128) q_from_reflectors_kernel<4><<<blocks, QR_WARPS * 32, 0, st>>>(V, ldv, k, n, Q, ldq);
+  else if (n <= 256) q_from_reflectors_kernel<8><<<blocks, QR_WARPS * 32, 0, st>>>(V, ldv, k, n, Q, ldq);
+  else return set_error(RQ_EUNSUPPORTED, "q_from_reflectors: %d rows > 256", n);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
 int tfactor_from_gram(const double* G, int64_t ldg, int k, double* T, int64_t ldt, cudaStream_t st,
                       int64_t* launches) {
   if (k <= 0) return RQ_OK;

@@ -792,6 +792,7 @@ struct SketchArgs {
   unsigned long long counter_base;  // its value when this launch starts
   int cache_cols;
   int spw;  // register kernel: shared-memory-resident columns per warp (0 = registers only)
+  int fixed_reducer;  // register kernel: CTA 0 always reduces the slots (no arrival atomic)
 };
 
 RQ_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -1268,13 +1269,20 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
     dbg_stamp(j, 3);
     // -------- C: arrive (relaxed); the last CTA reduces every slot and publishes the winner --------
     unsigned long long* wrw = reinterpret_cast<unsigned long long*>(wins) + par * 10;
-    if (threadIdx.x == 0) {
-      unsigned long long old;
-      asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.counter) : "memory");
-      sh.wsel[0] = (old + 1 == p.counter_base + (unsigned long long)(j + 1) * G) ? 1 : 0;
+    bool reducer;
+    if (p.fixed_reducer) {
+      // CTA 0 polls every slot's stamps directly: one L2 round trip fewer than arrive-then-read
+      reducer = blockIdx.x == 0;
+    } else {
+      if (threadIdx.x == 0) {
+        unsigned long long old;
+        asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.counter) : "memory");
+        sh.wsel[0] = (old + 1 == p.counter_base + (unsigned long long)(j + 1) * G) ? 1 : 0;
+      }
+      __syncthreads();
+      reducer = sh.wsel[0] != 0;
     }
-    __syncthreads();
-    if (sh.wsel[0]) {
+    if (reducer) {
       // one slot per thread (G <= NT): spin until its four words carry this step's stamp
       unsigned khi = 0u, klo = 0u;
       int kpos = INT_MAX, kcol = -1;
@@ -1557,6 +1565,13 @@ int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, con
     if (w.scratch_bytes >= need) {
       // step stamps are unique across launches: derived from the monotone counter base
       const unsigned long long stamp_base = counter_base;
+      static const int env_fr = [] {
+        // measured: faster in isolation (5.68 -> 5.26 us/step at n' = 10k) but slower inside the
+        // factorization (sketch phase 44.8 -> 48.2 ms at n = 10k), so off by default
+        const char* e = getenv("RQ_SK_FIXED_REDUCER");
+        return e ? atoi(e) : 0;
+      }();
+      a.fixed_reducer = env_fr;
       int rc, G = 0;
       if (m <= 96) rc = dispatch_sketch_reg<3>(a, n, slots, wins, stamp_base, st, launches, &G);
       else if (m <= 160) rc = dispatch_sketch_reg<5>(a, n, slots, wins, stamp_base, st, launches, &G);

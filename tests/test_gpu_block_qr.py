@@ -176,7 +176,8 @@ def test_diagonal_input_entry_set(rq):
     assert np.allclose(np.sort(np.abs(np.diag(f.r))), np.sort(np.abs(d)), rtol=1e-14)
 
 
-@pytest.mark.parametrize("m,n,b,p", [(300, 300, 50, 10), (257, 200, 32, 8), (500, 500, 64, 6)])
+@pytest.mark.parametrize("m,n,b,p", [(300, 300, 50, 10), (257, 200, 32, 8), (500, 500, 64, 6), (400, 300, 33, 3),
+                                     (1100, 1000, 128, 10)])
 def test_downdate_sketch_matches_hqrrp_oracle(rq, m, n, b, p):
     """HQRRP downdated sketch (Y2 <- Y2 - G1 R12) vs the oracle restatement."""
     from oracle import randqr_oracle as O
@@ -382,6 +383,36 @@ def test_cfg2_full_size_vs_reference_algorithm(rq):
     assert np.all(np.abs(d - do) <= 1e-10 * do + 1e-13 * np.linalg.norm(a))
     ratio = d / s  # rank-revealing: |R_jj| ~ s_j within modest factors on this spectrum
     assert np.all(ratio[: n // 2] > 1e-2) and np.all(ratio[: n // 2] < 1e2)
+
+
+@pytest.mark.parametrize("n", [3000, 10000])
+def test_lookahead_schedule_matches_plain_schedule(rq, n):
+    """The look-ahead driver (next panel's CPQR and moves before the trailing update, the rest of
+    A2 -= V W2 beside the next panel's leaves) factors exactly like the plain panel order:
+    identical pivots, R within 1e-13 ||A|| (bench size n = 10k, cfg 3: b = 256, p = 16)."""
+    import ctypes
+
+    import torch
+
+    from paper_1505_08115_b200 import _lib
+    from paper_1505_08115_b200.errors import check
+
+    b, p = 256, 16
+    eng = rq.Engine()
+    a0, ld = rq.gaussian_matrix_device(n, n, rq.RngState(0), engine=eng)
+    out = []
+    for flags in (0, _lib.RQ_FLAG_NO_LOOKAHEAD):
+        work = a0.clone()
+        perm = torch.empty(n, dtype=torch.int64, device=a0.device)
+        cfg = _lib.rq_config(b, p, 0, -1, _lib.RQ_PIVOT_PERMUTATION, 0, _lib.RQ_SKETCH_DOWNDATE, flags)
+        ctr = ctypes.c_uint64(0)
+        check(eng.lib.rq_factorize(eng.handle, ctypes.byref(cfg), n, n, ctypes.c_void_p(work.data_ptr()), ld,
+                                   ctypes.c_uint64(1), ctypes.byref(ctr), ctypes.c_void_p(perm.data_ptr())))
+        assert ctr.value == n * (b + p)
+        out.append((perm.cpu(), work[:n, :n].T.cpu()))
+    assert torch.equal(out[0][0], out[1][0])
+    anorm = float(torch.linalg.norm(a0[:n, :n]))
+    assert float((out[0][1] - out[1][1]).abs().max()) <= 1e-13 * anorm
 
 
 def test_cfg5_size_n40k_properties(rq):

@@ -202,3 +202,26 @@ if "leaf1" in which:
         check(lib.rq_test_leaf_qr(eng.handle, ctypes.c_void_p(buf.data_ptr()), ld, mm, w,
                                   ctypes.c_void_p(v.data_ptr()), ldv, ctypes.c_void_p(t.data_ptr()), ldt))
     torch.cuda.synchronize()
+
+if "prof" in which:
+    # one leaf (10000 x 16) and one sketch CPQR (272 x 10000, 256 steps), each run twice: the
+    # second launches are the ones an `ncu -k regex:"leaf_reg|sketch_reg" -s 1` capture reads
+    mm, w = 10000, 16
+    a0 = rng.standard_normal((mm, w))
+    lbuf, lld = dev(a0)
+    v, ldv = eng.alloc_matrix(mm, w)
+    t, ldt = eng.alloc_matrix(32, 32)
+    m, n, steps = 272, 10000, 256
+    y0 = rng.standard_normal((m, n))
+    ybuf, yld = dev(y0)
+    ywork, _ = eng.alloc_matrix(m, n)
+    ch = torch.zeros(steps, dtype=torch.int32, device=eng.device)
+    for _ in range(2):
+        lw = lbuf.clone()
+        check(lib.rq_test_leaf_qr(eng.handle, ctypes.c_void_p(lw.data_ptr()), lld, mm, w,
+                                  ctypes.c_void_p(v.data_ptr()), ldv, ctypes.c_void_p(t.data_ptr()), ldt))
+        ywork.copy_(ybuf)
+        check(lib.rq_test_sketch_cpqr(eng.handle, ctypes.c_void_p(ywork.data_ptr()), yld, m, n, steps,
+                                      ctypes.c_void_p(ch.data_ptr())))
+    torch.cuda.synchronize()
+    print("prof ok")
