@@ -218,7 +218,28 @@ int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_
   p.work_bytes = kwork ? kwork_bytes : 0;
   p.max_ctas = gemm_max_ctas;
   p.pdl = gemm_pdl;
+  RQ_TRY(sched_for(stream, &p.sched, &p.sched_base));
   return gemm_f64(p, stream, &launches);
+}
+
+int Ctx::sched_for(cudaStream_t st, unsigned long long** ctr, unsigned long long** base) {
+  // measured at n = 10k / 20k: 155.2 / 637.5 ms with it vs 155.0 / 635.7 without (the producer's
+  // atomic fetch per unit), so off by default; RQ_GEMM_DYN=1 turns it on
+  static const int env_dyn = [] {
+    const char* e = getenv("RQ_GEMM_DYN");
+    return e ? atoi(e) : 0;
+  }();
+  *ctr = nullptr;
+  *base = nullptr;
+  if (!env_dyn) return RQ_OK;
+  if (!gsched) {
+    RQ_CUDA_TRY(cudaMalloc(&gsched, 3 * sizeof(unsigned long long)));
+    RQ_CUDA_TRY(cudaMemset(gsched, 0, 3 * sizeof(unsigned long long)));
+  }
+  const int k = (side && st == side) ? 1 : (hip && st == hip) ? 2 : 0;
+  *ctr = gsched + k;
+  *base = &gsched_base[k];
+  return RQ_OK;
 }
 
 void Ctx::phase(int id) {
@@ -227,6 +248,14 @@ void Ctx::phase(int id) {
   if (cudaEventCreate(&e) != cudaSuccess) return;
   cudaEventRecord(e, stream);
   phase_ev.emplace_back(id, e);
+}
+
+void Ctx::side_phase(int id) {
+  if (!phases_on || !side) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, side);
+  side_ev.emplace_back(id, e);
 }
 
 void Ctx::phase_report() {
@@ -249,6 +278,20 @@ void Ctx::phase_report() {
   fprintf(stderr, "\n");
   for (auto& pe : phase_ev) cudaEventDestroy(pe.second);
   phase_ev.clear();
+  if (!side_ev.empty()) {
+    // side stream: id 0 = CPQR done (start of W), 1 = capped W part, 2 = rest of W, 3 = T
+    double sacc[4] = {0};
+    cudaEventSynchronize(side_ev.back().second);
+    for (size_t k = 1; k < side_ev.size(); k++) {
+      if (side_ev[k].first == 0) continue;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, side_ev[k - 1].second, side_ev[k].second);
+      sacc[side_ev[k].first] += ms;
+    }
+    fprintf(stderr, "[rq side] W capped=%.2f W rest=%.2f T=%.2f\n", sacc[1], sacc[2], sacc[3]);
+    for (auto& pe : side_ev) cudaEventDestroy(pe.second);
+    side_ev.clear();
+  }
 }
 
 // Pending look-ahead tiles [la.next, upto): beside a leaf kernel (programmatic dependent launch,
@@ -269,6 +312,7 @@ int Ctx::la_chunk(int64_t upto, bool beside_leaf) {
     }();
     p.max_ctas = beside_leaf ? kSMs - 16 : 0;
     p.pdl = beside_leaf && env_pdl != 0;
+    RQ_TRY(sched_for(stream, &p.sched, &p.sched_base));
     CatGuard g(cat, PROF_TRAIL);
     // (in a profiled step the events between the leaf and its chunk serialise them: the per-class
     //  breakdown is taken from a separate step, never from the timed ones)
@@ -661,6 +705,13 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       //   CPQR-done event between them for small_q; 3: the same without that event;
       // 4: CPQR on a highest-priority stream, W on a lowest-priority one.
       RQ_TRY(ensure_side());
+      if (phases_on) {  // fork time (main stream), the reference for the side-stream parts
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) == cudaSuccess) {
+          cudaEventRecord(e, stream);
+          side_ev.emplace_back(0, e);
+        }
+      }
       RQ_CUDA_TRY(cudaEventRecord(ev_v, stream));
       const bool pdl = env_overlap != 4;
       cudaStream_t cpqr_stream = pdl ? side : hip;
@@ -688,16 +739,30 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
           int64_t n_a = (int64_t)(cpqr_s * rate / (2.0 * b * (double)mp));
           n_a = std::max<int64_t>(128, (n_a + 127) / 128 * 128);
           if (n_a >= n2 - 256) n_a = n2;
+          // RQ_TN_SPLIT=0: one launch on the whole grid (with dynamic scheduling its CTAs that do not
+          // fit beside the CPQR start when it ends and take fewer units); measured slower
+          // (157.2 vs 155.0 ms at n = 10k), so the capped part + remainder split stays the default
+          static const int env_split = [] {
+            const char* e = getenv("RQ_TN_SPLIT");
+            return e ? atoi(e) : 1;
+          }();
+          if (env_split == 0) {
+            n_a = n2;
+            gemm_max_ctas = 0;
+          }
           rc = gemm(b, n_a, mp, op(V, mp + vpad, b, ldv, vpad), false, op(A, m, n, lda, s, s + b), L.wside, even(b),
                     1.0, 0.0);
           gemm_pdl = false;
           gemm_max_ctas = 0;
+          side_phase(1);
           if (rc == RQ_OK && n_a < n2)
             rc = gemm(b, n2 - n_a, mp, op(V, mp + vpad, b, ldv, vpad), false, op(A, m, n, lda, s, s + b + n_a),
                       L.wside + n_a * even(b), even(b), 1.0, 0.0);
         }
         gemm_pdl = false;
+        side_phase(2);
         if (rc == RQ_OK) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
+        side_phase(3);
         if (rc == RQ_OK) rc = cudaEventRecord(ev_side, side) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
       }
       gemm_max_ctas = 0;
@@ -1298,6 +1363,7 @@ int Ctx::step_panel_apply(const double* V, int64_t ldv, const double* T, int64_t
 
 Ctx::~Ctx() {
   if (sk_counter) cudaFree(sk_counter);
+  if (gsched) cudaFree(gsched);
   for (auto e : ev_pool) cudaEventDestroy(e);
   arena.release();
   qarena.release();

@@ -118,6 +118,11 @@ struct Ctx {
   std::function<void(int64_t, int64_t)> on_cols_final;
   int gemm_max_ctas = 0;
   bool gemm_pdl = false;
+  // dynamic GEMM unit scheduling: one monotone device counter per stream (main, side, hip) and
+  // its host mirror (GEMMs on one stream never overlap each other, so a counter is never shared)
+  unsigned long long* gsched = nullptr;
+  unsigned long long gsched_base[3] = {0, 0, 0};
+  int sched_for(cudaStream_t st, unsigned long long** ctr, unsigned long long** base);
   int ensure_side();
   // look-ahead (factorize_perm, downdated sketches): the previous panel's A2 -= V W2 on the
   // columns after the current panel, issued in tile-range chunks, each launched right behind one
@@ -133,7 +138,9 @@ struct Ctx {
   // between a leaf and its look-ahead chunk); per-phase totals printed to stderr per call
   bool phases_on = false;
   std::vector<std::pair<int, cudaEvent_t>> phase_ev;
+  std::vector<std::pair<int, cudaEvent_t>> side_ev;  // side stream: W GEMM parts and T
   void phase(int id);
+  void side_phase(int id);
   void phase_report();
   int la_flush() { return la.on ? la_chunk(la.tiles, false) : RQ_OK; }
   // scratch views used by helpers

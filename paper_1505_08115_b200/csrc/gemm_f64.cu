@@ -71,6 +71,8 @@ struct KArgs {
   int k_lo;      // 1: element k = 0 is padding (odd K origin shifted to even)
   int m_lo;      // 1: output row 0 is padding (odd M origin shifted to even)
   int u0, u1;    // unit range of this launch (a tile-range chunk of a larger GEMM, or all units)
+  unsigned long long* sched;       // non-null: units handed out by an atomic counter (dynamic)
+  unsigned long long sched_base;   // the counter's value when this launch starts
 };
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
@@ -86,7 +88,7 @@ struct GemmCfg {
   static constexpr int A_BYTES_AL = (A_BYTES + 1023) / 1024 * 1024;
   static constexpr int B_BYTES = BN * BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES_AL + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 2 * STAGES * 8;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 2 * STAGES * 8 + 8 * 4 /*unit ring*/;
   static_assert(WTM % 16 == 0 && WTN % 8 == 0, "warp tile");
   static_assert(B_BYTES % 1024 == 0, "swizzle-128B stage alignment");
 };
@@ -102,33 +104,42 @@ RQ_DEV double ld_kmajor(const char* tile, int r, int k) {
   return *reinterpret_cast<const double*>(tile + off);
 }
 
-// Walks this CTA's (unit, k-chunk) sequence; units are assigned round-robin.
+// Walks this CTA's (unit, k-chunk) sequence.  Units are assigned round-robin (static) or, with
+// a.sched, taken from an atomic counter as the producer reaches them (dynamic: CTAs that start
+// late, e.g. behind a concurrent kernel, simply take fewer units).  In dynamic mode the producer
+// publishes each unit it starts in a shared-memory ring (entry -1: no more units) that the
+// consumer warps read after the unit's first stage is full.  Every unit has >= 1 k-chunk.
 struct ChunkCursor {
   int u;
   int64_t kc, kc_end;
   bool valid;
+  int seq;
   RQ_DEV void unit_range(const KArgs& a) {
     const int split = u % a.splitk;
     kc = (int64_t)split * a.kchunks_per_split;
     kc_end = kc + a.kchunks_per_split;
     if (kc_end > a.kchunks) kc_end = a.kchunks;
   }
-  RQ_DEV void start(const KArgs& a, int units) {
-    u = a.u0 + blockIdx.x;
+  RQ_DEV void begin_unit(const KArgs& a, int units, int* ring) {
     valid = u < units;
+    if (a.sched) ring[seq & 7] = valid ? u : -1;
+    seq++;
     if (valid) unit_range(a);
-    skip_empty(a, units);
   }
-  RQ_DEV void skip_empty(const KArgs& a, int units) {
-    while (valid && kc >= kc_end) {
-      u += gridDim.x;
-      valid = u < units;
-      if (valid) unit_range(a);
-    }
+  RQ_DEV int fetch(const KArgs& a) {
+    const unsigned long long t = atomicAdd(a.sched, 1ull) - a.sched_base;
+    return a.u0 + (int)min(t, (unsigned long long)0x3fffffff);
   }
-  RQ_DEV void next(const KArgs& a, int units) {
+  RQ_DEV void start(const KArgs& a, int units, int* ring) {
+    seq = 0;
+    u = a.sched ? fetch(a) : a.u0 + (int)blockIdx.x;
+    begin_unit(a, units, ring);
+  }
+  RQ_DEV void next(const KArgs& a, int units, int* ring) {
     kc++;
-    skip_empty(a, units);
+    if (kc < kc_end) return;
+    u = a.sched ? fetch(a) : u + (int)gridDim.x;
+    begin_unit(a, units, ring);
   }
 };
 
@@ -163,6 +174,8 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
   unsigned char* smem = smem_raw + ((1024u - mis) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
+  int* ring = reinterpret_cast<int*>(empty + STAGES);
+  const bool dyn = args.sched != nullptr;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -172,6 +185,7 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
   ChunkCursor prod;
   int pstage = 0;
   uint32_t pphase = 0;
+  bool pterm = false;  // dynamic: the "no more units" stage was signalled
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; s++) {
       mbar_init(&full[s], 1);
@@ -180,10 +194,17 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
-    prod.start(args, units);
-    for (int s = 0; s < STAGES && prod.valid; s++) {
-      issue_stage<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(&tmA, &tmB, args, smem, full, pstage, prod);
-      prod.next(args, units);
+    prod.start(args, units, ring);
+    for (int s = 0; s < STAGES; s++) {
+      if (prod.valid) {
+        issue_stage<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(&tmA, &tmB, args, smem, full, pstage, prod);
+        prod.next(args, units, ring);
+      } else if (dyn && !pterm) {
+        mbar_arrive(&full[pstage]);  // empty stage: the consumers read ring entry -1 and stop
+        pterm = true;
+      } else {
+        break;
+      }
       if (++pstage == STAGES) {
         pstage = 0;
         pphase ^= 1;
@@ -200,7 +221,16 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
   int stage = 0;
   uint32_t phase = 0;
 
-  for (int u = args.u0 + blockIdx.x; u < units; u += gridDim.x) {
+  int cseq = 0;
+  for (int u = args.u0 + blockIdx.x;; u += gridDim.x) {
+    if (dyn) {
+      mbar_wait(&full[stage], phase);  // the unit's first stage (or the terminal signal)
+      u = ring[cseq & 7];
+      cseq++;
+      if (u < 0) break;
+    } else if (u >= units) {
+      break;
+    }
     const int split = u % args.splitk;
     const int t = u / args.splitk;
     const int tm = t % args.tiles_m;
@@ -290,10 +320,15 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       // producer: refill this stage with the chunk STAGES ahead once every warp released it
-      if (threadIdx.x == 0 && prod.valid) {
+      if (threadIdx.x == 0 && (prod.valid || (dyn && !pterm))) {
         mbar_wait(&empty[pstage], pphase ^ 1);
-        issue_stage<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(&tmA, &tmB, args, smem, full, pstage, prod);
-        prod.next(args, units);
+        if (prod.valid) {
+          issue_stage<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(&tmA, &tmB, args, smem, full, pstage, prod);
+          prod.next(args, units, ring);
+        } else {
+          mbar_arrive(&full[pstage]);
+          pterm = true;
+        }
         if (++pstage == STAGES) {
           pstage = 0;
           pphase ^= 1;
@@ -459,6 +494,7 @@ static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launch
   a.kchunks = ceil_div(a.K, BK);
   a.splitk = p.splitk > 1 ? p.splitk : 1;
   a.kchunks_per_split = (int)ceil_div(a.kchunks, a.splitk);
+  a.splitk = (int)ceil_div(a.kchunks, a.kchunks_per_split);  // no empty splits
   a.work = p.work;
   const int64_t all_units = (int64_t)a.tiles_m * a.tiles_n * a.splitk;
   a.u0 = 0;
@@ -470,6 +506,8 @@ static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launch
     if (a.u1 <= a.u0) return RQ_OK;
   }
   const int64_t units = a.u1 - a.u0;
+  a.sched = p.sched;
+  a.sched_base = p.sched ? *p.sched_base : 0;
   static int per_sm = 0;
   if (per_sm == 0) {
     RQ_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::SMEM));
@@ -504,6 +542,7 @@ static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launch
     }
   }
   if (launches) (*launches)++;
+  if (p.sched) *p.sched_base += (unsigned long long)units + (unsigned long long)grid;  // one failing fetch per CTA
   if (a.splitk > 1) {
     const int64_t total = a.M * a.N;
     int blocks = (int)ceil_div(total, 256);

@@ -39,6 +39,8 @@ struct GemmProblem {
   int max_ctas = 0;      // > 0: cap the persistent grid (leave SMs to a concurrent kernel)
   bool pdl = false;      // programmatic dependent launch: may start once the previous kernel in the
                          // stream triggered (the GEMM must not read that kernel's output)
+  unsigned long long* sched = nullptr;       // device counter: dynamic unit scheduling (see gemm_f64.cu)
+  unsigned long long* sched_base = nullptr;  // host mirror of its value; advanced by every launch
   int64_t tile_begin = 0, tile_end = 0;  // tile_end > 0: only output tiles [tile_begin, tile_end)
                                          // (column-major tile order; see gemm_f64_tiles)
 };
