@@ -223,12 +223,20 @@ __global__ void __launch_bounds__(PL_THREADS) leaf_qr_kernel(double* __restrict_
 // ---------------------------------------------------------------------------
 __device__ unsigned long long g_leaf_dbg[64 * 8];
 __device__ int g_leaf_dbg_on;
+// Compiled in only with -DRQ_STAMPS (tuning builds): reading the flag from global memory on
+// every call put an L2 round trip after each cluster acquire (which invalidates L1) on the
+// per-column critical path.
 RQ_DEV void leaf_stamp(int j, int k) {
-  if (g_leaf_dbg_on && j < 64 && blockIdx.x == 0 && threadIdx.x == 0) {
+#ifdef RQ_STAMPS
+  if (blockIdx.x == 0 && threadIdx.x == 0 && j < 64 && g_leaf_dbg_on) {
     unsigned long long c;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
     g_leaf_dbg[j * 8 + k] = c;
   }
+#else
+  (void)j;
+  (void)k;
+#endif
 }
 int leaf_debug_timing(int on, unsigned long long* host, int count) {
   RQ_CUDA_TRY(cudaMemcpyToSymbol(g_leaf_dbg_on, &on, sizeof(int)));

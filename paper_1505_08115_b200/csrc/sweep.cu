@@ -279,12 +279,18 @@ RQ_DEV void cluster_barrier() {
 // Optional phase timestamps (rank 0, thread 0, first 64 steps) for tuning.
 __device__ unsigned long long g_sweep_dbg[64 * 8];
 __device__ int g_sweep_dbg_on;
+// Compiled in only with -DRQ_STAMPS (tuning builds; see leaf_stamp in panel.cu).
 RQ_DEV void dbg_stamp(int j, int k) {
-  if (g_sweep_dbg_on && j < 64 && blockIdx.x == 0 && threadIdx.x == 0) {
+#ifdef RQ_STAMPS
+  if (blockIdx.x == 0 && threadIdx.x == 0 && j < 64 && g_sweep_dbg_on) {
     unsigned long long c;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
     g_sweep_dbg[j * 8 + k] = c;
   }
+#else
+  (void)j;
+  (void)k;
+#endif
 }
 
 RQ_DEV void dsmem_st_f64(double* local, unsigned rank, double v) {
