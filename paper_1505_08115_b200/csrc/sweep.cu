@@ -1511,7 +1511,8 @@ static int dispatch_sketch_reg(SketchArgs a, int n, SkSlot2* slots, SkWin* wins,
   struct Opt {
     int warps, cpw;
   };
-  const Opt opts[] = {{16, 1}, {16, 2}, {16, 3}, {8, 6}, {8, 10}};
+  // (8, 8) and (8, 9): n' ~ 8.5k..10.6k on 139..148 CTAs instead of 107..125 with (8, 10)
+  const Opt opts[] = {{16, 1}, {16, 2}, {16, 3}, {8, 6}, {8, 8}, {8, 9}, {8, 10}};
   a.spw = 0;
   for (const Opt& o : opts) {
     if (RPL * o.cpw > (o.warps == 16 ? 30 : 92)) continue;  // register budget
@@ -1522,6 +1523,11 @@ static int dispatch_sketch_reg(SketchArgs a, int n, SkSlot2* slots, SkWin* wins,
     if (o.warps == 16 && o.cpw == 2) return launch_sketch_reg<RPL, 2, 16>(a, G, slots, wins, stamp_base, st, launches);
     if (o.warps == 16 && o.cpw == 3) return launch_sketch_reg<RPL, 3, 16>(a, G, slots, wins, stamp_base, st, launches);
     if (o.cpw == 6) return launch_sketch_reg<RPL, 6, 8>(a, G, slots, wins, stamp_base, st, launches);
+    if constexpr (RPL == 9) {
+      if (o.cpw == 8) return launch_sketch_reg<RPL, 8, 8>(a, G, slots, wins, stamp_base, st, launches);
+      if (o.cpw == 9) return launch_sketch_reg<RPL, 9, 8>(a, G, slots, wins, stamp_base, st, launches);
+    }
+    if (o.cpw == 8 || o.cpw == 9) continue;
     return launch_sketch_reg<RPL, 10, 8>(a, G, slots, wins, stamp_base, st, launches);
   }
   if constexpr (RPL == 9) {

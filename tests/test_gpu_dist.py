@@ -140,7 +140,8 @@ def test_distributed_world1_nccl_matches_single_gpu(m, n, b, p):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,steps", [(900, 256), (9000, 256), (13000, 256), (21500, 96), (24000, 40)])
+@pytest.mark.parametrize("n,steps", [(900, 256), (8800, 256), (9000, 256), (10000, 256), (11000, 128), (13000, 256),
+                                     (21500, 96), (24000, 40)])
 def test_sketch_select_every_kernel_tier(n, steps):
     """The sketch CPQR picks the reference's pivots in every tier: register-resident
     (n' <= 11840), registers + shared memory (<= ~23k), and the L2-streaming fallback."""
