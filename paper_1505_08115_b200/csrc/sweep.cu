@@ -1117,6 +1117,32 @@ RQ_DEV void sk_apply1(double (&y)[RPL], const double* u, int lane) {
   for (int k = K0; k < RPL; k++) y[k] -= d * u[lane + 32 * k];
 }
 
+// Two shared-memory columns at once (same arithmetic per column as sk_apply1): their
+// reductions interleave, halving the latency-bound chain of the shared-memory tier.
+template <int K0, int RPL>
+RQ_DEV void sk_apply2(double (&y0)[RPL], double (&y1)[RPL], const double* u, int lane) {
+  double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+  for (int k = K0; k < RPL; k++) {
+    const double uk = u[lane + 32 * k];
+    d0 = fma(uk, y0[k], d0);
+    d1 = fma(uk, y1[k], d1);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+    d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+  }
+  d0 *= 2.0;
+  d1 *= 2.0;
+#pragma unroll
+  for (int k = K0; k < RPL; k++) {
+    const double uk = u[lane + 32 * k];
+    y0[k] -= d0 * uk;
+    y1[k] -= d1 * uk;
+  }
+}
+
 // Columns beyond the register capacity live in shared memory, [column][slot k][lane].
 struct SkSmem {
   double* xs;
@@ -1172,30 +1198,56 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
     }
     int bcol = bq >= 0 ? cbase + bq : -1;
     if constexpr (SMEM) {
-      for (int s2 = 0; s2 < sm.spw; s2++) {
-        const int sc = warp * sm.spw + s2;
-        if (!sm.sact[sc]) continue;  // warp-uniform
-        double* col = sm.xs + (int64_t)sc * RPL * 32 + lane;
-        double y[RPL];
+      // pairs of shared-memory columns (an odd last one is paired with itself, result unused)
+      for (int s2 = 0; s2 < sm.spw; s2 += 2) {
+        const int sc0 = warp * sm.spw + s2;
+        const bool has1 = s2 + 1 < sm.spw;
+        const int sc1 = has1 ? sc0 + 1 : sc0;
+        const bool a0 = sm.sact[sc0] != 0, a1 = has1 && sm.sact[sc1] != 0;  // warp-uniform
+        if (!a0 && !a1) continue;
+        double* col0 = sm.xs + (int64_t)sc0 * RPL * 32 + lane;
+        double* col1 = sm.xs + (int64_t)sc1 * RPL * 32 + lane;
+        double y0[RPL], y1[RPL];
 #pragma unroll
-        for (int k = KL; k < RPL; k++) y[k] = col[k * 32];
-        if (have_refl) {
-          if (KJ > 0 && jl == 0) sk_apply1<KL, RPL>(y, u, lane);
-          else sk_apply1<KJ, RPL>(y, u, lane);
+        for (int k = KL; k < RPL; k++) {
+          y0[k] = col0[k * 32];
+          y1[k] = col1[k * 32];
         }
-        const double yv = at_or_below ? y[KJ] : 0.0;
-        double tt = yv * yv;
+        if (have_refl) {
+          if (KJ > 0 && jl == 0) sk_apply2<KL, RPL>(y0, y1, u, lane);
+          else sk_apply2<KJ, RPL>(y0, y1, u, lane);
+        }
+        const double yv0 = at_or_below ? y0[KJ] : 0.0, yv1 = at_or_below ? y1[KJ] : 0.0;
+        double t0 = yv0 * yv0, t1 = yv1 * yv1;
 #pragma unroll
-        for (int k = KJ + 1; k < RPL; k++) tt = fma(y[k], y[k], tt);
+        for (int k = KJ + 1; k < RPL; k++) {
+          t0 = fma(y0[k], y0[k], t0);
+          t1 = fma(y1[k], y1[k], t1);
+        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tt += __shfl_xor_sync(0xffffffffu, tt, o);
+        for (int o = 16; o > 0; o >>= 1) {
+          t0 += __shfl_xor_sync(0xffffffffu, t0, o);
+          t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+        }
+        if (a0) {
 #pragma unroll
-        for (int k = KL; k < RPL; k++) col[k * 32] = y[k];
-        const int ps = sm.spos[sc];
-        if (bcol < 0 || piv_better(tt, ps, bkey, bpos)) {
-          bkey = tt;
-          bpos = ps;
-          bcol = sm.cbase_s + s2;
+          for (int k = KL; k < RPL; k++) col0[k * 32] = y0[k];
+          const int ps = sm.spos[sc0];
+          if (bcol < 0 || piv_better(t0, ps, bkey, bpos)) {
+            bkey = t0;
+            bpos = ps;
+            bcol = sm.cbase_s + s2;
+          }
+        }
+        if (a1) {
+#pragma unroll
+          for (int k = KL; k < RPL; k++) col1[k * 32] = y1[k];
+          const int ps = sm.spos[sc1];
+          if (bcol < 0 || piv_better(t1, ps, bkey, bpos)) {
+            bkey = t1;
+            bpos = ps;
+            bcol = sm.cbase_s + s2 + 1;
+          }
         }
       }
     }
