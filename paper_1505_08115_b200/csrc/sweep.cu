@@ -799,6 +799,8 @@ struct SketchArgs {
   int cache_cols;
   int spw;  // register kernel: shared-memory-resident columns per warp (0 = registers only)
   int fixed_reducer;  // register kernel: CTA 0 always reduces the slots (no arrival atomic)
+  int cl;             // register kernel: cluster size (> 1: two-level exchange, see SkClu)
+  int per;            // register kernel: columns per CTA (column id -> CTA)
 };
 
 RQ_DEV unsigned long long ld_acquire_u64(const unsigned long long* p) {
@@ -1144,12 +1146,26 @@ RQ_DEV void sk_apply2(double (&y0)[RPL], double (&y1)[RPL], const double* u, int
 }
 
 // Columns beyond the register capacity live in shared memory, [column][slot k][lane].
+// Two-level exchange (cluster launch, p.cl = CS > 1): each CTA pushes its candidate record
+// (6 words: key, pos|col, tail, x_j, CTA, pad) into its cluster leader's table through
+// st.async; the leader (cluster rank 0) reduces its CS records, publishes the cluster's best as
+// an LL slot, polls the slots of all G/CS leaders (one L2 round trip, no arrival atomic), and
+// pushes the winner record back to the members of its cluster.  Every leader computes the same
+// winner from the same slots.
+struct SkClu {
+  unsigned long long keys[2][16][6];  // leader: member records, by step parity
+  unsigned long long win[2][6];       // every CTA: winner record from its leader
+  unsigned long long kbar[2];         // leader: member records of step j complete on kbar[j & 1]
+  unsigned long long wbar[2];         // winner record of step j complete on wbar[j & 1]
+};
+
 struct SkSmem {
   double* xs;
   int* spos;
   int* sact;
   int spw;      // columns per warp
   int cbase_s;  // global id of this warp's first shared-memory column
+  SkClu* cl;    // two-level exchange state (p.cl > 1)
 };
 
 // Steps j in [32*KJ, jend): row j lives in register slot KJ (lane j & 31), so
@@ -1163,10 +1179,20 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
   const int G = gridDim.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = p.m;
+  const int CS = p.cl;
+  unsigned crank = 0, cid = 0;
+  if (CS > 1) {
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+    asm("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
+  }
   for (int j = 32 * KJ; j < jend; j++) {
     const int par = j & 1;
     const int jl = j & 31;
     dbg_stamp(j, 0);
+    if (CS > 1 && threadIdx.x == 0) {
+      mbar_expect_tx(&sm.cl->wbar[par], 6 * 8);
+      if (crank == 0) mbar_expect_tx(&sm.cl->kbar[par], (unsigned)CS * 6 * 8);
+    }
     // -------- A: apply the pending reflector (row j-1), score rows >= j --------
     if (have_refl) {
       if (KJ > 0 && jl == 0) sk_apply<(KJ > 0 ? KJ - 1 : 0), RPL, CPW>(x, act, u, lane);
@@ -1270,11 +1296,22 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
       const int wl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);  // warp-uniform, same in every warp
       if (wl < 0) {
         if (warp == 0 && lane == 0) {
-          unsigned long long* me = slw + (int64_t)blockIdx.x * 8;
-          st_ll2(me, ll_word(0u, stamp), ll_word(0u, stamp));
-          st_ll2(me + 2, ll_word((unsigned)INT_MAX, stamp), ll_word(0xffffffffu, stamp));
-          st_ll2(me + 4, ll_word(0u, stamp), ll_word(0u, stamp));
-          st_ll2(me + 6, ll_word(0u, stamp), ll_word(0u, stamp));
+          if (CS > 1) {
+            const uint32_t dst = cluster_map(smem_u32(&sm.cl->keys[par][crank][0]), 0u);
+            const uint32_t mb = cluster_map(smem_u32(&sm.cl->kbar[par]), 0u);
+            st_async_u64(dst, 0ull, mb);
+            st_async_u64(dst + 8, ((unsigned long long)0xffffffffu << 32) | (unsigned)INT_MAX, mb);
+            st_async_u64(dst + 16, 0ull, mb);
+            st_async_u64(dst + 24, 0ull, mb);
+            st_async_u64(dst + 32, 0ull, mb);
+            st_async_u64(dst + 40, 0ull, mb);
+          } else {
+            unsigned long long* me = slw + (int64_t)blockIdx.x * 8;
+            st_ll2(me, ll_word(0u, stamp), ll_word(0u, stamp));
+            st_ll2(me + 2, ll_word((unsigned)INT_MAX, stamp), ll_word(0xffffffffu, stamp));
+            st_ll2(me + 4, ll_word(0u, stamp), ll_word(0u, stamp));
+            st_ll2(me + 6, ll_word(0u, stamp), ll_word(0u, stamp));
+          }
         }
       } else if (wl == warp) {
         const SkKey b = sh.wk[warp];
@@ -1296,12 +1333,24 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) tl += __shfl_xor_sync(0xffffffffu, tl, o);
           if (lane == 0) {
-            unsigned long long* me = slw + (int64_t)blockIdx.x * 8;
             const unsigned long long tb = __double_as_longlong(tl), xb = __double_as_longlong(xj);
-            st_ll2(me, ll_word(b.hi, stamp), ll_word(b.lo, stamp));
-            st_ll2(me + 2, ll_word((unsigned)b.pos, stamp), ll_word((unsigned)b.col, stamp));
-            st_ll2(me + 4, ll_word((unsigned)(tb >> 32), stamp), ll_word((unsigned)tb, stamp));
-            st_ll2(me + 6, ll_word((unsigned)(xb >> 32), stamp), ll_word((unsigned)xb, stamp));
+            if (CS > 1) {
+              // (the column's LL words above are read only once the winner is known)
+              const uint32_t dst = cluster_map(smem_u32(&sm.cl->keys[par][crank][0]), 0u);
+              const uint32_t mb = cluster_map(smem_u32(&sm.cl->kbar[par]), 0u);
+              st_async_u64(dst, ((unsigned long long)b.hi << 32) | b.lo, mb);
+              st_async_u64(dst + 8, ((unsigned long long)(unsigned)b.col << 32) | (unsigned)b.pos, mb);
+              st_async_u64(dst + 16, tb, mb);
+              st_async_u64(dst + 24, xb, mb);
+              st_async_u64(dst + 32, (unsigned long long)blockIdx.x, mb);
+              st_async_u64(dst + 40, 0ull, mb);
+            } else {
+              unsigned long long* me = slw + (int64_t)blockIdx.x * 8;
+              st_ll2(me, ll_word(b.hi, stamp), ll_word(b.lo, stamp));
+              st_ll2(me + 2, ll_word((unsigned)b.pos, stamp), ll_word((unsigned)b.col, stamp));
+              st_ll2(me + 4, ll_word((unsigned)(tb >> 32), stamp), ll_word((unsigned)tb, stamp));
+              st_ll2(me + 6, ll_word((unsigned)(xb >> 32), stamp), ll_word((unsigned)xb, stamp));
+            }
           }
         };
         bool done = false;
@@ -1327,6 +1376,99 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
     dbg_stamp(j, 3);
     // -------- C: arrive (relaxed); the last CTA reduces every slot and publishes the winner --------
     unsigned long long* wrw = reinterpret_cast<unsigned long long*>(wins) + par * 10;
+    if (CS > 1) {
+      const int L = G / CS;  // leaders (G is a multiple of CS)
+      if (crank == 0) {
+        // (1) the cluster's best of its CS member records -> LL slot `cid` (same 8-word format as
+        //     the single-level slots; the winning CTA follows from the column id: col / p.per)
+        if (warp == 0) {
+          mbar_wait_cluster(&sm.cl->kbar[par], (unsigned)(j >> 1) & 1u);
+          unsigned khi = 0u, klo = 0u;
+          int kpos = INT_MAX, kcol = -1;
+          unsigned long long ktb = 0ull, kxb = 0ull;
+          if (lane < CS) {
+            const unsigned long long* r = sm.cl->keys[par][lane];
+            khi = (unsigned)(r[0] >> 32);
+            klo = (unsigned)r[0];
+            kpos = (int)(unsigned)r[1];
+            kcol = (int)(unsigned)(r[1] >> 32);
+            ktb = r[2];
+            kxb = r[3];
+          }
+          const int bl = warp_argmax(khi, klo, kpos, kcol >= 0);
+          if (lane == (bl < 0 ? 0 : bl)) {
+            unsigned long long* me = slw + (int64_t)cid * 8;
+            const int cc = bl < 0 ? -1 : kcol;
+            st_ll2(me, ll_word(bl < 0 ? 0u : khi, stamp), ll_word(bl < 0 ? 0u : klo, stamp));
+            st_ll2(me + 2, ll_word((unsigned)(bl < 0 ? INT_MAX : kpos), stamp), ll_word((unsigned)cc, stamp));
+            st_ll2(me + 4, ll_word((unsigned)(ktb >> 32), stamp), ll_word((unsigned)ktb, stamp));
+            st_ll2(me + 6, ll_word((unsigned)(kxb >> 32), stamp), ll_word((unsigned)kxb, stamp));
+          }
+        }
+        // (2) every leader reads all L slots (one per thread) and resolves the same winner
+        unsigned khi = 0u, klo = 0u;
+        int kpos = INT_MAX, kcol = -1;
+        unsigned long long ktb = 0ull, kxb = 0ull;
+        if ((int)threadIdx.x < L) {
+          const unsigned long long* sp = slw + (int64_t)threadIdx.x * 8;
+          unsigned long long a0, a1, a2, a3, a4, a5, a6, a7;
+          do {
+            ld_ll2(sp, a0, a1);
+            ld_ll2(sp + 2, a2, a3);
+            ld_ll2(sp + 4, a4, a5);
+            ld_ll2(sp + 6, a6, a7);
+          } while ((unsigned)a0 != stamp || (unsigned)a1 != stamp || (unsigned)a2 != stamp || (unsigned)a3 != stamp ||
+                   (unsigned)a4 != stamp || (unsigned)a5 != stamp || (unsigned)a6 != stamp || (unsigned)a7 != stamp);
+          khi = (unsigned)(a0 >> 32);
+          klo = (unsigned)(a1 >> 32);
+          kpos = (int)(a2 >> 32);
+          kcol = (int)(a3 >> 32);
+          ktb = (a4 & 0xffffffff00000000ull) | (a5 >> 32);
+          kxb = (a6 & 0xffffffff00000000ull) | (a7 >> 32);
+        }
+        if (warp * 32 < L) {
+          const int wl = warp_argmax(khi, klo, kpos, kcol >= 0);
+          if (lane == (wl < 0 ? 0 : wl)) {
+            sh.wk[warp] = SkKey{khi, klo, kpos, wl < 0 ? -1 : kcol};
+            sh.wbits[warp][0] = ktb;
+            sh.wbits[warp][1] = kxb;
+          }
+        }
+        __syncthreads();
+        // (3) push the winner record to every member of this cluster
+        if (warp == 0) {
+          const int nw = (L + 31) / 32;
+          const SkKey r = lane < nw ? sh.wk[lane] : SkKey{0u, 0u, INT_MAX, -1};
+          const int gl = warp_argmax(r.hi, r.lo, r.pos, r.col >= 0);
+          const int src = gl < 0 ? 0 : gl;
+          const unsigned whi = __shfl_sync(0xffffffffu, r.hi, src), wlo = __shfl_sync(0xffffffffu, r.lo, src);
+          const int wps = __shfl_sync(0xffffffffu, r.pos, src), wcl = __shfl_sync(0xffffffffu, r.col, src);
+          if (lane < CS) {
+            const unsigned long long tb = sh.wbits[src][0], xb = sh.wbits[src][1];
+            const int col = gl < 0 ? -1 : wcl;
+            const int cta = col >= 0 ? col / p.per : 0;
+            const uint32_t dst = cluster_map(smem_u32(&sm.cl->win[par][0]), (unsigned)lane);
+            const uint32_t mb = cluster_map(smem_u32(&sm.cl->wbar[par]), (unsigned)lane);
+            st_async_u64(dst, ((unsigned long long)whi << 32) | wlo, mb);
+            st_async_u64(dst + 8, ((unsigned long long)(unsigned)col << 32) | (unsigned)wps, mb);
+            st_async_u64(dst + 16, tb, mb);
+            st_async_u64(dst + 24, xb, mb);
+            st_async_u64(dst + 32, (unsigned long long)cta, mb);
+            st_async_u64(dst + 40, 0ull, mb);
+          }
+        }
+      }
+      if (warp == 0) {
+        mbar_wait_cluster(&sm.cl->wbar[par], (unsigned)(j >> 1) & 1u);
+        if (lane == 0) {
+          const unsigned long long* r = sm.cl->win[par];
+          sh.win = SkKey{(unsigned)(r[0] >> 32), (unsigned)r[0], (int)(unsigned)r[1], (int)(unsigned)(r[1] >> 32)};
+          sh.wtail = __longlong_as_double((long long)r[2]);
+          sh.wxj = __longlong_as_double((long long)r[3]);
+          sh.wsel[1] = (int)r[4];
+        }
+      }
+    } else {
     bool reducer;
     if (p.fixed_reducer) {
       // CTA 0 polls every slot's stamps directly: one L2 round trip fewer than arrive-then-read
@@ -1411,6 +1553,7 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
         sh.wxj = __longlong_as_double((long long)((t4a & 0xffffffff00000000ull) | (t4b >> 32)));
       }
     }
+    }  // single-level exchange
     __syncthreads();
     dbg_stamp(j, 4);
     // -------- E: reflector from the winning column (LL words in L2); u = 0 outside [j, m) --------
@@ -1495,7 +1638,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
   const int spw = SMEM ? p.spw : 0;
   const int per = WARPS * CPW + WARPS * spw;
   const int cbase = blockIdx.x * per + warp * CPW;
-  SkSmem sm{sk_dyn, spos_s, sact_s, spw, (int)blockIdx.x * per + WARPS * CPW + warp * spw};
+  __shared__ SkClu clu;
+  SkSmem sm{sk_dyn, spos_s, sact_s, spw, (int)blockIdx.x * per + WARPS * CPW + warp * spw, &clu};
+  if (p.cl > 1) {
+    if (threadIdx.x == 0) {
+      mbar_init(&clu.kbar[0], 1);
+      mbar_init(&clu.kbar[1], 1);
+      mbar_init(&clu.wbar[0], 1);
+      mbar_init(&clu.wbar[1], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   double x[CPW][RPL];
   int pos[CPW];
   bool act[CPW];
@@ -1534,6 +1689,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
     sk_dispatch<0, RPL, CPW, WARPS, SMEM>(kj, p, slots, wins, stamp_base, x, pos, act, have_refl, u, sh, cbase, jend,
                                           sm);
   }
+  if (p.cl > 1)  // no CTA leaves while a cluster peer may still push into its shared memory
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 template <int RPL, int CPW, int WARPS, bool SMEM = false>
@@ -1548,6 +1705,45 @@ static int launch_sketch_reg(const SketchArgs& a, int G, SkSlot2* slots, SkWin* 
       RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
+  }
+  // two-level exchange over clusters of CS CTAs when the rounded-up grid is co-resident
+  // (RQ_SK_CLUSTER=4).  Correct (same pivots) but measured slower: 9.10 vs 5.21 us/step at
+  // n' = 10k (35 leaders each polling all 35 slots contend like the flat all-gather did), so off
+  static const int env_cl = [] {
+    const char* e = getenv("RQ_SK_CLUSTER");
+    return e ? atoi(e) : 0;
+  }();
+  SketchArgs ac = a;
+  ac.cl = 0;
+  ac.per = a.spw * WARPS + CPW * WARPS;
+  for (int CS = env_cl; CS >= 2; CS /= 2) {
+    const int Gc = (G + CS - 1) / CS * CS;
+    if (Gc > kSMs) continue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(Gc);
+    cfg.blockDim = dim3(WARPS * 32);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclu = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclu, kern, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (nclu * CS < Gc) continue;  // every CTA must be resident: they wait on one another
+    cfg.numAttrs = 2;
+    ac.cl = CS;
+    RQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ac, slots, wins, stamp_base));
+    if (launches) (*launches)++;
+    return RQ_OK;
   }
   RQ_CUDA_TRY(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(WARPS * 32), args, dyn, st));
   if (launches) (*launches)++;
