@@ -336,6 +336,9 @@ int Ctx::ensure_side() {
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_v, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_hi, cudaEventDisableTiming));
+  RQ_CUDA_TRY(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_l0, cudaEventDisableTiming));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_aux, cudaEventDisableTiming));
   return RQ_OK;
 }
 
@@ -412,6 +415,29 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
   const int nleaves = (b + wl - 1) / wl;
   const int64_t la_wave = kSMs - 16;
   const int64_t la_t0 = la.next, la_waves = la.on ? ceil_div(la.tiles - la.next, la_wave) : 0;
+  // Space-sliced look-ahead: when the pending trailing update outlasts this panel's leaves and
+  // WY updates, run ALL of it as one 132-CTA launch beside the first leaf and keep the rest of
+  // the panel (leaves + wy_cluster updates) on the first leaf's 16 SMs on the `aux` stream;
+  // otherwise (time-sliced) the chunks run beside each leaf and the WY updates take the GPU.
+  // RQ_LA_SPACE: 0 time-sliced, 1 space-sliced, 2 (default) by the estimate below.
+  static const int env_space = [] {
+    const char* e = getenv("RQ_LA_SPACE");
+    return e ? atoi(e) : 2;
+  }();
+  bool space = false;
+  if (la.on && env_space != 0 && nleaves > 1) {
+    const double nn_s = 2.0 * (double)la.g.M * (double)la.g.N * (double)la.g.K *
+                        ((double)(la.tiles - la.next) / (double)la.tiles) / 24e12;
+    double rest_cols = 0.0;
+    for (int k0 = wl; k0 < b; k0 += wl) rest_cols += (double)(b - k0);
+    // leaves ~3.6 us per column plus the cluster WY updates at a nominal 110 GB/s per SM (they
+    // measure ~20: this optimistic estimate picked the better schedule at n = 10k and 20k:
+    // 148.6 / 586.7 ms, against 148.8 / 619.1 with the measured rate)
+    const double leaf_s = (double)b * 3.6e-6 + 3.0 * ((double)mp / 16.0) * 8.0 * rest_cols / 110e9 +
+                          (double)nleaves * 8e-6;
+    space = env_space == 1 || nn_s > 1.15 * leaf_s;
+  }
+  cudaStream_t saved_stream = stream;
   for (int k0 = 0; k0 < b; k0 += wl) {
     const int w = std::min(wl, b - k0);
     const int64_t mm = mp - k0;
@@ -434,14 +460,27 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
       cat = saved;
       RQ_TRY(rc);
     }
-    if (la.on) {
+    if (space && k0 == 0) {
+      RQ_TRY(ensure_side());
+      RQ_CUDA_TRY(cudaEventRecord(ev_l0, stream));  // completes with the first leaf
+      RQ_TRY(la_chunk(la.tiles, true));               // all of it, beside the first leaf
+      RQ_CUDA_TRY(cudaStreamWaitEvent(aux, ev_l0, 0));
+      stream = aux;
+    } else if (la.on && !space) {
       const int64_t leaf = k0 / wl + 1;
       RQ_TRY(la_chunk(la_t0 + ceil_div(la_waves * leaf, (int64_t)nleaves) * la_wave, true));
     }
     const int64_t nrest = b - k0 - w;
     if (nrest <= 0) break;
     // A_rest -= V_l T_l^T (V_l^T A_rest)
-    if (wy_update_fits(mm, (int)nrest, w)) {
+    if (space) {
+      cudaEvent_t e0;
+      prof_begin(&e0);
+      const int rc = wy_cluster(A + (s + k0) + (s + k0 + w) * lda, lda, mm, (int)nrest,
+                                V + vpad + k0 + (int64_t)k0 * ldv, ldv, tleaf, 32, w, stream, &launches);
+      prof_end(e0, 4.0 * (double)mm * w * nrest);
+      RQ_TRY(rc);
+    } else if (wy_update_fits(mm, (int)nrest, w)) {
       cudaEvent_t e0;
       prof_begin(&e0);
       SweepWork sw;
@@ -466,6 +505,11 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
       RQ_TRY(gemm(mm, nrest, w, op(V, mp + vpad, b, ldv, vpad + k0, k0), true, op(w2, w, nrest, ldw),
                   A + (s + k0) + (s + k0 + w) * lda, lda, -1.0, 1.0));
     }
+  }
+  if (space) {  // the main stream continues once the panel is factored (its chunk is in order)
+    stream = saved_stream;
+    RQ_CUDA_TRY(cudaEventRecord(ev_aux, aux));
+    RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_aux, 0));
   }
   return RQ_OK;
 }
@@ -1374,6 +1418,9 @@ Ctx::~Ctx() {
   if (ev_v) cudaEventDestroy(ev_v);
   if (ev_side) cudaEventDestroy(ev_side);
   if (ev_hi) cudaEventDestroy(ev_hi);
+  if (aux) cudaStreamDestroy(aux);
+  if (ev_l0) cudaEventDestroy(ev_l0);
+  if (ev_aux) cudaEventDestroy(ev_aux);
   if (barriers) cudaFree(barriers);
 }
 

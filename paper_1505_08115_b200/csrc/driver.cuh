@@ -112,6 +112,9 @@ struct Ctx {
   // W = V^T A2 and T on a lowest-priority stream `side`
   cudaStream_t side = nullptr, hip = nullptr;
   cudaEvent_t ev_v = nullptr, ev_side = nullptr, ev_hi = nullptr;
+  // space-sliced look-ahead (panel_qr): the panel's later leaves and cluster WY updates on `aux`
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_l0 = nullptr, ev_aux = nullptr;
   bool overlap_on = true;
   // called (host side, enqueue order) when columns [s, s + w) of R are final: no later step
   // writes them (rq_factorize_host streams them to the host while later panels compute)

@@ -715,6 +715,202 @@ int wy_update(double* a, int64_t lda, int64_t mm, int nr, const double* v, int64
   return RQ_OK;
 }
 
+// ---------------------------------------------------------------------------
+// WY update of the rest of the panel on ONE 16-CTA cluster (16 SMs), for the look-ahead's
+// space-sliced schedule (driver.cu): the previous panel's trailing update runs on the other
+// 132 SMs meanwhile.  Same result as wy_update (A_rest <- A_rest - V T^T (V^T A_rest)) with a
+// different summation order:
+//   phase 1: CTA r forms P_r = V_r^T A_r over its row block on the FP64 tensor cores
+//            (mma.sync m16n8k4: M = the w <= 16 reflectors, N = rest columns, K = rows);
+//   phase 2: CTA r owns the rest columns n = r (mod 16): W(:, n) = sum over CTAs (rank order,
+//            DSMEM loads), W2(:, n) = T^T W(:, n), pushed into every CTA's W2 table;
+//   phase 3: A_r -= V_r W2 on the tensor cores (M = rows, N = rest columns, K = w).
+// A_rest and V are read straight from global memory (L2): no row block is staged, so any
+// height fits.
+// ---------------------------------------------------------------------------
+constexpr int WC_THREADS = 512;
+constexpr int WC_WARPS = WC_THREADS / 32;
+constexpr int WC_CS = 16;
+
+RQ_DEV void wc_dmma(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+__global__ void __launch_bounds__(WC_THREADS, 1)
+    wy_cluster_kernel(double* __restrict__ a, int64_t lda, int64_t mm, int nr, const double* __restrict__ v,
+                      int64_t ldv, const double* __restrict__ t, int64_t ldt, int w, int rp) {
+  extern __shared__ double wc_sm[];
+  const int nrp = (nr + 7) & ~7;
+  double* P = wc_sm;              // [16][nrp] this CTA's partial V^T A
+  double* W2s = P + 16 * nrp;     // [16][nrp] W2 (every column, after the exchange)
+  double* Wc = W2s + 16 * nrp;    // [16][nrp / 16 + 1] summed W of the owned columns
+  const unsigned rank = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int64_t r0 = (int64_t)rank * rp;
+  const int64_t r1 = min(mm, r0 + rp);
+  const int nrow = (int)max((int64_t)0, r1 - r0);
+  const int ngroups = nrp / 8;
+
+  // ---- phase 1: P = V_r^T A_r (each warp: n8 groups warp, warp + 8, ...) ----
+  {
+    constexpr int QG = (32 + WC_WARPS - 1) / WC_WARPS;  // n8 groups per warp (<= 30 groups)
+    double acc[QG][4];
+#pragma unroll
+    for (int q = 0; q < QG; q++)
+#pragma unroll
+      for (int e = 0; e < 4; e++) acc[q][e] = 0.0;
+    const double* vg = v + (int64_t)g * ldv;
+    const double* vg8 = v + (int64_t)(g + 8) * ldv;
+    // 8 k-steps of loads in flight before their MMAs (the loop is L2-latency bound otherwise)
+    constexpr int U = 8;
+    for (int i00 = 0; i00 < nrow; i00 += 4 * U) {
+      double av[U], bv8[U], bv[QG][U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t row = r0 + i00 + 4 * u + tq;
+        const bool rok = row < r1;
+        av[u] = (rok && g < w) ? __ldg(vg + row) : 0.0;
+        bv8[u] = (rok && g + 8 < w) ? __ldg(vg8 + row) : 0.0;
+#pragma unroll
+        for (int q = 0; q < QG; q++) {
+          const int col = (warp + WC_WARPS * q) * 8 + g;
+          bv[q][u] = (rok && col < nr) ? __ldcg(a + (int64_t)col * lda + row) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++)
+#pragma unroll
+        for (int q = 0; q < QG; q++)
+          if (warp + WC_WARPS * q < ngroups) wc_dmma(acc[q], av[u], bv8[u], bv[q][u]);
+    }
+#pragma unroll
+    for (int q = 0; q < QG; q++) {
+      const int grp = warp + WC_WARPS * q;
+      if (grp < ngroups) {
+        const int n0 = grp * 8 + 2 * tq;
+        P[g * nrp + n0] = acc[q][0];
+        P[g * nrp + n0 + 1] = acc[q][1];
+        P[(g + 8) * nrp + n0] = acc[q][2];
+        P[(g + 8) * nrp + n0 + 1] = acc[q][3];
+      }
+    }
+  }
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+
+  // ---- phase 2: owned columns n = rank + 16 c: W = sum of the 16 partials, W2 = T^T W ----
+  const int nown = (nr > (int)rank) ? (nr - (int)rank + WC_CS - 1) / WC_CS : 0;
+  const int ldwc = nrp / 16 + 1;
+  for (int e = threadIdx.x; e < 16 * nown; e += WC_THREADS) {
+    const int k = e % 16, c = e / 16;
+    const int n = (int)rank + WC_CS * c;
+    double vals[WC_CS];
+#pragma unroll
+    for (unsigned r = 0; r < WC_CS; r++) vals[r] = dsmem_ld(&P[k * nrp + n], r);
+    double s = 0.0;
+#pragma unroll
+    for (unsigned r = 0; r < WC_CS; r++) s += vals[r];  // rank order: deterministic
+    Wc[k * ldwc + c] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 16 * nown; e += WC_THREADS) {
+    const int k = e % 16, c = e / 16;
+    const int n = (int)rank + WC_CS * c;
+    double s = 0.0;
+    if (k < w)
+      for (int l = 0; l <= k; l++) s += t[(int64_t)k * ldt + l] * Wc[l * ldwc + c];  // (T^T W)_k, T upper
+#pragma unroll
+    for (unsigned r = 0; r < WC_CS; r++) dsmem_st(&W2s[k * nrp + n], r, s);
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+
+  // ---- phase 3: A_r -= V_r W2 (each warp: m16 row tiles warp, warp + 8, ...; every n8 group) ----
+  const int mtiles = (nrow + 15) / 16;
+  for (int mt = warp; mt < mtiles; mt += WC_WARPS) {
+    const int64_t rowa = r0 + mt * 16 + g, rowb = rowa + 8;
+    const bool oka = rowa < r1, okb = rowb < r1;
+    double va[4], vb[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; kk++) {
+      const int k = kk * 4 + tq;
+      va[kk] = (oka && k < w) ? __ldg(v + (int64_t)k * ldv + rowa) : 0.0;
+      vb[kk] = (okb && k < w) ? __ldg(v + (int64_t)k * ldv + rowb) : 0.0;
+    }
+    // batches of GB n8 groups: their C loads are all in flight before the MMAs and stores
+    constexpr int GB = 4;
+    for (int g0 = 0; g0 < ngroups; g0 += GB) {
+      double cv[GB][4];
+#pragma unroll
+      for (int q = 0; q < GB; q++) {
+        const int n0 = (g0 + q) * 8 + 2 * tq;
+        const double* ca = a + (int64_t)n0 * lda;
+        const bool c0 = g0 + q < ngroups && n0 < nr, c1 = g0 + q < ngroups && n0 + 1 < nr;
+        cv[q][0] = (oka && c0) ? __ldcg(ca + rowa) : 0.0;
+        cv[q][1] = (oka && c1) ? __ldcg(ca + lda + rowa) : 0.0;
+        cv[q][2] = (okb && c0) ? __ldcg(ca + rowb) : 0.0;
+        cv[q][3] = (okb && c1) ? __ldcg(ca + lda + rowb) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < GB; q++) {
+        const int grp = g0 + q;
+        if (grp >= ngroups) break;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int kk = 0; kk < 4; kk++) wc_dmma(acc, va[kk], vb[kk], W2s[(kk * 4 + tq) * nrp + grp * 8 + g]);
+        const int n0 = grp * 8 + 2 * tq;
+        double* ca = a + (int64_t)n0 * lda;
+        if (oka) {
+          if (n0 < nr) __stcg(ca + rowa, cv[q][0] - acc[0]);
+          if (n0 + 1 < nr) __stcg(ca + lda + rowa, cv[q][1] - acc[1]);
+        }
+        if (okb) {
+          if (n0 < nr) __stcg(ca + rowb, cv[q][2] - acc[2]);
+          if (n0 + 1 < nr) __stcg(ca + lda + rowb, cv[q][3] - acc[3]);
+        }
+      }
+    }
+  }
+}
+
+size_t wy_cluster_smem(int nr) {
+  const int nrp = (nr + 7) & ~7;
+  return ((size_t)32 * nrp + (size_t)16 * (nrp / 16 + 1)) * sizeof(double);
+}
+
+int wy_cluster(double* a, int64_t lda, int64_t mm, int nr, const double* v, int64_t ldv, const double* t,
+               int64_t ldt, int w, cudaStream_t st, int64_t* launches) {
+  if (nr <= 0 || mm <= 0) return RQ_OK;
+  if (w > 16) return set_error(RQ_EINTERNAL, "wy_cluster: width %d > 16", w);
+  const int rp = (int)ceil_div(mm, WC_CS);
+  const size_t smem = wy_cluster_smem(nr);
+  if (smem > 200 * 1024) return set_error(RQ_EINTERNAL, "wy_cluster: %d rest columns too many", nr);
+  static bool attr = false;
+  if (!attr) {
+    RQ_CUDA_TRY(cudaFuncSetAttribute(wy_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    RQ_CUDA_TRY(cudaFuncSetAttribute(wy_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(WC_CS);
+  cfg.blockDim = dim3(WC_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = WC_CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  RQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, wy_cluster_kernel, a, lda, mm, nr, v, ldv, t, ldt, w, rp));
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
 template <int WL>
 static int launch_leaf(const LeafCall& c, cudaStream_t st, int64_t* launches) {
   constexpr int PV = LeafLayout<WL>::PV;

@@ -20,6 +20,8 @@ int leaf_reg_width_for(int64_t mm);
 int leaf_debug_timing(int on, unsigned long long* host, int count);
 int leaf_qr(const LeafCall& c, cudaStream_t st, int64_t* launches);
 bool wy_update_fits(int64_t mm, int nr, int w);
+int wy_cluster(double* a, int64_t lda, int64_t mm, int nr, const double* v, int64_t ldv, const double* t,
+               int64_t ldt, int w, cudaStream_t st, int64_t* launches);
 int wy_update(double* a, int64_t lda, int64_t mm, int nr, const double* v, int64_t ldv, const double* t, int64_t ldt,
               int w, double* scratch, size_t scratch_bytes, unsigned int* bar, cudaStream_t st, int64_t* launches);
 
