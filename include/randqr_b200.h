@@ -174,6 +174,11 @@ int rq_test_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K,
 int rq_test_sketch_cpqr(rq_ctx* ctx, double* dY, int64_t ld, int32_t m, int32_t n, int32_t steps, int32_t* dChosen);
 int rq_test_leaf_qr(rq_ctx* ctx, double* dA, int64_t lda, int64_t mm, int32_t w, double* dV, int64_t ldv,
                     double* dT, int64_t ldt);
+/* Test hook: A (mm x nr) <- A - V T^T (V^T A) for one leaf's w <= 16 reflectors V (mm x w) and
+ * T (w x w): cluster != 0 runs the 16-CTA cluster kernel (space-sliced look-ahead), 0 the
+ * whole-GPU cooperative kernel. */
+int rq_test_wy_update(rq_ctx* ctx, int32_t cluster, double* dA, int64_t lda, int64_t mm, int32_t nr, const double* dV,
+                      int64_t ldv, const double* dT, int64_t ldt, int32_t w);
 
 /* Test hook: per-phase clock64 stamps of the cluster sweep (first 64 steps, 8 per step). */
 int rq_test_debug_timing(int32_t on, uint64_t* host, int32_t count);

@@ -67,6 +67,7 @@ _SIGS = {
                                     _i64, _i64, _i64, _i64, _vp, _i64, ctypes.c_double, ctypes.c_double]),
     "rq_test_sketch_cpqr": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp]),
     "rq_test_leaf_qr": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i32, _vp, _i64, _vp, _i64]),
+    "rq_test_wy_update": (ctypes.c_int, [_vp, _i32, _vp, _i64, _i64, _i32, _vp, _i64, _vp, _i64, _i32]),
     "rq_test_debug_timing": (ctypes.c_int, [_i32, _vp, _i32]),
     "rq_launch_count": (_i64, [_vp]),
     "rq_set_profiling": (ctypes.c_int, [_vp, _i32]),

@@ -372,6 +372,21 @@ int rq_test_leaf_qr(rq_ctx* ctx, double* dA, int64_t lda, int64_t mm, int32_t w,
   return rq::leaf_qr(lc, ctx->c.stream, &ctx->c.launches);
 }
 
+int rq_test_wy_update(rq_ctx* ctx, int32_t cluster, double* dA, int64_t lda, int64_t mm, int32_t nr, const double* dV,
+                      int64_t ldv, const double* dT, int64_t ldt, int32_t w) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  Ctx& c = ctx->c;
+  if (cluster)
+    return rq::wy_cluster(dA, lda, mm, nr, 0, 0, mm, nr, dV, ldv, mm, w, 0, 0, dT, ldt, w, c.stream, &c.launches);
+  if (!rq::wy_update_fits(mm, nr, w)) return rq::set_error(RQ_EUNSUPPORTED, "wy_update does not fit");
+  const size_t kb = (size_t)rq::kSMs * 16 * 256 * 8 + 16 * 256 * 8;
+  RQ_TRY(c.qarena.reserve(kb));
+  RQ_CUDA_TRY(cudaMemsetAsync(c.barriers, 0, sizeof(unsigned) * 64, c.stream));
+  return rq::wy_update(dA, lda, mm, nr, dV, ldv, dT, ldt, w, (double*)c.qarena.base, kb, c.barriers, c.stream,
+                       &c.launches);
+}
+
 int rq_test_debug_timing(int32_t on, uint64_t* host, int32_t count) {
   // on: 1 = cluster/sketch sweeps, 2 = panel leaf
   if (on == 2 || (on == 0 && count < 0)) return rq::leaf_debug_timing(on == 2, (unsigned long long*)host, -count);

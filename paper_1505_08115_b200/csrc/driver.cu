@@ -476,8 +476,8 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
     if (space) {
       cudaEvent_t e0;
       prof_begin(&e0);
-      const int rc = wy_cluster(A + (s + k0) + (s + k0 + w) * lda, lda, mm, (int)nrest,
-                                V + vpad + k0 + (int64_t)k0 * ldv, ldv, tleaf, 32, w, stream, &launches);
+      const int rc = wy_cluster(A, lda, m, n, s + k0, s + k0 + w, mm, (int)nrest, V, ldv, mp + vpad, b, vpad + k0, k0,
+                                tleaf, 32, w, stream, &launches);
       prof_end(e0, 4.0 * (double)mm * w * nrest);
       RQ_TRY(rc);
     } else if (wy_update_fits(mm, (int)nrest, w)) {

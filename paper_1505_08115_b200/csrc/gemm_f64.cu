@@ -440,6 +440,13 @@ static int make_map(CUtensorMap* map, const GemmOperand& op, uint32_t box0, uint
   return RQ_OK;
 }
 
+int make_tensor_map_f64(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box0,
+                        int box1, bool swizzle) {
+  RQ_TRY(get_encoder());
+  GemmOperand o{base, rows, cols, ld, 0, 0};
+  return make_map(map, o, (uint32_t)box0, (uint32_t)box1, swizzle);
+}
+
 static int num_sms() {
   static int sms = 0;
   if (sms == 0) {

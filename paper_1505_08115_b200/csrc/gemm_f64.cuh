@@ -47,6 +47,10 @@ struct GemmProblem {
 
 int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches);
 int64_t gemm_f64_tiles(const GemmProblem& p);
+// 2-D fp64 tensor map (rows contiguous, ld elements between columns), box box0 x box1,
+// optionally 128B-swizzled (box0 = 16 then); for kernels outside the GEMM (wy_cluster).
+int make_tensor_map_f64(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box0,
+                        int box1, bool swizzle);
 size_t gemm_splitk_workspace(int64_t M, int64_t N, int splitk);
 
 }  // namespace rq

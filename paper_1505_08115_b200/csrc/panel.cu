@@ -16,6 +16,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "gemm_f64.cuh"
 #include "panel.cuh"
 
 namespace cg = cooperative_groups;
@@ -739,53 +740,122 @@ RQ_DEV void wc_dmma(double (&c)[4], double a0, double a1, double b0) {
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
+// Row chunks of A_r (16 rows x all rest columns, one TMA box, 128B-swizzled) stream through
+// WC_STAGES shared-memory stages; thread 0 issues the boxes and mbarriers track them, so no
+// thread spends issue slots on addresses (per-element cp.async / loads left the kernel at
+// ~20 GB/s per SM).  V_r fragments come from global memory (L1).
+constexpr int WC_RC = 16;      // rows per chunk = one 128B swizzle row per column
+constexpr int WC_STAGES = 4;
+
+RQ_DEV void wc_mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+}
+RQ_DEV void wc_mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WCW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WCW_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+RQ_DEV void wc_tma(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+// element (row k of the chunk, column c) of a 128B-swizzled [column][16] chunk
+RQ_DEV double wc_ld(const double* tile, int c, int k) {
+  return *reinterpret_cast<const double*>(reinterpret_cast<const char*>(tile) + c * 128 +
+                                          ((((k >> 1) ^ (c & 7))) << 4) + ((k & 1) << 3));
+}
+
 __global__ void __launch_bounds__(WC_THREADS, 1)
-    wy_cluster_kernel(double* __restrict__ a, int64_t lda, int64_t mm, int nr, const double* __restrict__ v,
-                      int64_t ldv, const double* __restrict__ t, int64_t ldt, int w, int rp) {
-  extern __shared__ double wc_sm[];
+    wy_cluster_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmV,
+                      double* __restrict__ a, int64_t lda, int64_t mm, int nr, int64_t grow0, int64_t gcol0,
+                      int64_t vrow0, int64_t vcol0, const double* __restrict__ t, int64_t ldt, int w, int rp) {
+  extern __shared__ unsigned char wc_raw[];
+  // 1024-B aligned stages (the 128B swizzle pattern repeats every 1 KB)
+  const uint32_t mis = (uint32_t)__cvta_generic_to_shared(wc_raw) & 1023u;
+  unsigned char* base = wc_raw + ((1024u - mis) & 1023u);
   const int nrp = (nr + 7) & ~7;
-  double* P = wc_sm;              // [16][nrp] this CTA's partial V^T A
-  double* W2s = P + 16 * nrp;     // [16][nrp] W2 (every column, after the exchange)
-  double* Wc = W2s + 16 * nrp;    // [16][nrp / 16 + 1] summed W of the owned columns
+  const uint32_t a_bytes = (uint32_t)nrp * 128u;
+  const uint32_t stage_bytes = a_bytes + 16u * 128u;                        // A box + V box
+  double* stA = reinterpret_cast<double*>(base);  // [WC_STAGES] x {A [nrp][16], V [16][16]} (swizzled)
+  double* P = reinterpret_cast<double*>(base + WC_STAGES * stage_bytes);    // [16][nrp]
+  double* W2s = P + 16 * nrp;                                               // [16][nrp]
+  double* Wc = W2s + 16 * nrp;                                              // [16][nrp / 16 + 1]
+  __shared__ __align__(8) uint64_t full[WC_STAGES];
   const unsigned rank = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int64_t r0 = (int64_t)rank * rp;
   const int64_t r1 = min(mm, r0 + rp);
   const int nrow = (int)max((int64_t)0, r1 - r0);
+  const int shift = (int)((grow0 + r0) & 1);  // chunk boxes start at an even global row
+  const int64_t cbase = r0 - shift;           // relative row of chunk 0's first row
+  const int nchunks = nrow > 0 ? (nrow + shift + WC_RC - 1) / WC_RC : 0;
   const int ngroups = nrp / 8;
+  constexpr int QG = (32 + WC_WARPS - 1) / WC_WARPS;  // n8 groups per warp (<= 30 groups)
+  if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < WC_STAGES; s2++) wc_mbar_init(&full[s2]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // load number q (phase 1: q = c, phase 3: q = nchunks + c) of chunk c goes to stage q % WC_STAGES;
+  // that stage's barrier completes for the (q / WC_STAGES)-th time
+  auto issue = [&](int q, int c) {
+    double* st = stA + (size_t)(q % WC_STAGES) * (stage_bytes / 8);
+    uint64_t* bar = &full[q % WC_STAGES];
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(stage_bytes)
+                 : "memory");
+    const int rr = (int)(cbase + c * WC_RC);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(st)),
+        "l"(&tmA), "r"(smem_u32(bar)), "r"((int)(grow0 + rr)), "r"((int)gcol0)
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(st + nrp * 16)),
+        "l"(&tmV), "r"(smem_u32(bar)), "r"((int)(vrow0 + rr)), "r"((int)vcol0)
+        : "memory");
+  };
 
-  // ---- phase 1: P = V_r^T A_r (each warp: n8 groups warp, warp + 8, ...) ----
+  // ---- phase 1: P = V_r^T A_r (each warp: n8 groups warp, warp + WC_WARPS, ...) ----
   {
-    constexpr int QG = (32 + WC_WARPS - 1) / WC_WARPS;  // n8 groups per warp (<= 30 groups)
     double acc[QG][4];
 #pragma unroll
     for (int q = 0; q < QG; q++)
 #pragma unroll
       for (int e = 0; e < 4; e++) acc[q][e] = 0.0;
-    const double* vg = v + (int64_t)g * ldv;
-    const double* vg8 = v + (int64_t)(g + 8) * ldv;
-    // 8 k-steps of loads in flight before their MMAs (the loop is L2-latency bound otherwise)
-    constexpr int U = 8;
-    for (int i00 = 0; i00 < nrow; i00 += 4 * U) {
-      double av[U], bv8[U], bv[QG][U];
+    if (threadIdx.x == 0)
+      for (int c = 0; c < WC_STAGES && c < nchunks; c++) issue(c, c);
+    for (int c = 0; c < nchunks; c++) {
+      wc_mbar_wait(&full[c % WC_STAGES], (c / WC_STAGES) & 1);
+      const double* As = stA + (size_t)(c % WC_STAGES) * (stage_bytes / 8);
+      const double* Vs = As + nrp * 16;  // [reflector column][16 rows]
 #pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int64_t row = r0 + i00 + 4 * u + tq;
-        const bool rok = row < r1;
-        av[u] = (rok && g < w) ? __ldg(vg + row) : 0.0;
-        bv8[u] = (rok && g + 8 < w) ? __ldg(vg8 + row) : 0.0;
+      for (int kk = 0; kk < 4; kk++) {
+        const int k = kk * 4 + tq;                       // chunk row
+        const int64_t row = cbase + c * WC_RC + k;       // relative to A_rest row 0
+        const bool rok = row >= r0 && row < r1;          // (the box also holds neighbours' rows)
+        const double a0 = (rok && g < w) ? wc_ld(Vs, g, k) : 0.0;
+        const double a1 = (rok && g + 8 < w) ? wc_ld(Vs, g + 8, k) : 0.0;
 #pragma unroll
         for (int q = 0; q < QG; q++) {
-          const int col = (warp + WC_WARPS * q) * 8 + g;
-          bv[q][u] = (rok && col < nr) ? __ldcg(a + (int64_t)col * lda + row) : 0.0;
+          const int grp = warp + WC_WARPS * q;
+          if (grp < ngroups) wc_dmma(acc[q], a0, a1, wc_ld(As, grp * 8 + g, k));
         }
       }
-#pragma unroll
-      for (int u = 0; u < U; u++)
-#pragma unroll
-        for (int q = 0; q < QG; q++)
-          if (warp + WC_WARPS * q < ngroups) wc_dmma(acc[q], av[u], bv8[u], bv[q][u]);
+      __syncthreads();  // every warp is done with this stage
+      if (threadIdx.x == 0 && c + WC_STAGES < nchunks) issue(c + WC_STAGES, c + WC_STAGES);
     }
 #pragma unroll
     for (int q = 0; q < QG; q++) {
@@ -799,6 +869,9 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       }
     }
   }
+  // phase 3's first chunks load while the cluster exchanges W
+  if (threadIdx.x == 0)
+    for (int c = 0; c < WC_STAGES && c < nchunks; c++) issue(nchunks + c, c);
   __syncthreads();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 
@@ -828,70 +901,69 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   }
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 
-  // ---- phase 3: A_r -= V_r W2 (each warp: m16 row tiles warp, warp + 8, ...; every n8 group) ----
-  const int mtiles = (nrow + 15) / 16;
-  for (int mt = warp; mt < mtiles; mt += WC_WARPS) {
-    const int64_t rowa = r0 + mt * 16 + g, rowb = rowa + 8;
-    const bool oka = rowa < r1, okb = rowb < r1;
+  // ---- phase 3: A_r -= V_r W2, chunk by chunk (each warp: its n8 groups of the 16-row chunk) ----
+  for (int c = 0; c < nchunks; c++) {
+    const int q = nchunks + c;
+    const int64_t rowa = cbase + c * WC_RC + g, rowb = rowa + 8;  // relative to A_rest row 0
+    const bool oka = rowa >= r0 && rowa < r1, okb = rowb >= r0 && rowb < r1;
+    wc_mbar_wait(&full[q % WC_STAGES], (q / WC_STAGES) & 1);
+    const double* As = stA + (size_t)(q % WC_STAGES) * (stage_bytes / 8);
+    const double* Vs = As + nrp * 16;
     double va[4], vb[4];
 #pragma unroll
     for (int kk = 0; kk < 4; kk++) {
       const int k = kk * 4 + tq;
-      va[kk] = (oka && k < w) ? __ldg(v + (int64_t)k * ldv + rowa) : 0.0;
-      vb[kk] = (okb && k < w) ? __ldg(v + (int64_t)k * ldv + rowb) : 0.0;
+      va[kk] = (k < w) ? wc_ld(Vs, k, g) : 0.0;
+      vb[kk] = (k < w) ? wc_ld(Vs, k, g + 8) : 0.0;
     }
-    // batches of GB n8 groups: their C loads are all in flight before the MMAs and stores
-    constexpr int GB = 4;
-    for (int g0 = 0; g0 < ngroups; g0 += GB) {
-      double cv[GB][4];
 #pragma unroll
-      for (int q = 0; q < GB; q++) {
-        const int n0 = (g0 + q) * 8 + 2 * tq;
-        const double* ca = a + (int64_t)n0 * lda;
-        const bool c0 = g0 + q < ngroups && n0 < nr, c1 = g0 + q < ngroups && n0 + 1 < nr;
-        cv[q][0] = (oka && c0) ? __ldcg(ca + rowa) : 0.0;
-        cv[q][1] = (oka && c1) ? __ldcg(ca + lda + rowa) : 0.0;
-        cv[q][2] = (okb && c0) ? __ldcg(ca + rowb) : 0.0;
-        cv[q][3] = (okb && c1) ? __ldcg(ca + lda + rowb) : 0.0;
+    for (int q = 0; q < QG; q++) {
+      const int grp = warp + WC_WARPS * q;
+      if (grp >= ngroups) break;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int kk = 0; kk < 4; kk++) wc_dmma(acc, va[kk], vb[kk], W2s[(kk * 4 + tq) * nrp + grp * 8 + g]);
+      const int n0 = grp * 8 + 2 * tq;
+      double* ca = a + (int64_t)n0 * lda;
+      if (oka) {
+        if (n0 < nr) __stcg(ca + rowa, wc_ld(As, n0, g) - acc[0]);
+        if (n0 + 1 < nr) __stcg(ca + lda + rowa, wc_ld(As, n0 + 1, g) - acc[1]);
       }
-#pragma unroll
-      for (int q = 0; q < GB; q++) {
-        const int grp = g0 + q;
-        if (grp >= ngroups) break;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int kk = 0; kk < 4; kk++) wc_dmma(acc, va[kk], vb[kk], W2s[(kk * 4 + tq) * nrp + grp * 8 + g]);
-        const int n0 = grp * 8 + 2 * tq;
-        double* ca = a + (int64_t)n0 * lda;
-        if (oka) {
-          if (n0 < nr) __stcg(ca + rowa, cv[q][0] - acc[0]);
-          if (n0 + 1 < nr) __stcg(ca + lda + rowa, cv[q][1] - acc[1]);
-        }
-        if (okb) {
-          if (n0 < nr) __stcg(ca + rowb, cv[q][2] - acc[2]);
-          if (n0 + 1 < nr) __stcg(ca + lda + rowb, cv[q][3] - acc[3]);
-        }
+      if (okb) {
+        if (n0 < nr) __stcg(ca + rowb, wc_ld(As, n0, g + 8) - acc[2]);
+        if (n0 + 1 < nr) __stcg(ca + lda + rowb, wc_ld(As, n0 + 1, g + 8) - acc[3]);
       }
     }
+    __syncthreads();
+    if (threadIdx.x == 0 && c + WC_STAGES < nchunks) issue(q + WC_STAGES, c + WC_STAGES);
   }
 }
 
 size_t wy_cluster_smem(int nr) {
   const int nrp = (nr + 7) & ~7;
-  return ((size_t)32 * nrp + (size_t)16 * (nrp / 16 + 1)) * sizeof(double);
+  return 1024 + (size_t)WC_STAGES * (nrp * 128 + 2048) +
+         ((size_t)32 * nrp + (size_t)16 * (nrp / 16 + 1)) * sizeof(double);
 }
 
-int wy_cluster(double* a, int64_t lda, int64_t mm, int nr, const double* v, int64_t ldv, const double* t,
-               int64_t ldt, int w, cudaStream_t st, int64_t* launches) {
+int wy_cluster(double* A, int64_t lda, int64_t m_total, int64_t n_total, int64_t row0, int64_t col0, int64_t mm,
+               int nr, const double* Vb, int64_t ldv, int64_t v_rows, int64_t v_cols, int64_t vrow0, int64_t vcol0,
+               const double* t, int64_t ldt, int w, cudaStream_t st, int64_t* launches) {
   if (nr <= 0 || mm <= 0) return RQ_OK;
   if (w > 16) return set_error(RQ_EINTERNAL, "wy_cluster: width %d > 16", w);
-  const int rp = (int)ceil_div(mm, WC_CS);
+  const int nrp = (nr + 7) & ~7;
+  if (nrp > 256) return set_error(RQ_EINTERNAL, "wy_cluster: %d rest columns > 256", nr);
+  // rows per CTA: even, so every CTA's first row has the parity of row0
+  const int rp = (int)((ceil_div(mm, WC_CS) + 1) & ~int64_t(1));
   const size_t smem = wy_cluster_smem(nr);
-  if (smem > 200 * 1024) return set_error(RQ_EINTERNAL, "wy_cluster: %d rest columns too many", nr);
+  if (smem > 220 * 1024) return set_error(RQ_EINTERNAL, "wy_cluster: %d rest columns too many", nr);
+  if (((row0 ^ vrow0) & 1) != 0) return set_error(RQ_EINTERNAL, "wy_cluster: A and V row origins differ in parity");
+  CUtensorMap map, vmap;
+  RQ_TRY(make_tensor_map_f64(&map, A, m_total, n_total, lda, 16, nrp, true));
+  RQ_TRY(make_tensor_map_f64(&vmap, Vb, v_rows, v_cols, ldv, 16, 16, true));
   static bool attr = false;
   if (!attr) {
     RQ_CUDA_TRY(cudaFuncSetAttribute(wy_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    RQ_CUDA_TRY(cudaFuncSetAttribute(wy_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    RQ_CUDA_TRY(cudaFuncSetAttribute(wy_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -906,7 +978,9 @@ int wy_cluster(double* a, int64_t lda, int64_t mm, int nr, const double* v, int6
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  RQ_CUDA_TRY(cudaLaunchKernelEx(&cfg, wy_cluster_kernel, a, lda, mm, nr, v, ldv, t, ldt, w, rp));
+  double* a = A + row0 + col0 * lda;
+  RQ_CUDA_TRY(
+      cudaLaunchKernelEx(&cfg, wy_cluster_kernel, map, vmap, a, lda, mm, nr, row0, col0, vrow0, vcol0, t, ldt, w, rp));
   if (launches) (*launches)++;
   return RQ_OK;
 }

@@ -225,3 +225,31 @@ if "prof" in which:
                                       ctypes.c_void_p(ch.data_ptr())))
     torch.cuda.synchronize()
     print("prof ok")
+
+if "wy" in which:
+    # WY update of one leaf (w = 16) on the rest of the panel: whole-GPU kernel vs 16-CTA cluster
+    for (mm, nr) in [(20000, 240), (20000, 120), (10000, 240), (10000, 120), (40000, 120)]:
+        w = 16
+        a0 = torch.randn((nr, mm + (mm & 1)), dtype=torch.float64, device=eng.device)
+        vv = torch.randn((w, mm + (mm & 1)), dtype=torch.float64, device=eng.device) / mm ** 0.5
+        tt = torch.triu(torch.randn((32, 32), dtype=torch.float64, device=eng.device)).T.contiguous()
+        work = a0.clone()
+        res = {}
+        for cl in (0, 1):
+            def run():
+                check(lib.rq_test_wy_update(eng.handle, cl, ctypes.c_void_p(work.data_ptr()), mm + (mm & 1), mm, nr,
+                                            ctypes.c_void_p(vv.data_ptr()), mm + (mm & 1),
+                                            ctypes.c_void_p(tt.data_ptr()), 32, w))
+            try:
+                work.copy_(a0)
+                run()
+                torch.cuda.synchronize()
+                res[cl] = work.clone()
+                ms = timeit(run, reps=5)
+                gb = 3.0 * mm * nr * 8 / 1e9
+                print(f"wy {'cluster' if cl else 'grid   '} mm={mm} nr={nr}: {ms*1e3:7.1f} us  {gb/(ms*1e-3):6.0f} GB/s")
+            except Exception as e:
+                print(f"wy cl={cl} mm={mm} nr={nr}: {e}")
+        if 0 in res and 1 in res:
+            ref = a0.clone()
+            print("   max |grid - cluster| / max|A|:", float((res[0] - res[1]).abs().max() / a0.abs().max()))
