@@ -779,7 +779,11 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
           // the CPQR holds 16 SMs for ~b * 2.7 us: the first n_a columns of W run capped beside
           // it, the rest (launched once those finish) on the whole GPU
           CatGuard g(cat, PROF_TRAIL);
-          const double cpqr_s = (double)b * 2.7e-6, rate = 24e12;  // measured CPQR step, capped DMMA rate
+          // measured b x b CPQR step (2.26 us at b = 256) and capped DMMA rate; RQ_CPQR_US /
+          // RQ_CAPPED_TF override them (tuning)
+          static const double env_us = getenv("RQ_CPQR_US") ? atof(getenv("RQ_CPQR_US")) : 2.7;
+          static const double env_tf = getenv("RQ_CAPPED_TF") ? atof(getenv("RQ_CAPPED_TF")) : 24.0;
+          const double cpqr_s = (double)b * env_us * 1e-6, rate = env_tf * 1e12;
           int64_t n_a = (int64_t)(cpqr_s * rate / (2.0 * b * (double)mp));
           n_a = std::max<int64_t>(128, (n_a + 127) / 128 * 128);
           if (n_a >= n2 - 256) n_a = n2;
