@@ -788,9 +788,12 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
   const uint32_t a_bytes = (uint32_t)nrp * 128u;
   const uint32_t stage_bytes = a_bytes + 16u * 128u;                        // A box + V box
   double* stA = reinterpret_cast<double*>(base);  // [WC_STAGES] x {A [nrp][16], V [16][16]} (swizzled)
-  double* P = reinterpret_cast<double*>(base + WC_STAGES * stage_bytes);    // [16][nrp]
-  double* W2s = P + 16 * nrp;                                               // [16][nrp]
-  double* Wc = W2s + 16 * nrp;                                              // [16][nrp / 16 + 1]
+  // P and W2 rows padded to ldq = nrp + 4 (= 4 mod 16 doubles): the fragment reads of lanes
+  // (g, tq) at row tq, column g hit distinct bank pairs (nrp = 0 mod 16 gave 4-way conflicts)
+  const int ldq = nrp + 4;
+  double* P = reinterpret_cast<double*>(base + WC_STAGES * stage_bytes);    // [16][ldq]
+  double* W2s = P + 16 * ldq;                                               // [16][ldq]
+  double* Wc = W2s + 16 * ldq;                                              // [16][nrp / 16 + 1]
   __shared__ __align__(8) uint64_t full[WC_STAGES];
   const unsigned rank = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -862,10 +865,10 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       const int grp = warp + WC_WARPS * q;
       if (grp < ngroups) {
         const int n0 = grp * 8 + 2 * tq;
-        P[g * nrp + n0] = acc[q][0];
-        P[g * nrp + n0 + 1] = acc[q][1];
-        P[(g + 8) * nrp + n0] = acc[q][2];
-        P[(g + 8) * nrp + n0 + 1] = acc[q][3];
+        P[g * ldq + n0] = acc[q][0];
+        P[g * ldq + n0 + 1] = acc[q][1];
+        P[(g + 8) * ldq + n0] = acc[q][2];
+        P[(g + 8) * ldq + n0 + 1] = acc[q][3];
       }
     }
   }
@@ -883,7 +886,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
     const int n = (int)rank + WC_CS * c;
     double vals[WC_CS];
 #pragma unroll
-    for (unsigned r = 0; r < WC_CS; r++) vals[r] = dsmem_ld(&P[k * nrp + n], r);
+    for (unsigned r = 0; r < WC_CS; r++) vals[r] = dsmem_ld(&P[k * ldq + n], r);
     double s = 0.0;
 #pragma unroll
     for (unsigned r = 0; r < WC_CS; r++) s += vals[r];  // rank order: deterministic
@@ -897,7 +900,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
     if (k < w)
       for (int l = 0; l <= k; l++) s += t[(int64_t)k * ldt + l] * Wc[l * ldwc + c];  // (T^T W)_k, T upper
 #pragma unroll
-    for (unsigned r = 0; r < WC_CS; r++) dsmem_st(&W2s[k * nrp + n], r, s);
+    for (unsigned r = 0; r < WC_CS; r++) dsmem_st(&W2s[k * ldq + n], r, s);
   }
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 
@@ -922,7 +925,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
       if (grp >= ngroups) break;
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int kk = 0; kk < 4; kk++) wc_dmma(acc, va[kk], vb[kk], W2s[(kk * 4 + tq) * nrp + grp * 8 + g]);
+      for (int kk = 0; kk < 4; kk++) wc_dmma(acc, va[kk], vb[kk], W2s[(kk * 4 + tq) * ldq + grp * 8 + g]);
       const int n0 = grp * 8 + 2 * tq;
       double* ca = a + (int64_t)n0 * lda;
       if (oka) {
@@ -942,7 +945,7 @@ __global__ void __launch_bounds__(WC_THREADS, 1)
 size_t wy_cluster_smem(int nr) {
   const int nrp = (nr + 7) & ~7;
   return 1024 + (size_t)WC_STAGES * (nrp * 128 + 2048) +
-         ((size_t)32 * nrp + (size_t)16 * (nrp / 16 + 1)) * sizeof(double);
+         ((size_t)32 * (nrp + 4) + (size_t)16 * (nrp / 16 + 1)) * sizeof(double);
 }
 
 int wy_cluster(double* A, int64_t lda, int64_t m_total, int64_t n_total, int64_t row0, int64_t col0, int64_t mm,
