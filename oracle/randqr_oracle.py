@@ -545,6 +545,13 @@ def block_qr_downdate(a, cfg, rng):
     after each panel Y2 <- Y2 - G1 R12 with G1 = Y1 R11^{-1}, the sketch
     columns following every column move.  Pivot selection, the two-stage panel
     and the trailing update are those of block_qr (blocked.py:175-219).
+
+    The downdate is evaluated in its pre-rotation form, as the B200 driver does
+    (driver.cu form_g1): with the panel's unpivoted R' (first stage of
+    qr_tall_pivoted), R11 = Q2^T R'11 P-hat and R12 = Q2^T R'12, so
+    G1 R12 = Y1' R'11^{-1} R'12 with Y1' the selected sketch columns before
+    P-hat -- the same product without Q2 or P-hat (they agree in exact
+    arithmetic; this restatement fixes the rounding the GPU path follows).
     """
     from scipy.linalg import solve_triangular
 
@@ -572,15 +579,16 @@ def block_qr_downdate(a, cfg, rng):
         pivot = select_pivot_permutation(yt[:, start:].T, b)
         work[:, start:] = pivot.apply_right(work[:, start:])
         yt[:, start:] = yt[:, start:][:, pivot.order]
+        # G1' = Y1' R'11^{-1} from the unpivoted first stage (see the docstring)
+        first = qr_unpivoted(work[start:, start: start + b])
+        g1 = solve_triangular(first.r[:b, :b].T, yt[:, start: start + b].T, lower=True).T
+        a2 = work[start:, start + b:].copy()
         res = qr_tall_pivoted(work[start:, start: start + b])
         work[:start, start: start + b] = work[:start, start: start + b][:, res.perm]
-        yt[:, start: start + b] = yt[:, start: start + b][:, res.perm]
         work[start:, start: start + b] = res.r
         work[start:, start + b:] = apply_wy_left(res.q, work[start:, start + b:], transposed=True)
-        r11 = work[start: start + b, start: start + b]
-        r12 = work[start: start + b, start + b:]
-        g1 = solve_triangular(r11.T, yt[:, start: start + b].T, lower=True).T  # Y1 R11^{-1}
-        yt[:, start + b:] -= g1 @ r12
+        r12p = apply_wy_left(wy_accumulate(first.refl, work.shape[0] - start), a2, transposed=True)[:b]  # R'12
+        yt[:, start + b:] -= g1 @ r12p
         f.q_transforms.append((start, res.q, None))
         f.p_transforms.append((start, pivot))
         f.p_transforms.append((start, PermPivot(res.perm)))

@@ -13,7 +13,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librandqr_b200.so")
+LIB_PATH = os.environ.get("RQ_LIB_PATH") or os.path.join(_HERE, "librandqr_b200.so")  # override: tuning builds
 
 RQ_OK, RQ_EDIM, RQ_EVALUE, RQ_ECONV, RQ_ECUDA, RQ_EINTERNAL, RQ_EUNSUPPORTED = range(7)
 RQ_PIVOT_PERMUTATION, RQ_PIVOT_REFLECTORS = 0, 1

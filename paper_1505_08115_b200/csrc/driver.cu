@@ -405,7 +405,8 @@ int Ctx::sweep_raw(SweepCall c) {
 // Panel QR of A[s:, s:s+b] (m' x b): leaf kernels + WY updates of the rest.
 // ---------------------------------------------------------------------------
 int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, double* V, int64_t ldv,
-                  int vpad, double* tleaf, double* w1, double* w2) {
+                  int vpad, double* tleaf, double* w1, double* w2, double* T, int64_t ldt, bool* t_done) {
+  if (t_done) *t_done = false;
   CatGuard guard(cat, PROF_PANEL_GEMM);
   int wl_max = leaf_reg_width_for(mp);
   if (wl_max == 0) wl_max = leaf_width_for(mp);
@@ -424,7 +425,7 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
     const char* e = getenv("RQ_LA_SPACE");
     return e ? atoi(e) : 2;
   }();
-  bool space = false;
+  bool space = false, t_on_aux = false;
   if (la.on && env_space != 0 && nleaves > 1) {
     const double nn_s = 2.0 * (double)la.g.M * (double)la.g.N * (double)la.g.K *
                         ((double)(la.tiles - la.next) / (double)la.tiles) / 24e12;
@@ -436,6 +437,9 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
     const double leaf_s = (double)b * 3.6e-6 + 3.0 * ((double)mp / 16.0) * 8.0 * rest_cols / 110e9 +
                           (double)nleaves * 8e-6;
     space = env_space == 1 || nn_s > 1.15 * leaf_s;
+    // and the panel's T on the same 16 SMs when the trailing update still outlasts that too
+    const double t_s = 2.0 * (double)mp * (double)b * (double)b / (16.0 * 0.15e12) + 60e-6;
+    t_on_aux = space && nn_s > 1.5 * (leaf_s + t_s);
   }
   cudaStream_t saved_stream = stream;
   for (int k0 = 0; k0 < b; k0 += wl) {
@@ -505,6 +509,28 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
       RQ_TRY(gemm(mm, nrest, w, op(V, mp + vpad, b, ldv, vpad + k0, k0), true, op(w2, w, nrest, ldw),
                   A + (s + k0) + (s + k0 + w) * lda, lda, -1.0, 1.0));
     }
+  }
+  if (space && t_on_aux && T && t_done) {
+    // the panel's T on the same 16 SMs, while the trailing update still holds the others (it
+    // outlasts the leaves here); the main stream's split-K slabs and Gram scratch are idle now
+    static const int env_taux = [] {
+      const char* e = getenv("RQ_T_AUX");
+      return e ? atoi(e) : 1;
+    }();
+    if (env_taux) {
+      gemm_max_ctas = 16;
+      const int rc = tfactor(V, mp, b, ldv, vpad, T, ldt, gram_aux);
+      gemm_max_ctas = 0;
+      RQ_TRY(rc);
+      *t_done = true;
+    }
+  }
+  if (space && aux_g1 && t_on_aux) {  // the downdate's G1' too (form_g1), on the same 16 SMs
+    gemm_max_ctas = 16;
+    const int rc = aux_g1();
+    gemm_max_ctas = 0;
+    RQ_TRY(rc);
+    g1_done = true;
   }
   if (space) {  // the main stream continues once the panel is factored (its chunk is in order)
     stream = saved_stream;
@@ -713,7 +739,24 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * b * sizeof(double), stream));
     launches++;
     // (look-ahead: L.w2 holds the previous panel's W2 until its last chunk ran; ttop is free)
-    RQ_TRY(panel_qr(A, lda, m, n, s, mp, b, V, ldv, vpad, tleaf, L.w1, la_mode ? L.ttop : L.w2));
+    gram_aux = L.gram;
+    bool t_done = false;
+    g1_done = false;
+    if (downdate && !refl_piv && np > b) {  // G1' from R'11 and the selected sketch columns (form_g1)
+      aux_g1 = [this, A, lda, s, b, wdt, n, &L]() { return form_g1(A, lda, s, b, wdt, n, L); };
+    }
+    RQ_TRY(panel_qr(A, lda, m, n, s, mp, b, V, ldv, vpad, tleaf, L.w1, la_mode ? L.ttop : L.w2, T, ldt, &t_done));
+    // G1' not formed on aux: with the overlap below it runs on the high-priority stream once the
+    // b x b CPQR is done (beside the rest of W); otherwise here
+    static const int env_hip = [] {
+      const char* e = getenv("RQ_HIP_TAIL");
+      return e ? atoi(e) : 1;
+    }();
+    const bool hip_tail = env_hip != 0 && overlap_on && np - b > 0;
+    if (aux_g1 && (g1_done || !hip_tail)) {
+      if (!g1_done) RQ_TRY(aux_g1());
+      aux_g1 = nullptr;
+    }
     RQ_TRY(la_flush());
     phase(1);
     const int64_t n2 = np - b;
@@ -809,7 +852,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
         }
         gemm_pdl = false;
         side_phase(2);
-        if (rc == RQ_OK) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
+        if (rc == RQ_OK && !t_done) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
         side_phase(3);
         if (rc == RQ_OK) rc = cudaEventRecord(ev_side, side) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
       }
@@ -824,6 +867,19 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       RQ_TRY(sweep(ss));
     }
     phase(2);
+    // the small post-CPQR work (G1', Q2, R, the rows above) on the highest-priority stream: its
+    // CTAs take the SMs the CPQR frees before the queued CTAs of the rest of W
+    cudaStream_t tail_saved = stream;
+    const bool on_hip = overlap && hip_tail;
+    if (on_hip) {
+      RQ_CUDA_TRY(cudaEventRecord(ev_v, stream));
+      RQ_CUDA_TRY(cudaStreamWaitEvent(hip, ev_v, 0));
+      stream = hip;
+    }
+    if (aux_g1) {
+      RQ_TRY(aux_g1());  // (before R overwrites R'11 in A)
+      aux_g1 = nullptr;
+    }
     RQ_TRY(small_q(V2, L.lds_small, b, Q2, ldt, L));
     phase(11);
     if (refl_piv)
@@ -834,14 +890,16 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     MoveCall mv2{A, lda, s, 0, s, L.cap, L.iota_b, nullptr, b, L.stage, even(m), L.orig, L.ostage};
     RQ_TRY(move_columns(mv2, stream, &launches));
     if (on_cols_final) on_cols_final(s, b);  // later steps only touch columns >= s + b
-    if (downdate) {  // P-hat on the sketch's panel columns
-      MoveCall my2{L.yt, L.ldy, s, 0, wdt, L.cap, L.iota_b, nullptr, b, L.stage, L.ldy, nullptr, nullptr};
-      RQ_TRY(move_columns(my2, stream, &launches));
+    // (the sketch's panel columns are not needed after form_g1: no P-hat on them)
+    if (on_hip) {
+      RQ_CUDA_TRY(cudaEventRecord(ev_hi, hip));
+      stream = tail_saved;
+      RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_hi, 0));
     }
     phase(12);
     // ---------------- 8: T of the panel reflectors (on the side stream when overlapped) ----------------
     if (overlap) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_side, 0));
-    else RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
+    else if (!t_done) RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
     phase(3);
     // ---------------- 9: trailing update ----------------
     if (la_mode && n2 > 0) {
@@ -854,11 +912,10 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L,
                                        overlap ? L.wside : nullptr));
     if (downdate && n2 > 0) {
-      // Y2 <- Y2 - G1 R12 with G1 = Y1 R11^{-1}: the sketch of the new trailing block
-      const int64_t ldb2 = even(b), ldg = even(wdt);
-      RQ_TRY(trinv_upper(A + s + s * lda, lda, b, L.rinv, ldb2, stream, &launches));
-      RQ_TRY(gemm(wdt, b, b, op(L.yt, wdt, n, L.ldy, 0, s), true, op(L.rinv, b, b, ldb2), L.g1, ldg, 1.0, 0.0));
-      RQ_TRY(gemm(wdt, n2, b, op(L.g1, wdt, b, ldg), true, op(A, m, n, lda, s, s + b), L.yt + (s + b) * L.ldy,
+      // Y2 <- Y2 - G1' R'12 (form_g1 ran after the panel QR; R'12 = the top rows before Q2^T,
+      // which trailing_update left in L.ttop): the sketch of the new trailing block
+      const int64_t ldg = even(wdt);
+      RQ_TRY(gemm(wdt, n2, b, op(L.g1, wdt, b, ldg), true, op(L.ttop, b, n2, even(b)), L.yt + (s + b) * L.ldy,
                   L.ldy, -1.0, 1.0));
     }
     factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2, ldt});
@@ -920,7 +977,7 @@ int Ctx::factorize_unpivoted(int64_t m, int64_t n, double* A, int64_t lda, int b
     double* T = fc.take<double>((size_t)ldt * b);
     RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * w * sizeof(double), stream));
     launches++;
-    RQ_TRY(panel_qr(A, lda, m, n, s, mp, w, V, ldv, vpad, L.tleaf, L.w1, L.w2));
+    RQ_TRY(panel_qr(A, lda, m, n, s, mp, w, V, ldv, vpad, L.tleaf, L.w1, L.w2, nullptr, 0, nullptr));
     RQ_TRY(tfactor(V, mp, w, ldv, vpad, T, ldt, L.gram));
     const int64_t n2 = n - s - w;
     if (n2 > 0) RQ_TRY(trailing_update(A, lda, m, n, s, mp, w, n2, V, ldv, vpad, T, ldt, nullptr, L));
@@ -973,6 +1030,18 @@ int Ctx::sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t
   return gemm(wdt, np, mp, Om, false, X, L.yt, L.ldy, 1.0, 0.0);
 }
 
+// G1' = Y1 R'11^{-1} for the downdate, from the panel's leaf R' (before the b x b CPQR) and the
+// sketch columns of the panel as selected (before P-hat): the downdate
+//   Y2 <- Y2 - G1 R12 = Y2 - Y1 R11^{-1} R12 = Y2 - (Y1 P^T)(Q2^T R'11)^{-1}... = Y2 - G1' R'12
+// (R11 = Q2^T R'11 P-hat, R12 = Q2^T R'12, Y1 = Y1' P-hat) needs neither Q2 nor P-hat, so G1'
+// is formed while the panel's trailing update still runs, and R'12 (the top rows before Q2^T)
+// is the copy the Q2^T product reads anyway.
+int Ctx::form_g1(double* A, int64_t lda, int64_t s, int b, int wdt, int64_t n, Layout& L) {
+  const int64_t ldb2 = even(b), ldg = even(wdt);
+  RQ_TRY(trinv_upper(A + s + s * lda, lda, b, L.rinv, ldb2, stream, &launches));
+  return gemm(wdt, b, b, op(L.yt, wdt, n, L.ldy, 0, s), true, op(L.rinv, b, b, ldb2), L.g1, ldg, 1.0, 0.0);
+}
+
 // Look-ahead tail of a non-final panel at s (downdated sketches, permutation pivots):
 //   W2 = T^T W;  top b rows: R12 = Q2^T (A2_top - V_top W2)  (final);
 //   Y2 <- Y2 - G1 R12 (the next panel's sketch);
@@ -1008,17 +1077,19 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
     CatGuard guard(cat, PROF_TRAIL);
     return gemm(mp - b, n2, b, Vlow, true, op(L.w2, b, n2, ldw), A + (s + b) + (s + b) * lda, lda, -1.0, 1.0);
   }
-  // Y2 <- Y2 - G1 R12 with G1 = Y1 R11^{-1}
+  // Y2 <- Y2 - G1' R'12 (form_g1; R'12 = the top rows before Q2^T, kept in L.ttop)
   const int64_t ldg = even(wdt);
-  RQ_TRY(trinv_upper(A + s + s * lda, lda, b, L.rinv, ldw, stream, &launches));
-  RQ_TRY(gemm(wdt, b, b, op(L.yt, wdt, n, L.ldy, 0, s), true, op(L.rinv, b, b, ldw), L.g1, ldg, 1.0, 0.0));
-  RQ_TRY(gemm(wdt, n2, b, op(L.g1, wdt, b, ldg), true, op(A, m, n, lda, s, s + b), L.yt + (s + b) * L.ldy, L.ldy,
-              -1.0, 1.0));
+  RQ_TRY(gemm(wdt, n2, b, op(L.g1, wdt, b, ldg), true, op(L.ttop, b, n2, ldw), L.yt + (s + b) * L.ldy, L.ldy, -1.0,
+              1.0));
   phase(5);
   // the next panel's pivots (b-step CPQR of a copy of its sketch) and moves
   const int64_t s2 = s + b;
-  RQ_TRY(copy2d(L.yt + s2 * L.ldy, L.ldy, L.ybuf, L.ldy, wdt, np2, 0, stream, &launches));
-  RQ_TRY(sketch_select(L.ybuf, L.ldy, wdt, (int)np2, b, rank, L.cap));
+  if (sketch_cpqr_preserves_input(wdt, (int)np2)) {  // (the register tiers only read Y)
+    RQ_TRY(sketch_select(L.yt + s2 * L.ldy, L.ldy, wdt, (int)np2, b, rank, L.cap));
+  } else {
+    RQ_TRY(copy2d(L.yt + s2 * L.ldy, L.ldy, L.ybuf, L.ldy, wdt, np2, 0, stream, &launches));
+    RQ_TRY(sketch_select(L.ybuf, L.ldy, wdt, (int)np2, b, rank, L.cap));
+  }
   phase(6);
   PlanCall pc{L.cap, b, lorder, (int)np2, L.flag, L.newloc, L.src, L.dst, L.nmoves, lorder_n, rank_n};
   RQ_TRY(plan_moves(pc, stream, &launches));
@@ -1159,7 +1230,7 @@ int Ctx::factorize_rrqr(const rq_config& cfg0, int64_t m, int64_t n, double* A, 
     double* Vt = fc.take<double>((size_t)ldt * b);
     RQ_CUDA_TRY(cudaMemsetAsync(V, 0, (size_t)ldv * w * sizeof(double), stream));
     launches++;
-    RQ_TRY(panel_qr(A, lda, m, n, s, mp, w, V, ldv, vpad, L.tleaf, L.w1, L.w2));
+    RQ_TRY(panel_qr(A, lda, m, n, s, mp, w, V, ldv, vpad, L.tleaf, L.w1, L.w2, nullptr, 0, nullptr));
     {
       cudaEvent_t e0;
       const int saved = cat;

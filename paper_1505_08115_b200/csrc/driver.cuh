@@ -176,7 +176,12 @@ struct Ctx {
   unsigned long long sk_counter_base = 0;    // host mirror of its value
   int sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen);
   int panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, double* V, int64_t ldv,
-               int vpad, double* tleaf, double* w1, double* w2);
+               int vpad, double* tleaf, double* w1, double* w2, double* T = nullptr, int64_t ldt = 0,
+               bool* t_done = nullptr);
+  double* gram_aux = nullptr;  // Gram scratch for the panel's T computed on the aux stream
+  std::function<int()> aux_g1;  // form_g1 of the current panel (run on aux in space mode)
+  bool g1_done = false;
+  int form_g1(double* A, int64_t lda, int64_t s, int b, int wdt, int64_t n, Layout& L);
   int tfactor(const double* V, int64_t rows, int k, int64_t ldv, int vpad, double* T, int64_t ldt, double* gram);
   int sketch(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int64_t np,
              Layout& L, bool want_y = false);

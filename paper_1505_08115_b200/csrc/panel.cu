@@ -229,7 +229,7 @@ __device__ int g_leaf_dbg_on;
 // per-column critical path.
 RQ_DEV void leaf_stamp(int j, int k) {
 #ifdef RQ_STAMPS
-  if (blockIdx.x == 0 && threadIdx.x == 0 && j < 64 && g_leaf_dbg_on) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && j < 64) {  // (stamps build: always on)
     unsigned long long c;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
     g_leaf_dbg[j * 8 + k] = c;

@@ -282,7 +282,7 @@ __device__ int g_sweep_dbg_on;
 // Compiled in only with -DRQ_STAMPS (tuning builds; see leaf_stamp in panel.cu).
 RQ_DEV void dbg_stamp(int j, int k) {
 #ifdef RQ_STAMPS
-  if (blockIdx.x == 0 && threadIdx.x == 0 && j < 64 && g_sweep_dbg_on) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && j < 64) {  // (stamps build: always on)
     unsigned long long c;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
     g_sweep_dbg[j * 8 + k] = c;
@@ -1471,8 +1471,9 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
     } else {
     bool reducer;
     if (p.fixed_reducer) {
-      // CTA 0 polls every slot's stamps directly: one L2 round trip fewer than arrive-then-read
-      reducer = blockIdx.x == 0;
+      // a fixed CTA polls every slot's stamps directly: one L2 round trip fewer than
+      // arrive-then-read (1: CTA 0; 2: the last CTA, which holds the fewest columns)
+      reducer = blockIdx.x == (p.fixed_reducer == 2 ? gridDim.x - 1 : 0);
     } else {
       if (threadIdx.x == 0) {
         unsigned long long old;
@@ -1794,6 +1795,26 @@ static int dispatch_sketch_reg(SketchArgs a, int n, SkSlot2* slots, SkWin* wins,
 }
 
 size_t sketch_ll_column_bytes(int m) { return 2 * (size_t)kSMs * 2 * ((size_t)m + 2) * 8; }
+// True when sketch_cpqr_launch(m, n) runs a register / shared-memory tier, which only reads Y
+// (the L2-streaming fallback overwrites it).  Mirrors dispatch_sketch_reg's choice.
+bool sketch_cpqr_preserves_input(int m, int n) {
+  if (m > 288) return false;
+  const int rpl = m <= 96 ? 3 : (m <= 160 ? 5 : 9);
+  const int opts[][2] = {{16, 1}, {16, 2}, {16, 3}, {8, 6}, {8, 8}, {8, 9}, {8, 10}};
+  for (const auto& o : opts) {
+    if (rpl * o[1] > (o[0] == 16 ? 30 : 92)) continue;
+    if ((o[1] == 8 || o[1] == 9) && rpl != 9) continue;
+    if ((n + o[0] * o[1] - 1) / (o[0] * o[1]) <= kSMs) return true;
+  }
+  if (rpl == 9) {
+    const int W = 12, C = 6;
+    const int per_needed = (n + kSMs - 1) / kSMs;
+    const int spw = std::max(1, (per_needed - W * C + W - 1) / W);
+    if (spw <= 7 && (size_t)W * spw * 9 * 32 * 8 <= 200 * 1024) return true;
+  }
+  return false;
+}
+
 size_t sketch_workspace_bytes(int m) { return ((2 * (size_t)kSMs * 64 + 255) & ~size_t(255)) + 256 + sketch_ll_column_bytes(m); }
 
 static size_t sketch_fixed_smem(int m, int per) {
