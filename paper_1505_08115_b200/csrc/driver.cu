@@ -753,6 +753,13 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       return e ? atoi(e) : 1;
     }();
     const bool hip_tail = env_hip != 0 && overlap_on && np - b > 0;
+    // and the panel's T there too (instead of after W on the side stream): RQ_T_HIP=1; measured
+    // slower (n = 10k 146.7 -> 148.7 ms: its Gram GEMM competes with the rest of W), so off
+    static const int env_thip = [] {
+      const char* e = getenv("RQ_T_HIP");
+      return e ? atoi(e) : 0;
+    }();
+    const bool t_on_hip = hip_tail && env_thip != 0 && !t_done;
     if (aux_g1 && (g1_done || !hip_tail)) {
       if (!g1_done) RQ_TRY(aux_g1());
       aux_g1 = nullptr;
@@ -852,7 +859,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
         }
         gemm_pdl = false;
         side_phase(2);
-        if (rc == RQ_OK && !t_done) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
+        if (rc == RQ_OK && !t_done && !(t_on_hip && hip_tail)) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
         side_phase(3);
         if (rc == RQ_OK) rc = cudaEventRecord(ev_side, side) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
       }
@@ -880,6 +887,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       RQ_TRY(aux_g1());  // (before R overwrites R'11 in A)
       aux_g1 = nullptr;
     }
+    if (on_hip && t_on_hip) RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
     RQ_TRY(small_q(V2, L.lds_small, b, Q2, ldt, L));
     phase(11);
     if (refl_piv)
