@@ -337,6 +337,7 @@ int Ctx::ensure_side() {
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_hi, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_w2, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_l0, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_aux, cudaEventDisableTiming));
   return RQ_OK;
@@ -775,6 +776,11 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       return e ? atoi(e) : 1;
     }();
     const bool overlap = overlap_on && env_overlap != 0 && n2 > 0;
+    static const int env_w2s = [] {
+      const char* e = getenv("RQ_W2_SIDE");
+      return e ? atoi(e) : 1;
+    }();
+    w2_side = overlap && la_mode && env_w2s != 0 && !(t_on_hip && hip_tail);
     // ---------------- 6: b x b CPQR of R' (reflectors V2), then Q2 = I - V2 T2 V2^T ----------------
     double* S = L.small;
     double* V2 = L.small + (int64_t)b * L.lds_small;
@@ -862,6 +868,13 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
         if (rc == RQ_OK && !t_done && !(t_on_hip && hip_tail)) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
         side_phase(3);
         if (rc == RQ_OK) rc = cudaEventRecord(ev_side, side) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
+        // look-ahead: W2 = T^T W (needed only by the trailing update of the rows below the top,
+        // after the next panel's CPQR) stays on the side stream, off the tail's critical path
+        if (rc == RQ_OK && w2_side) {
+          CatGuard g(cat, PROF_TRAIL);
+          rc = gemm(b, n2, b, op(T, b, b, ldt), false, op(L.wside, b, n2, even(b)), L.w2, even(b), 1.0, 0.0);
+          if (rc == RQ_OK) rc = cudaEventRecord(ev_w2, side) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
+        }
       }
       gemm_max_ctas = 0;
       gemm_pdl = false;
@@ -878,6 +891,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     // CTAs take the SMs the CPQR frees before the queued CTAs of the rest of W
     cudaStream_t tail_saved = stream;
     const bool on_hip = overlap && hip_tail;
+    (void)on_hip;
     if (on_hip) {
       RQ_CUDA_TRY(cudaEventRecord(ev_v, stream));
       RQ_CUDA_TRY(cudaStreamWaitEvent(hip, ev_v, 0));
@@ -1070,9 +1084,16 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
     CatGuard guard(cat, PROF_TRAIL);
     const double* W = Wpre ? Wpre : L.w1;
     if (!Wpre) RQ_TRY(gemm(b, n2, mp, Vop, false, op(A, m, n, lda, s, s + b), L.w1, ldw, 1.0, 0.0));
-    RQ_TRY(gemm(b, n2, b, op(T, b, b, ldt), false, op(W, b, n2, ldw), L.w2, ldw, 1.0, 0.0));
-    // top b rows: A2_top -= V_top W2, then Q2^T
-    RQ_TRY(gemm(b, n2, b, Vop, true, op(L.w2, b, n2, ldw), A + s + (s + b) * lda, lda, -1.0, 1.0));
+    if (w2_side) {
+      // top b rows: A2_top -= (V_top T^T) W while the side stream forms W2 = T^T W
+      RQ_TRY(transpose(T, ldt, L.jw, ldw, b, b, stream, &launches));
+      RQ_TRY(gemm(b, b, b, Vop, true, op(L.jw, b, b, ldw), L.jv, ldw, 1.0, 0.0));
+      RQ_TRY(gemm(b, n2, b, op(L.jv, b, b, ldw), true, op(W, b, n2, ldw), A + s + (s + b) * lda, lda, -1.0, 1.0));
+    } else {
+      RQ_TRY(gemm(b, n2, b, op(T, b, b, ldt), false, op(W, b, n2, ldw), L.w2, ldw, 1.0, 0.0));
+      // top b rows: A2_top -= V_top W2, then Q2^T
+      RQ_TRY(gemm(b, n2, b, Vop, true, op(L.w2, b, n2, ldw), A + s + (s + b) * lda, lda, -1.0, 1.0));
+    }
     RQ_TRY(copy2d(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
     RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldt), false, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
   }
@@ -1083,6 +1104,7 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
   const bool next_full = np2 > b;
   if (!next_full) {
     CatGuard guard(cat, PROF_TRAIL);
+    if (w2_side) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_w2, 0));
     return gemm(mp - b, n2, b, Vlow, true, op(L.w2, b, n2, ldw), A + (s + b) + (s + b) * lda, lda, -1.0, 1.0);
   }
   // Y2 <- Y2 - G1' R'12 (form_g1; R'12 = the top rows before Q2^T, kept in L.ttop)
@@ -1105,6 +1127,7 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
   RQ_TRY(move_columns(mv, stream, &launches));
   MoveCall my{L.yt, L.ldy, s2, 0, wdt, L.src, L.dst, L.nmoves, 2 * b, L.stage, L.ldy, nullptr, nullptr};
   RQ_TRY(move_columns(my, stream, &launches));
+  if (w2_side) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_w2, 0));
   MoveCall mw{L.w2, ldw, 0, 0, b, L.src, L.dst, L.nmoves, 2 * b, L.stage, even(m), nullptr, nullptr};
   RQ_TRY(move_columns(mw, stream, &launches));
   // the next panel's columns first; the rest pending
@@ -1504,6 +1527,7 @@ Ctx::~Ctx() {
   if (aux) cudaStreamDestroy(aux);
   if (ev_l0) cudaEventDestroy(ev_l0);
   if (ev_aux) cudaEventDestroy(ev_aux);
+  if (ev_w2) cudaEventDestroy(ev_w2);
   if (barriers) cudaFree(barriers);
 }
 

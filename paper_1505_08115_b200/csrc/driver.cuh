@@ -115,6 +115,8 @@ struct Ctx {
   // space-sliced look-ahead (panel_qr): the panel's later leaves and cluster WY updates on `aux`
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_l0 = nullptr, ev_aux = nullptr;
+  cudaEvent_t ev_w2 = nullptr;  // look-ahead: W2 = T^T W formed on the side stream
+  bool w2_side = false;
   bool overlap_on = true;
   // called (host side, enqueue order) when columns [s, s + w) of R are final: no later step
   // writes them (rq_factorize_host streams them to the host while later panels compute)
