@@ -203,7 +203,7 @@ def run_distributed(args, dist, rank, world, local):
     def step():
         with torch.cuda.stream(stream):
             work.copy_(a0_loc)
-            rqd.factorize_local(work, lda, m, n, cfg, rq.RngState(1), engine=se)
+            rqd.factorize_local(work, lda, m, n, cfg, rq.RngState(1), engine=se, sketch=args.sketch)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -252,7 +252,7 @@ def run_distributed(args, dist, rank, world, local):
         def e2e_step():
             with torch.cuda.stream(stream):
                 work.copy_(ha, non_blocking=True)
-                rqd.factorize_local(work, lda, m, n, cfg, rq.RngState(1), engine=se)
+                rqd.factorize_local(work, lda, m, n, cfg, rq.RngState(1), engine=se, sketch=args.sketch)
                 hr.copy_(work, non_blocking=True)
             stream.synchronize()
 
@@ -277,9 +277,9 @@ def run_distributed(args, dist, rank, world, local):
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg3 HQRRP fp64 n={n} b={b} p={p} q=0, fresh sketch (reference semantics), "
+            "config": {"workload": f"cfg3 HQRRP fp64 n={n} b={b} p={p} q=0, {args.sketch} sketch, "
                                    f"1-D block-cyclic columns over {world} GPU(s)",
-                       "n": n, "b": b, "p": p, "q": 0, "sketch": "fresh", "method": "m1", "matrix": "gauss",
+                       "n": n, "b": b, "p": p, "q": 0, "sketch": args.sketch, "method": "m1", "matrix": "gauss",
                        "parallelism": f"block-cyclic columns x{world} (NCCL all-gather / send-recv / broadcast)",
                        "l2": "inputs (800 MB) larger than L2 (126 MB)"},
             "fraction_of_fp64_peak": value / (FP64_PEAK_TFLOPS * world),
@@ -406,7 +406,7 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         if args.method == "m1" and args.q == 0 and args.matrix == "gauss":
-            return run_distributed(args, dist, rank, world, local)  # fresh sketches (dist.py scope)
+            return run_distributed(args, dist, rank, world, local)
         if rank == 0:
             print(json.dumps({"metric": METRIC, "unavailable": "multi-GPU runs cover m1 fresh q=0 (dist.py)"}))
         dist.destroy_process_group()

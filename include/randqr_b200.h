@@ -134,6 +134,10 @@ int rq_trailing_frobenius(rq_ctx* ctx, const double* dR, int64_t n, int64_t ldr,
 /* C (M x N) = alpha op(A) B + beta C, op(A) = A^T (A is K x M, a_mmajor = 0) or A
  * (A is M x K, a_mmajor = 1); B is K x N.  Views start at element (r0, c0) of
  * buffers with rows x cols extents (FP64 DMMA GEMM). */
+/* Panel step (multi-GPU downdated sketch): X = R^{-1} for the k x k upper-triangular R
+ * (k <= 512), on the context's stream. */
+int rq_trinv_upper(rq_ctx* ctx, const double* dR, int64_t ldr, int32_t k, double* dX, int64_t ldx);
+
 int rq_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, const double* dA, int64_t lda,
             int64_t a_rows, int64_t a_cols, int64_t a_r0, int64_t a_c0, const double* dB, int64_t ldb, int64_t b_rows,
             int64_t b_cols, int64_t b_r0, int64_t b_c0, double* dC, int64_t ldc, double alpha, double beta);

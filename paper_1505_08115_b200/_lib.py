@@ -54,6 +54,7 @@ _SIGS = {
     "rq_snapshot": (ctypes.c_int, [_vp, _vp, _i64]),
     "rq_householder_sweep": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i32]),
     "rq_gaussian_matrix": (ctypes.c_int, [_vp, _i64, _i64, _u64, _u64, _vp, _i64]),
+    "rq_trinv_upper": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _i64]),
     "rq_splitmix_words": (ctypes.c_int, [_vp, _u64, _u64, _i64, _vp]),
     "rq_qr_unpivoted": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i64, _i32]),
     "rq_trailing_frobenius": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp]),

@@ -311,6 +311,14 @@ int rq_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, cons
   return c.gemm(M, N, K, A, a_mmajor != 0, B, dC, ldc, alpha, beta);
 }
 
+int rq_trinv_upper(rq_ctx* ctx, const double* dR, int64_t ldr, int32_t k, double* dX, int64_t ldx) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (k < 0) return rq::set_error(RQ_EDIM, "trinv: negative order");
+  Ctx& c = ctx->c;
+  return rq::trinv_upper(dR, ldr, k, dX, ldx, c.stream, &c.launches);
+}
+
 int rq_sketch_select(rq_ctx* ctx, double* dY, int64_t ldy, int32_t m, int32_t n, int32_t steps,
                      const int32_t* dInitPos, int32_t* dChosen) {
   CTX_CHECK(ctx);

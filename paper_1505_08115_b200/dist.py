@@ -25,9 +25,9 @@ After the last panel the slots hold R's columns in the reference's order, so
 
 Device work goes through an *engine*; the product engine is ``CudaStepEngine``
 (the C ABI's panel-step entry points).  Collectives are torch.distributed calls
-(NCCL between GPUs).  Fresh sketches, q = 0, permutation pivots and m >= n are
-supported; power iterations, reflector pivots and block_rrqr run on one GPU
-(hqrrp.block_qr / block_rrqr).
+(NCCL between GPUs).  Fresh or downdated sketches (``sketch=``), q = 0, permutation
+pivots and m >= n are supported; power iterations, reflector pivots and block_rrqr run on
+one GPU (hqrrp.block_qr / block_rrqr).
 """
 
 from __future__ import annotations
@@ -97,6 +97,24 @@ class CudaStepEngine:
         v, ldv, t, ldt, q2, ldq = fac
         check(self.lib.rq_panel_apply(self.h, _ptr(v), ldv, _ptr(t), ldt, _ptr(q2), ldq, mp, b, _ptr(a), lda,
                                       a_rows, a_cols, r0, c0, n2))
+
+    def downdate_g1(self, y, ldy, wdt, c0, ph, p, ldp, b, g1, ldg):
+        """G1 = Y1 R11^{-1} (written into g1, wdt x b): Y1 = the panel's sketch columns c0.. of y
+        in P-hat order, R11 = the factored panel's top b x b (downdated sketch)."""
+        torch = self.torch
+        y1, ldy1 = self.alloc(wdt, b)
+        y1[:b, :wdt].copy_(y[c0:c0 + b, :wdt].index_select(0, ph.to(torch.int64)))
+        x, ldx = self.alloc(b, b)
+        check(self.lib.rq_trinv_upper(self.h, _ptr(p), ldp, b, _ptr(x), ldx))
+        check(self.lib.rq_gemm(self.h, 1, wdt, b, b, _ptr(y1), ldy1, wdt, b, 0, 0, _ptr(x), ldx, b, b, 0, 0,
+                               _ptr(g1), ldg, 1.0, 0.0))
+
+    def downdate_apply(self, g1, ldg, wdt, b, a, lda, a_rows, a_cols, s, t1, n2, y, ldy):
+        """Y2 <- Y2 - G1 R12 on the local columns t1 .. t1+n2 (R12 = their final top rows s..s+b)."""
+        if n2 <= 0:
+            return
+        check(self.lib.rq_gemm(self.h, 1, wdt, n2, b, _ptr(g1), ldg, wdt, b, 0, 0, _ptr(a), lda, a_rows, a_cols, s,
+                               t1, _ptr(y[t1:]), ldy, -1.0, 1.0))
 
     def final_block(self, blk, ldb, mp, w):
         """Column-pivoted sweep of an mp x w block in place; returns perm (position t holds column perm[t])."""
@@ -252,8 +270,15 @@ class DistResult:
     perm: np.ndarray   # perm[j] = original column at position j (A[:, perm] = Q R)
 
 
-def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=None, engine=None):
-    """HQRRP (fresh sketches, permutation pivots) on this rank's block-cyclic columns.
+def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=None, engine=None,
+                    sketch: str = "fresh"):
+    """HQRRP (permutation pivots) on this rank's block-cyclic columns.
+
+    ``sketch="fresh"`` draws a new Omega per panel (the reference's semantics);
+    ``sketch="downdate"`` is HQRRP's downdated sketch: G is drawn once
+    (counter += m (b+p)), Y_loc = G A_loc, the Y columns travel with their matrix columns, and
+    after each panel every rank updates its own columns Y2_loc -= G1 R12_loc with
+    G1 = Y1 R11^{-1} broadcast by the panel's owner together with V, T, Q2 and P-hat.
 
     ``a_loc`` is the (n_local, lda) column-major storage of the slot blocks this rank
     owns (see ``BlockCyclic``); it is overwritten with the rank's columns of R.
@@ -283,12 +308,26 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
             break
         if wdt > n - s:
             bad = s
-            rng.counter += sum((m - t) * wdt for t in range(0, bad, b))
+            if sketch == "downdate":  # G was drawn before the loop (oracle block_qr_downdate)
+                rng.counter += m * wdt
+            else:
+                rng.counter += sum((m - t) * wdt for t in range(0, bad, b))
             raise ValueError(f"sketch width {wdt} exceeds the {n - s} columns being pivoted")
+    if sketch not in ("fresh", "downdate"):
+        raise ValueError(f"sketch must be 'fresh' or 'downdate', got {sketch!r}")
+    downdate = sketch == "downdate" and n > b
     slot_orig = np.arange(n, dtype=np.int64)
     slot_lpos = np.arange(n, dtype=np.int64)
     counts_cache = {}
     ph_pending = []
+    y_loc, ldyl = None, 0
+    if downdate:
+        # G drawn once (the same stream on every rank), Y_loc = G A_loc
+        g_om, ldgo = engine.gaussian(m, wdt, rng.seed, rng.counter)
+        rng.counter += m * wdt
+        y_loc, ldyl = engine.sketch(g_om, ldgo, a_loc, lda, m, nloc, 0, 0, m, nloc, wdt, nloc)
+        del g_om
+        ldg = wdt + (wdt & 1)
     for i in range(lay.nblk):
         s = i * b
         np_ = n - s
@@ -298,17 +337,23 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
             _apply_pending_phat(slot_orig, ph_pending)
             _final_block(a_loc, lda, m, n, s, i, lay, rank, slot_orig, slot_lpos, d, engine)
             break
-        # ---- 1: sketch of the local trailing columns (same Omega on every rank) ----
-        om, ldo = engine.gaussian(mp, wdt, rng.seed, rng.counter)
-        rng.counter += mp * wdt
+        # ---- 1: sketch of the local trailing columns (same Omega on every rank), or the
+        #      downdated Y_loc (kept current by step 6) ----
         counts = counts_cache.get(i)
         if counts is None:
             counts = [lay.n_local(q) - lay.local_from(q, i) for q in range(d.world)]
             counts_cache[i] = counts
         cmax = max(counts)
         t0 = lay.local_from(rank, i)
-        y, ldy = engine.sketch(om, ldo, a_loc, lda, m, nloc, s, t0, mp, counts[rank], wdt, cmax)
-        del om
+        if downdate:
+            y, ldy = engine.alloc(wdt, max(cmax, 1))
+            if counts[rank] > 0:
+                y[:counts[rank], :wdt].copy_(y_loc[t0:t0 + counts[rank], :wdt])
+        else:
+            om, ldo = engine.gaussian(mp, wdt, rng.seed, rng.counter)
+            rng.counter += mp * wdt
+            y, ldy = engine.sketch(om, ldo, a_loc, lda, m, nloc, s, t0, mp, counts[rank], wdt, cmax)
+            del om
         # ---- 2: all-gather Y, identical pivot selection everywhere ----
         if d.world > 1:
             gathered = torch.empty((d.world * cmax, ldy), dtype=y.dtype, device=y.device)
@@ -326,6 +371,8 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         # ---- 3: move the chosen columns into the panel slots ----
         moves = plan_moves(chosen, s, b)
         _exchange_columns(a_loc, m, lay, rank, moves, d, engine)
+        if downdate:  # the sketch columns follow their matrix columns
+            _exchange_columns(y_loc, wdt, lay, rank, moves, d, engine)
         _apply_moves_host(slot_orig, moves)
         _apply_moves_host(slot_lpos, moves)
         rest = np.arange(s + b, n, dtype=np.int64)
@@ -335,13 +382,17 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         # ---- 4: panel on the owner; V, T, Q2, P-hat broadcast in one message ----
         ldv = mp + (mp & 1)
         ldb = b + (b & 1)
+        ng1 = b * ldg if downdate else 0
         nfac = b * ldv + 2 * b * ldb + b
-        pack = torch.empty(nfac, dtype=a_loc.dtype, device=a_loc.device)  # P-hat exact in fp32 too (b < 2^24)
+        pack = torch.empty(nfac + ng1, dtype=a_loc.dtype, device=a_loc.device)  # P-hat exact in fp32 too (b < 2^24)
         if rank == o:
             lo = lay.local_off(i)
             p, ldp = engine.alloc(mp, b)
             p[:b, :mp].copy_(a_loc[lo:lo + b, s:m])
             fac, ph = engine.panel_factor(p, ldp, mp, b)
+            if downdate:  # G1 = Y1 R11^{-1} from the factored panel (R11 = p's top b x b)
+                g1b = pack[nfac:].view(b, ldg)
+                engine.downdate_g1(y_loc, ldyl, wdt, lo, ph, p, ldp, b, g1b, ldg)
             a_loc[lo:lo + b, s:m].copy_(p[:b, :mp])
             if s > 0:  # rows above follow P-hat
                 a_loc[lo:lo + b, :s] = a_loc[lo:lo + b, :s].index_select(0, ph)
@@ -349,7 +400,7 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
             pack[:b * ldv].copy_(v[:b, :ldv].reshape(-1))
             pack[b * ldv:b * ldv + b * ldb].copy_(t[:b, :ldb].reshape(-1))
             pack[b * ldv + b * ldb:b * ldv + 2 * b * ldb].copy_(q2[:b, :ldb].reshape(-1))
-            pack[nfac - b:].copy_(ph.to(pack.dtype))
+            pack[nfac - b:nfac].copy_(ph.to(pack.dtype))
         if d.world > 1:
             d.dist.broadcast(pack, src=d.global_rank(o), group=d.group)
         v = pack[:b * ldv].view(b, ldv)
@@ -357,12 +408,16 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         q2 = pack[b * ldv + b * ldb:b * ldv + 2 * b * ldb].view(b, ldb)
         # P-hat reorders the panel's slots; those never compete for pivots again, so only
         # the final perm needs it: keep it on the device (no host sync here), apply at the end
-        ph_pending.append((s, pack[nfac - b:].clone()))
+        ph_pending.append((s, pack[nfac - b:nfac].clone()))
         # ---- 5: trailing update of the local columns ----
         t1 = lay.local_from(rank, i + 1)
         n2 = nloc - t1
         if n2 > 0:
             engine.panel_apply((v, ldv, t, ldb, q2, ldb), mp, b, a_loc, lda, m, nloc, s, t1, n2)
+            # ---- 6 (downdate): Y2_loc -= G1 R12_loc on the local trailing columns ----
+            if downdate and n - (s + b) > b:
+                engine.downdate_apply(pack[nfac:].view(b, ldg), ldg, wdt, b, a_loc, lda, m, nloc, s, t1, n2,
+                                      y_loc, ldyl)
         del pack
     _apply_pending_phat(slot_orig, ph_pending)
     return DistResult(a_loc, lda, m, n, lay, slot_orig)
@@ -444,7 +499,7 @@ def gather_r(res: DistResult, engine, group=None):
     return full
 
 
-def block_qr_distributed(a, cfg: BlockConfig, rng: RngState, *, group=None, engine=None):
+def block_qr_distributed(a, cfg: BlockConfig, rng: RngState, *, group=None, engine=None, sketch="fresh"):
     """``block_qr(a, cfg, rng)`` (blocked.py:175) with the columns spread over the
     ranks of ``group``; every rank passes the same ``a`` and gets (R, perm) back.
     R is upper trapezoidal (m x n, numpy), perm as in ``Factorization.perm``."""
@@ -456,7 +511,7 @@ def block_qr_distributed(a, cfg: BlockConfig, rng: RngState, *, group=None, engi
     full[:n, :m].copy_(engine.torch.from_numpy(np.ascontiguousarray(a.T)))
     a_loc, lda = scatter_columns(full, m, n, cfg.block, d.world, d.rank, engine)
     del full
-    res = factorize_local(a_loc, lda, m, n, cfg, rng, group=group, engine=engine)
+    res = factorize_local(a_loc, lda, m, n, cfg, rng, group=group, engine=engine, sketch=sketch)
     r_full = gather_r(res, engine, group)
     r = np.asfortranarray(r_full[:n, :m].cpu().numpy().T)
     return np.triu(r), res.perm

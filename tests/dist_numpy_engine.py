@@ -101,6 +101,19 @@ class NumpyStepEngine:
         x[:b] = q2.T @ x[:b]
         self._put(a, x, r0, c0)
 
+    def downdate_g1(self, y, ldy, wdt, c0, ph, p, ldp, b, g1, ldg):
+        y1 = self._get(y, wdt, b, 0, c0)[:, np.asarray(ph, dtype=np.int64)]
+        r11 = np.triu(self._get(p, b, b))
+        self._put(g1, np.linalg.solve(r11.T, y1.T).T)  # Y1 R11^{-1}
+
+    def downdate_apply(self, g1, ldg, wdt, b, a, lda, a_rows, a_cols, s, t1, n2, y, ldy):
+        if n2 <= 0:
+            return
+        g = self._get(g1, wdt, b)
+        r12 = self._get(a, b, n2, s, t1)
+        yy = self._get(y, wdt, n2, 0, t1)
+        self._put(y, yy - g @ r12, 0, t1)
+
     def final_block(self, blk, ldb, mp, w):
         x = self._get(blk, mp, w)
         v = np.zeros((mp, w), order="F")

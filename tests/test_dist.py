@@ -70,7 +70,7 @@ def test_plan_moves_is_the_reference_permutation(seed):
 # ---------------------------------------------------------------------------
 # world_size > 1 over gloo
 # ---------------------------------------------------------------------------
-def _worker(rank, world, port, a, b, p, seed, out_dir):
+def _worker(rank, world, port, a, b, p, seed, out_dir, sketch="fresh"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -83,7 +83,7 @@ def _worker(rank, world, port, a, b, p, seed, out_dir):
         rng = RngState(seed)
         cfg = BlockConfig(b, SketchConfig(b, p, 0))
         try:
-            r, perm = block_qr_distributed(a, cfg, rng, engine=NumpyStepEngine())
+            r, perm = block_qr_distributed(a, cfg, rng, engine=NumpyStepEngine(), sketch=sketch)
             np.savez(os.path.join(out_dir, f"r{rank}.npz"), r=r, perm=perm, counter=rng.counter, err="")
         except ValueError as e:
             np.savez(os.path.join(out_dir, f"r{rank}.npz"), r=np.zeros(1), perm=np.zeros(1), counter=rng.counter,
@@ -92,9 +92,9 @@ def _worker(rank, world, port, a, b, p, seed, out_dir):
         dist.destroy_process_group()
 
 
-def _run(world, a, b, p, seed):
+def _run(world, a, b, p, seed, sketch="fresh"):
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), a, b, p, seed, d), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), a, b, p, seed, d, sketch), nprocs=world, join=True)
         return [dict(np.load(os.path.join(d, f"r{q}.npz"))) for q in range(world)]
 
 
@@ -115,6 +115,25 @@ def test_distributed_matches_reference_algorithm(world, m, n, b, p):
     # every rank holds the same gathered result
     for o in outs[1:]:
         assert np.array_equal(o["r"], outs[0]["r"])
+
+
+@pytest.mark.parametrize("world,m,n,b,p", [(2, 300, 300, 50, 10), (3, 260, 230, 40, 8)])
+def test_distributed_downdate_matches_hqrrp_oracle(world, m, n, b, p):
+    """HQRRP's downdated sketch over the ranks (G1 broadcast with the panel
+    factors, Y2_loc -= G1 R12_loc, Y columns moving with their matrix columns) against the
+    oracle restatement block_qr_downdate: same pivots, R to 1e-12 ||A||, same RNG counter."""
+    import randqr_oracle as orc
+
+    a = np.random.default_rng(11).standard_normal((m, n))
+    ref_rng = orc.RngState(3)
+    f = orc.block_qr_downdate(a, orc.BlockConfig(b, orc.SketchConfig(b, p, 0)), ref_rng)
+    outs = _run(world, a, b, p, 3, "downdate")
+    nrm = np.linalg.norm(a)
+    for o in outs:
+        assert str(o["err"]) == ""
+        assert np.array_equal(o["perm"], f.perm())
+        assert np.abs(o["r"] - np.triu(f.r)).max() <= 1e-12 * nrm
+        assert int(o["counter"]) == ref_rng.counter == m * (b + p)
 
 
 def test_distributed_value_error_like_reference():

@@ -111,6 +111,38 @@ def _free_port():
 
 
 @pytest.mark.parametrize("m,n,b,p", [(800, 800, 64, 8), (700, 530, 96, 10)])
+def test_distributed_downdate_world1_nccl(m, n, b, p):
+    """The block-cyclic driver's downdated sketch on the GPU step engine (G1 via rq_trinv_upper +
+    rq_gemm, Y2 -= G1 R12 per rank) vs the oracle's block_qr_downdate and the single-GPU driver."""
+    import torch.distributed as dist
+
+    import randqr_oracle as orc
+    from paper_1505_08115_b200 import hqrrp
+    from paper_1505_08115_b200.dist import block_qr_distributed
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        a = np.random.default_rng(m + n + 1).standard_normal((m, n))
+        cfg = hqrrp.BlockConfig(b, hqrrp.SketchConfig(b, p, 0))
+        rng = hqrrp.RngState(3)
+        r, perm = block_qr_distributed(a, cfg, rng, sketch="downdate")
+        rng1 = hqrrp.RngState(3)
+        f = hqrrp.block_qr(a, cfg, rng1, sketch="downdate")
+        ref_rng = orc.RngState(3)
+        fo = orc.block_qr_downdate(a, orc.BlockConfig(b, orc.SketchConfig(b, p, 0)), ref_rng)
+        nrm = np.linalg.norm(a)
+        assert np.array_equal(perm, fo.perm())
+        assert np.array_equal(perm, f.perm)
+        assert np.abs(r - np.triu(fo.r)).max() <= 1e-12 * nrm
+        assert np.abs(r - np.triu(f.r)).max() <= 1e-12 * nrm
+        assert rng.counter == rng1.counter == ref_rng.counter == m * (b + p)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,n,b,p", [(800, 800, 64, 8), (700, 530, 96, 10)])
 def test_distributed_world1_nccl_matches_single_gpu(m, n, b, p):
     import torch.distributed as dist
 
