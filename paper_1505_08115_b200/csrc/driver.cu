@@ -333,6 +333,8 @@ int Ctx::ensure_side() {
   RQ_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   RQ_CUDA_TRY(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
   RQ_CUDA_TRY(cudaStreamCreateWithPriority(&hip, cudaStreamNonBlocking, hi));
+  RQ_CUDA_TRY(cudaStreamCreateWithPriority(&hip2, cudaStreamNonBlocking, hi));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_q2, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_v, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_hi, cudaEventDisableTiming));
@@ -899,12 +901,23 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       RQ_CUDA_TRY(cudaStreamWaitEvent(hip, ev_v, 0));
       stream = hip;
     }
+    // Q2 (small_q) and G1' (form_g1) are independent: Q2 on a second high-priority stream
+    const bool q2_par = on_hip && aux_g1 && hip2 != nullptr;
+    if (q2_par) {
+      RQ_CUDA_TRY(cudaEventRecord(ev_v, hip));
+      RQ_CUDA_TRY(cudaStreamWaitEvent(hip2, ev_v, 0));
+      stream = hip2;
+      RQ_TRY(small_q(V2, L.lds_small, b, Q2, ldt, L));
+      RQ_CUDA_TRY(cudaEventRecord(ev_q2, hip2));
+      stream = hip;
+    }
     if (aux_g1) {
       RQ_TRY(aux_g1());  // (before R overwrites R'11 in A)
       aux_g1 = nullptr;
     }
     if (on_hip && t_on_hip) RQ_TRY(tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram));
-    RQ_TRY(small_q(V2, L.lds_small, b, Q2, ldt, L));
+    if (q2_par) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_q2, 0));
+    else RQ_TRY(small_q(V2, L.lds_small, b, Q2, ldt, L));
     phase(11);
     if (refl_piv)
       RQ_CUDA_TRY(cudaMemcpyAsync(rfactors.back().phat, L.cap, (size_t)b * sizeof(int), cudaMemcpyDeviceToDevice,
@@ -1530,6 +1543,8 @@ Ctx::~Ctx() {
   if (ev_l0) cudaEventDestroy(ev_l0);
   if (ev_aux) cudaEventDestroy(ev_aux);
   if (ev_w2) cudaEventDestroy(ev_w2);
+  if (hip2) cudaStreamDestroy(hip2);
+  if (ev_q2) cudaEventDestroy(ev_q2);
   if (barriers) cudaFree(barriers);
 }
 

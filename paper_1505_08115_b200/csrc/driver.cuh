@@ -116,6 +116,8 @@ struct Ctx {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_l0 = nullptr, ev_aux = nullptr;
   cudaEvent_t ev_w2 = nullptr;  // look-ahead: W2 = T^T W formed on the side stream
+  cudaStream_t hip2 = nullptr;  // second highest-priority stream (Q2 beside G1')
+  cudaEvent_t ev_q2 = nullptr;
   bool w2_side = false;
   bool overlap_on = true;
   // called (host side, enqueue order) when columns [s, s + w) of R are final: no later step
