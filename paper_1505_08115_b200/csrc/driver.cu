@@ -335,6 +335,8 @@ int Ctx::ensure_side() {
   RQ_CUDA_TRY(cudaStreamCreateWithPriority(&hip, cudaStreamNonBlocking, hi));
   RQ_CUDA_TRY(cudaStreamCreateWithPriority(&hip2, cudaStreamNonBlocking, hi));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_q2, cudaEventDisableTiming));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_gram, cudaEventDisableTiming));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_t, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_v, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_hi, cudaEventDisableTiming));
@@ -863,13 +865,35 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
           gemm_pdl = false;
           gemm_max_ctas = 0;
           side_phase(1);
+          // the panel's T: its Gram GEMM here (whole GPU, short), its latency-bound triangular
+          // inverse on the second high-priority stream beside the rest of W (RQ_TINV_HIP=1;
+          // measured neutral to slightly slower: n = 10k 143.8 vs 144.6 ms, so off)
+          static const int env_th = [] {
+            const char* e = getenv("RQ_TINV_HIP");
+            return e ? atoi(e) : 0;
+          }();
+          tinv_par = rc == RQ_OK && env_th != 0 && hip2 != nullptr && !t_done && !(t_on_hip && hip_tail) &&
+                     n_a < n2;
+          if (tinv_par) {
+            CatGuard gt(cat, PROF_TFACTOR);
+            const int64_t ldg2 = even(b);
+            rc = gemm(b, b, mp, op(V, mp + vpad, b, ldv, vpad), false, op(V, mp + vpad, b, ldv, vpad), L.gram2, ldg2,
+                      1.0, 0.0);
+            if (rc == RQ_OK) rc = cudaEventRecord(ev_gram, side) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "ev");
+            if (rc == RQ_OK) rc = cudaStreamWaitEvent(hip2, ev_gram, 0) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "w");
+            if (rc == RQ_OK) rc = tfactor_from_gram(L.gram2, ldg2, b, T, even(b), hip2, &launches);
+            if (rc == RQ_OK) rc = cudaEventRecord(ev_t, hip2) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "ev");
+          }
           if (rc == RQ_OK && n_a < n2)
             rc = gemm(b, n2 - n_a, mp, op(V, mp + vpad, b, ldv, vpad), false, op(A, m, n, lda, s, s + b + n_a),
                       L.wside + n_a * even(b), even(b), 1.0, 0.0);
         }
         gemm_pdl = false;
         side_phase(2);
-        if (rc == RQ_OK && !t_done && !(t_on_hip && hip_tail)) rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
+        if (rc == RQ_OK && !t_done && !(t_on_hip && hip_tail) && !tinv_par)
+          rc = tfactor(V, mp, b, ldv, vpad, T, even(b), L.gram2);
+        if (rc == RQ_OK && tinv_par)  // T done on hip2: the side stream's completion includes it
+          rc = cudaStreamWaitEvent(side, ev_t, 0) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "w");
         side_phase(3);
         if (rc == RQ_OK) rc = cudaEventRecord(ev_side, side) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
         // look-ahead: W2 = T^T W (needed only by the trailing update of the rows below the top,
@@ -1545,6 +1569,8 @@ Ctx::~Ctx() {
   if (ev_w2) cudaEventDestroy(ev_w2);
   if (hip2) cudaStreamDestroy(hip2);
   if (ev_q2) cudaEventDestroy(ev_q2);
+  if (ev_gram) cudaEventDestroy(ev_gram);
+  if (ev_t) cudaEventDestroy(ev_t);
   if (barriers) cudaFree(barriers);
 }
 

@@ -117,7 +117,8 @@ struct Ctx {
   cudaEvent_t ev_l0 = nullptr, ev_aux = nullptr;
   cudaEvent_t ev_w2 = nullptr;  // look-ahead: W2 = T^T W formed on the side stream
   cudaStream_t hip2 = nullptr;  // second highest-priority stream (Q2 beside G1')
-  cudaEvent_t ev_q2 = nullptr;
+  cudaEvent_t ev_q2 = nullptr, ev_gram = nullptr, ev_t = nullptr;
+  bool tinv_par = false;  // the panel's T inverse on hip2 beside the rest of W
   bool w2_side = false;
   bool overlap_on = true;
   // called (host side, enqueue order) when columns [s, s + w) of R are final: no later step
