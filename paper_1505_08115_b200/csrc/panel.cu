@@ -278,6 +278,11 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
   __shared__ double scal[4];                      // refl, beta, h*inv, inv
   __shared__ double Ts[16][17];
   __shared__ __align__(8) unsigned long long lmbar[2];  // pushes of step j complete on lmbar[j & 1]
+  // T is formed once per leaf, after the column loop: every CTA's partial Gram V_own^T V_own
+  // (the 120 pairs k < l) is pushed to rank 0, which sums them in rank order and runs the T
+  // recurrence -- none of it on the per-column critical path any more
+  __shared__ double gin[16][120];
+  __shared__ __align__(8) unsigned long long gbar;
   constexpr unsigned CS = 16;  // launch_leaf_reg: one 16-CTA cluster
   // look-ahead (driver.cu): a chunk of the previous panel's trailing update launched after this
   // kernel with programmatic stream serialization starts once the cluster is resident, on the
@@ -309,17 +314,18 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
   if (threadIdx.x == 0) {
     mbar_init(&lmbar[0], 1);
     mbar_init(&lmbar[1], 1);
+    mbar_init(&gbar, 1);
     mbar_init_fence();
   }
   __syncthreads();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 
-  for (int j = 0; j <= w; j++) {
-    const bool final_round = (j == w);
+  for (int j = 0; j < w; j++) {
+    const bool final_round = false;
     const int par = j & 1;
     leaf_stamp(j, 0);
-    // this step's pushes: 32 partial sums from every CTA, plus row j from its owner
-    if (threadIdx.x == 0) mbar_expect_tx(&lmbar[par], CS * 32 * 8 + (final_round ? 0 : 16 * 8));
+    // this step's pushes: 16 partial sums from every CTA, plus row j from its owner
+    if (threadIdx.x == 0) mbar_expect_tx(&lmbar[par], CS * 16 * 8 + 16 * 8);
     // ---- apply the pending reflector j-1 to the window (columns j..) ----
     if (refl_prev && !final_round) {
       double s[WL];
@@ -330,36 +336,23 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
 #pragma unroll
         for (int o = 0; o < WL; o++) x[q][o] -= s[o] * uprev[q];
     }
-    // ---- partials: dv[o] = sum x_j x_{j+o} (o = 0: tail), gv[k] = V_k . u_{j-1} ----
-    double dv[16], gv[16];
+    // ---- partials: dv[o] = sum x_j x_{j+o} (o = 0: tail) ----
+    double dv[16];
 #pragma unroll
-    for (int e = 0; e < 16; e++) {
-      dv[e] = 0.0;
-      gv[e] = 0.0;
-    }
+    for (int e = 0; e < 16; e++) dv[e] = 0.0;
 #pragma unroll
     for (int q = 0; q < RPT; q++) {
-      if (grow[q] > j && grow[q] < mm && !final_round) {
+      if (grow[q] > j && grow[q] < mm) {
 #pragma unroll
         for (int o = 0; o < WL; o++) dv[o] += x[q][0] * x[q][o];
       }
-      if (j >= 2) {
-        const int lr = threadIdx.x + LR_THREADS * q;
-#pragma unroll
-        for (int k = 0; k < WL; k++)
-          if (k < j - 1) gv[k] += Vs[k * VLD + lr] * uprev[q];
-      }
-      if (grow[q] == j && !final_round)
+      if (grow[q] == j)
 #pragma unroll
         for (int o = 0; o < WL; o++) rowj[o] = x[q][o];
     }
     leaf_stamp(j, 1);
     const double dsum = warp_reduce_scatter16(dv, lane);
-    const double gsum = warp_reduce_scatter16(gv, lane);
-    if (lane < 16) {
-      wpart[warp][lane] = dsum;
-      wpart[warp][16 + lane] = gsum;
-    }
+    if (lane < 16) wpart[warp][lane] = dsum;
     leaf_stamp(j, 2);
     __syncthreads();
     leaf_stamp(j, 3);
@@ -377,34 +370,22 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
 #pragma unroll
       for (unsigned dst = warp; dst < CS; dst += LR_WARPS) {
         const uint32_t mb = cluster_map(mb_l, dst);
-        st_async_f64(cluster_map(pin_l, dst), sum, mb);
+        if (lane < 16) st_async_f64(cluster_map(pin_l, dst), sum, mb);
         if (owner && lane < 16) st_async_f64(cluster_map(row_l, dst), rv, mb);
       }
     }
     leaf_stamp(j, 4);
-    // warps 0 and 1 consume the pushed partials; the others meet them at the __syncthreads below
-    if (warp <= 1) mbar_wait_cluster(&lmbar[par], (unsigned)(j >> 1) & 1u);
+    // warp 0 consumes the pushed partials; the others meet it at the __syncthreads below
+    if (warp == 0) mbar_wait_cluster(&lmbar[par], (unsigned)(j >> 1) & 1u);
     leaf_stamp(j, 5);
-    if (warp <= 1) {
+    if (warp == 0) {
       double t = 0.0;
       double pv[CS];
 #pragma unroll
-      for (unsigned r = 0; r < CS; r++) pv[r] = pin[par][r][lane];
+      for (unsigned r = 0; r < CS; r++) pv[r] = (lane < 16) ? pin[par][r][lane] : 0.0;
 #pragma unroll
       for (unsigned r = 0; r < CS; r++) t += pv[r];  // rank order
-      if (warp == 1) {
-        // T column j-1 from the Gram totals (lanes 16.. hold gram k = lane - 16); off the critical path
-        if (j >= 1) {
-          const int jc = j - 1;
-          double tcol = 0.0;
-          for (int kk = jc - 1; kk >= 0; kk--) {
-            const double g = __shfl_sync(0xffffffffu, t, 16 + kk);
-            if (lane <= kk) tcol += Ts[lane][kk] * g;
-          }
-          if (lane < jc) Ts[lane][jc] = -2.0 * tcol;
-          if (lane == 0) Ts[jc][jc] = 2.0;
-        }
-      } else if (!final_round) {
+      {
         // row j entries (window order), pushed by the CTA that owns row j
         const double rj = (lane < 16 && j + lane < w) ? rowp[par][lane] : 0.0;
         const double tail = __shfl_sync(0xffffffffu, t, 0);
@@ -461,8 +442,48 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
     if (grow[q] < mm)
       for (int c = 0; c < w; c++) v[(int64_t)c * ldv + grow[q]] = Vs[c * VLD + lr];
   }
-  if (rank == 0 && tl)
-    for (int e = threadIdx.x; e < w * w; e += LR_THREADS) tl[(int64_t)(e / w) * ldt + e % w] = Ts[e % w][e / w];
+  // ---- T (w x w): T_jj = 2, T(0:j, j) = -2 T(0:j, 0:j) (V(:, 0:j)^T u_j), from the Gram ----
+  if (tl) {
+    if (rank == 0 && threadIdx.x == 0) mbar_expect_tx(&gbar, CS * 120 * 8);
+    // pairs p <-> (k, l), k < l < 16, l-major; warp w sums pairs w, w + 8, ... over its CTA's rows
+    const uint32_t gin_l = smem_u32(&gin[rank][0]);
+    const uint32_t gb0 = cluster_map(smem_u32(&gbar), 0u);
+    for (int p = warp; p < 120; p += LR_WARPS) {
+      int l = 1;
+      while (l * (l + 1) / 2 <= p) l++;
+      const int k = p - l * (l - 1) / 2;
+      double acc = 0.0;
+      if (l < w)
+        for (int i = lane; i < VLD; i += 32) acc = fma(Vs[k * VLD + i], Vs[l * VLD + i], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) st_async_f64(cluster_map(gin_l + 8 * p, 0u), acc, gb0);
+    }
+    if (rank == 0) {
+      // Gram entries g(k, l): the 16 partials summed in rank order, one pair per thread
+      mbar_wait_cluster(&gbar, 0u);
+      if (threadIdx.x < 120) {
+        double g = 0.0;
+#pragma unroll
+        for (unsigned r = 0; r < CS; r++) g += gin[r][threadIdx.x];
+        gin[0][threadIdx.x] = g;  // (own slot: every read of this pair is done)
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // T column by column (lane = row): T(0:jc, jc) = -2 T(0:jc, 0:jc) g(0:jc, jc)
+        for (int jc = 0; jc < w; jc++) {
+          double tcol = 0.0;
+          const int p0 = jc * (jc - 1) / 2;
+          for (int kk = jc - 1; kk >= 0; kk--)
+            if (lane <= kk) tcol += Ts[lane][kk] * gin[0][p0 + kk];
+          if (lane < jc) Ts[lane][jc] = -2.0 * tcol;
+          if (lane == jc) Ts[jc][jc] = 2.0;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < w * w; e += LR_THREADS) tl[(int64_t)(e / w) * ldt + e % w] = Ts[e % w][e / w];
+    }
+  }
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
