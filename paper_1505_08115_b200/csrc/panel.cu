@@ -321,13 +321,12 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 
   for (int j = 0; j < w; j++) {
-    const bool final_round = false;
     const int par = j & 1;
     leaf_stamp(j, 0);
     // this step's pushes: 16 partial sums from every CTA, plus row j from its owner
     if (threadIdx.x == 0) mbar_expect_tx(&lmbar[par], CS * 16 * 8 + 16 * 8);
     // ---- apply the pending reflector j-1 to the window (columns j..) ----
-    if (refl_prev && !final_round) {
+    if (refl_prev) {
       double s[WL];
 #pragma unroll
       for (int o = 0; o < WL; o++) s[o] = sc[o + 1];  // window shifted by one since step j-1
@@ -362,7 +361,7 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
       double sum = 0.0;
 #pragma unroll
       for (int ww = 0; ww < LR_WARPS; ww++) sum += wpart[ww][lane];
-      const bool owner = !final_round && (unsigned)(j / rows_per) == rank;  // this CTA holds row j
+      const bool owner = (unsigned)(j / rows_per) == rank;  // this CTA holds row j
       const double rv = (owner && lane < 16) ? rowj[lane] : 0.0;
       const uint32_t pin_l = smem_u32(&pin[par][rank][lane]);
       const uint32_t row_l = smem_u32(&rowp[par][lane & 15]);
@@ -410,7 +409,6 @@ __global__ void __launch_bounds__(LR_THREADS, 1) leaf_reg_kernel(double* __restr
         }
       }
     }
-    if (final_round) break;
     leaf_stamp(j, 6);
     __syncthreads();
     leaf_stamp(j, 7);
