@@ -10,6 +10,9 @@ covers inputs without fixtures.  Bars (BASELINE.json north_star):
   * ||AP - QR||_F <= 1e-13 ||A||_F and ||Q^T Q - I||_F <= 1e-13 sqrt(n).
 """
 
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -449,3 +452,46 @@ def test_cfg5_size_n40k_properties(rq):
     assert float(torch.linalg.norm(ax - qm @ rx) / (anorm * torch.linalg.norm(x))) <= 1e-13
     y = torch.randn(n, 2, dtype=torch.float64, device=a0.device, generator=g)
     assert float(torch.linalg.norm(qm.T @ (qm @ y) - y) / torch.linalg.norm(y)) <= 1e-13 * np.sqrt(n)
+
+
+_SPACE_SCRIPT = r"""
+import ctypes, sys
+import numpy as np, torch
+sys.path.insert(0, ".")
+import paper_1505_08115_b200 as rq
+from paper_1505_08115_b200 import _lib
+from paper_1505_08115_b200.errors import check
+m, n, b, p = (int(x) for x in sys.argv[1:5])
+eng = rq.Engine()
+a0, ld = rq.gaussian_matrix_device(m, n, rq.RngState(4), engine=eng)
+out = []
+for flags in (0, _lib.RQ_FLAG_NO_LOOKAHEAD):
+    work = a0.clone()
+    perm = torch.empty(n, dtype=torch.int64, device=a0.device)
+    cfg = _lib.rq_config(b, p, 0, -1, _lib.RQ_PIVOT_PERMUTATION, 0, _lib.RQ_SKETCH_DOWNDATE, flags)
+    ctr = ctypes.c_uint64(0)
+    check(eng.lib.rq_factorize(eng.handle, ctypes.byref(cfg), m, n, ctypes.c_void_p(work.data_ptr()), ld,
+                               ctypes.c_uint64(1), ctypes.byref(ctr), ctypes.c_void_p(perm.data_ptr())))
+    out.append((perm.cpu(), work[:n, :m].T.cpu()))
+same = torch.equal(out[0][0], out[1][0])
+err = float((out[0][1] - out[1][1]).abs().max() / torch.linalg.norm(a0[:n, :m]))
+print("RESULT", int(same), err)
+"""
+
+
+@pytest.mark.parametrize("m,n,b,p", [(3000, 3000, 256, 16), (3300, 3000, 200, 10), (4100, 4000, 96, 8)])
+def test_space_sliced_lookahead_matches_plain_schedule(m, n, b, p):
+    """The space-sliced look-ahead forced on every panel (RQ_LA_SPACE=1: the trailing update as
+    one 132-CTA launch, leaves + 16-CTA cluster WY updates + T and G1' on the aux stream) on
+    tall / non-multiple-of-b shapes factors like the plain panel order: identical pivots,
+    R within 1e-13 ||A||."""
+    import subprocess
+
+    env = dict(os.environ, RQ_LA_SPACE="1", RQ_T_AUX="1")
+    root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
+    res = subprocess.run([sys.executable, "-c", _SPACE_SCRIPT, str(m), str(n), str(b), str(p)], env=env, cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = [ln for ln in res.stdout.splitlines() if ln.startswith("RESULT")][-1].split()
+    assert line[1] == "1"
+    assert float(line[2]) <= 1e-13
