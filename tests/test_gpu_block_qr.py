@@ -331,20 +331,24 @@ def test_bench_workload_n10k_properties_and_leading_pivots(rq):
     assert rng.counter == sum((n - s) * (b + p) for s in range(0, n - b, b))
 
 
-@pytest.mark.parametrize("m,n,b,p,kind", [(700, 650, 64, 8, "permutation"), (520, 500, 96, 10, "reflectors")])
+@pytest.mark.parametrize("m,n,b,p,kind", [(700, 650, 64, 8, "permutation"), (520, 500, 96, 10, "reflectors"),
+                                          (700, 650, 64, 8, "downdate"), (3000, 3000, 256, 16, "downdate")])
 def test_host_entry_streams_r_identically(rq, m, n, b, p, kind):
     """rq_factorize_host (host buffers, R streamed back panel by panel while later panels
-    compute) returns exactly the device path's R and permutation."""
+    compute -- with the downdated sketch from the look-ahead's high-priority stream) returns
+    exactly the device path's R and permutation."""
     import ctypes
 
     from paper_1505_08115_b200 import _lib
     from paper_1505_08115_b200.errors import check
 
     a = np.asfortranarray(np.random.default_rng(m + n).standard_normal((m, n)))
-    f = rq.block_qr(a, _cfg(rq, b, p, 0, refl=(kind == "reflectors")), rq.RngState(3))
+    dd = kind == "downdate"
+    f = rq.block_qr(a, _cfg(rq, b, p, 0, refl=(kind == "reflectors")), rq.RngState(3),
+                    **({"sketch": "downdate"} if dd else {}))
     eng = rq.Engine()
-    pk = _lib.RQ_PIVOT_PERMUTATION if kind == "permutation" else _lib.RQ_PIVOT_REFLECTORS
-    cfg = _lib.rq_config(b, p, 0, -1, pk, 0, _lib.RQ_SKETCH_FRESH, 0)
+    pk = _lib.RQ_PIVOT_REFLECTORS if kind == "reflectors" else _lib.RQ_PIVOT_PERMUTATION
+    cfg = _lib.rq_config(b, p, 0, -1, pk, 0, _lib.RQ_SKETCH_DOWNDATE if dd else _lib.RQ_SKETCH_FRESH, 0)
     hr = np.zeros((m, n), order="F")
     hp = np.zeros(n, dtype=np.int64)
     ctr = ctypes.c_uint64(0)
@@ -352,7 +356,7 @@ def test_host_entry_streams_r_identically(rq, m, n, b, p, kind):
                                     ctypes.c_uint64(3), ctypes.byref(ctr), hr.ctypes.data_as(ctypes.c_void_p), m,
                                     hp.ctypes.data_as(ctypes.c_void_p)))
     assert np.array_equal(np.triu(hr), f.r)
-    if kind == "permutation":
+    if kind != "reflectors":
         assert np.array_equal(hp, f.perm)
 
 
