@@ -1079,6 +1079,56 @@ RQ_DEV void ld_ll2(const unsigned long long* p, unsigned long long& a, unsigned 
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
+// Warp sums of P values at once (P a power of two <= 16): a reduce-scatter butterfly (each
+// round a lane sends the half of its values its xor-partner keeps, so P - 1 shuffles instead of
+// 5 P over the first log2 P rounds, one value per round after that), then every lane reads each
+// total from the lane that owns it.  Every lane ends with the same bits of every sum.
+template <int P, int OFF, int N>
+RQ_DEV void warp_sum_pow2(double (&v)[N], int lane) {
+  constexpr int LOGP = P >= 16 ? 4 : P >= 8 ? 3 : P >= 4 ? 2 : P >= 2 ? 1 : 0;
+  double w[P];
+#pragma unroll
+  for (int i = 0; i < P; i++) w[i] = v[OFF + i];
+#pragma unroll
+  for (int r = 0; r < 5; r++) {
+    const int o = 16 >> r;
+    const int c = P >> r;  // values still held (0 or 1: the plain butterfly)
+    if (c >= 2) {
+      const int h = c / 2;
+      const bool hi = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < h; i++) {
+        const double send = hi ? w[i] : w[i + h];
+        const double keep = hi ? w[i + h] : w[i];
+        w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    } else {
+      w[0] += __shfl_xor_sync(0xffffffffu, w[0], o);
+    }
+  }
+  if constexpr (P == 1) {
+    v[OFF] = w[0];
+  } else {
+#pragma unroll
+    for (int q = 0; q < P; q++) {
+      int src = 0;
+#pragma unroll
+      for (int r = 0; r < LOGP; r++) src |= ((q >> (LOGP - 1 - r)) & 1) << (4 - r);
+      v[OFF + q] = __shfl_sync(0xffffffffu, w[0], src);
+    }
+  }
+}
+
+// Warp sums of v[OFF..OFF+C), split into power-of-two groups (C = 9: 8 + 1).
+template <int C, int OFF, int N>
+RQ_DEV void warp_sum_all(double (&v)[N], int lane) {
+  if constexpr (C > 0) {
+    constexpr int P = C >= 16 ? 16 : C >= 8 ? 8 : C >= 4 ? 4 : C >= 2 ? 2 : 1;
+    warp_sum_pow2<P, OFF, N>(v, lane);
+    warp_sum_all<C - P, OFF + P, N>(v, lane);
+  }
+}
+
 // Apply the pending reflector u (rows >= 32*K0 may be non-zero; u is exactly 0
 // above the reflector row and below m) to every column the warp owns.
 template <int K0, int RPL, int CPW>
@@ -1094,10 +1144,7 @@ RQ_DEV void sk_apply(double (&x)[CPW][RPL], const bool (&act)[CPW], const double
     for (int k = K0; k < RPL; k++) acc = fma(uk[k], x[q][k], acc);
     d[q] = acc;
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int q = 0; q < CPW; q++) d[q] += __shfl_xor_sync(0xffffffffu, d[q], o);
+  warp_sum_all<CPW, 0, CPW>(d, lane);
 #pragma unroll
   for (int q = 0; q < CPW; q++) {
     const double dd = act[q] ? 2.0 * d[q] : 0.0;
@@ -1123,20 +1170,15 @@ RQ_DEV void sk_apply1(double (&y)[RPL], const double* u, int lane) {
 // reductions interleave, halving the latency-bound chain of the shared-memory tier.
 template <int K0, int RPL>
 RQ_DEV void sk_apply2(double (&y0)[RPL], double (&y1)[RPL], const double* u, int lane) {
-  double d0 = 0.0, d1 = 0.0;
+  double dd[2] = {0.0, 0.0};
 #pragma unroll
   for (int k = K0; k < RPL; k++) {
     const double uk = u[lane + 32 * k];
-    d0 = fma(uk, y0[k], d0);
-    d1 = fma(uk, y1[k], d1);
+    dd[0] = fma(uk, y0[k], dd[0]);
+    dd[1] = fma(uk, y1[k], dd[1]);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    d0 += __shfl_xor_sync(0xffffffffu, d0, o);
-    d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-  }
-  d0 *= 2.0;
-  d1 *= 2.0;
+  warp_sum_all<2, 0, 2>(dd, lane);
+  const double d0 = 2.0 * dd[0], d1 = 2.0 * dd[1];
 #pragma unroll
   for (int k = K0; k < RPL; k++) {
     const double uk = u[lane + 32 * k];
@@ -1208,10 +1250,7 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
       for (int k = KJ + 1; k < RPL; k++) acc = fma(x[q][k], x[q][k], acc);
       t[q] = acc;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int q = 0; q < CPW; q++) t[q] += __shfl_xor_sync(0xffffffffu, t[q], o);
+    warp_sum_all<CPW, 0, CPW>(t, lane);
     double bkey = -1.0;
     int bpos = INT_MAX, bq = -1;
 #pragma unroll
@@ -1244,17 +1283,14 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
           else sk_apply2<KJ, RPL>(y0, y1, u, lane);
         }
         const double yv0 = at_or_below ? y0[KJ] : 0.0, yv1 = at_or_below ? y1[KJ] : 0.0;
-        double t0 = yv0 * yv0, t1 = yv1 * yv1;
+        double tt[2] = {yv0 * yv0, yv1 * yv1};
 #pragma unroll
         for (int k = KJ + 1; k < RPL; k++) {
-          t0 = fma(y0[k], y0[k], t0);
-          t1 = fma(y1[k], y1[k], t1);
+          tt[0] = fma(y0[k], y0[k], tt[0]);
+          tt[1] = fma(y1[k], y1[k], tt[1]);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          t0 += __shfl_xor_sync(0xffffffffu, t0, o);
-          t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-        }
+        warp_sum_all<2, 0, 2>(tt, lane);
+        const double t0 = tt[0], t1 = tt[1];
         if (a0) {
 #pragma unroll
           for (int k = KL; k < RPL; k++) col0[k * 32] = y0[k];
