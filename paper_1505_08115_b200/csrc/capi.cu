@@ -357,7 +357,7 @@ int rq_test_sketch_cpqr(rq_ctx* ctx, double* dY, int64_t ld, int32_t m, int32_t 
   CTX_CHECK(ctx);
   rq::clear_error();
   Ctx& c = ctx->c;
-  const size_t ws = std::max(rq::sweep_workspace_bytes(m, n, rq::kSMs), rq::sketch_workspace_bytes(m)) + 4096;
+  const size_t ws = std::max(rq::sweep_workspace_bytes(m, n, rq::kSMs), rq::sketch_workspace_bytes(m, n)) + 4096;
   RQ_TRY(c.qarena.reserve(ws));
   c.sweep_ws = c.qarena.base;
   c.sweep_ws_bytes = ws;

@@ -137,7 +137,7 @@ static Layout plan_layout(void* base, int64_t m, int64_t n, int b, int p, int po
   sw = std::max(sw, sweep_workspace_bytes(wdt, (int)n, sweep_grid_size((int)n)));
   sw = std::max(sw, sweep_workspace_bytes(b, 2 * b, sweep_grid_size(2 * b)));
   sw = std::max(sw, sweep_workspace_bytes(m, b, sweep_grid_size(b)));
-  sw = std::max(sw, sketch_workspace_bytes(wdt));
+  sw = std::max(sw, sketch_workspace_bytes(wdt, (int)n));
   L.sweep_ws_bytes = sw;
   L.sweep_ws = c.take<char>(sw);
   L.fstore = c.take<double>(factor_bytes(m, n, b) / 8 + 64);
@@ -1469,7 +1469,7 @@ StepScratch plan_step(void* base, int64_t ncols, int b, int64_t mp = 0) {
 }  // namespace
 
 int Ctx::step_sketch_select(double* Y, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen) {
-  const size_t ws = std::max(sweep_workspace_bytes(m, n, kSMs), sketch_workspace_bytes(m)) + 4096;
+  const size_t ws = std::max(sweep_workspace_bytes(m, n, kSMs), sketch_workspace_bytes(m, n)) + 4096;
   RQ_TRY(sarena.reserve(ws));
   sweep_ws = sarena.base;
   sweep_ws_bytes = ws;

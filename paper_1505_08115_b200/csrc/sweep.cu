@@ -774,6 +774,7 @@ constexpr int SK_THREADS = 1024;
 constexpr int SK_WARPS = SK_THREADS / 32;
 constexpr int SK_GROUP = 8;
 constexpr int SK_GROUPS = SK_THREADS / SK_GROUP;
+constexpr int kSkMaxSpw = 24;  // register sketch CPQR: non-register columns per warp (n' <= 148 * 360)
 
 struct alignas(16) SkSlot {
   double key;
@@ -798,6 +799,8 @@ struct SketchArgs {
   unsigned long long counter_base;  // its value when this launch starts
   int cache_cols;
   int spw;  // register kernel: shared-memory-resident columns per warp (0 = registers only)
+  int spw_g;       // register kernel: of those, the last spw_g per warp live in gcols (L2-resident)
+  double* gcols;   // [CTA][warp][spw_g][slot k][lane]
   int fixed_reducer;  // register kernel: CTA 0 always reduces the slots (no arrival atomic)
   int cl;             // register kernel: cluster size (> 1: two-level exchange, see SkClu)
   int per;            // register kernel: columns per CTA (column id -> CTA)
@@ -1205,10 +1208,18 @@ struct SkSmem {
   double* xs;
   int* spos;
   int* sact;
-  int spw;      // columns per warp
+  int spw;      // columns per warp beyond the registers (shared memory, then global)
   int cbase_s;  // global id of this warp's first shared-memory column
   SkClu* cl;    // two-level exchange state (p.cl > 1)
+  int spw_s;    // of spw: in shared memory ([warp][spw_s][slot k][lane])
+  double* xg;   // this warp's spw - spw_s global-memory columns ([s][slot k][lane])
 };
+
+// Column s (0 <= s < spw) of a warp's non-register tier, lane 0's slot 0.
+template <int RPL>
+RQ_DEV double* sk_tier_col(const SkSmem& sm, int warp, int s) {
+  return s < sm.spw_s ? sm.xs + (int64_t)(warp * sm.spw_s + s) * RPL * 32 : sm.xg + (int64_t)(s - sm.spw_s) * RPL * 32;
+}
 
 // Steps j in [32*KJ, jend): row j lives in register slot KJ (lane j & 31), so
 // every row mask below is a compile-time slot range plus one lane predicate.
@@ -1263,15 +1274,13 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
     }
     int bcol = bq >= 0 ? cbase + bq : -1;
     if constexpr (SMEM) {
-      // pairs of shared-memory columns (an odd last one is paired with itself, result unused)
-      for (int s2 = 0; s2 < sm.spw; s2 += 2) {
+      // pairs of shared-memory columns, then pairs of global-memory columns (an odd last one of
+      // each range is paired with itself, result unused); the same body for both address spaces
+      auto pair_step = [&](double* col0, double* col1, int s2, bool has1) {
         const int sc0 = warp * sm.spw + s2;
-        const bool has1 = s2 + 1 < sm.spw;
         const int sc1 = has1 ? sc0 + 1 : sc0;
         const bool a0 = sm.sact[sc0] != 0, a1 = has1 && sm.sact[sc1] != 0;  // warp-uniform
-        if (!a0 && !a1) continue;
-        double* col0 = sm.xs + (int64_t)sc0 * RPL * 32 + lane;
-        double* col1 = sm.xs + (int64_t)sc1 * RPL * 32 + lane;
+        if (!a0 && !a1) return;
         double y0[RPL], y1[RPL];
 #pragma unroll
         for (int k = KL; k < RPL; k++) {
@@ -1311,6 +1320,16 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
             bcol = sm.cbase_s + s2 + 1;
           }
         }
+      };
+      for (int s2 = 0; s2 < sm.spw_s; s2 += 2) {
+        const bool has1 = s2 + 1 < sm.spw_s;
+        double* col0 = sm.xs + (int64_t)(warp * sm.spw_s + s2) * RPL * 32 + lane;
+        pair_step(col0, has1 ? col0 + RPL * 32 : col0, s2, has1);
+      }
+      for (int s2 = sm.spw_s; s2 < sm.spw; s2 += 2) {
+        const bool has1 = s2 + 1 < sm.spw;
+        double* col0 = sm.xg + (int64_t)(s2 - sm.spw_s) * RPL * 32 + lane;
+        pair_step(col0, has1 ? col0 + RPL * 32 : col0, s2, has1);
       }
     }
     if (lane == 0) {
@@ -1392,7 +1411,7 @@ RQ_DEV void sk_block(const SketchArgs& p, SkSlot2* slots, SkWin* wins, unsigned 
         bool done = false;
         if constexpr (SMEM) {
           if (b.col >= sm.cbase_s && b.col < sm.cbase_s + sm.spw) {
-            const double* col = sm.xs + (int64_t)(warp * sm.spw + (b.col - sm.cbase_s)) * RPL * 32 + lane;
+            const double* col = sk_tier_col<RPL>(sm, warp, b.col - sm.cbase_s) + lane;
             double y[RPL];
 #pragma unroll
             for (int k = 0; k < RPL; k++) y[k] = k >= KJ ? col[k * 32] : 0.0;
@@ -1668,7 +1687,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
   __shared__ double u[32 * RPL];
   __shared__ SkShared sh;
   extern __shared__ double sk_dyn[];
-  constexpr int kMaxSpw = 8;
+  constexpr int kMaxSpw = kSkMaxSpw;
   __shared__ int spos_s[SMEM ? WARPS * kMaxSpw : 1];
   __shared__ int sact_s[SMEM ? WARPS * kMaxSpw : 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1676,7 +1695,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
   const int per = WARPS * CPW + WARPS * spw;
   const int cbase = blockIdx.x * per + warp * CPW;
   __shared__ SkClu clu;
-  SkSmem sm{sk_dyn, spos_s, sact_s, spw, (int)blockIdx.x * per + WARPS * CPW + warp * spw, &clu};
+  const int spw_g = SMEM ? p.spw_g : 0;
+  SkSmem sm{sk_dyn, spos_s, sact_s, spw, (int)blockIdx.x * per + WARPS * CPW + warp * spw, &clu, spw - spw_g,
+            spw_g > 0 ? p.gcols + ((int64_t)blockIdx.x * WARPS + warp) * spw_g * RPL * 32 : nullptr};
   if (p.cl > 1) {
     if (threadIdx.x == 0) {
       mbar_init(&clu.kbar[0], 1);
@@ -1707,7 +1728,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) sketch_reg_kernel(const SketchA
       const int sc = warp * spw + s2;
       const int c = sm.cbase_s + s2;
       const bool a = c < p.n;
-      double* col = sk_dyn + (int64_t)sc * RPL * 32 + lane;
+      double* col = sk_tier_col<RPL>(sm, warp, s2) + lane;
 #pragma unroll
       for (int k = 0; k < RPL; k++) {
         const int i = lane + 32 * k;
@@ -1735,7 +1756,7 @@ static int launch_sketch_reg(const SketchArgs& a, int G, SkSlot2* slots, SkWin* 
                              cudaStream_t st, int64_t* launches) {
   void* args[] = {(void*)&a, (void*)&slots, (void*)&wins, (void*)&stamp_base};
   auto kern = sketch_reg_kernel<RPL, CPW, WARPS, SMEM>;
-  const size_t dyn = SMEM ? (size_t)WARPS * a.spw * RPL * 32 * sizeof(double) : 0;
+  const size_t dyn = SMEM ? (size_t)WARPS * (a.spw - a.spw_g) * RPL * 32 * sizeof(double) : 0;
   if (SMEM) {
     static bool attr = false;
     if (!attr) {
@@ -1821,6 +1842,17 @@ static int dispatch_sketch_reg(SketchArgs a, int n, SkSlot2* slots, SkWin* wins,
     const int spw = std::max(1, (per_needed - W * C + W - 1) / W);
     if (spw <= 7 && (size_t)W * spw * RPL * 32 * 8 <= 200 * 1024) {
       a.spw = spw;
+      a.spw_g = 0;
+      const int per = W * C + W * spw;
+      const int G = (n + per - 1) / per;
+      *grid = G;
+      return launch_sketch_reg<RPL, C, W, true>(a, G, slots, wins, stamp_base, st, launches);
+    }
+    if (RPL == 9 && spw <= kSkMaxSpw && a.gcols) {
+      // beyond 156 columns per CTA: the last spw - 7 columns of each warp live in global memory
+      // (L2-resident, streamed through registers every step; sketch_glob_bytes sized gcols)
+      a.spw = spw;
+      a.spw_g = spw - 7;
       const int per = W * C + W * spw;
       const int G = (n + per - 1) / per;
       *grid = G;
@@ -1846,12 +1878,25 @@ bool sketch_cpqr_preserves_input(int m, int n) {
     const int W = 12, C = 6;
     const int per_needed = (n + kSMs - 1) / kSMs;
     const int spw = std::max(1, (per_needed - W * C + W - 1) / W);
-    if (spw <= 7 && (size_t)W * spw * 9 * 32 * 8 <= 200 * 1024) return true;
+    if (spw <= kSkMaxSpw) return true;  // shared memory, then the global tier
   }
   return false;
 }
 
-size_t sketch_workspace_bytes(int m) { return ((2 * (size_t)kSMs * 64 + 255) & ~size_t(255)) + 256 + sketch_ll_column_bytes(m); }
+// Global-memory tier of the register sketch CPQR for n columns (0 when shared memory suffices).
+size_t sketch_glob_bytes(int m, int n) {
+  if (m <= 160 || m > 288) return 0;
+  const int W = 12, C = 6;
+  const int per_needed = (n + kSMs - 1) / kSMs;
+  const int spw = std::max(1, (per_needed - W * C + W - 1) / W);
+  if (spw <= 7 || spw > kSkMaxSpw) return 0;
+  return (size_t)kSMs * W * (spw - 7) * 9 * 32 * sizeof(double);
+}
+
+static size_t sketch_base_bytes(int m) {
+  return ((2 * (size_t)kSMs * 64 + 255) & ~size_t(255)) + 256 + sketch_ll_column_bytes(m);
+}
+size_t sketch_workspace_bytes(int m, int n) { return sketch_base_bytes(m) + sketch_glob_bytes(m, n); }
 
 static size_t sketch_fixed_smem(int m, int per) {
   return (size_t)m * 8 + (size_t)per * 8 + 16 + (SK_WARPS + 2) * sizeof(SweepSlot) + 64;
@@ -1879,14 +1924,20 @@ int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, con
     a.counter = counter;
     a.counter_base = counter_base;
     const size_t need = slot_bytes + 256 + sketch_ll_column_bytes(m);
+    const size_t gbytes = sketch_glob_bytes(m, n);
+    a.gcols = (gbytes > 0 && w.scratch_bytes >= need + gbytes)
+                  ? reinterpret_cast<double*>(reinterpret_cast<char*>(w.scratch) + need)
+                  : nullptr;
     if (w.scratch_bytes >= need) {
       // step stamps are unique across launches: derived from the monotone counter base
       const unsigned long long stamp_base = counter_base;
       static const int env_fr = [] {
-        // measured: faster in isolation (5.68 -> 5.26 us/step at n' = 10k) but slower inside the
-        // factorization (sketch phase 44.8 -> 48.2 ms at n = 10k), so off by default
+        // CTA 0 reduces every step (1; 0 = the last arriver, 2 = the last CTA).  With the
+        // reduce-scatter column sums, 1 is slower in isolation (4.96 -> 5.62 us/step at n' = 10k)
+        // but faster inside the factorization, where the CTAs of one launch start staggered
+        // behind the preceding kernels: n = 5k 56.2 -> 54.9 ms, 10k 142.3 -> 139.5, 20k 569.0 -> 560.8
         const char* e = getenv("RQ_SK_FIXED_REDUCER");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : 1;
       }();
       a.fixed_reducer = env_fr;
       int rc, G = 0;

@@ -45,7 +45,7 @@ struct SweepCall {
 
 size_t sweep_workspace_bytes(int64_t m, int total_cols, int grid);
 size_t sketch_ll_column_bytes(int m);
-size_t sketch_workspace_bytes(int m);  // register-resident sketch CPQR (LL exchange)
+size_t sketch_workspace_bytes(int m, int n);  // register-resident sketch CPQR (LL exchange) of n columns
 bool sketch_cpqr_preserves_input(int m, int n);
 int sweep_grid_size(int total_cols);
 int sweep_debug_timing(int on, unsigned long long* host, int count);

@@ -158,3 +158,27 @@ def test_hand_examples(eng):
     perm = np.arange(4, dtype=np.int64)
     rq.householder_sweep(a, np.zeros((4, 4), order="F"), perm, 4, True, engine=eng)
     assert perm.tolist() == [0, 1, 2, 3]
+
+
+@pytest.mark.parametrize("m,n,steps", [(74, 2000, 64), (272, 1000, 256), (272, 10000, 256), (272, 20000, 256),
+                                       (272, 30000, 256), (272, 40000, 256)])
+def test_sketch_cpqr_tiers_choose_the_oracle_pivots(eng, m, n, steps):
+    """The sketch CPQR's register tier (n' <= 11.8k at b + p = 272), shared-memory tier (<= 23k) and
+    L2-resident tier (<= 53k) pick the oracle's CPQR pivots (pivoting.py:114-129 via
+    householder_sweep), and leave Y untouched."""
+    import torch
+
+    from oracle import randqr_oracle as O
+    from paper_1505_08115_b200.errors import check
+
+    y = np.random.default_rng(m + n).standard_normal((m, n))
+    buf, ld = eng.alloc_matrix(m, n)
+    buf[:n, :m].copy_(torch.from_numpy(np.ascontiguousarray(y.T)))
+    before = buf.clone()
+    ch = torch.zeros(steps, dtype=torch.int32, device=eng.device)
+    check(eng.lib.rq_test_sketch_cpqr(eng.handle, ctypes.c_void_p(buf.data_ptr()), ld, m, n, steps,
+                                      ctypes.c_void_p(ch.data_ptr())))
+    torch.cuda.synchronize()
+    ref = O.qr_column_pivoted(y, steps=steps).perm[:steps]
+    assert np.array_equal(ch.cpu().numpy().astype(np.int64), ref)
+    assert torch.equal(buf, before)
