@@ -41,6 +41,9 @@ enum { RQ_PIVOT_PERMUTATION = 0, RQ_PIVOT_REFLECTORS = 1 };
 enum { RQ_SKETCH_FRESH = 0, RQ_SKETCH_DOWNDATE = 1 };
 
 typedef struct rq_ctx rq_ctx;
+/* The compact factors of one factorization, detached from its context
+ * (Factorization's q_transforms / p_transforms, blocked.py:122-149). */
+typedef struct rq_factors rq_factors;
 
 /* Mirrors BlockConfig (blocked.py:42-50) + SketchConfig (pivoting.py:28-51). */
 typedef struct rq_config {
@@ -93,9 +96,41 @@ int rq_form_q(rq_ctx* ctx, int64_t cols, double* dQ, int64_t ldq);
 /* Factorization.expand_p() (blocked.py:143-149): dP is n x n. */
 int rq_form_p(rq_ctx* ctx, double* dP, int64_t ldp);
 
+/* Ownership of a factorization's factors (blocked.py:122-149: each Factorization owns its
+ * transforms).  rq_factors_detach moves the context's stored factors -- and the device
+ * workspace they live in -- into a new rq_factors; the context's next factorization then
+ * reserves fresh workspace, so the detached factors stay valid until rq_factors_destroy.
+ * rq_factors_form_q / _form_p are rq_form_q / rq_form_p on detached factors (enqueued on
+ * ctx's stream; ctx must be on the device the factors live on). */
+int rq_factors_detach(rq_ctx* ctx, rq_factors** out);
+int rq_factors_destroy(rq_factors* f);
+int rq_factors_form_q(rq_ctx* ctx, const rq_factors* f, int64_t cols, double* dQ, int64_t ldq);
+int rq_factors_form_p(rq_ctx* ctx, const rq_factors* f, double* dP, int64_t ldp);
+
+/* Per-panel transforms (Factorization.q_transforms / p_transforms, blocked.py:77-119), for
+ * detached factors f or, with f = NULL, the context's stored factorization.
+ * rq_factors_info: which = 0 lists the left factors (offset s_i, reflector count), which = 1 the
+ * orthogonal right factors of reflector pivots (offset, width n - s_i; 0 entries for
+ * permutation pivots, whose per-panel orders follow from the composite permutation);
+ * *count receives the number of factors, the first min(count, cap) are written.
+ * rq_apply_q: X (m x cols) <- U_first ... U_{first+count-1} X (trans = 0) or its transpose
+ * applied (trans = 1), U_i = (I - V T V^T) diag(Q2, I) on rows s_i.. (QTransform.left_multiply).
+ * rq_apply_p: X (rows x n) <- X P_first ... P_{first+count-1} (RightTransform.right_multiply;
+ * reflector pivots only). */
+int rq_factors_info(rq_ctx* ctx, const rq_factors* f, int32_t which, int32_t cap, int64_t* offsets,
+                    int32_t* widths, int32_t* count);
+int rq_apply_q(rq_ctx* ctx, const rq_factors* f, int32_t first, int32_t count, int32_t trans, int64_t cols,
+               double* dX, int64_t ldx);
+int rq_apply_p(rq_ctx* ctx, const rq_factors* f, int32_t first, int32_t count, int64_t rows, double* dX,
+               int64_t ldx);
+
 /* Working matrix after the current panel, in the reference's column order
  * (the matrix `inspect` receives).  Host destination, m x n, ldh >= m. */
 int rq_snapshot(rq_ctx* ctx, double* hW, int64_t ldh);
+/* Test hook for the HQRRP downdate (RQ_SKETCH_DOWNDATE, inside the inspect callback): the
+ * downdated sketch of the trailing block, (b+p) x (n - s) into hY (ldh >= b+p), and the
+ * composite permutation so far (n entries, A[:, perm] = A P) into hperm; reference order. */
+int rq_snapshot_sketch(rq_ctx* ctx, double* hY, int64_t ldh, int64_t* hperm);
 
 /* Kernel-plugin level (backend.get_kernels(), backend.py:42-47):
  * householder_sweep(a, v, perm, steps, pivot) (_kernels_numpy.py:11-22) on

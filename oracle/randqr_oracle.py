@@ -536,7 +536,7 @@ def block_qr(a, cfg, rng, inspect=None, max_panels=None):
     return f
 
 
-def block_qr_downdate(a, cfg, rng):
+def block_qr_downdate(a, cfg, rng, form="pre"):
     """HQRRP downdated-sketch variant of block_qr (NOT in the reference package).
 
     Oracle for the B200 ``sketch="downdate"`` mode, restating the HQRRP
@@ -552,6 +552,11 @@ def block_qr_downdate(a, cfg, rng):
     G1 R12 = Y1' R'11^{-1} R'12 with Y1' the selected sketch columns before
     P-hat -- the same product without Q2 or P-hat (they agree in exact
     arithmetic; this restatement fixes the rounding the GPU path follows).
+
+    ``form="post"`` is the independent restatement of SURVEY section 8's derivation, in the
+    order it is written there: P-hat is applied to the sketch columns too, G1 = Y1 R11^{-1}
+    with the FINAL R11 (after the b x b CPQR), and Y2 -= G1 R12 with the final R12 (the top
+    b rows after the trailing update).  It shares no evaluation order with the GPU path.
     """
     from scipy.linalg import solve_triangular
 
@@ -579,6 +584,20 @@ def block_qr_downdate(a, cfg, rng):
         pivot = select_pivot_permutation(yt[:, start:].T, b)
         work[:, start:] = pivot.apply_right(work[:, start:])
         yt[:, start:] = yt[:, start:][:, pivot.order]
+        if form == "post":
+            res = qr_tall_pivoted(work[start:, start: start + b])
+            work[:start, start: start + b] = work[:start, start: start + b][:, res.perm]
+            work[start:, start: start + b] = res.r
+            work[start:, start + b:] = apply_wy_left(res.q, work[start:, start + b:], transposed=True)
+            y1 = yt[:, start: start + b][:, res.perm]
+            r11 = res.r[:b, :b]
+            g1 = solve_triangular(r11.T, y1.T, lower=True).T  # G1 = Y1 R11^{-1}
+            yt[:, start + b:] -= g1 @ work[start: start + b, start + b:]
+            f.q_transforms.append((start, res.q, None))
+            f.p_transforms.append((start, pivot))
+            f.p_transforms.append((start, PermPivot(res.perm)))
+            start += b
+            continue
         # G1' = Y1' R'11^{-1} from the unpivoted first stage (see the docstring)
         first = qr_unpivoted(work[start:, start: start + b])
         g1 = solve_triangular(first.r[:b, :b].T, yt[:, start: start + b].T, lower=True).T

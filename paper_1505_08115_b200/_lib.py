@@ -52,6 +52,14 @@ _SIGS = {
     "rq_form_q": (ctypes.c_int, [_vp, _i64, _vp, _i64]),
     "rq_form_p": (ctypes.c_int, [_vp, _vp, _i64]),
     "rq_snapshot": (ctypes.c_int, [_vp, _vp, _i64]),
+    "rq_snapshot_sketch": (ctypes.c_int, [_vp, _vp, _i64, _vp]),
+    "rq_factors_detach": (ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+    "rq_factors_destroy": (ctypes.c_int, [_vp]),
+    "rq_factors_form_q": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64]),
+    "rq_factors_form_p": (ctypes.c_int, [_vp, _vp, _vp, _i64]),
+    "rq_factors_info": (ctypes.c_int, [_vp, _vp, _i32, _i32, _vp, _vp, ctypes.POINTER(_i32)]),
+    "rq_apply_q": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i32, _i64, _vp, _i64]),
+    "rq_apply_p": (ctypes.c_int, [_vp, _vp, _i32, _i32, _i64, _vp, _i64]),
     "rq_householder_sweep": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _i32]),
     "rq_gaussian_matrix": (ctypes.c_int, [_vp, _i64, _i64, _u64, _u64, _vp, _i64]),
     "rq_trinv_upper": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp, _i64]),

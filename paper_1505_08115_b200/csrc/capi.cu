@@ -81,7 +81,10 @@ static int validate(const rq_config* cfg, int64_t m, int64_t n, uint64_t* counte
   for (int64_t s = 0; n - s > b; s += b) {
     const int64_t np = n - s;
     if (wdt > np) {
-      if (counter && cfg->sketch_mode == RQ_SKETCH_FRESH) *counter += drawn;
+      // fresh: the panels before this one drew their Omegas (pivoting.py:100-101); downdate:
+      // G (m x (b+p)) is drawn before the panel loop (the oracle's block_qr_downdate, and
+      // dist.factorize_local), so the error comes after those m(b+p) draws
+      if (counter) *counter += cfg->sketch_mode == RQ_SKETCH_FRESH ? drawn : (uint64_t)m * (uint64_t)wdt;
       return rq::set_error(RQ_EVALUE, "sketch width %d exceeds the %lld columns being pivoted", wdt, (long long)np);
     }
     drawn += (uint64_t)(m - s) * (uint64_t)wdt;
@@ -114,6 +117,9 @@ int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, c
   CTX_CHECK(ctx);
   rq::clear_error();
   if (!counter) return rq::set_error(RQ_EVALUE, "null counter");
+  if (!hA) return rq::set_error(RQ_EVALUE, "null hA");
+  if (lda < m) return rq::set_error(RQ_EVALUE, "lda (%lld) < m (%lld)", (long long)lda, (long long)m);
+  if (hR && ldr < m) return rq::set_error(RQ_EVALUE, "ldr (%lld) < m (%lld)", (long long)ldr, (long long)m);
   RQ_TRY(validate(cfg, m, n, counter));
   Ctx& c = ctx->c;
   const int64_t ldd = rq::even(m);
@@ -127,26 +133,35 @@ int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, c
   int rc = RQ_OK;
   cudaError_t e = cudaMemcpy2DAsync(dA, ldd * 8, hA, lda * 8, m * 8, n, cudaMemcpyHostToDevice, c.stream);
   if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "H2D: %s", cudaGetErrorString(e));
-  // R streams back panel by panel on a copy stream while later panels compute
-  static thread_local cudaStream_t cs = nullptr;
-  static thread_local cudaEvent_t ev = nullptr;
-  if (rc == RQ_OK && hR && !cs) {
-    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+  // R streams back panel by panel on the context's copy stream (created on its device) while
+  // later panels compute
+  if (rc == RQ_OK && hR && !c.copy_stream) {
+    if (cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c.copy_ev, cudaEventDisableTiming) != cudaSuccess)
       rc = rq::set_error(RQ_ECUDA, "copy stream");
   }
-  int64_t copied = 0;  // columns [0, copied) queued
+  int64_t copied = 0;   // columns [0, copied) queued
+  bool streamed = false;
+  cudaError_t cb_err = cudaSuccess;  // first failure inside the callback
   if (rc == RQ_OK && hR) {
     c.on_cols_final = [&](int64_t s, int64_t w) {
-      if (s != copied) return;  // keep the watermark contiguous; the rest goes at the end
-      cudaEventRecord(ev, c.stream);
-      cudaStreamWaitEvent(cs, ev, 0);
-      cudaMemcpy2DAsync(hR + s * ldr, ldr * 8, dA + s * ldd, ldd * 8, m * 8, w, cudaMemcpyDeviceToHost, cs);
+      if (s != copied || cb_err != cudaSuccess) return;  // keep the watermark contiguous
+      cudaError_t x = cudaEventRecord(c.copy_ev, c.stream);
+      if (x == cudaSuccess) x = cudaStreamWaitEvent(c.copy_stream, c.copy_ev, 0);
+      if (x == cudaSuccess)
+        x = cudaMemcpy2DAsync(hR + s * ldr, ldr * 8, dA + s * ldd, ldd * 8, m * 8, w, cudaMemcpyDeviceToHost,
+                              c.copy_stream);
+      if (x != cudaSuccess) {
+        cb_err = x;
+        return;
+      }
+      streamed = true;
       copied = s + w;
     };
   }
   if (rc == RQ_OK) rc = rq_factorize(ctx, cfg, m, n, dA, ldd, seed, counter, dp);
   c.on_cols_final = nullptr;
+  if (rc == RQ_OK && cb_err != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "D2H (streamed R): %s", cudaGetErrorString(cb_err));
   if (rc == RQ_OK && hR && copied < n) {
     e = cudaMemcpy2DAsync(hR + copied * ldr, ldr * 8, dA + copied * ldd, ldd * 8, m * 8, n - copied,
                           cudaMemcpyDeviceToHost, c.stream);
@@ -156,36 +171,155 @@ int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, c
     e = cudaMemcpyAsync(hperm, dp, n * 8, cudaMemcpyDeviceToHost, c.stream);
     if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "D2H perm: %s", cudaGetErrorString(e));
   }
-  if (cs && copied > 0) {  // dA is freed on the main stream: after the streamed copies
-    cudaEventRecord(ev, cs);
-    cudaStreamWaitEvent(c.stream, ev, 0);
+  if (streamed) {  // the buffer is reused by the next call on the main stream: after the copies
+    e = cudaEventRecord(c.copy_ev, c.copy_stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.stream, c.copy_ev, 0);
+    if (rc == RQ_OK && e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "copy join: %s", cudaGetErrorString(e));
   }
   e = cudaStreamSynchronize(c.stream);
   if (rc == RQ_OK && e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "sync: %s", cudaGetErrorString(e));
+  if (streamed) {
+    e = cudaStreamSynchronize(c.copy_stream);
+    if (rc == RQ_OK && e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "copy sync: %s", cudaGetErrorString(e));
+  }
   return rc;
+}
+
+static int form_q_checked(Ctx& c, const rq::FactorSet& F, int64_t cols, double* dQ, int64_t ldq) {
+  if (!F.have) return rq::set_error(RQ_EVALUE, "no factorization stored in this context");
+  if (F.device != c.device) return rq::set_error(RQ_EVALUE, "the factors live on device %d, the context on %d",
+                                                 F.device, c.device);
+  if (cols < F.fn || cols > F.fm)
+    return rq::set_error(RQ_EDIM, "cols must lie in [%lld, %lld]", (long long)F.fn, (long long)F.fm);
+  if (ldq < F.fm || (ldq & 1) || ((uintptr_t)dQ & 15))
+    return rq::set_error(RQ_EVALUE, "dQ must be 16-byte aligned with an even ldq >= m");
+  return c.form_q(F, cols, dQ, ldq);
+}
+
+static int form_p_checked(Ctx& c, const rq::FactorSet& F, double* dP, int64_t ldp) {
+  if (!F.have) return rq::set_error(RQ_EVALUE, "no factorization stored in this context");
+  if (F.device != c.device) return rq::set_error(RQ_EVALUE, "the factors live on device %d, the context on %d",
+                                                 F.device, c.device);
+  if (ldp < F.fn) return rq::set_error(RQ_EVALUE, "ldp < n");
+  return c.form_p(F, dP, ldp);
 }
 
 int rq_form_q(rq_ctx* ctx, int64_t cols, double* dQ, int64_t ldq) {
   CTX_CHECK(ctx);
   rq::clear_error();
-  if (!ctx->c.have_factors) return rq::set_error(RQ_EVALUE, "no factorization stored in this context");
-  if (cols < ctx->c.fn || cols > ctx->c.fm)
-    return rq::set_error(RQ_EDIM, "cols must lie in [%lld, %lld]", (long long)ctx->c.fn, (long long)ctx->c.fm);
-  if (ldq < ctx->c.fm || (ldq & 1) || ((uintptr_t)dQ & 15))
-    return rq::set_error(RQ_EVALUE, "dQ must be 16-byte aligned with an even ldq >= m");
-  return ctx->c.form_q(cols, dQ, ldq);
+  return form_q_checked(ctx->c, ctx->c.view(), cols, dQ, ldq);
 }
 
 int rq_form_p(rq_ctx* ctx, double* dP, int64_t ldp) {
   CTX_CHECK(ctx);
   rq::clear_error();
-  if (ldp < ctx->c.fn) return rq::set_error(RQ_EVALUE, "ldp < n");
-  return ctx->c.form_p(dP, ldp);
+  return form_p_checked(ctx->c, ctx->c.view(), dP, ldp);
+}
+
+static const rq::FactorSet* pick(Ctx& c, const rq_factors* f, rq::FactorSet& tmp) {
+  if (f) return &f->f;
+  tmp = c.view();
+  return &tmp;
+}
+
+int rq_factors_info(rq_ctx* ctx, const rq_factors* f, int32_t which, int32_t cap, int64_t* offsets, int32_t* widths,
+                    int32_t* count) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  rq::FactorSet tmp;
+  const rq::FactorSet* F = pick(ctx->c, f, tmp);
+  if (!F->have) return rq::set_error(RQ_EVALUE, "no factorization stored in this context");
+  if (!count) return rq::set_error(RQ_EVALUE, "null count");
+  if (which == 0) {
+    *count = (int32_t)F->factors.size();
+    for (int32_t i = 0; i < *count && i < cap; i++) {
+      if (offsets) offsets[i] = F->factors[i].s;
+      if (widths) widths[i] = F->factors[i].k;
+    }
+  } else {
+    *count = F->p_is_perm ? 0 : (int32_t)F->rfactors.size();
+    for (int32_t i = 0; i < *count && i < cap; i++) {
+      if (offsets) offsets[i] = F->rfactors[i].s;
+      if (widths) widths[i] = (int32_t)F->rfactors[i].np;
+    }
+  }
+  return RQ_OK;
+}
+
+int rq_apply_q(rq_ctx* ctx, const rq_factors* f, int32_t first, int32_t count, int32_t trans, int64_t cols,
+               double* dX, int64_t ldx) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  rq::FactorSet tmp;
+  const rq::FactorSet* F = pick(ctx->c, f, tmp);
+  if (!F->have) return rq::set_error(RQ_EVALUE, "no factorization stored in this context");
+  if (F->device != ctx->c.device) return rq::set_error(RQ_EVALUE, "factors and context on different devices");
+  if (cols < 0) return rq::set_error(RQ_EDIM, "cols < 0");
+  if (ldx < F->fm || (ldx & 1) || ((uintptr_t)dX & 15))
+    return rq::set_error(RQ_EVALUE, "dX must be 16-byte aligned with an even ldx >= m");
+  return ctx->c.apply_q(*F, first, count, trans != 0, false, cols, dX, ldx);
+}
+
+int rq_apply_p(rq_ctx* ctx, const rq_factors* f, int32_t first, int32_t count, int64_t rows, double* dX,
+               int64_t ldx) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  rq::FactorSet tmp;
+  const rq::FactorSet* F = pick(ctx->c, f, tmp);
+  if (!F->have) return rq::set_error(RQ_EVALUE, "no factorization stored in this context");
+  if (F->device != ctx->c.device) return rq::set_error(RQ_EVALUE, "factors and context on different devices");
+  if (rows < 0) return rq::set_error(RQ_EDIM, "rows < 0");
+  if (ldx < rows || (ldx & 1) || ((uintptr_t)dX & 15))
+    return rq::set_error(RQ_EVALUE, "dX must be 16-byte aligned with an even ldx >= rows");
+  return ctx->c.apply_p(*F, first, count, rows, dX, ldx);
+}
+
+int rq_factors_detach(rq_ctx* ctx, rq_factors** out) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (!out) return rq::set_error(RQ_EVALUE, "null output pointer");
+  *out = nullptr;
+  rq_factors* f = new (std::nothrow) rq_factors;
+  if (!f) return rq::set_error(RQ_EINTERNAL, "out of host memory");
+  int rc = ctx->c.detach(&f->f);
+  if (rc != RQ_OK) {
+    delete f;
+    return rc;
+  }
+  *out = f;
+  return RQ_OK;
+}
+
+int rq_factors_destroy(rq_factors* f) {
+  if (!f) return RQ_OK;
+  cudaSetDevice(f->f.device);
+  f->f.arena.release();
+  delete f;
+  return RQ_OK;
+}
+
+int rq_factors_form_q(rq_ctx* ctx, const rq_factors* f, int64_t cols, double* dQ, int64_t ldq) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (!f) return rq::set_error(RQ_EVALUE, "null rq_factors");
+  return form_q_checked(ctx->c, f->f, cols, dQ, ldq);
+}
+
+int rq_factors_form_p(rq_ctx* ctx, const rq_factors* f, double* dP, int64_t ldp) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (!f) return rq::set_error(RQ_EVALUE, "null rq_factors");
+  return form_p_checked(ctx->c, f->f, dP, ldp);
 }
 
 int rq_snapshot(rq_ctx* ctx, double* hW, int64_t ldh) {
   CTX_CHECK(ctx);
   return ctx->c.snapshot(hW, ldh);
+}
+
+int rq_snapshot_sketch(rq_ctx* ctx, double* hY, int64_t ldh, int64_t* hperm) {
+  CTX_CHECK(ctx);
+  return ctx->c.snapshot_sketch(hY, ldh, hperm);
 }
 
 int rq_householder_sweep(rq_ctx* ctx, double* dA, int64_t m, int64_t n, int64_t lda, double* dV, int64_t ldv,

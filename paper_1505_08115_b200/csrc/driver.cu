@@ -34,6 +34,9 @@ int Arena::reserve(size_t bytes) {
   cap = 0;
   RQ_CUDA_TRY(cudaMalloc(&base, bytes));
   cap = bytes;
+  // fresh memory may hold another context's data (same address after a free): the sketch
+  // CPQR's stamped exchange words must never match a live stamp, so start from zeros
+  RQ_CUDA_TRY(cudaMemset(base, 0, bytes));
   return RQ_OK;
 }
 void Arena::release() {
@@ -613,7 +616,11 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
   cur_m = m;
   cur_n = n;
   cur_orig = L.orig;
+  cur_yt = cfg.sketch_mode == RQ_SKETCH_DOWNDATE ? L.yt : nullptr;
+  cur_ldy = L.ldy;
+  cur_wdt = wdt;
 
+  have_factors = false;  // a failed run leaves nothing readable
   factors.clear();
   rfactors.clear();
   const bool refl_piv = cfg.pivot_kind == RQ_PIVOT_REFLECTORS;
@@ -996,6 +1003,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     }
   }
   cur_lorder = nullptr;
+  cur_yt = nullptr;
   if (dperm) {
     RQ_CUDA_TRY(cudaMemcpyAsync(dperm, L.orig, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, stream));
     launches++;
@@ -1020,6 +1028,7 @@ int Ctx::factorize_unpivoted(int64_t m, int64_t n, double* A, int64_t lda, int b
   kwork_bytes = L.kwork_bytes;
   sweep_ws = L.sweep_ws;
   sweep_ws_bytes = L.sweep_ws_bytes;
+  have_factors = false;  // a failed run leaves nothing readable
   factors.clear();
   rfactors.clear();
   p_is_perm = true;
@@ -1276,6 +1285,7 @@ int Ctx::factorize_rrqr(const rq_config& cfg0, int64_t m, int64_t n, double* A, 
   cur_lda = lda;
   cur_m = m;
   cur_n = n;
+  have_factors = false;  // a failed run leaves nothing readable
   factors.clear();
   rfactors.clear();
   p_is_perm = false;
@@ -1343,11 +1353,55 @@ int Ctx::factorize_rrqr(const rq_config& cfg0, int64_t m, int64_t n, double* A, 
 // Q = U_1 ... U_L applied to eye(m, cols) (blocked.py:134-141), backwards, on
 // the trailing block X = Q[s:, s:] only (columns < s are untouched unit vectors).
 // ---------------------------------------------------------------------------
-int Ctx::form_q(int64_t cols, double* Q, int64_t ldq) {
+FactorSet Ctx::view() const {
+  FactorSet F;
+  F.factors = factors;
+  F.rfactors = rfactors;
+  F.p_is_perm = p_is_perm;
+  F.perm = factors_perm;
+  F.fm = fm;
+  F.fn = fn;
+  F.fb = fb;
+  F.have = have_factors;
+  F.device = device;
+  return F;
+}
+
+// The stored factors live in `arena`: hand the arena over with them.  The next
+// factorization on this context reserves a fresh arena.
+int Ctx::detach(FactorSet* out) {
   if (!have_factors) return set_error(RQ_EVALUE, "no factorization stored in this context");
-  const int64_t m = fm;
-  RQ_TRY(fill_eye(Q, ldq, m, cols, 0, stream, &launches));
-  const int b = fb;
+  RQ_CUDA_TRY(cudaStreamSynchronize(stream));
+  *out = view();
+  out->arena = arena;
+  arena = Arena{};
+  have_factors = false;  // a failed run leaves nothing readable
+  factors.clear();
+  rfactors.clear();
+  factors_perm = nullptr;
+  have_factors = false;
+  cur_A = nullptr;
+  return RQ_OK;
+}
+
+int Ctx::form_q(const FactorSet& F, int64_t cols, double* Q, int64_t ldq) {
+  if (!F.have) return set_error(RQ_EVALUE, "no factorization stored in this context");
+  RQ_TRY(fill_eye(Q, ldq, F.fm, cols, 0, stream, &launches));
+  return apply_q(F, 0, (int)F.factors.size(), false, true, cols, Q, ldq);
+}
+
+// X (m x cols) <- U_first ... U_last X  (trans: U_last^T ... U_first^T X), U_i = (I - V T V^T) diag(Q2, I)
+// on rows s_i.. (QTransform.left_multiply, blocked.py:90-99).  eye: X is the identity on entry, so
+// U_i only touches the block X[s_i:, s_i:] (columns < s_i are untouched unit vectors).
+int Ctx::apply_q(const FactorSet& F, int first, int count, bool trans, bool eye, int64_t cols, double* Q,
+                 int64_t ldq) {
+  if (!F.have) return set_error(RQ_EVALUE, "no factorization stored in this context");
+  const int nf = (int)F.factors.size();
+  if (first < 0 || count < 0 || first + count > nf)
+    return set_error(RQ_EVALUE, "panel range [%d, %d) outside the %d stored panels", first, first + count, nf);
+  if (count == 0 || cols == 0) return RQ_OK;
+  const int64_t m = F.fm;
+  const int b = F.fb;
   const int64_t ldw = even(std::max(b, 2));
   size_t need = (size_t)3 * ldw * cols * 8 + (size_t)kSMs * b * b * 8 + 1024;
   RQ_TRY(qarena.reserve(need));
@@ -1360,39 +1414,54 @@ int Ctx::form_q(int64_t cols, double* Q, int64_t ldq) {
   kwork = c.take<double>((size_t)kSMs * b * b);
   kwork_bytes = (size_t)kSMs * b * b * 8;
   int rc = RQ_OK;
-  for (int i = (int)factors.size() - 1; i >= 0 && rc == RQ_OK; i--) {
-    const PanelFactors& f = factors[i];
-    const int64_t s = f.s, mp = m - s, nc = cols - s;
+  for (int it = 0; it < count && rc == RQ_OK; it++) {
+    const PanelFactors& f = F.factors[trans ? first + it : first + count - 1 - it];
+    const int64_t s = f.s, mp = m - s;
+    const int64_t c0 = eye ? s : 0, nc = cols - c0;
     if (nc <= 0) continue;
-    double* X = Q + s + s * ldq;
-    if (f.q2) {
-      // X[0:k] <- Q2 X[0:k]   (NN with A = Q2)
-      rc = copy2d(X, ldq, tt, ldw, f.k, nc, 0, stream, &launches);
-      if (rc == RQ_OK)
-        rc = gemm(f.k, nc, f.k, op(f.q2, f.k, f.k, f.ldq2), true, op(tt, f.k, nc, ldw), X, ldq, 1.0, 0.0);
-    }
-    if (rc != RQ_OK) break;
-    // X <- X - V T (V^T X)
+    double* X = Q + s + c0 * ldq;
     const GemmOperand Vop = op(f.v, mp + f.vpad, f.k, f.ldv, f.vpad);
-    rc = gemm(f.k, nc, mp, Vop, false, op(Q, m, cols, ldq, s, s), w1, ldw, 1.0, 0.0);
+    auto small = [&]() {  // X[0:k] <- Q2 X[0:k]  (trans: Q2^T)
+      int r = copy2d(X, ldq, tt, ldw, f.k, nc, 0, stream, &launches);
+      if (r == RQ_OK)
+        r = gemm(f.k, nc, f.k, op(f.q2, f.k, f.k, f.ldq2), !trans, op(tt, f.k, nc, ldw), X, ldq, 1.0, 0.0);
+      return r;
+    };
+    if (f.q2 && !trans) rc = small();
+    if (rc != RQ_OK) break;
+    // X <- X - V T (V^T X)   (trans: T^T)
+    rc = gemm(f.k, nc, mp, Vop, false, op(Q, m, cols, ldq, s, c0), w1, ldw, 1.0, 0.0);
     if (rc == RQ_OK)
-      rc = gemm(f.k, nc, f.k, op(f.t, f.k, f.k, f.ldt), true, op(w1, f.k, nc, ldw), w2, ldw, 1.0, 0.0);
-    if (rc == RQ_OK)
-      rc = gemm(mp, nc, f.k, Vop, true, op(w2, f.k, nc, ldw), X, ldq, -1.0, 1.0);
+      rc = gemm(f.k, nc, f.k, op(f.t, f.k, f.k, f.ldt), !trans, op(w1, f.k, nc, ldw), w2, ldw, 1.0, 0.0);
+    if (rc == RQ_OK) rc = gemm(mp, nc, f.k, Vop, true, op(w2, f.k, nc, ldw), X, ldq, -1.0, 1.0);
+    if (rc == RQ_OK && f.q2 && trans) rc = small();
   }
   kwork = save_kw;
   kwork_bytes = save_kb;
   return rc;
 }
 
-int Ctx::form_p(double* P, int64_t ldp) {
-  if (!have_factors) return set_error(RQ_EVALUE, "no factorization stored in this context");
-  if (p_is_perm) return perm_to_dense(factors_perm, fn, P, ldp, stream, &launches);
+int Ctx::form_p(const FactorSet& F, double* P, int64_t ldp) {
+  if (!F.have) return set_error(RQ_EVALUE, "no factorization stored in this context");
+  if (F.p_is_perm) return perm_to_dense(F.perm, F.fn, P, ldp, stream, &launches);
   // P = prod_i (S_i, P-hat_i) applied to I in order (Factorization.expand_p, blocked.py:143-149)
-  const int64_t n = fn;
-  RQ_TRY(fill_eye(P, ldp, n, n, 0, stream, &launches));
-  const int b = fb;
-  const int64_t ldz = even(n), ldk = even(b);
+  RQ_TRY(fill_eye(P, ldp, F.fn, F.fn, 0, stream, &launches));
+  return apply_p(F, 0, (int)F.rfactors.size(), F.fn, P, ldp);
+}
+
+// X (rows x n) <- X P_first ... P_last for orthogonal (reflector-pivot) right factors
+// (RightTransform.right_multiply, blocked.py:108-119): S_i = I - V_S T_S V_S^T, then P-hat_i, then
+// the panel SVD's V~ (DenseOrtho, blocked.py:53-63).
+int Ctx::apply_p(const FactorSet& F, int first, int count, int64_t rows, double* P, int64_t ldp) {
+  if (!F.have) return set_error(RQ_EVALUE, "no factorization stored in this context");
+  if (F.p_is_perm) return set_error(RQ_EUNSUPPORTED, "permutation pivots: apply the permutation instead");
+  const int nf = (int)F.rfactors.size();
+  if (first < 0 || count < 0 || first + count > nf)
+    return set_error(RQ_EVALUE, "panel range [%d, %d) outside the %d stored right factors", first, first + count, nf);
+  if (count == 0 || rows == 0) return RQ_OK;
+  const int64_t n = F.fn;
+  const int b = F.fb;
+  const int64_t ldz = even(rows), ldk = even(b);
   const size_t need = (size_t)3 * ldz * b * 8 + (size_t)ldk * n * 8 + (size_t)ldz * b * 8 + (size_t)n * 4 * 2 + 8192;
   RQ_TRY(qarena.reserve(need));
   Carver c(qarena.base);
@@ -1402,17 +1471,18 @@ int Ctx::form_p(double* P, int64_t ldp) {
   double* stage = c.take<double>((size_t)ldz * std::max<int64_t>(b, 1) * 2);
   int* io = c.take<int>((size_t)n);
   RQ_TRY(iota(io, (int)n, nullptr, 0, stream, &launches));
-  for (const RightFactors& f : rfactors) {
+  for (int i = first; i < first + count; i++) {
+    const RightFactors& f = F.rfactors[i];
     if (f.k > 0)
-      RQ_TRY(apply_right_wy(P, ldp, n, n, f.s, f.np, f.k, f.vs, f.ldvs, f.ts, f.ldts, vst, z, z2, ldz));
+      RQ_TRY(apply_right_wy(P, ldp, rows, n, f.s, f.np, f.k, f.vs, f.ldvs, f.ts, f.ldts, vst, z, z2, ldz));
     if (f.nphat > 0) {
-      MoveCall mv{P, ldp, f.s, 0, n, f.phat, io, nullptr, f.nphat, stage, ldz, nullptr, nullptr};
+      MoveCall mv{P, ldp, f.s, 0, rows, f.phat, io, nullptr, f.nphat, stage, ldz, nullptr, nullptr};
       RQ_TRY(move_columns(mv, stream, &launches));
     }
     if (f.dense) {  // DenseOrtho (blocked.py:53-63): P[:, s:s+w] <- P[:, s:s+w] V~
-      RQ_TRY(copy2d(P + f.s * ldp, ldp, z, ldz, n, f.wd, 0, stream, &launches));
-      RQ_TRY(gemm(n, f.wd, f.wd, op(z, n, f.wd, ldz), true, op(f.dense, f.wd, f.wd, f.ldd), P + f.s * ldp, ldp, 1.0,
-                  0.0));
+      RQ_TRY(copy2d(P + f.s * ldp, ldp, z, ldz, rows, f.wd, 0, stream, &launches));
+      RQ_TRY(gemm(rows, f.wd, f.wd, op(z, rows, f.wd, ldz), true, op(f.dense, f.wd, f.wd, f.ldd), P + f.s * ldp,
+                  ldp, 1.0, 0.0));
     }
   }
   return RQ_OK;
@@ -1428,6 +1498,32 @@ int Ctx::snapshot(double* hW, int64_t ldh) {
     RQ_CUDA_TRY(cudaMemcpy(lo.data(), cur_lorder, (n - s) * sizeof(int), cudaMemcpyDeviceToHost));
     for (int64_t r = 0; r < n - s; r++)
       RQ_CUDA_TRY(cudaMemcpy(hW + (s + r) * ldh, cur_A + (s + lo[r]) * cur_lda, m * 8, cudaMemcpyDeviceToHost));
+  }
+  return RQ_OK;
+}
+
+// The downdated sketch of the current trailing block (Y2 = G2 A22' in exact arithmetic, SURVEY
+// section 8 "Two sketch modes") and the composite permutation so far, both in the reference's
+// column order: hY is wdt x (n - s) (ldh >= wdt), hperm has n entries.  Test hook for the
+// downdate identity; valid inside the inspect callback of a downdated-sketch run.
+int Ctx::snapshot_sketch(double* hY, int64_t ldh, int64_t* hperm) {
+  if (!cur_A || !cur_yt) return set_error(RQ_EVALUE, "no downdated-sketch factorization in progress");
+  if (ldh < cur_wdt) return set_error(RQ_EVALUE, "ldh < sketch width %d", cur_wdt);
+  RQ_CUDA_TRY(cudaStreamSynchronize(stream));
+  const int64_t n = cur_n, s = cur_lorder ? cur_s : n;
+  std::vector<int> lo((size_t)(n - s));
+  for (int64_t r = 0; r < n - s; r++) lo[r] = (int)r;
+  if (cur_lorder && s < n)
+    RQ_CUDA_TRY(cudaMemcpy(lo.data(), cur_lorder, (n - s) * sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> orig((size_t)n);
+  RQ_CUDA_TRY(cudaMemcpy(orig.data(), cur_orig, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  for (int64_t r = 0; r < n - s; r++)
+    if (hY)
+      RQ_CUDA_TRY(cudaMemcpy(hY + r * ldh, cur_yt + (s + lo[r]) * cur_ldy, (size_t)cur_wdt * 8,
+                             cudaMemcpyDeviceToHost));
+  if (hperm) {
+    for (int64_t j = 0; j < s; j++) hperm[j] = orig[j];
+    for (int64_t r = 0; r < n - s; r++) hperm[s + r] = orig[s + lo[r]];
   }
   return RQ_OK;
 }
@@ -1560,6 +1656,8 @@ Ctx::~Ctx() {
   harena.release();
   if (side) cudaStreamDestroy(side);
   if (hip) cudaStreamDestroy(hip);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (copy_ev) cudaEventDestroy(copy_ev);
   if (ev_v) cudaEventDestroy(ev_v);
   if (ev_side) cudaEventDestroy(ev_side);
   if (ev_hi) cudaEventDestroy(ev_hi);

@@ -88,6 +88,21 @@ struct RightFactors {
   int wd;
 };
 
+// A factorization's compact factors, detached from the context that computed them
+// (rq_factors_detach): the set owns the device workspace they live in, so later
+// factorizations on the context allocate fresh workspace and never overwrite them.
+struct FactorSet {
+  Arena arena;
+  std::vector<PanelFactors> factors;
+  std::vector<RightFactors> rfactors;
+  bool p_is_perm = true;
+  int64_t* perm = nullptr;
+  int64_t fm = 0, fn = 0;
+  int fb = 0;
+  bool have = false;
+  int device = 0;
+};
+
 struct Ctx {
   int device = 0;
   // profiling
@@ -105,6 +120,8 @@ struct Ctx {
   int64_t launches = 0;
   Arena arena, qarena, sarena;  // factorization, Q/P formation + test hooks, panel-step API
   Arena harena;                 // rq_factorize_host: device copy of A and the permutation
+  cudaStream_t copy_stream = nullptr;  // rq_factorize_host: R streams to the host on this stream
+  cudaEvent_t copy_ev = nullptr;
   unsigned int* barriers = nullptr;
   int nbarriers = 0;
   int next_barrier = 0;
@@ -169,6 +186,9 @@ struct Ctx {
   int64_t cur_lda = 0, cur_m = 0, cur_n = 0, cur_s = 0, cur_np = 0;
   int* cur_lorder = nullptr;
   int64_t* cur_orig = nullptr;
+  double* cur_yt = nullptr;  // downdated sketch (rq_snapshot_sketch): wdt x n, physical column slots
+  int64_t cur_ldy = 0;
+  int cur_wdt = 0;
 
   ~Ctx();
   int gemm(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmajor, const GemmOperand& B, double* C,
@@ -207,7 +227,9 @@ struct Ctx {
   int orth(double* src, int64_t rows, int cols, int64_t ld, Layout& L);
   int reflector_pivot(const rq_config& cfg, double* A, int64_t lda, int64_t m, int64_t n, int64_t s, Layout& L,
                       void* fc_ptr, uint64_t seed, uint64_t* counter);
-  int form_q(int64_t cols, double* Q, int64_t ldq);
+  FactorSet view() const;     // the stored factorization (no workspace ownership)
+  int detach(FactorSet* out);  // move the stored factorization and its workspace out
+  int form_q(const FactorSet& F, int64_t cols, double* Q, int64_t ldq);
   int factorize_unpivoted(int64_t m, int64_t n, double* A, int64_t lda, int b);
   // Panel-step API for drivers that own the column distribution (multi-GPU, dist.py)
   int step_sketch_select(double* Y, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen);
@@ -216,12 +238,19 @@ struct Ctx {
   int step_panel_apply(const double* V, int64_t ldv, const double* T, int64_t ldt, const double* Q2, int64_t ldq2,
                        int64_t mp, int b, double* A, int64_t lda, int64_t a_rows, int64_t a_cols, int64_t r0,
                        int64_t c0, int64_t n2);
-  int form_p(double* P, int64_t ldp);
+  int form_p(const FactorSet& F, double* P, int64_t ldp);
+  int apply_q(const FactorSet& F, int first, int count, bool trans, bool eye, int64_t cols, double* X, int64_t ldx);
+  int apply_p(const FactorSet& F, int first, int count, int64_t rows, double* X, int64_t ldx);
   int snapshot(double* hW, int64_t ldh);
+  int snapshot_sketch(double* hY, int64_t ldh, int64_t* hperm);
 };
 
 }  // namespace rq
 
 struct rq_ctx {
   rq::Ctx c;
+};
+
+struct rq_factors {
+  rq::FactorSet f;
 };

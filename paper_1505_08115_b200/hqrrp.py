@@ -17,6 +17,7 @@ reference's exceptions.  PyTorch is used to own device memory and streams.
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -91,6 +92,20 @@ class Engine:
         check(self.lib.rq_ctx_create(ctypes.byref(h), self.device.index, ctypes.c_void_p(self.stream.cuda_stream)))
         self.handle = h
         self._cb = None
+        self._owner = None  # weakref to the Factorization whose factors the context holds
+
+    def _release_factors(self):
+        """Before the context overwrites its stored factors: hand them to the Factorization that
+        still refers to them (blocked.py:122-149: a Factorization owns its transforms)."""
+        owner = self._owner() if self._owner is not None else None
+        self._owner = None
+        if owner is not None and owner._fset is None:
+            h = ctypes.c_void_p()
+            check(self.lib.rq_factors_detach(self.handle, ctypes.byref(h)))
+            owner._fset = _FactorHandle(self.lib, h)
+
+    def _adopt(self, f):
+        self._owner = weakref.ref(f)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -174,20 +189,114 @@ def _check_input(a):
 # --------------------------------------------------------------------------
 # Result object
 # --------------------------------------------------------------------------
-class _PermTransform:
-    """RightTransform-like view of the composite permutation (blocked.py:101-119)."""
+class _FactorHandle:
+    """Owns a detached ``rq_factors`` (rq_factors_detach); frees it with the Factorization."""
 
-    def __init__(self, perm):
-        self.offset = 0
-        self.order = perm
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.lib.rq_factors_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class _PermOrder:
+    """PermutationPivot-like op (pivoting.py:55-61): ``order`` of the columns it acts on."""
+
+    def __init__(self, order):
+        self.order = order
+
+    def apply_right(self, a):
+        return np.array(np.asarray(a)[:, self.order], order="F")
+
+
+class PermTransform:
+    """RightTransform (blocked.py:101-119) of one panel with permutation pivots.
+
+    ``order`` acts on columns ``offset..n-1``: the panel's b selected columns in their final
+    order (the sketch's pivot order composed with the panel's inner P-hat), then the rest in
+    their previous relative order, as the reference keeps them (pivoting.py:125-128).  The
+    reference stores the selection and P-hat as two transforms; their product is this one.
+    """
+
+    def __init__(self, offset, order):
+        self.offset = int(offset)
+        self.op = _PermOrder(order)
+
+    @property
+    def order(self):
+        return self.op.order
 
     def right_multiply(self, a):
         out = np.array(a, dtype=np.float64, order="F", copy=True)
-        return np.array(out[:, self.order], order="F")
+        w = len(self.op.order)
+        out[:, self.offset:self.offset + w] = out[:, self.offset:self.offset + w][:, self.op.order]
+        return out
+
+
+def panel_orders(perm, offsets):
+    """Per-panel PermTransforms from the composite permutation (A[:, perm] = A P).
+
+    After panel i the first s_i + w_i entries of ``perm`` are final; the reference keeps the
+    columns it did not select in their previous relative order, so the column order before each
+    panel -- and hence each panel's order -- follows from ``perm`` alone.
+    """
+    perm = np.asarray(perm, dtype=np.int64)
+    n = len(perm)
+    cur = np.arange(n, dtype=np.int64)  # reference column order before the panel
+    out = []
+    bounds = list(offsets) + [n]
+    for i, s in enumerate(offsets):
+        e = bounds[i + 1]
+        tail = cur[s:]
+        pos = np.empty(n, dtype=np.int64)
+        pos[tail] = np.arange(len(tail))
+        chosen = perm[s:e]
+        mask = np.ones(len(tail), dtype=bool)
+        mask[pos[chosen]] = False
+        order = np.concatenate([pos[chosen], np.nonzero(mask)[0]])
+        out.append(PermTransform(s, order))
+        cur = np.concatenate([cur[:s], tail[order]])
+    return out
+
+
+class QPanel:
+    """QTransform-like proxy of one panel's left factor U_i = (I - V T V^T) diag(Q2, I) on rows
+    offset.. (blocked.py:77-99); the factors stay on the device."""
+
+    def __init__(self, fact, index, offset, count):
+        self._f, self.index, self.offset, self.count = fact, index, int(offset), int(count)
+
+    def left_multiply(self, a):
+        """U_i @ a (dense expansion helper), on the GPU."""
+        return self._f._apply_q(self.index, 1, False, a)
+
+    def left_multiply_transposed(self, a):
+        """U_i^T @ a."""
+        return self._f._apply_q(self.index, 1, True, a)
+
+
+class PTransform:
+    """RightTransform-like proxy of one orthogonal right factor (reflector pivots: S_i, P-hat_i
+    and, for block_rrqr, the panel SVD's V~) on columns offset.. (blocked.py:101-119)."""
+
+    def __init__(self, fact, index, offset, width):
+        self._f, self.index, self.offset, self.width = fact, index, int(offset), int(width)
+
+    def right_multiply(self, a):
+        return self._f._apply_p(self.index, 1, a)
 
 
 class Factorization:
-    """A P = Q R with Q, P held on the device in compact form (blocked.py:122-149)."""
+    """A P = Q R with Q, P held on the device in compact form (blocked.py:122-149).
+
+    Each Factorization owns its factors: when its Engine factorizes again while this object is
+    alive, the factors are detached into it first (rq_factors_detach).
+    """
 
     def __init__(self, engine, m, n, b, method, r_dev, ld, perm_dev):
         self.m, self.n, self.b, self.method = m, n, b, method
@@ -197,6 +306,11 @@ class Factorization:
         self._perm_dev = perm_dev
         self._r = None
         self._perm = None
+        self._fset = None  # _FactorHandle once detached from the engine
+        engine._adopt(self)
+
+    def _fptr(self):
+        return self._fset.h if self._fset is not None else None
 
     @property
     def r(self):
@@ -223,15 +337,63 @@ class Factorization:
             self._perm = self._perm_dev.cpu().numpy().astype(np.int64)
         return self._perm
 
+    def _info(self, which):
+        eng = self._engine
+        cnt = ctypes.c_int32()
+        check(eng.lib.rq_factors_info(eng.handle, self._fptr(), which, 0, None, None, ctypes.byref(cnt)))
+        k = cnt.value
+        offs = np.zeros(max(k, 1), dtype=np.int64)
+        wid = np.zeros(max(k, 1), dtype=np.int32)
+        check(eng.lib.rq_factors_info(eng.handle, self._fptr(), which, k, offs.ctypes.data_as(ctypes.c_void_p),
+                                      wid.ctypes.data_as(ctypes.c_void_p), ctypes.byref(cnt)))
+        return offs[:k], wid[:k]
+
+    @property
+    def q_transforms(self):
+        """Per-panel left factors, in order (Q = U_1 ... U_L), as device-backed proxies."""
+        offs, wid = self._info(0)
+        return [QPanel(self, i, o, w) for i, (o, w) in enumerate(zip(offs, wid))]
+
     @property
     def p_transforms(self):
-        return [_PermTransform(self.perm)] if self._perm_dev is not None else []
+        """Per-panel right factors, in order (P = P_1 ... P_L)."""
+        if self._perm_dev is not None:
+            offs, _ = self._info(0)
+            return panel_orders(self.perm, offs)
+        offs, wid = self._info(1)
+        return [PTransform(self, i, o, w) for i, (o, w) in enumerate(zip(offs, wid))]
+
+    def _apply_q(self, first, count, trans, a):
+        eng = self._engine
+        a = np.asarray(a, dtype=np.float64)
+        if a.ndim != 2 or a.shape[0] != self.m:
+            raise DimensionError(f"expected {self.m} rows, got shape {a.shape}")
+        buf, ld, m, cols = eng.upload(a)
+        check(eng.lib.rq_apply_q(eng.handle, self._fptr(), first, count, int(trans), cols,
+                                 ctypes.c_void_p(buf.data_ptr()), ld))
+        return Engine.download(buf, m, cols)
+
+    def _apply_p(self, first, count, a):
+        eng = self._engine
+        a = np.asarray(a, dtype=np.float64)
+        if a.ndim != 2 or a.shape[1] != self.n:
+            raise DimensionError(f"expected {self.n} columns, got shape {a.shape}")
+        buf, ld, rows, n = eng.upload(a)
+        check(eng.lib.rq_apply_p(eng.handle, self._fptr(), first, count, rows, ctypes.c_void_p(buf.data_ptr()), ld))
+        return Engine.download(buf, rows, n)
+
+    def apply_q(self, a, transpose=False):
+        """Q @ a (or Q^T @ a) for an m-row array, without forming Q."""
+        return self._apply_q(0, len(self._info(0)[0]), transpose, a)
 
     def expand_q_device(self, cols=None):
         eng = self._engine
         cols = self.n if cols is None else int(cols)
         buf, ld = eng.alloc_matrix(self.m, cols)
-        check(eng.lib.rq_form_q(eng.handle, cols, ctypes.c_void_p(buf.data_ptr()), ld))
+        if self._fset is not None:
+            check(eng.lib.rq_factors_form_q(eng.handle, self._fset.h, cols, ctypes.c_void_p(buf.data_ptr()), ld))
+        else:
+            check(eng.lib.rq_form_q(eng.handle, cols, ctypes.c_void_p(buf.data_ptr()), ld))
         return buf, ld
 
     def expand_q(self, cols=None):
@@ -244,7 +406,10 @@ class Factorization:
         """Dense orthonormal P, n x n."""
         eng = self._engine
         buf, ld = eng.alloc_matrix(self.n, self.n)
-        check(eng.lib.rq_form_p(eng.handle, ctypes.c_void_p(buf.data_ptr()), ld))
+        if self._fset is not None:
+            check(eng.lib.rq_factors_form_p(eng.handle, self._fset.h, ctypes.c_void_p(buf.data_ptr()), ld))
+        else:
+            check(eng.lib.rq_form_p(eng.handle, ctypes.c_void_p(buf.data_ptr()), ld))
         return Engine.download(buf, self.n, self.n)
 
 
@@ -257,6 +422,7 @@ def _run(a, cfg, rng, inspect, rrqr, engine, sketch="fresh"):
     eng = engine if engine is not None else Engine()
     buf, ld, m, n = eng.upload(a)
     c = _make_config(cfg, rrqr, sketch)
+    eng._release_factors()
     counter = ctypes.c_uint64(int(rng.counter))
     perm = None if (rrqr or cfg.pivot_kind == "reflectors") else torch.empty(max(n, 1), dtype=torch.int64,
                                                                                device=eng.device)

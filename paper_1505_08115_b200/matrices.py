@@ -47,6 +47,7 @@ def haar_orthonormal_device(n, rng, *, engine=None, block=256):
 
     eng = engine if engine is not None else Engine()
     g, ld = gaussian_matrix_device(n, n, rng, engine=eng)
+    eng._release_factors()  # rq_qr_unpivoted replaces the context's stored factors
     check(eng.lib.rq_qr_unpivoted(eng.handle, n, n, _ptr(g), ld, min(block, n)))
     q, ldq = eng.alloc_matrix(n, n)
     check(eng.lib.rq_form_q(eng.handle, n, _ptr(q), ldq))

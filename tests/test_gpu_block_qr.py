@@ -193,6 +193,9 @@ def test_downdate_sketch_matches_hqrrp_oracle(rq, m, n, b, p):
     assert rng.counter == ref_rng.counter == m * (b + p)
     check_against(a, f, ref.r, ref.perm())
     check_factorization(a, f)
+    # the independent post-rotation restatement (G1 = Y1 R11^{-1} on the final R11)
+    post = O.block_qr_downdate(a, O.BlockConfig(b, O.SketchConfig(b, p, 0)), O.RngState(5), form="post")
+    check_against(a, f, post.r, post.perm())
 
 
 def test_downdate_rank_revealing_on_decaying_spectrum(golden, rq):
