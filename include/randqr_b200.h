@@ -226,11 +226,14 @@ int rq_test_debug_timing(int32_t on, uint64_t* host, int32_t count);
 int64_t rq_launch_count(rq_ctx* ctx);
 
 /* Instrumentation: with profiling on, CUDA events bracket every launch of a
- * kernel class (0 trailing-update GEMMs, 1 other GEMMs, 2 CPQR sweeps,
- * 3 panel leaves, 4 other); rq_profile_read sums their device time (ms) and
+ * kernel class (0 trailing-update GEMMs, 1 other GEMMs, 2 sketch CPQR, 3 panel leaves, 4 other,
+ * 5 b x b CPQR, 6 sketch GEMMs, 7 panel WY GEMMs, 8 T factors, 9-12 below); rq_profile_read sums their device time (ms) and
  * GEMM flops since the last rq_set_profiling call. */
 int rq_set_profiling(rq_ctx* ctx, int32_t on);
 int rq_profile_read(rq_ctx* ctx, int32_t category, double* ms, double* flops, int64_t* count);
+/* Bandwidth classes (9 column moves, 10 copy2d, 11 Gaussian fills, 12 GEMM split-K reductions):
+ * algorithmic HBM bytes moved since the last rq_set_profiling (pair with rq_profile_read's ms). */
+int rq_profile_bytes(rq_ctx* ctx, int32_t category, double* bytes);
 
 #ifdef __cplusplus
 }

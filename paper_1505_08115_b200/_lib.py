@@ -82,6 +82,7 @@ _SIGS = {
     "rq_set_profiling": (ctypes.c_int, [_vp, _i32]),
     "rq_profile_read": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(_i64)]),
+    "rq_profile_bytes": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_double)]),
 }
 
 _lib = None
@@ -98,6 +99,8 @@ def load():
                     f"{LIB_PATH} is not built; run __graft_entry__.build() (nvcc, sm_100a)")
             lib = ctypes.CDLL(LIB_PATH)
             for name, (res, args) in _SIGS.items():
+                if os.environ.get("RQ_LIB_PATH") and not hasattr(lib, name):
+                    continue  # an older tuning build (A/B runs): bind what it exports
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

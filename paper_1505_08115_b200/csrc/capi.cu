@@ -543,6 +543,23 @@ int rq_set_profiling(rq_ctx* ctx, int32_t on) {
   ctx->c.prof = on != 0;
   ctx->c.prof_recs.clear();
   ctx->c.ev_next = 0;
+  if (ctx->c.prof_dev_bytes) RQ_CUDA_TRY(cudaMemset(ctx->c.prof_dev_bytes, 0, 8));
+  return RQ_OK;
+}
+
+int rq_profile_bytes(rq_ctx* ctx, int32_t category, double* bytes) {
+  CTX_CHECK(ctx);
+  if (!bytes) return rq::set_error(RQ_EVALUE, "null bytes");
+  RQ_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
+  double b = 0.0;
+  for (const auto& r : ctx->c.prof_recs)
+    if (r.cat == category) b += r.bytes;
+  if (category == rq::PROF_MOVES && ctx->c.prof_dev_bytes) {
+    unsigned long long v = 0;
+    RQ_CUDA_TRY(cudaMemcpy(&v, ctx->c.prof_dev_bytes, 8, cudaMemcpyDeviceToHost));
+    b += (double)v;
+  }
+  *bytes = b;
   return RQ_OK;
 }
 

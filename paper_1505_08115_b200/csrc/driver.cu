@@ -135,6 +135,11 @@ static Layout plan_layout(void* base, int64_t m, int64_t n, int b, int p, int po
   L.flag = c.take<unsigned char>(n);
   L.orig = c.take<int64_t>(n);
   L.ostage = c.take<int64_t>(std::max<int64_t>(2 * b, n));
+  L.cap2 = c.take<int>(std::max<int64_t>(b, n));
+  L.stage2 = c.take<double>((size_t)even(m) * 2 * b + (size_t)even(m) * b);
+  L.ostage2 = c.take<int64_t>(std::max<int64_t>(2 * b, n));
+  L.sweep_ws2_bytes = sweep_workspace_bytes(b, 2 * b, sweep_grid_size(2 * b));
+  L.sweep_ws2 = c.take<char>(L.sweep_ws2_bytes);
   // sweep workspace: largest of (sketch: wdt rows x n cols), (small: b rows x 2b), (final: m rows x b)
   size_t sw = 0;
   sw = std::max(sw, sweep_workspace_bytes(wdt, (int)n, sweep_grid_size((int)n)));
@@ -162,6 +167,13 @@ static GemmOperand op(const double* base, int64_t rows, int64_t cols, int64_t ld
   return o;
 }
 
+struct CatGuard {
+  int& c;
+  int saved;
+  CatGuard(int& c_, int v) : c(c_), saved(c_) { c = v; }
+  ~CatGuard() { c = saved; }
+};
+
 cudaEvent_t Ctx::prof_event() {
   if (ev_next == ev_pool.size()) {
     cudaEvent_t e;
@@ -176,19 +188,54 @@ void Ctx::prof_begin(cudaEvent_t* e0) {
   *e0 = prof_event();
   cudaEventRecord(*e0, stream);
 }
-void Ctx::prof_end(cudaEvent_t e0, double flops) {
+void Ctx::prof_end(cudaEvent_t e0, double flops, double bytes) {
   if (!prof || !e0) return;
   cudaEvent_t e1 = prof_event();
   cudaEventRecord(e1, stream);
-  prof_recs.push_back(ProfRec{cat, e0, e1, flops});
+  prof_recs.push_back(ProfRec{cat, e0, e1, flops, bytes});
 }
 
-struct CatGuard {
-  int& c;
-  int saved;
-  CatGuard(int& c_, int v) : c(c_), saved(c_) { c = v; }
-  ~CatGuard() { c = saved; }
-};
+// Bandwidth-bound helpers with per-class timing and algorithmic bytes when profiling is on.
+int Ctx::copy2d_p(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows, int64_t cols, int upper_only,
+                  cudaStream_t st, int64_t* l) {
+  if (!prof) return copy2d(S, lds, D, ldd, rows, cols, upper_only, st, l);
+  double elems = 0.0;
+  if (!upper_only) elems = (double)rows * (double)cols;
+  else
+    for (int64_t j = 0; j < cols; j++) elems += (double)std::min<int64_t>(j + 1, rows);
+  CatGuard g(cat, PROF_COPY);
+  cudaEvent_t e0;
+  prof_begin(&e0);
+  const int rc = copy2d(S, lds, D, ldd, rows, cols, upper_only, st, l);
+  prof_end(e0, 0.0, 16.0 * elems);
+  return rc;
+}
+
+int Ctx::move_columns_p(MoveCall c, cudaStream_t st, int64_t* l) {
+  if (!prof) return move_columns(c, st, l);
+  if (!prof_dev_bytes) {
+    if (cudaMalloc(&prof_dev_bytes, 8) != cudaSuccess) return set_error(RQ_ECUDA, "profiling counter");
+    cudaMemset(prof_dev_bytes, 0, 8);
+  }
+  c.bytes = prof_dev_bytes;
+  CatGuard g(cat, PROF_MOVES);
+  cudaEvent_t e0;
+  prof_begin(&e0);
+  const int rc = move_columns(c, st, l);
+  prof_end(e0, 0.0, 0.0);  // bytes: the device counter (read by rq_profile_bytes)
+  return rc;
+}
+
+int Ctx::gaussian_fill_p(double* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t counter,
+                         cudaStream_t st, int64_t* l) {
+  if (!prof) return gaussian_fill(out, rows, cols, ld, seed, counter, st, l);
+  CatGuard g(cat, PROF_RNG);
+  cudaEvent_t e0;
+  prof_begin(&e0);
+  const int rc = gaussian_fill(out, rows, cols, ld, seed, counter, st, l);
+  prof_end(e0, 0.0, 8.0 * (double)rows * (double)cols);
+  return rc;
+}
 
 int Ctx::gemm(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmajor, const GemmOperand& B,
               double* C, int64_t ldc, double alpha, double beta) {
@@ -197,8 +244,21 @@ int Ctx::gemm(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_mmaj
   if (cat != PROF_TRAIL && cat != PROF_SKETCH_GEMM && cat != PROF_PANEL_GEMM && cat != PROF_TFACTOR)
     cat = PROF_GEMM_OTHER;
   prof_begin(&e0);
+  if (prof) {
+    gemm_mid = prof_event();
+    gemm_splitk = 1;
+  }
   int rc = gemm_raw(M, N, K, A, a_mmajor, B, C, ldc, alpha, beta);
-  prof_end(e0, 2.0 * (double)M * (double)N * (double)K);
+  if (prof && e0 && gemm_splitk > 1) {
+    // the GEMM up to its split-K reduce, then the reduce (slabs read, C read-modify-written)
+    prof_recs.push_back(ProfRec{cat, e0, gemm_mid, 2.0 * (double)M * (double)N * (double)K, 0.0});
+    cat = PROF_SPLITK;
+    const double mn = (double)M * (double)N;
+    prof_end(gemm_mid, 0.0, 8.0 * mn * (gemm_splitk + 1 + (beta != 0.0 ? 1 : 0)));
+  } else {
+    prof_end(e0, 2.0 * (double)M * (double)N * (double)K);
+  }
+  gemm_mid = nullptr;
   cat = saved;
   return rc;
 }
@@ -221,6 +281,8 @@ int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_
   p.work_bytes = kwork ? kwork_bytes : 0;
   p.max_ctas = gemm_max_ctas;
   p.pdl = gemm_pdl;
+  p.mid_event = gemm_mid;
+  p.splitk_used = gemm_mid ? &gemm_splitk : nullptr;
   RQ_TRY(sched_for(stream, &p.sched, &p.sched_base));
   return gemm_f64(p, stream, &launches);
 }
@@ -275,6 +337,16 @@ void Ctx::phase_report() {
   }
   float tot = 0.f;
   cudaEventElapsedTime(&tot, phase_ev.front().second, phase_ev.back().second);
+  static const bool seq = getenv("RQ_PHASES") && atoi(getenv("RQ_PHASES")) >= 2;
+  if (seq) {  // the raw sequence (id:ms since the previous event), for per-panel analysis
+    fprintf(stderr, "[rq phase-seq]");
+    for (size_t k = 1; k < phase_ev.size(); k++) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, phase_ev[k - 1].second, phase_ev[k].second);
+      fprintf(stderr, " %d:%.4f", phase_ev[k].first, ms);
+    }
+    fprintf(stderr, "\n");
+  }
   fprintf(stderr, "[rq phases] total %.2f ms:", tot);
   for (int i = 1; i < 13; i++)
     if (acc[i] > 0) fprintf(stderr, " %s=%.2f", names[i], acc[i]);
@@ -347,6 +419,8 @@ int Ctx::ensure_side() {
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_w2, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_l0, cudaEventDisableTiming));
   RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_aux, cudaEventDisableTiming));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_g1, cudaEventDisableTiming));
+  RQ_CUDA_TRY(cudaEventCreateWithFlags(&ev_hipdone, cudaEventDisableTiming));
   return RQ_OK;
 }
 
@@ -385,8 +459,8 @@ int Ctx::sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, c
     RQ_CUDA_TRY(cudaMalloc(&sk_counter, 256));
     RQ_CUDA_TRY(cudaMemsetAsync(sk_counter, 0, 256, stream));
   }
-  const int rc =
-      sketch_cpqr_launch(yt, ldy, m, n, steps, init_pos, chosen, w, sk_counter, sk_counter_base, stream, &launches);
+  const int rc = sketch_cpqr_launch(yt, ldy, m, n, steps, init_pos, chosen, w, sk_counter, sk_counter_base, stream,
+                                    &launches, sketch_gmax);
   prof_end(e0, 0.0);
   cat = saved;
   return rc;
@@ -655,7 +729,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
   phase(0);
   if (downdate && n > b) {
     // HQRRP: G = Omega^T drawn once (m(b+p) normals), Y = G A; downdated per panel
-    RQ_TRY(gaussian_fill(L.omega, m, wdt, L.ldo, seed, *counter, stream, &launches));
+    RQ_TRY(gaussian_fill_p(L.omega, m, wdt, L.ldo, seed, *counter, stream, &launches));
     *counter += (uint64_t)m * (uint64_t)wdt;
     RQ_TRY(gemm(wdt, n, m, op(L.omega, m, wdt, L.ldo), false, op(A, m, n, lda, 0, 0), L.yt, L.ldy, 1.0, 0.0));
   }
@@ -672,7 +746,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       const int steps = (int)std::min<int64_t>(mp, w);
       // bring the remaining columns into reference order
       MoveCall mv{A, lda, s, 0, m, lorder, L.iota_b, nullptr, w, L.stage, even(m), L.orig, L.ostage};
-      RQ_TRY(move_columns(mv, stream, &launches));
+      RQ_TRY(move_columns_p(mv, stream, &launches));
       const int64_t ldv = even(mp + 1);
       const int vpad = (int)(s & 1);
       double* Vf = fc.take<double>((size_t)ldv * steps);
@@ -692,10 +766,10 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       sc.r_out = L.stage;
       sc.ldr = even(mp);
       RQ_TRY(sweep(sc));
-      RQ_TRY(copy2d(L.stage, even(mp), A + s + s * lda, lda, mp, w, 0, stream, &launches));
+      RQ_TRY(copy2d_p(L.stage, even(mp), A + s + s * lda, lda, mp, w, 0, stream, &launches));
       // rows above and labels follow the final block's permutation
       MoveCall mv2{A, lda, s, 0, s, L.cap, L.iota_b, nullptr, w, L.stage, even(m), L.orig, L.ostage};
-      RQ_TRY(move_columns(mv2, stream, &launches));
+      RQ_TRY(move_columns_p(mv2, stream, &launches));
       RQ_TRY(tfactor(Vf, mp, steps, ldv, vpad, Tf, even(b), L.gram));
       factors.push_back(PanelFactors{s, steps, Vf, ldv, vpad, Tf, even(b), nullptr, 0});
       if (refl_piv) {
@@ -720,13 +794,13 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     // ---------------- 1-2: sketch Y^T = Omega^T X (fresh) or the downdated Y (HQRRP) ----------------
     double* ycur = L.yt;
     if (!downdate) {
-      RQ_TRY(gaussian_fill(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
+      RQ_TRY(gaussian_fill_p(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
       *counter += (uint64_t)mp * (uint64_t)wdt;
       RQ_TRY(sketch(cfg, A, lda, m, n, s, mp, np, L));
     } else {
       ycur = L.yt + s * L.ldy;
       // the CPQR overwrites its input: work on a copy of the trailing sketch columns
-      RQ_TRY(copy2d(ycur, L.ldy, L.ybuf, L.ldy, wdt, np, 0, stream, &launches));
+      RQ_TRY(copy2d_p(ycur, L.ldy, L.ybuf, L.ldy, wdt, np, 0, stream, &launches));
     }
     // ---------------- 3: b-step CPQR of Y^T ----------------
     RQ_TRY(sketch_select(downdate ? L.ybuf : L.yt, L.ldy, wdt, (int)np, b, rank, L.cap));
@@ -734,10 +808,10 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     PlanCall pc{L.cap, b, lorder, (int)np, L.flag, L.newloc, L.src, L.dst, L.nmoves, lorder_n, rank_n};
     RQ_TRY(plan_moves(pc, stream, &launches));
     MoveCall mv{A, lda, s, 0, m, L.src, L.dst, L.nmoves, 2 * b, L.stage, even(m), L.orig, L.ostage};
-    RQ_TRY(move_columns(mv, stream, &launches));
+    RQ_TRY(move_columns_p(mv, stream, &launches));
     if (downdate) {  // the sketch columns follow their matrix columns
       MoveCall my{L.yt, L.ldy, s, 0, wdt, L.src, L.dst, L.nmoves, 2 * b, L.stage, L.ldy, nullptr, nullptr};
-      RQ_TRY(move_columns(my, stream, &launches));
+      RQ_TRY(move_columns_p(my, stream, &launches));
     }
     }  // permutation pivots
     phase(la_mode ? 7 : 9);
@@ -794,10 +868,25 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       return e ? atoi(e) : 0;
     }();
     w2_side = overlap && la_mode && env_w2s != 0 && !(t_on_hip && hip_tail);
+    // RQ_CPQR_OFF=1: the b x b CPQR and its follow-ups (Q2, R, rows-above moves) leave the critical
+    // path -- the tail waits for W and T only, and the next panel's sketch CPQR (capped at
+    // kSkMinGrid CTAs) runs beside the CPQR's 16-SM cluster; the downdate uses R'12, so it needs
+    // neither Q2 nor P-hat (form_g1)
+    static const int env_off = [] {
+      const char* e = getenv("RQ_CPQR_OFF");
+      return e ? atoi(e) : 1;
+    }();
+    // Only where the CPQR outlasts W = V^T A2 (the late panels): the capped sketch grid costs
+    // ~25 % per step at n' ~ 10k, and early panels hide the CPQR behind W anyway.
+    static const double env_off_tf = getenv("RQ_CPQR_OFF_TF") ? atof(getenv("RQ_CPQR_OFF_TF")) : 20.0;
+    const double w_s = 2.0 * b * (double)mp * (double)n2 / (env_off_tf * 1e12);
+    const double cpqr_s = b * 2.2e-6;
+    cpqr_off = la_mode && overlap && env_off != 0 && b <= 256 && !w2_side && !t_on_hip &&
+               (env_off == 2 || w_s < cpqr_s) && hip2 != nullptr;
     // ---------------- 6: b x b CPQR of R' (reflectors V2), then Q2 = I - V2 T2 V2^T ----------------
     double* S = L.small;
     double* V2 = L.small + (int64_t)b * L.lds_small;
-    RQ_TRY(copy2d(A + s + s * lda, lda, S, L.lds_small, b, b, 1, stream, &launches));
+    RQ_TRY(copy2d_p(A + s + s * lda, lda, S, L.lds_small, b, b, 1, stream, &launches));
     RQ_CUDA_TRY(cudaMemsetAsync(V2, 0, (size_t)L.lds_small * b * sizeof(double), stream));
     launches++;
     SweepCall ss;
@@ -826,13 +915,22 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
         }
       }
       RQ_CUDA_TRY(cudaEventRecord(ev_v, stream));
-      const bool pdl = env_overlap != 4;
-      cudaStream_t cpqr_stream = pdl ? side : hip;
+      const bool pdl = env_overlap != 4 && !cpqr_off;  // off-chain: the CPQR on hip2, W on side
+      cudaStream_t cpqr_stream = cpqr_off ? hip2 : pdl ? side : hip;
       RQ_CUDA_TRY(cudaStreamWaitEvent(cpqr_stream, ev_v, 0));
       if (!pdl) RQ_CUDA_TRY(cudaStreamWaitEvent(side, ev_v, 0));
       cudaStream_t main_stream = stream;
       stream = cpqr_stream;
+      void* sws = sweep_ws;
+      const size_t swb = sweep_ws_bytes;
+      if (cpqr_off) {  // its own workspace and pivot buffer: the next sketch CPQR runs beside it
+        sweep_ws = L.sweep_ws2;
+        sweep_ws_bytes = L.sweep_ws2_bytes;
+        ss.col_at_pos = L.cap2;
+      }
       int rc = sweep(ss);
+      sweep_ws = sws;
+      sweep_ws_bytes = swb;
       const bool hi_event = env_overlap != 3;
       if (rc == RQ_OK && hi_event)
         rc = cudaEventRecord(ev_hi, cpqr_stream) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
@@ -917,11 +1015,51 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       kwork_bytes = kwb;
       stream = main_stream;
       RQ_TRY(rc);
-      RQ_CUDA_TRY(cudaStreamWaitEvent(stream, hi_event ? ev_hi : ev_side, 0));
+      if (!cpqr_off) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, hi_event ? ev_hi : ev_side, 0));
     } else {
       RQ_TRY(sweep(ss));
     }
     phase(2);
+    if (cpqr_off) {
+      // hip (highest priority): G1' first -- it reads R'11, which the R copy below overwrites --
+      // then, once the CPQR (hip2) is done, Q2, R and the rows above (its own stage buffers)
+      cudaStream_t main_stream = stream;
+      double* kw = kwork;
+      const size_t kwb = kwork_bytes;
+      RQ_CUDA_TRY(cudaStreamWaitEvent(hip, ev_v, 0));
+      stream = hip;
+      kwork = nullptr;  // no split-K slabs: the main stream's GEMMs own kwork
+      kwork_bytes = 0;
+      int rc = RQ_OK;
+      if (aux_g1) {
+        rc = aux_g1();
+        aux_g1 = nullptr;
+      }
+      if (rc == RQ_OK && cudaEventRecord(ev_g1, hip) != cudaSuccess) rc = set_error(RQ_ECUDA, "event");
+      if (rc == RQ_OK && cudaStreamWaitEvent(hip, ev_hi, 0) != cudaSuccess) rc = set_error(RQ_ECUDA, "wait");
+      if (rc == RQ_OK) rc = small_q(V2, L.lds_small, b, Q2, ldt, L);
+      if (rc == RQ_OK) rc = copy2d_p(L.rfin, L.lds_small, A + s + s * lda, lda, b, b, 0, stream, &launches);
+      if (rc == RQ_OK) {
+        MoveCall mv2{A, lda, s, 0, s, L.cap2, L.iota_b, nullptr, b, L.stage2, even(m), L.orig, L.ostage2};
+        rc = move_columns_p(mv2, stream, &launches);
+      }
+      if (rc == RQ_OK && on_cols_final) on_cols_final(s, b);
+      if (rc == RQ_OK && cudaEventRecord(ev_hipdone, hip) != cudaSuccess) rc = set_error(RQ_ECUDA, "event");
+      stream = main_stream;
+      kwork = kw;
+      kwork_bytes = kwb;
+      RQ_TRY(rc);
+      phase(12);
+      RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_g1, 0));    // G1' (the downdate)
+      RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_side, 0));  // W and T
+      phase(3);
+      RQ_TRY(lookahead_tail(cfg, A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L, L.wside, lorder, lorder_n,
+                            rank, rank_n));
+      cpqr_off = false;
+      factors.push_back(PanelFactors{s, b, V, ldv, vpad, T, ldt, Q2, ldt});
+      phase(7);
+      continue;
+    }
     // the small post-CPQR work (G1', Q2, R, the rows above) on the highest-priority stream: its
     // CTAs take the SMs the CPQR frees before the queued CTAs of the rest of W
     cudaStream_t tail_saved = stream;
@@ -954,9 +1092,9 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       RQ_CUDA_TRY(cudaMemcpyAsync(rfactors.back().phat, L.cap, (size_t)b * sizeof(int), cudaMemcpyDeviceToDevice,
                                   stream));
     // ---------------- 7: R and the rows above follow P-hat ----------------
-    RQ_TRY(copy2d(L.rfin, L.lds_small, A + s + s * lda, lda, b, b, 0, stream, &launches));
+    RQ_TRY(copy2d_p(L.rfin, L.lds_small, A + s + s * lda, lda, b, b, 0, stream, &launches));
     MoveCall mv2{A, lda, s, 0, s, L.cap, L.iota_b, nullptr, b, L.stage, even(m), L.orig, L.ostage};
-    RQ_TRY(move_columns(mv2, stream, &launches));
+    RQ_TRY(move_columns_p(mv2, stream, &launches));
     if (on_cols_final) on_cols_final(s, b);  // later steps only touch columns >= s + b
     // (the sketch's panel columns are not needed after form_g1: no P-hat on them)
     if (on_hip) {
@@ -1112,6 +1250,15 @@ int Ctx::form_g1(double* A, int64_t lda, int64_t s, int b, int wdt, int64_t n, L
   return gemm(wdt, b, b, op(L.yt, wdt, n, L.ldy, 0, s), true, op(L.rinv, b, b, ldb2), L.g1, ldg, 1.0, 0.0);
 }
 
+// Off-chain CPQR (cpqr_off): join the hip stream (Q2, R, rows-above moves of the panel at s) and
+// apply Q2^T to the top rows R'12 (kept in L.ttop): R12 = Q2^T R'12.
+int Ctx::finish_top(double* A, int64_t lda, int64_t s, int b, int64_t n2, const double* Q2, int64_t ldt, Layout& L) {
+  const int64_t ldw = even(b);
+  RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_hipdone, 0));
+  CatGuard guard(cat, PROF_TRAIL);
+  return gemm(b, n2, b, op(Q2, b, b, ldt), false, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0);
+}
+
 // Look-ahead tail of a non-final panel at s (downdated sketches, permutation pivots):
 //   W2 = T^T W;  top b rows: R12 = Q2^T (A2_top - V_top W2)  (final);
 //   Y2 <- Y2 - G1 R12 (the next panel's sketch);
@@ -1142,8 +1289,9 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
       // top b rows: A2_top -= V_top W2, then Q2^T
       RQ_TRY(gemm(b, n2, b, Vop, true, op(L.w2, b, n2, ldw), A + s + (s + b) * lda, lda, -1.0, 1.0));
     }
-    RQ_TRY(copy2d(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
-    RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldt), false, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
+    RQ_TRY(copy2d_p(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
+    if (!cpqr_off)
+      RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldt), false, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
   }
   phase(4);
   std::swap(lorder, lorder_n);
@@ -1151,6 +1299,7 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
   const int64_t np2 = n - s - b;  // the next panel's columns
   const bool next_full = np2 > b;
   if (!next_full) {
+    if (cpqr_off) RQ_TRY(finish_top(A, lda, s, b, n2, Q2, ldt, L));
     CatGuard guard(cat, PROF_TRAIL);
     if (w2_side) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_w2, 0));
     return gemm(mp - b, n2, b, Vlow, true, op(L.w2, b, n2, ldw), A + (s + b) + (s + b) * lda, lda, -1.0, 1.0);
@@ -1162,22 +1311,27 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
   phase(5);
   // the next panel's pivots (b-step CPQR of a copy of its sketch) and moves
   const int64_t s2 = s + b;
-  if (sketch_cpqr_preserves_input(wdt, (int)np2)) {  // (the register tiers only read Y)
-    RQ_TRY(sketch_select(L.yt + s2 * L.ldy, L.ldy, wdt, (int)np2, b, rank, L.cap));
+  sketch_gmax = cpqr_off ? kSkMinGrid : 0;  // leave the b x b CPQR's cluster its 16 SMs
+  int rc;
+  if (sketch_cpqr_preserves_input(wdt, (int)np2, sketch_gmax)) {  // (the register tiers only read Y)
+    rc = sketch_select(L.yt + s2 * L.ldy, L.ldy, wdt, (int)np2, b, rank, L.cap);
   } else {
-    RQ_TRY(copy2d(L.yt + s2 * L.ldy, L.ldy, L.ybuf, L.ldy, wdt, np2, 0, stream, &launches));
-    RQ_TRY(sketch_select(L.ybuf, L.ldy, wdt, (int)np2, b, rank, L.cap));
+    rc = copy2d_p(L.yt + s2 * L.ldy, L.ldy, L.ybuf, L.ldy, wdt, np2, 0, stream, &launches);
+    if (rc == RQ_OK) rc = sketch_select(L.ybuf, L.ldy, wdt, (int)np2, b, rank, L.cap);
   }
+  sketch_gmax = 0;
+  RQ_TRY(rc);
   phase(6);
+  if (cpqr_off) RQ_TRY(finish_top(A, lda, s, b, n2, Q2, ldt, L));  // before the moves touch the top rows
   PlanCall pc{L.cap, b, lorder, (int)np2, L.flag, L.newloc, L.src, L.dst, L.nmoves, lorder_n, rank_n};
   RQ_TRY(plan_moves(pc, stream, &launches));
   MoveCall mv{A, lda, s2, 0, m, L.src, L.dst, L.nmoves, 2 * b, L.stage, even(m), L.orig, L.ostage};
-  RQ_TRY(move_columns(mv, stream, &launches));
+  RQ_TRY(move_columns_p(mv, stream, &launches));
   MoveCall my{L.yt, L.ldy, s2, 0, wdt, L.src, L.dst, L.nmoves, 2 * b, L.stage, L.ldy, nullptr, nullptr};
-  RQ_TRY(move_columns(my, stream, &launches));
+  RQ_TRY(move_columns_p(my, stream, &launches));
   if (w2_side) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_w2, 0));
   MoveCall mw{L.w2, ldw, 0, 0, b, L.src, L.dst, L.nmoves, 2 * b, L.stage, even(m), nullptr, nullptr};
-  RQ_TRY(move_columns(mw, stream, &launches));
+  RQ_TRY(move_columns_p(mw, stream, &launches));
   // the next panel's columns first; the rest pending
   {
     CatGuard guard(cat, PROF_TRAIL);
@@ -1216,7 +1370,7 @@ int Ctx::trailing_update(double* A, int64_t lda, int64_t m, int64_t n, int64_t s
   RQ_TRY(gemm(mp, n2, b, Vop, true, op(L.w2, b, n2, ldw), A + s + (s + b) * lda, lda, -1.0, 1.0));
   if (Q2) {
     // top b rows <- Q2^T top   (TN with A = Q2)
-    RQ_TRY(copy2d(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
+    RQ_TRY(copy2d_p(A + s + (s + b) * lda, lda, L.ttop, ldw, b, n2, 0, stream, &launches));
     RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldt), false, op(L.ttop, b, n2, ldw), A + s + (s + b) * lda, lda, 1.0, 0.0));
   }
   return RQ_OK;
@@ -1229,7 +1383,7 @@ int Ctx::orth(double* src, int64_t rows, int cols, int64_t ld, Layout& L) {
   double* E = L.oe;
   double* Vo = L.ov;
   const int64_t ldc = even(cols);
-  RQ_TRY(copy2d(src, ld, E, lde, rows, cols, 0, stream, &launches));
+  RQ_TRY(copy2d_p(src, ld, E, lde, rows, cols, 0, stream, &launches));
   RQ_CUDA_TRY(cudaMemsetAsync(Vo, 0, (size_t)lde * cols * sizeof(double), stream));
   launches++;
   RQ_TRY(panel_qr(E, lde, rows, cols, 0, rows, cols, Vo, lde, 0, L.tleaf, L.w1, L.w2));
@@ -1238,7 +1392,7 @@ int Ctx::orth(double* src, int64_t rows, int cols, int64_t ld, Layout& L) {
   RQ_TRY(gemm(cols, cols, rows, op(Vo, rows, cols, lde), false, op(E, rows, cols, lde), L.w1, ldc, 1.0, 0.0));
   RQ_TRY(gemm(cols, cols, cols, op(L.ot, cols, cols, ldc), true, op(L.w1, cols, cols, ldc), L.w2, ldc, 1.0, 0.0));
   RQ_TRY(gemm(rows, cols, cols, op(Vo, rows, cols, lde), true, op(L.w2, cols, cols, ldc), E, lde, -1.0, 1.0));
-  return copy2d(E, lde, src, ld, rows, cols, 0, stream, &launches);
+  return copy2d_p(E, lde, src, ld, rows, cols, 0, stream, &launches);
 }
 
 // Reflector pivot of the panel at s: sketch Y, its first b unpivoted reflectors,
@@ -1248,7 +1402,7 @@ int Ctx::reflector_pivot(const rq_config& cfg, double* A, int64_t lda, int64_t m
   Carver& fc = *reinterpret_cast<Carver*>(fc_ptr);
   const int b = cfg.block, wdt = cfg.block + cfg.oversample;
   const int64_t mp = m - s, np = n - s;
-  RQ_TRY(gaussian_fill(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
+  RQ_TRY(gaussian_fill_p(L.omega + (s & 1), mp, wdt, L.ldo, seed, *counter, stream, &launches));
   *counter += (uint64_t)mp * (uint64_t)wdt;
   RQ_TRY(sketch(cfg, A, lda, m, n, s, mp, np, L, true));  // Y (np x wdt) in ybuf
   const int64_t ldvs = even(np), ldt = even(b);
@@ -1324,7 +1478,7 @@ int Ctx::factorize_rrqr(const rq_config& cfg0, int64_t m, int64_t n, double* A, 
     }
     // rows above: A[:s, s:s+w] <- A[:s, s:s+w] V~   (blocked.py:265)
     if (s > 0) {
-      RQ_TRY(copy2d(A + s * lda, lda, L.stage, even(m), s, w, 0, stream, &launches));
+      RQ_TRY(copy2d_p(A + s * lda, lda, L.stage, even(m), s, w, 0, stream, &launches));
       RQ_TRY(gemm(s, w, w, op(L.stage, s, w, even(m)), true, op(Vt, w, w, ldt), A + s * lda, lda, 1.0, 0.0));
     }
     RQ_TRY(tfactor(V, mp, w, ldv, vpad, T, ldt, L.gram));
@@ -1422,7 +1576,7 @@ int Ctx::apply_q(const FactorSet& F, int first, int count, bool trans, bool eye,
     double* X = Q + s + c0 * ldq;
     const GemmOperand Vop = op(f.v, mp + f.vpad, f.k, f.ldv, f.vpad);
     auto small = [&]() {  // X[0:k] <- Q2 X[0:k]  (trans: Q2^T)
-      int r = copy2d(X, ldq, tt, ldw, f.k, nc, 0, stream, &launches);
+      int r = copy2d_p(X, ldq, tt, ldw, f.k, nc, 0, stream, &launches);
       if (r == RQ_OK)
         r = gemm(f.k, nc, f.k, op(f.q2, f.k, f.k, f.ldq2), !trans, op(tt, f.k, nc, ldw), X, ldq, 1.0, 0.0);
       return r;
@@ -1477,10 +1631,10 @@ int Ctx::apply_p(const FactorSet& F, int first, int count, int64_t rows, double*
       RQ_TRY(apply_right_wy(P, ldp, rows, n, f.s, f.np, f.k, f.vs, f.ldvs, f.ts, f.ldts, vst, z, z2, ldz));
     if (f.nphat > 0) {
       MoveCall mv{P, ldp, f.s, 0, rows, f.phat, io, nullptr, f.nphat, stage, ldz, nullptr, nullptr};
-      RQ_TRY(move_columns(mv, stream, &launches));
+      RQ_TRY(move_columns_p(mv, stream, &launches));
     }
     if (f.dense) {  // DenseOrtho (blocked.py:53-63): P[:, s:s+w] <- P[:, s:s+w] V~
-      RQ_TRY(copy2d(P + f.s * ldp, ldp, z, ldz, rows, f.wd, 0, stream, &launches));
+      RQ_TRY(copy2d_p(P + f.s * ldp, ldp, z, ldz, rows, f.wd, 0, stream, &launches));
       RQ_TRY(gemm(rows, f.wd, f.wd, op(z, rows, f.wd, ldz), true, op(f.dense, f.wd, f.wd, f.ldd), P + f.s * ldp,
                   ldp, 1.0, 0.0));
     }
@@ -1588,7 +1742,7 @@ int Ctx::step_panel_factor(double* P, int64_t ldp, int64_t mp, int b, double* V,
   // 6: b x b CPQR of R' (reflectors V2), Q2 = I - V2 T2 V2^T
   double* Sm = S.small;
   double* V2 = S.small + (int64_t)b * lds;
-  RQ_TRY(copy2d(P, ldp, Sm, lds, b, b, 1, stream, &launches));
+  RQ_TRY(copy2d_p(P, ldp, Sm, lds, b, b, 1, stream, &launches));
   RQ_CUDA_TRY(cudaMemsetAsync(V2, 0, (size_t)lds * b * sizeof(double), stream));
   launches++;
   SweepCall ss;
@@ -1611,7 +1765,7 @@ int Ctx::step_panel_factor(double* P, int64_t ldp, int64_t mp, int b, double* V,
   L.w2 = S.w2;
   RQ_TRY(small_q(V2, lds, b, Q2, ldq2, L));
   // 7: R of the panel (columns in P-hat order)
-  RQ_TRY(copy2d(S.rfin, lds, P, ldp, b, b, 0, stream, &launches));
+  RQ_TRY(copy2d_p(S.rfin, lds, P, ldp, b, b, 0, stream, &launches));
   // 8: T of the panel reflectors
   return tfactor(V, mp, b, ldv, 0, T, ldt, S.gram);
 }
@@ -1631,7 +1785,7 @@ int Ctx::step_panel_apply(const double* V, int64_t ldv, const double* T, int64_t
   GemmOperand Vop = op(V, mp, b, ldv, 0);
   if (odd) {
     const int64_t ldp = even(mp + 1);
-    RQ_TRY(copy2d(V, ldv, S.vpad + 1, ldp, mp, b, 0, stream, &launches));
+    RQ_TRY(copy2d_p(V, ldv, S.vpad + 1, ldp, mp, b, 0, stream, &launches));
     Vop = op(S.vpad, mp + 1, b, ldp, 1);
   }
   CatGuard guard(cat, PROF_TRAIL);
@@ -1640,7 +1794,7 @@ int Ctx::step_panel_apply(const double* V, int64_t ldv, const double* T, int64_t
   RQ_TRY(gemm(b, n2, b, op(T, b, b, ldt), false, op(S.w1, b, n2, ldw), S.w2, ldw, 1.0, 0.0));
   RQ_TRY(gemm(mp, n2, b, Vop, true, op(S.w2, b, n2, ldw), A2, lda, -1.0, 1.0));
   if (Q2) {
-    RQ_TRY(copy2d(A2, lda, S.ttop, ldw, b, n2, 0, stream, &launches));
+    RQ_TRY(copy2d_p(A2, lda, S.ttop, ldw, b, n2, 0, stream, &launches));
     RQ_TRY(gemm(b, n2, b, op(Q2, b, b, ldq2), false, op(S.ttop, b, n2, ldw), A2, lda, 1.0, 0.0));
   }
   return RQ_OK;
@@ -1657,6 +1811,8 @@ Ctx::~Ctx() {
   if (side) cudaStreamDestroy(side);
   if (hip) cudaStreamDestroy(hip);
   if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (ev_g1) cudaEventDestroy(ev_g1);
+  if (ev_hipdone) cudaEventDestroy(ev_hipdone);
   if (copy_ev) cudaEventDestroy(copy_ev);
   if (ev_v) cudaEventDestroy(ev_v);
   if (ev_side) cudaEventDestroy(ev_side);

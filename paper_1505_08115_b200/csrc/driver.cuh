@@ -5,6 +5,7 @@
 
 #include "common.cuh"
 #include "gemm_f64.cuh"
+#include "misc.cuh"
 #include "sweep.cuh"
 
 namespace rq {
@@ -31,6 +32,12 @@ struct Layout {
   int *chosen, *lorderA, *lorderB, *rankA, *rankB, *newloc, *src, *dst, *nmoves, *cap, *iota_b;
   unsigned char* flag;
   int64_t *orig, *ostage;
+  // the b x b CPQR's own buffers when it runs beside the next panel's sketch CPQR (cpqr_off)
+  int* cap2;
+  double* stage2;
+  int64_t* ostage2;
+  void* sweep_ws2;
+  size_t sweep_ws2_bytes;
   void* sweep_ws;
   size_t sweep_ws_bytes;
   size_t kwork_bytes;
@@ -63,13 +70,18 @@ enum ProfCat {
   PROF_SKETCH_GEMM = 6, // Y = Omega^T X (+ power iterations)
   PROF_PANEL_GEMM = 7,  // WY updates between panel leaves
   PROF_TFACTOR = 8,     // Gram V^T V + T back substitution, small Q2
-  PROF_NCAT = 9
+  PROF_MOVES = 9,       // column moves (gather + scatter at full height)
+  PROF_COPY = 10,       // copy2d
+  PROF_RNG = 11,        // Gaussian fills
+  PROF_SPLITK = 12,     // split-K reductions of the GEMMs
+  PROF_NCAT = 13
 };
 
 struct ProfRec {
   int cat;
   cudaEvent_t e0, e1;
   double flops;
+  double bytes = 0.0;  // algorithmic HBM bytes (bandwidth classes)
 };
 
 // Right factor of one panel with reflector pivots: S = I - V_S T_S V_S^T on
@@ -113,7 +125,13 @@ struct Ctx {
   size_t ev_next = 0;
   cudaEvent_t prof_event();
   void prof_begin(cudaEvent_t* e0);
-  void prof_end(cudaEvent_t e0, double flops);
+  void prof_end(cudaEvent_t e0, double flops, double bytes = 0.0);
+  unsigned long long* prof_dev_bytes = nullptr;  // device counter: bytes of the column moves
+  int copy2d_p(const double* S, int64_t lds, double* D, int64_t ldd, int64_t rows, int64_t cols, int upper_only,
+               cudaStream_t st, int64_t* l);
+  int move_columns_p(MoveCall c, cudaStream_t st, int64_t* l);
+  int gaussian_fill_p(double* out, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t counter,
+                      cudaStream_t st, int64_t* l);
   cudaStream_t stream = nullptr;
   rq_panel_cb inspect_cb = nullptr;
   void* inspect_user = nullptr;
@@ -143,6 +161,8 @@ struct Ctx {
   std::function<void(int64_t, int64_t)> on_cols_final;
   int gemm_max_ctas = 0;
   bool gemm_pdl = false;
+  cudaEvent_t gemm_mid = nullptr;  // profiling: split-K reduce boundary of the current GEMM
+  int gemm_splitk = 1;
   // dynamic GEMM unit scheduling: one monotone device counter per stream (main, side, hip) and
   // its host mirror (GEMMs on one stream never overlap each other, so a counter is never shared)
   unsigned long long* gsched = nullptr;
@@ -197,6 +217,13 @@ struct Ctx {
                int64_t ldc, double alpha, double beta);
   int sweep(SweepCall c);
   int sweep_raw(SweepCall c);
+  // off-chain b x b CPQR (look-ahead, RQ_CPQR_OFF): panel i's CPQR, Q2, R and rows-above moves run
+  // on the 16-SM cluster / hip stream beside panel i+1's sketch CPQR, which is capped at
+  // kSkMinGrid CTAs; the main stream joins them (ev_hipdone) before it moves panel i+1's columns
+  bool cpqr_off = false;
+  int sketch_gmax = 0;
+  cudaEvent_t ev_g1 = nullptr, ev_hipdone = nullptr;
+  int finish_top(double* A, int64_t lda, int64_t s, int b, int64_t n2, const double* Q2, int64_t ldt, Layout& L);
   unsigned long long* sk_counter = nullptr;  // device: monotone arrival counter of the sketch CPQR
   unsigned long long sk_counter_base = 0;    // host mirror of its value
   int sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen);

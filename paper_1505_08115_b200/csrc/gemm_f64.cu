@@ -550,7 +550,9 @@ static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launch
   }
   if (launches) (*launches)++;
   if (p.sched) *p.sched_base += (unsigned long long)units + (unsigned long long)grid;  // one failing fetch per CTA
+  if (p.splitk_used) *p.splitk_used = a.splitk > 1 ? a.splitk : 1;
   if (a.splitk > 1) {
+    if (p.mid_event) cudaEventRecord(p.mid_event, stream);
     const int64_t total = a.M * a.N;
     int blocks = (int)ceil_div(total, 256);
     if (blocks > 4 * num_sms()) blocks = 4 * num_sms();

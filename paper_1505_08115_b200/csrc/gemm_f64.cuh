@@ -43,6 +43,8 @@ struct GemmProblem {
   unsigned long long* sched_base = nullptr;  // host mirror of its value; advanced by every launch
   int64_t tile_begin = 0, tile_end = 0;  // tile_end > 0: only output tiles [tile_begin, tile_end)
                                          // (column-major tile order; see gemm_f64_tiles)
+  cudaEvent_t mid_event = nullptr;  // profiling: recorded between the GEMM and its split-K reduce
+  int* splitk_used = nullptr;       // profiling: receives the split-K factor used (1 = none)
 };
 
 int gemm_f64(const GemmProblem& p, cudaStream_t stream, int64_t* launches);

@@ -363,10 +363,13 @@ __global__ void __launch_bounds__(MV_THREADS) gather_cols_kernel(const double* _
                                                                  const int* __restrict__ count, int maxn,
                                                                  double* __restrict__ stage, int64_t lds,
                                                                  const int64_t* __restrict__ orig,
-                                                                 int64_t* __restrict__ ostage) {
+                                                                 int64_t* __restrict__ ostage,
+                                                                 unsigned long long* bytes) {
   const int n = count ? *count : maxn;
   const int t = blockIdx.y;
   if (t >= n) return;
+  if (bytes && blockIdx.x == 0 && threadIdx.x == 0)  // gather + scatter: 2 reads + 2 writes per element
+    atomicAdd(bytes, (unsigned long long)(r1 > r0 ? r1 - r0 : 0) * 32ull);
   const double* s = A + (coff + src[t]) * lda;
   double* d = stage + (int64_t)t * lds;
   const int64_t i0 = r0 + (int64_t)blockIdx.x * MV_CHUNK + threadIdx.x;
@@ -416,7 +419,7 @@ int move_columns(const MoveCall& c, cudaStream_t st, int64_t* launches) {
   const int64_t rows = c.r1 > c.r0 ? c.r1 - c.r0 : 0;
   const dim3 grid((unsigned)std::max<int64_t>(1, ceil_div(rows, MV_CHUNK)), (unsigned)c.maxn);
   gather_cols_kernel<<<grid, MV_THREADS, 0, st>>>(c.A, c.lda, c.coff, c.r0, c.r1, c.src, c.count, c.maxn, c.stage,
-                                                  c.lds, c.orig, c.ostage);
+                                                  c.lds, c.orig, c.ostage, c.bytes);
   RQ_CUDA_TRY(cudaGetLastError());
   scatter_cols_kernel<<<grid, MV_THREADS, 0, st>>>(c.A, c.lda, c.coff, c.r0, c.r1, c.dst, c.count, c.maxn, c.stage,
                                                    c.lds, c.orig, c.ostage);

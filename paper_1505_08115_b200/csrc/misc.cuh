@@ -39,6 +39,7 @@ struct MoveCall {
   int64_t lds;
   int64_t* orig;     // optional label array moved alongside
   int64_t* ostage;
+  unsigned long long* bytes = nullptr;  // profiling: += HBM bytes moved (device counter)
 };
 int move_columns(const MoveCall& c, cudaStream_t st, int64_t* launches);
 

@@ -1813,7 +1813,7 @@ static int launch_sketch_reg(const SketchArgs& a, int G, SkSlot2* slots, SkWin* 
 // 7 shared-memory columns per warp (<= 200 KB), 156 columns per CTA.
 template <int RPL>
 static int dispatch_sketch_reg(SketchArgs a, int n, SkSlot2* slots, SkWin* wins, unsigned long long stamp_base,
-                               cudaStream_t st, int64_t* launches, int* grid) {
+                               cudaStream_t st, int64_t* launches, int* grid, int gmax) {
   struct Opt {
     int warps, cpw;
   };
@@ -1823,7 +1823,7 @@ static int dispatch_sketch_reg(SketchArgs a, int n, SkSlot2* slots, SkWin* wins,
   for (const Opt& o : opts) {
     if (RPL * o.cpw > (o.warps == 16 ? 30 : 92)) continue;  // register budget
     const int G = (n + o.warps * o.cpw - 1) / (o.warps * o.cpw);
-    if (G > kSMs) continue;
+    if (G > gmax) continue;
     *grid = G;
     if (o.warps == 16 && o.cpw == 1) return launch_sketch_reg<RPL, 1, 16>(a, G, slots, wins, stamp_base, st, launches);
     if (o.warps == 16 && o.cpw == 2) return launch_sketch_reg<RPL, 2, 16>(a, G, slots, wins, stamp_base, st, launches);
@@ -1838,7 +1838,7 @@ static int dispatch_sketch_reg(SketchArgs a, int n, SkSlot2* slots, SkWin* wins,
   }
   if constexpr (RPL == 9) {
     constexpr int W = 12, C = 6;
-    const int per_needed = (n + kSMs - 1) / kSMs;
+    const int per_needed = (n + gmax - 1) / gmax;
     const int spw = std::max(1, (per_needed - W * C + W - 1) / W);
     if (spw <= 7 && (size_t)W * spw * RPL * 32 * 8 <= 200 * 1024) {
       a.spw = spw;
@@ -1865,18 +1865,19 @@ static int dispatch_sketch_reg(SketchArgs a, int n, SkSlot2* slots, SkWin* wins,
 size_t sketch_ll_column_bytes(int m) { return 2 * (size_t)kSMs * 2 * ((size_t)m + 2) * 8; }
 // True when sketch_cpqr_launch(m, n) runs a register / shared-memory tier, which only reads Y
 // (the L2-streaming fallback overwrites it).  Mirrors dispatch_sketch_reg's choice.
-bool sketch_cpqr_preserves_input(int m, int n) {
+bool sketch_cpqr_preserves_input(int m, int n, int gmax) {
+  if (gmax <= 0 || gmax > kSMs) gmax = kSMs;
   if (m > 288) return false;
   const int rpl = m <= 96 ? 3 : (m <= 160 ? 5 : 9);
   const int opts[][2] = {{16, 1}, {16, 2}, {16, 3}, {8, 6}, {8, 8}, {8, 9}, {8, 10}};
   for (const auto& o : opts) {
     if (rpl * o[1] > (o[0] == 16 ? 30 : 92)) continue;
     if ((o[1] == 8 || o[1] == 9) && rpl != 9) continue;
-    if ((n + o[0] * o[1] - 1) / (o[0] * o[1]) <= kSMs) return true;
+    if ((n + o[0] * o[1] - 1) / (o[0] * o[1]) <= gmax) return true;
   }
   if (rpl == 9) {
     const int W = 12, C = 6;
-    const int per_needed = (n + kSMs - 1) / kSMs;
+    const int per_needed = (n + gmax - 1) / gmax;
     const int spw = std::max(1, (per_needed - W * C + W - 1) / W);
     if (spw <= kSkMaxSpw) return true;  // shared memory, then the global tier
   }
@@ -1887,7 +1888,7 @@ bool sketch_cpqr_preserves_input(int m, int n) {
 size_t sketch_glob_bytes(int m, int n) {
   if (m <= 160 || m > 288) return 0;
   const int W = 12, C = 6;
-  const int per_needed = (n + kSMs - 1) / kSMs;
+  const int per_needed = (n + kSkMinGrid - 1) / kSkMinGrid;  // the most columns per CTA a launch uses
   const int spw = std::max(1, (per_needed - W * C + W - 1) / W);
   if (spw <= 7 || spw > kSkMaxSpw) return 0;
   return (size_t)kSMs * W * (spw - 7) * 9 * 32 * sizeof(double);
@@ -1904,8 +1905,10 @@ static size_t sketch_fixed_smem(int m, int per) {
 
 int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, const int* init_pos, int* chosen,
                        SweepWork& w, unsigned long long* counter, unsigned long long& counter_base, cudaStream_t st,
-                       int64_t* launches) {
+                       int64_t* launches, int gmax) {
   if (steps <= 0) return RQ_OK;
+  if (gmax <= 0 || gmax > kSMs) gmax = kSMs;
+  if (gmax < kSkMinGrid) gmax = kSkMinGrid;
   if (m <= 288) {
     SketchArgs a{};
     a.y = y;
@@ -1941,9 +1944,9 @@ int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, con
       }();
       a.fixed_reducer = env_fr;
       int rc, G = 0;
-      if (m <= 96) rc = dispatch_sketch_reg<3>(a, n, slots, wins, stamp_base, st, launches, &G);
-      else if (m <= 160) rc = dispatch_sketch_reg<5>(a, n, slots, wins, stamp_base, st, launches, &G);
-      else rc = dispatch_sketch_reg<9>(a, n, slots, wins, stamp_base, st, launches, &G);
+      if (m <= 96) rc = dispatch_sketch_reg<3>(a, n, slots, wins, stamp_base, st, launches, &G, gmax);
+      else if (m <= 160) rc = dispatch_sketch_reg<5>(a, n, slots, wins, stamp_base, st, launches, &G, gmax);
+      else rc = dispatch_sketch_reg<9>(a, n, slots, wins, stamp_base, st, launches, &G, gmax);
       if (rc >= 0) {
         counter_base += (unsigned long long)steps * G;  // every CTA arrives once per step
         return rc;
@@ -1951,7 +1954,7 @@ int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, con
     }
   }
   int G = (n + 15) / 16;  // >= 16 columns per CTA
-  if (G > kSMs) G = kSMs;
+  if (G > gmax) G = gmax;
   if (G < 1) G = 1;
   const int per = (n + G - 1) / G;
   const size_t kMax = 220 * 1024;

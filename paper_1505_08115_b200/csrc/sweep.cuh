@@ -46,7 +46,10 @@ struct SweepCall {
 size_t sweep_workspace_bytes(int64_t m, int total_cols, int grid);
 size_t sketch_ll_column_bytes(int m);
 size_t sketch_workspace_bytes(int m, int n);  // register-resident sketch CPQR (LL exchange) of n columns
-bool sketch_cpqr_preserves_input(int m, int n);
+// Smallest grid a sketch CPQR launch is given (the overlapped schedule leaves 16 SMs to the b x b
+// CPQR's cluster); workspace sizes cover it.
+constexpr int kSkMinGrid = kSMs - 16;
+bool sketch_cpqr_preserves_input(int m, int n, int gmax = 0);
 int sweep_grid_size(int total_cols);
 int sweep_debug_timing(int on, unsigned long long* host, int count);
 int sweep_launch(const SweepCall& c, SweepWork& w, cudaStream_t st, int64_t* launches);
@@ -55,6 +58,6 @@ int sweep_launch(const SweepCall& c, SweepWork& w, cudaStream_t st, int64_t* lau
 // y (m x n, ld) is overwritten.  m <= 1024.
 int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, const int* init_pos, int* chosen,
                        SweepWork& w, unsigned long long* counter, unsigned long long& counter_base, cudaStream_t st,
-                       int64_t* launches);
+                       int64_t* launches, int gmax = 0);
 
 }  // namespace rq
