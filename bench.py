@@ -47,6 +47,35 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 36.96  # measured DMMA m16n8k4 peak on this pool's B200 (profiles/probe_r01.jsonl)
+CATS = ["trailing_gemm", "other_gemm", "sketch_cpqr", "panel_leaf", "other", "small_cpqr", "sketch_gemm",
+        "panel_gemm", "tfactor", "moves", "copy2d", "rng", "splitk_reduce"]
+BW_CATS = {"moves": 9, "copy2d": 10, "rng": 11, "splitk_reduce": 12}
+
+
+def hbm_peak():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else the recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
+    except Exception:
+        return 7700.0, "B200 nominal 7.7 TB/s (B200_PROFILING.md fallback)"
+
+
+def read_breakdown(lib, handle, check):
+    """Per-class device time of one profiled step, plus algorithmic GB/s for the bandwidth classes."""
+    cats = {}
+    peak, src = hbm_peak()
+    for c, name in enumerate(CATS):
+        t, f, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        check(lib.rq_profile_read(handle, c, ctypes.byref(t), ctypes.byref(f), ctypes.byref(k)))
+        cats[name] = {"ms": t.value, "launches": k.value}
+        if name in BW_CATS:
+            by = ctypes.c_double()
+            check(lib.rq_profile_bytes(handle, c, ctypes.byref(by)))
+            gbs = by.value / (t.value * 1e-3) / 1e9 if t.value > 0 else None
+            cats[name].update({"bytes": by.value, "gbs": gbs, "frac_of_hbm": (gbs / peak) if gbs else None})
+    cats["hbm_peak_gbs"] = {"value": peak, "source": src}
+    return cats
 METRIC = "fp64 TFLOP/s (4/3·n³ count) for HQRRP at n=10k–40k; % of FP64 TC peak"
 
 
@@ -124,6 +153,18 @@ def cpu_oracle_sample(n, b, p, panels, threads=None):
     return nominal_panel_flops(n, n, b, panels) / dt / 1e12, dt
 
 
+def cpu_oracle_full(n, b, p):
+    """One complete oracle factorization (fresh sketch) of an n x n N(0,1) matrix: (seconds, TFLOP/s)."""
+    from oracle import randqr_oracle as O
+
+    a = O.gaussian_matrix(n, n, O.RngState(0))
+    cfg = O.BlockConfig(b, O.SketchConfig(b, p, 0))
+    t0 = time.perf_counter()
+    O.block_qr(a, cfg, O.RngState(1))
+    dt = time.perf_counter() - t0
+    return dt, 4.0 / 3.0 * n ** 3 / dt / 1e12
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -162,6 +203,44 @@ def run_reference(args, rank, world):
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def device_time_n(eng, lib, check, torch, stream, n, b, p, mode, pk, steps=None):
+    """One n x n factorization per step on the device (A resident, pristine copy per step)."""
+    import paper_1505_08115_b200 as rq
+    from paper_1505_08115_b200 import _lib
+
+    steps = steps or (2 if n <= 20000 else 1)
+    with torch.cuda.stream(stream):
+        a0, ld = rq.gaussian_matrix_device(n, n, rq.RngState(0), engine=eng)
+        work = torch.empty_like(a0)
+        perm = torch.empty(n, dtype=torch.int64, device=eng.device)
+    cfg = _lib.rq_config(b, p, 0, -1, pk, 0, mode, 0)
+
+    def step():
+        with torch.cuda.stream(stream):
+            work.copy_(a0)
+        ctr = ctypes.c_uint64(0)
+        check(lib.rq_factorize(eng.handle, ctypes.byref(cfg), n, n, ctypes.c_void_p(work.data_ptr()), ld,
+                               ctypes.c_uint64(1), ctypes.byref(ctr), ctypes.c_void_p(perm.data_ptr())))
+
+    step()
+    torch.cuda.synchronize()
+    clocks = Clocks(eng.device.index)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    clk = clocks.stop()
+    tf = 4.0 / 3.0 * n ** 3 / (ms * 1e-3) / 1e12
+    del a0, work, perm
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "value": tf, "unit": "TFLOP/s", "fraction_of_fp64_peak": tf / FP64_PEAK_TFLOPS,
+            "steps": steps, "warmup": 1, "sm_mhz": clk.get("sm_mhz"), "reasons": clk.get("reasons")}
 
 
 def trailing_flops_rank(m, n, b, world, rank):
@@ -227,12 +306,7 @@ def run_distributed(args, dist, rank, world, local):
     check(eng.lib.rq_set_profiling(eng.handle, 1))  # breakdown from one separate profiled step
     step()
     torch.cuda.synchronize()
-    cats = {}
-    for c, name in enumerate(["trailing_gemm", "other_gemm", "sketch_cpqr", "panel_leaf", "other", "small_cpqr",
-                              "sketch_gemm", "panel_gemm", "tfactor"]):
-        t, f, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
-        check(eng.lib.rq_profile_read(eng.handle, c, ctypes.byref(t), ctypes.byref(f), ctypes.byref(k)))
-        cats[name] = {"ms": t.value, "launches": k.value}
+    cats = read_breakdown(eng.lib, eng.handle, check)
     check(eng.lib.rq_set_profiling(eng.handle, 0))
     tt = torch.tensor([ms], device=eng.device, dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -373,6 +447,8 @@ def main():
                     help="headline sketch mode: downdate = HQRRP (Y = G A once, Y2 <- Y2 - G1 R12 per panel, "
                          "the north star's hot path); fresh = the reference's per-panel fresh sketch")
     ap.add_argument("--no-variant", action="store_true", help="skip timing the other sketch mode")
+    ap.add_argument("--per-n", default="20000,40000",
+                    help="extra sizes timed on the device in the same run (reported under per_n; '' = none)")
     ap.add_argument("--method", default="m1", choices=["m1", "m2", "m3"],
                     help="m1 block_qr permutation pivots (headline), m2 reflector pivots, m3 block_rrqr")
     ap.add_argument("--q", type=int, default=0, help="power iterations of the sketch")
@@ -478,12 +554,7 @@ def main():
     check(lib.rq_set_profiling(eng.handle, 1))
     step()
     torch.cuda.synchronize()
-    cats = {}
-    for c, name in enumerate(["trailing_gemm", "other_gemm", "sketch_cpqr", "panel_leaf", "other", "small_cpqr",
-                              "sketch_gemm", "panel_gemm", "tfactor"]):
-        t, f, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
-        check(lib.rq_profile_read(eng.handle, c, ctypes.byref(t), ctypes.byref(f), ctypes.byref(k)))
-        cats[name] = {"ms": t.value, "launches": k.value}
+    cats = read_breakdown(lib, eng.handle, check)
     check(lib.rq_set_profiling(eng.handle, 0))
     ms_max = ms
     if dist is not None:
@@ -509,6 +580,14 @@ def main():
         vms = ev0.elapsed_time(ev1) / args.steps
         variant = {"sketch": other, "value": flops_step / (vms * 1e-3) / 1e12, "ms_per_step": vms}
         cfg.sketch_mode = mode
+
+    # device-time sub-results at the north star's larger sizes (cfg 5 family), same mode and timer
+    per_n = None
+    if args.per_n and args.method == "m1" and args.matrix == "gauss" and world == 1:
+        per_n = {}
+        for n_big in [int(x) for x in args.per_n.split(",") if x]:
+            per_n[str(n_big)] = device_time_n(eng, lib, check, torch, stream, n_big, b, p, mode, pk)
+        torch.cuda.synchronize()
 
     # dominant kernel roofline: the trailing-update DMMA GEMMs
     t_trail = cats["trailing_gemm"]["ms"]
@@ -546,9 +625,16 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         val, dt = cpu_oracle_sample(n, b, p, args.cpu_panels)
+        full = []
+        for (fn_, fb_, fp_) in ((2000, 64, 10), (4000, 128, 10)):
+            sec, tf = cpu_oracle_full(fn_, fb_, fp_)
+            full.append({"n": fn_, "b": fb_, "p": fp_, "seconds": sec, "value": tf, "unit": "TFLOP/s"})
         cpu = {"value": val, "unit": "TFLOP/s", "cores": host_cores(), "kind": "port",
-               "sample": f"oracle block_qr, first {args.cpu_panels} panels of n={n} ({dt:.1f} s), "
-                         f"credited 4 m' b n2 per panel"}
+               "sample": f"PORT (oracle/: restatement of the reference's numba sweeps + OpenBLAS GEMMs, fresh "
+                         f"sketch), PANEL SAMPLE: the first {args.cpu_panels} panels of the n={n} factorization "
+                         f"({dt:.1f} s), EXTRAPOLATED: rate = those panels' 4 m' b n2 credit / their time",
+               "full_factorizations": full,
+               "full_note": "complete oracle block_qr runs (N(0,1), seed 0 / sketch seed 1) timed in the same run"}
 
     if rank == 0:
         line = {
@@ -577,6 +663,7 @@ def main():
             "breakdown_note": "one separate profiled step (CUDA events per launch); classes overlap in time "
                               "(W = V^T A2 and T run beside the b x b CPQR)",
             "variant": variant,
+            "per_n": per_n,
             "clocks": clk,
             "gpu_launches": launches,
             "e2e": e2e,

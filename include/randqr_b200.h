@@ -157,6 +157,12 @@ int rq_qr_unpivoted(rq_ctx* ctx, int64_t m, int64_t n, double* dA, int64_t lda, 
  * dense expansion): A P = Q R gives ||A - Q(:,1:k) R(1:k,:) P^T||_F = ||R(k:, k:)||_F, so for the
  * n x n upper-triangular block dR this writes dE2[k] = ||R(k:, k:)||_F^2, k = 0..n (n+1 values). */
 int rq_trailing_frobenius(rq_ctx* ctx, const double* dR, int64_t n, int64_t ldr, double* dE2);
+/* Spectral truncation errors (metrics.truncation_errors, metrics.py:37-52; core.spectral_norm is the
+ * largest singular value, core.py:39-46): hOut[i] = ||R(k:, k:)||_2 for k = hks[i] (host arrays),
+ * via the Jacobi SVD kernel when n - k <= 512 (hHow[i] = 0), else power iteration on R22^T R22 to a
+ * relative change below 1e-13 (hHow[i] = 1); hHow[i] = 2 for k = n.  Synchronous. */
+int rq_trailing_spectral(rq_ctx* ctx, const double* dR, int64_t n, int64_t ldr, const int64_t* hks, int32_t nks,
+                         double* hOut, int32_t* hHow);
 
 /* ---- Panel-step API: one HQRRP panel at a time on caller-owned device buffers.
  * Used by a driver that owns the column distribution (paper_1505_08115_b200/dist.py,

@@ -66,6 +66,7 @@ _SIGS = {
     "rq_splitmix_words": (ctypes.c_int, [_vp, _u64, _u64, _i64, _vp]),
     "rq_qr_unpivoted": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i64, _i32]),
     "rq_trailing_frobenius": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp]),
+    "rq_trailing_spectral": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i32, _vp, _vp]),
     "rq_gemm": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64,
                                _i64, _i64, _i64, _i64, _vp, _i64, ctypes.c_double, ctypes.c_double]),
     "rq_sketch_select": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),

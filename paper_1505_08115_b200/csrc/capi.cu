@@ -421,6 +421,15 @@ int rq_trailing_frobenius(rq_ctx* ctx, const double* dR, int64_t n, int64_t ldr,
   return rq::trailing_frobenius(dR, n, ldr, dE2, ctx->c.stream, &ctx->c.launches);
 }
 
+int rq_trailing_spectral(rq_ctx* ctx, const double* dR, int64_t n, int64_t ldr, const int64_t* hks, int32_t nks,
+                         double* hOut, int32_t* hHow) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (n < 0 || ldr < n || (ldr & 1) || ((uintptr_t)dR & 15)) return rq::set_error(RQ_EDIM, "trailing_spectral: bad shape");
+  if (nks < 0 || (nks > 0 && (!hks || !hOut || !hHow))) return rq::set_error(RQ_EVALUE, "trailing_spectral: null");
+  return ctx->c.trailing_spectral(dR, n, ldr, reinterpret_cast<const int64_t*>(hks), nks, hOut, hHow);
+}
+
 // ---------------------------------------------------------------------------
 // Panel-step API (multi-GPU driver, dist.py)
 // ---------------------------------------------------------------------------

@@ -1642,6 +1642,103 @@ int Ctx::apply_p(const FactorSet& F, int first, int count, int64_t rows, double*
   return RQ_OK;
 }
 
+// Spectral truncation errors ||R(k:, k:)||_2 (metrics.truncation_errors' spectral half,
+// metrics.py:37-52, via A P = Q R).  Blocks up to 512 wide: largest singular value from the
+// Jacobi SVD kernel (the reference's core.spectral_norm is its Jacobi svd_values, core.py:39-46);
+// wider: power iteration on R22^T R22 (DMMA GEMMs), stopped at a relative change below 1e-13 or
+// after 2000 iterations.  how[i] = 0 exact (Jacobi), 1 power iteration, 2 empty block.
+int Ctx::trailing_spectral(const double* R, int64_t n, int64_t ldr, const int64_t* ks, int nks, double* out,
+                           int32_t* how) {
+  const int64_t wmax = 512;
+  const int64_t ldw = wmax;
+  const int64_t ldx = even(n) + 2;
+  const size_t need = (size_t)4 * ldw * wmax * 8 + (size_t)wmax * 8 + 64 + (size_t)ldx * 2 * 8 * 2 + 4096 * 8 +
+                      (size_t)kSMs * 8 * 8 * 64;
+  RQ_TRY(qarena.reserve(need));
+  Carver c(qarena.base);
+  double* wb = c.take<double>((size_t)ldw * wmax);
+  double* vb = c.take<double>((size_t)ldw * wmax);
+  double* ub = c.take<double>((size_t)ldw * wmax);
+  double* vt = c.take<double>((size_t)ldw * wmax);
+  double* d = c.take<double>((size_t)wmax);
+  int* status = c.take<int>(16);
+  double* x = c.take<double>((size_t)ldx * 2);
+  double* y = c.take<double>((size_t)ldx * 2);
+  double* norms = c.take<double>(4096);
+  double* save_kw = kwork;
+  const size_t save_kb = kwork_bytes;
+  kwork = nullptr;
+  kwork_bytes = 0;
+  int rc = RQ_OK;
+  for (int i = 0; i < nks && rc == RQ_OK; i++) {
+    const int64_t k = ks[i];
+    if (k < 0 || k > n) {
+      rc = set_error(RQ_EVALUE, "ranks must lie in [0, %lld]", (long long)n);
+      break;
+    }
+    const int64_t w = n - k;
+    const double* Rk = R + k + k * ldr;
+    if (w == 0) {
+      out[i] = 0.0;
+      how[i] = 2;
+      continue;
+    }
+    if (w <= wmax) {
+      rc = jacobi_svd(Rk, ldr, (int)w, wb, ldw, vb, ldw, d, ub, ldw, vt, ldw, status, stream, &launches);
+      if (rc != RQ_OK) break;
+      int st = 0;
+      double d0 = 0.0;
+      if (cudaMemcpyAsync(&st, status, sizeof(int), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+          cudaMemcpyAsync(&d0, d, 8, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+          cudaStreamSynchronize(stream) != cudaSuccess) {
+        rc = set_error(RQ_ECUDA, "spectral: readback");
+        break;
+      }
+      if (st < 0) {
+        rc = set_error(RQ_ECONV, "Jacobi SVD did not converge in 60 sweeps");
+        break;
+      }
+      out[i] = d0;
+      how[i] = 0;
+      continue;
+    }
+    // power iteration: x <- R22^T (R22 x) / ||.||, start from the all-ones vector (deterministic)
+    std::vector<double> ones((size_t)ldx * 2, 0.0);
+    for (int64_t r = 0; r < w; r++) ones[r] = 1.0;
+    if (cudaMemcpyAsync(x, ones.data(), (size_t)ldx * 2 * 8, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess) {
+      rc = set_error(RQ_ECUDA, "spectral: upload");
+      break;
+    }
+    const GemmOperand Rop = op(R, n, n, ldr, k, k);  // R22 (w x w), NN / TN views
+    double prev = -1.0, est = 0.0;
+    const int batch = 20, max_it = 2000;
+    for (int it = 0; it < max_it && rc == RQ_OK; it += batch) {
+      for (int t = 0; t < batch && rc == RQ_OK; t++) {
+        rc = gemm(w, 2, w, Rop, true, op(x, ldx, 2, ldx), y, ldx, 1.0, 0.0);            // y = R22 x
+        if (rc == RQ_OK) rc = gemm(w, 2, w, Rop, false, op(y, ldx, 2, ldx), x, ldx, 1.0, 0.0);  // x = R22^T y
+        if (rc == RQ_OK) rc = normalize_col(x, w, norms, t, stream, &launches);
+      }
+      if (rc != RQ_OK) break;
+      std::vector<double> hn(batch);
+      if (cudaMemcpyAsync(hn.data(), norms, batch * 8, cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+          cudaStreamSynchronize(stream) != cudaSuccess) {
+        rc = set_error(RQ_ECUDA, "spectral: readback");
+        break;
+      }
+      est = std::sqrt(hn[batch - 1]);  // ||R22^T R22 x|| -> sigma_max^2 for unit x
+      const double before = std::sqrt(hn[batch - 2]);
+      if (std::fabs(est - before) <= 1e-13 * est || (prev >= 0.0 && std::fabs(est - prev) <= 1e-13 * est)) break;
+      prev = est;
+    }
+    out[i] = est;
+    how[i] = 1;
+  }
+  kwork = save_kw;
+  kwork_bytes = save_kb;
+  return rc;
+}
+
 int Ctx::snapshot(double* hW, int64_t ldh) {
   if (!cur_A) return set_error(RQ_EVALUE, "no factorization in progress");
   RQ_CUDA_TRY(cudaStreamSynchronize(stream));

@@ -269,6 +269,8 @@ struct Ctx {
   int apply_q(const FactorSet& F, int first, int count, bool trans, bool eye, int64_t cols, double* X, int64_t ldx);
   int apply_p(const FactorSet& F, int first, int count, int64_t rows, double* X, int64_t ldx);
   int snapshot(double* hW, int64_t ldh);
+  int trailing_spectral(const double* R, int64_t n, int64_t ldr, const int64_t* ks, int nks, double* out,
+                        int32_t* how);
   int snapshot_sketch(double* hY, int64_t ldh, int64_t* hperm);
 };
 

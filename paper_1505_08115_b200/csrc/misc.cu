@@ -592,4 +592,35 @@ int widen(const int* a, int n, int64_t off, int64_t* out, cudaStream_t st, int64
   return RQ_OK;
 }
 
+// Power-iteration step helper (trailing spectral norms): x <- x / ||x||, norms[it] = ||x||.
+// One CTA, fixed reduction order (deterministic).
+__global__ void __launch_bounds__(1024) normalize_col_kernel(double* __restrict__ x, int64_t n,
+                                                             double* __restrict__ norms, int it) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc = fma(x[i], x[i], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double nrm = sqrt(red[0]);
+  const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] *= inv;
+  if (threadIdx.x == 0) norms[it] = nrm;
+}
+
+int normalize_col(double* x, int64_t n, double* norms, int it, cudaStream_t st, int64_t* launches) {
+  normalize_col_kernel<<<1, 1024, 0, st>>>(x, n, norms, it);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
 }  // namespace rq

@@ -5,6 +5,7 @@
 namespace rq {
 
 int trailing_frobenius(const double* R, int64_t n, int64_t ldr, double* e2, cudaStream_t st, int64_t* launches);
+int normalize_col(double* x, int64_t n, double* norms, int it, cudaStream_t st, int64_t* launches);
 int trinv_upper(const double* R, int64_t ldr, int k, double* X, int64_t ldx, cudaStream_t st, int64_t* launches);
 int q_from_reflectors(const double* V, int64_t ldv, int k, int n, double* Q, int64_t ldq, cudaStream_t st,
                       int64_t* launches);

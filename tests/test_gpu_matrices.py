@@ -75,3 +75,31 @@ def test_truncation_errors_frobenius_vs_dense():
     for k, e in zip(ks, got):
         dense = np.linalg.norm(a - q[:, :k] @ rp[:k, :]) if k > 0 else np.linalg.norm(a)
         assert abs(e - dense) <= 1e-12 * np.linalg.norm(a) + 1e-10 * dense
+
+
+def test_truncation_errors_spectral_and_frobenius_match_dense():
+    """metrics.truncation_errors (metrics.py:37-52) from R on the device -- Jacobi SVD kernel for
+    trailing blocks <= 512 wide, power iteration beyond -- against the dense definition."""
+    import paper_1505_08115_b200 as rq
+    from paper_1505_08115_b200 import metrics
+
+    rng = np.random.default_rng(4)
+    n = 700
+    s = 10.0 ** (-3.0 * np.arange(n) / n)
+    u, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = np.asfortranarray((u * s) @ v.T)
+    f = rq.block_qr(a, rq.BlockConfig(64, rq.SketchConfig(64, 8, 0)), rq.RngState(1))
+    ks = [0, 64, 150, 188, 600, 700]
+    c = metrics.truncation_errors(a, f, ks)
+    q, p = f.expand_q(), f.expand_p()
+    rp = f.r[:n, :] @ p.T
+    for i, k in enumerate(ks):
+        resid = a - q[:, :k] @ rp[:k, :] if k else a
+        fro = np.linalg.norm(resid)
+        sp = np.linalg.norm(resid, 2) if k < n else 0.0
+        assert abs(c.frobenius[i] - fro) <= 1e-12 * np.linalg.norm(a), (k, c.frobenius[i], fro)
+        tol = 1e-9 if n - k > 512 else 1e-12
+        assert abs(c.spectral[i] - sp) <= tol * max(sp, 1e-300) + 1e-13 * np.linalg.norm(a), (k, c.spectral[i], sp)
+    d = metrics.diag_comparison(f, s)
+    assert np.array_equal(d.r_abs, np.abs(np.diag(f.r)))
