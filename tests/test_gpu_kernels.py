@@ -182,3 +182,78 @@ def test_sketch_cpqr_tiers_choose_the_oracle_pivots(eng, m, n, steps):
     ref = O.qr_column_pivoted(y, steps=steps).perm[:steps]
     assert np.array_equal(ch.cpu().numpy().astype(np.int64), ref)
     assert torch.equal(buf, before)
+
+
+def test_exchange_kernels_repeatable_under_stress():
+    """compute-sanitizer is closed on this pool (profiles/sanitizer_r02_closed.txt), so the
+    fence-free exchanges (LL-stamped grid words of sketch_reg_kernel, st.async cluster pushes of
+    sweep_reg_kernel / leaf_reg_kernel) are stress-tested instead: many back-to-back launches on
+    fresh inputs, every result bitwise equal to a first run and the pivots to the oracle's."""
+    import ctypes
+
+    import torch
+
+    import paper_1505_08115_b200 as rq
+    from oracle import randqr_oracle as O
+    from paper_1505_08115_b200.errors import check
+
+    eng = rq.Engine()
+    lib = eng.lib
+    rng = np.random.default_rng(123)
+
+    def dev(x):
+        buf, ld = eng.alloc_matrix(*x.shape)
+        buf[: x.shape[1], : x.shape[0]].copy_(torch.from_numpy(np.ascontiguousarray(x.T)))
+        return buf, ld
+
+    for (m, n, steps) in [(272, 3000, 256), (74, 1200, 64), (272, 9000, 128)]:
+        y0 = rng.standard_normal((m, n))
+        src, ld = dev(y0)
+        work, _ = eng.alloc_matrix(m, n)
+        outs = []
+        for _ in range(40):
+            work.copy_(src)
+            ch = torch.zeros(steps, dtype=torch.int32, device=eng.device)
+            check(lib.rq_test_sketch_cpqr(eng.handle, ctypes.c_void_p(work.data_ptr()), ld, m, n, steps,
+                                          ctypes.c_void_p(ch.data_ptr())))
+            outs.append(ch)
+        ref = outs[0].cpu().numpy()
+        for o in outs[1:]:
+            assert np.array_equal(o.cpu().numpy(), ref)
+        assert np.array_equal(ref.astype(np.int64), O.qr_column_pivoted(y0, steps=steps).perm[:steps]), (m, n)
+    for k in (96, 256):
+        a0 = rng.standard_normal((k, k))
+        src, ld = dev(a0)
+        work, _ = eng.alloc_matrix(k, k)
+        v, ldv = eng.alloc_matrix(k, k)
+        first = None
+        for _ in range(60):
+            work.copy_(src)
+            v.zero_()
+            perm = torch.arange(k, dtype=torch.int64, device=eng.device)
+            check(lib.rq_householder_sweep(eng.handle, ctypes.c_void_p(work.data_ptr()), k, k, ld,
+                                           ctypes.c_void_p(v.data_ptr()), ldv, ctypes.c_void_p(perm.data_ptr()), k, 1))
+            got = (perm.cpu().numpy(), work[:k, :k].cpu().numpy().copy())
+            if first is None:
+                first = got
+            else:
+                assert np.array_equal(got[0], first[0]) and np.array_equal(got[1], first[1])
+        assert np.array_equal(first[0], O.qr_column_pivoted(a0).perm)
+    for (mm, w) in [(3000, 16), (700, 32)]:
+        a0 = rng.standard_normal((mm, w))
+        src, ld = dev(a0)
+        work, _ = eng.alloc_matrix(mm, w)
+        v, ldv = eng.alloc_matrix(mm, w)
+        t, ldt = eng.alloc_matrix(32, 32)
+        first = None
+        for _ in range(60):
+            work.copy_(src)
+            check(lib.rq_test_leaf_qr(eng.handle, ctypes.c_void_p(work.data_ptr()), ld, mm, w,
+                                      ctypes.c_void_p(v.data_ptr()), ldv, ctypes.c_void_p(t.data_ptr()), ldt))
+            got = work[:w, :mm].cpu().numpy().copy()
+            if first is None:
+                first = got
+            else:
+                assert np.array_equal(got, first)
+        r_ref = O.qr_unpivoted(a0).r[:w, :]
+        assert np.abs(np.triu(first.T[:w, :]) - r_ref).max() <= 1e-12 * np.linalg.norm(a0)
