@@ -179,6 +179,14 @@ int rq_trailing_spectral(rq_ctx* ctx, const double* dR, int64_t n, int64_t ldr, 
  * (k <= 512), on the context's stream. */
 int rq_trinv_upper(rq_ctx* ctx, const double* dR, int64_t ldr, int32_t k, double* dX, int64_t ldx);
 
+/* fp32 GEMM on the tcgen05 tensor cores (3xTF32 split products, FP32 accumulation in TMEM, TMA
+ * staging; the fp32 path's sketch, trailing update and Q formation): the same operands and views
+ * as rq_gemm with fp32 buffers, ld % 4 == 0 and 16-byte aligned bases. */
+int rq_gemm_f32(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, const float* dA, int64_t lda,
+                int64_t a_rows, int64_t a_cols, int64_t a_r0, int64_t a_c0, const float* dB, int64_t ldb,
+                int64_t b_rows, int64_t b_cols, int64_t b_r0, int64_t b_c0, float* dC, int64_t ldc, double alpha,
+                double beta);
+
 int rq_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, const double* dA, int64_t lda,
             int64_t a_rows, int64_t a_cols, int64_t a_r0, int64_t a_c0, const double* dB, int64_t ldb, int64_t b_rows,
             int64_t b_cols, int64_t b_r0, int64_t b_c0, double* dC, int64_t ldc, double alpha, double beta);

@@ -69,6 +69,8 @@ _SIGS = {
     "rq_trailing_spectral": (ctypes.c_int, [_vp, _vp, _i64, _i64, _vp, _i32, _vp, _vp]),
     "rq_gemm": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64,
                                _i64, _i64, _i64, _i64, _vp, _i64, ctypes.c_double, ctypes.c_double]),
+    "rq_gemm_f32": (ctypes.c_int, [_vp, _i32, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64,
+                                   _i64, _i64, _i64, _i64, _vp, _i64, ctypes.c_double, ctypes.c_double]),
     "rq_sketch_select": (ctypes.c_int, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
     "rq_panel_factor": (ctypes.c_int, [_vp, _vp, _i64, _i64, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     "rq_panel_apply": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i32, _vp, _i64, _i64, _i64,

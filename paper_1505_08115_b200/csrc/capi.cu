@@ -2,6 +2,7 @@
 #include <new>
 
 #include "driver.cuh"
+#include "gemm_tf32.cuh"
 #include "misc.cuh"
 #include "panel.cuh"
 
@@ -434,6 +435,30 @@ int rq_trailing_spectral(rq_ctx* ctx, const double* dR, int64_t n, int64_t ldr, 
 // Panel-step API (multi-GPU driver, dist.py)
 // ---------------------------------------------------------------------------
 static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int rq_gemm_f32(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, const float* dA, int64_t lda,
+                int64_t a_rows, int64_t a_cols, int64_t a_r0, int64_t a_c0, const float* dB, int64_t ldb,
+                int64_t b_rows, int64_t b_cols, int64_t b_r0, int64_t b_c0, float* dC, int64_t ldc, double alpha,
+                double beta) {
+  CTX_CHECK(ctx);
+  rq::clear_error();
+  if (M < 0 || N < 0 || K < 0) return rq::set_error(RQ_EDIM, "gemm_f32: negative extent");
+  if ((lda & 3) || (ldb & 3) || !al16(dA) || !al16(dB))
+    return rq::set_error(RQ_EVALUE, "gemm_f32: operands need ld %% 4 == 0 and 16-byte aligned bases");
+  if (M == 0 || N == 0) return RQ_OK;
+  rq::GemmProblemF32 p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.A = rq::GemmOperandF32{dA, a_rows, a_cols, lda, a_r0, a_c0};
+  p.a_mmajor = a_mmajor != 0;
+  p.B = rq::GemmOperandF32{dB, b_rows, b_cols, ldb, b_r0, b_c0};
+  p.C = dC;
+  p.ldc = ldc;
+  p.alpha = alpha;
+  p.beta = beta;
+  return rq::gemm_tf32x3(p, ctx->c.stream, &ctx->c.launches);
+}
 
 int rq_gemm(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, const double* dA, int64_t lda,
             int64_t a_rows, int64_t a_cols, int64_t a_r0, int64_t a_c0, const double* dB, int64_t ldb, int64_t b_rows,

@@ -1,0 +1,390 @@
+// FP32 GEMM on the 5th-generation tensor cores for sm_100a: 3xTF32 split products on
+// tcgen05.mma (kind::tf32), operands staged by TMA, the accumulator in TMEM.
+//
+//   C[M x N] = alpha * op(A) * B + beta * C        (fp32, column-major)
+//     op(A) = A^T, A stored K x M (a_mmajor = false, "TN")  /  op(A) = A, A stored M x K ("NN")
+//     B stored K x N (K contiguous)
+//
+// TF32 keeps 10 mantissa bits, so one TF32 product cannot meet the fp32 path's 1e-5 bar.  Every
+// operand x is split as hi = x with the low 13 mantissa bits cleared (exact in TF32) and
+// lo = x - hi (exact in fp32; its TF32 rounding costs ~2^-22 |x|), and each k-block issues
+// A_hi B_hi + A_hi B_lo + A_lo B_hi into one FP32 TMEM accumulator (the lo x lo term is below
+// fp32 rounding).  Roles per CTA (one 128 x 128 output tile, BK = 32):
+//   warp 0      TMA producer: raw fp32 tiles of A and B into a 2-deep ring (mbarrier complete_tx)
+//   warps 2-5   converters: raw -> hi / lo tiles in the canonical K-major SWIZZLE_128B layout
+//               (an M-major A is transposed here), zeroing k outside the view; then the epilogue
+//   warp 1      TMEM allocation and the single-thread tcgen05.mma issue, tcgen05.commit frees a
+//               converted stage / signals the epilogue
+// Epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32 (w % 4) ..), alpha / beta, coalesced
+// column stores (lanes = consecutive rows).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "gemm_tf32.cuh"
+
+namespace rq {
+
+namespace {
+
+constexpr int TBM = 128, TBN = 128, TBK = 32;
+constexpr int kTile = TBM * TBK * 4;      // 16 KB: one 128 x 32 fp32 tile
+constexpr int kRawStages = 2, kConvStages = 2;
+constexpr int kThreads = 192;             // warps 0 (TMA), 1 (MMA), 2-5 (convert + epilogue)
+constexpr int kConvThreads = 128;
+constexpr int kSmem = kRawStages * 2 * kTile + kConvStages * 4 * kTile + 1024 + 256;
+
+struct TArgs {
+  int M, N, Kv;        // output extent (M includes m_lo padding rows), valid k range [k_lo, Kv)
+  int k_lo, m_lo;
+  int a_c0, a_c1, b_c0, b_c1;
+  float* C;
+  int64_t ldc;
+  float alpha, beta;
+  int tiles_m;
+  int kblocks;
+};
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+          s_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          s_u32(dst)),
+      "l"(m), "r"(s_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (sm100 layout type 2, version 1): rows of
+// 128 B (32 fp32 along K), 8-row atoms 1024 B apart (stride byte offset).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
+                            ((uint32_t)(TBM >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s_u32(bar))
+               : "memory");
+}
+
+// byte offset of element (row r, k) in a 128-row x 32-k K-major SWIZZLE_128B tile
+__device__ __forceinline__ int sw_off(int r, int k) {
+  return (r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ (r & 7))) << 4) + ((k & 3) << 2);
+}
+
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  lo = x - hi;
+}
+
+template <bool A_MMAJOR>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, const TArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* raw = sm;                                   // [stage][A, B] 16 KB each
+  unsigned char* conv = sm + kRawStages * 2 * kTile;         // [stage][Ahi, Alo, Bhi, Blo]
+  uint64_t* bars = (uint64_t*)(conv + kConvStages * 4 * kTile);
+  uint64_t* raw_full = bars;
+  uint64_t* raw_empty = bars + 2;
+  uint64_t* conv_full = bars + 4;
+  uint64_t* conv_empty = bars + 6;
+  uint64_t* tmem_full = bars + 8;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 10);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tm = blockIdx.x % a.tiles_m, tn = blockIdx.x / a.tiles_m;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; s++) {
+      bar_init(&raw_full[s], 1);
+      bar_init(&raw_empty[s], kConvThreads);
+      bar_init(&conv_full[s], kConvThreads);
+      bar_init(&conv_empty[s], 1);
+    }
+    bar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&ma) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mb) : "memory");
+  }
+  if (warp == 1) {  // 128 TMEM columns: the 128 x 128 fp32 accumulator
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(s_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      for (int kb = 0; kb < a.kblocks; kb++) {
+        const int s = kb & 1;
+        bar_wait(&raw_empty[s], ((kb >> 1) & 1) ^ 1);
+        bar_expect_tx(&raw_full[s], 2 * kTile);
+        unsigned char* ra = raw + (s * 2) * kTile;
+        unsigned char* rb = raw + (s * 2 + 1) * kTile;
+        if (A_MMAJOR)
+          tma2d(ra, &ma, &raw_full[s], a.a_c0 + tm * TBM, a.a_c1 + kb * TBK);
+        else
+          tma2d(ra, &ma, &raw_full[s], a.a_c0 + kb * TBK, a.a_c1 + tm * TBM);
+        tma2d(rb, &mb, &raw_full[s], a.b_c0 + kb * TBK, a.b_c1 + tn * TBN);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread) ----------------
+    if (lane == 0) {
+      for (int kb = 0; kb < a.kblocks; kb++) {
+        const int s = kb & 1;
+        bar_wait(&conv_full[s], (kb >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t base = s_u32(conv + (s * 4) * kTile);
+        const uint32_t ahi = base, alo = base + kTile, bhi = base + 2 * kTile, blo = base + 3 * kTile;
+#pragma unroll
+        for (int kk = 0; kk < TBK / 8; kk++) {  // 8 tf32 (32 B) per MMA along K
+          const uint32_t o = kk * 32;
+          umma_tf32(tmem, sw128_desc(ahi + o), sw128_desc(bhi + o), (kb | kk) != 0);
+          umma_tf32(tmem, sw128_desc(ahi + o), sw128_desc(blo + o), 1u);
+          umma_tf32(tmem, sw128_desc(alo + o), sw128_desc(bhi + o), 1u);
+        }
+        umma_commit(&conv_empty[s]);  // the stage's smem is free once these MMAs completed
+      }
+      umma_commit(tmem_full);
+    }
+  } else {
+    // ---------------- converters (then the epilogue) ----------------
+    const int c = threadIdx.x - 64;
+    for (int kb = 0; kb < a.kblocks; kb++) {
+      const int s = kb & 1;
+      const uint32_t ph = (kb >> 1) & 1;
+      bar_wait(&raw_full[s], ph);
+      bar_wait(&conv_empty[s], ph ^ 1);
+      const unsigned char* ra = raw + (s * 2) * kTile;
+      const unsigned char* rb = raw + (s * 2 + 1) * kTile;
+      unsigned char* ahi = conv + (s * 4) * kTile;
+      unsigned char* alo = ahi + kTile;
+      unsigned char* bhi = ahi + 2 * kTile;
+      unsigned char* blo = ahi + 3 * kTile;
+      const int kbase = kb * TBK;
+      // B (and a K-major A): the raw tile already has the target layout; split in place order
+#pragma unroll
+      for (int t = 0; t < 8; t++) {
+        const int v = c + kConvThreads * t;  // 16-byte vector index 0..1023
+        const int r = v >> 3;
+        const int k0 = (((v & 7) ^ (r & 7)) << 2);
+        float4 x = *reinterpret_cast<const float4*>(rb + v * 16);
+        float xs[4] = {x.x, x.y, x.z, x.w};
+        float h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+          const int kg = kbase + k0 + e;
+          const float val = (kg >= a.k_lo && kg < a.Kv) ? xs[e] : 0.0f;
+          split_tf32(val, h[e], l[e]);
+        }
+        *reinterpret_cast<float4*>(bhi + v * 16) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(blo + v * 16) = make_float4(l[0], l[1], l[2], l[3]);
+        if (!A_MMAJOR) {
+          x = *reinterpret_cast<const float4*>(ra + v * 16);
+          float ys[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            const int kg = kbase + k0 + e;
+            const float val = (kg >= a.k_lo && kg < a.Kv) ? ys[e] : 0.0f;
+            split_tf32(val, h[e], l[e]);
+          }
+          *reinterpret_cast<float4*>(ahi + v * 16) = make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(alo + v * 16) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+      }
+      if (A_MMAJOR) {
+        // raw A: 32 k-rows of 128 contiguous m (no swizzle) -> K-major SWIZZLE_128B hi / lo
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+          const int v = c + kConvThreads * t;
+          const int k = v >> 5, m0 = (v & 31) << 2;
+          const float4 x = *reinterpret_cast<const float4*>(ra + v * 16);
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+          const int kg = kbase + k;
+          const bool ok = kg >= a.k_lo && kg < a.Kv;
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            float h, l;
+            split_tf32(ok ? xs[e] : 0.0f, h, l);
+            const int off = sw_off(m0 + e, k);
+            *reinterpret_cast<float*>(ahi + off) = h;
+            *reinterpret_cast<float*>(alo + off) = l;
+          }
+        }
+      }
+      // generic-proxy smem writes -> the tensor core's async proxy
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_arrive(&raw_empty[s]);
+      bar_arrive(&conv_full[s]);
+    }
+    // ---------------- epilogue ----------------
+    bar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3;  // TMEM lanes 32q .. 32q + 31
+    const int m = tm * TBM + q * 32 + lane;
+    const bool mok = m >= a.m_lo && m < a.M;
+#pragma unroll 1
+    for (int cb = 0; cb < TBN / 32; cb++) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+          "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (mok) {
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+          const int n = tn * TBN + cb * 32 + j;
+          if (n < a.N) {
+            float* cp = a.C + (int64_t)n * a.ldc + m;
+            float v = a.alpha * __uint_as_float(r[j]);
+            if (a.beta != 0.0f) v = fmaf(a.beta, *cp, v);
+            *cp = v;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_enc32 = nullptr;
+
+int encoder() {
+  static std::once_flag once;
+  static int rc = RQ_OK;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || fn == nullptr || q != cudaDriverEntryPointSuccess)
+      rc = set_error(RQ_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    else
+      g_enc32 = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return rc;
+}
+
+int map_f32(CUtensorMap* map, const GemmOperandF32& op, uint32_t box0, uint32_t box1, bool swizzle) {
+  if (((uintptr_t)op.base & 15) != 0 || (op.ld & 3) != 0)
+    return set_error(RQ_EVALUE, "fp32 GEMM operand needs a 16-byte aligned base and ld % 4 == 0 (ld %lld)",
+                     (long long)op.ld);
+  cuuint64_t dims[2] = {(cuuint64_t)op.rows, (cuuint64_t)op.cols};
+  cuuint64_t strides[1] = {(cuuint64_t)op.ld * 4};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_enc32(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(op.base), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_error(RQ_ECUDA, "cuTensorMapEncodeTiled (fp32) failed (%d): %llu x %llu ld %lld", (int)r,
+                     (unsigned long long)op.rows, (unsigned long long)op.cols, (long long)op.ld);
+  return RQ_OK;
+}
+
+template <bool A_MMAJOR>
+int launch(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
+  auto kern = gemm_tf32x3_kernel<A_MMAJOR>;
+  static bool attr = false;
+  if (!attr) {
+    RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr = true;
+  }
+  // TMA origins along a contiguous dimension are rounded down to 16 bytes (4 fp32); the
+  // converters zero the padding k's, the epilogue skips the padding rows.
+  const int kshift = (int)(p.B.r0 & 3);
+  if (!A_MMAJOR && (int)(p.A.r0 & 3) != kshift)
+    return set_error(RQ_EINTERNAL, "fp32 gemm: K origins of A (%lld) and B (%lld) differ mod 4", (long long)p.A.r0,
+                     (long long)p.B.r0);
+  const int ashift = A_MMAJOR ? (int)(p.A.r0 & 3) : 0;  // M-major A: pad rows of the output
+  CUtensorMap ma, mb;
+  if (A_MMAJOR)
+    RQ_TRY(map_f32(&ma, p.A, TBM, TBK, false));
+  else
+    RQ_TRY(map_f32(&ma, p.A, TBK, TBM, true));
+  RQ_TRY(map_f32(&mb, p.B, TBK, TBN, true));
+  TArgs a;
+  a.M = (int)(p.M + ashift);
+  a.N = (int)p.N;
+  a.k_lo = kshift;
+  a.Kv = (int)(p.K + kshift);
+  a.m_lo = ashift;
+  if (A_MMAJOR) {
+    a.a_c0 = (int)(p.A.r0 - ashift);
+    a.a_c1 = (int)(p.A.c0 - kshift);  // the k coordinate is the outer dimension: shifted with B's k
+  } else {
+    a.a_c0 = (int)(p.A.r0 - kshift);
+    a.a_c1 = (int)p.A.c0;
+  }
+  a.b_c0 = (int)(p.B.r0 - kshift);
+  a.b_c1 = (int)p.B.c0;
+  a.C = p.C - ashift;
+  a.ldc = p.ldc;
+  a.alpha = (float)p.alpha;
+  a.beta = (float)p.beta;
+  a.tiles_m = (int)ceil_div(a.M, TBM);
+  const int tiles_n = (int)ceil_div(a.N, TBN);
+  a.kblocks = (int)ceil_div(a.Kv, TBK);
+  const int64_t grid = (int64_t)a.tiles_m * tiles_n;
+  if (grid > 0x7fffffff) return set_error(RQ_EUNSUPPORTED, "fp32 gemm: too many tiles");
+  kern<<<(unsigned)grid, kThreads, kSmem, st>>>(ma, mb, a);
+  RQ_CUDA_TRY(cudaGetLastError());
+  if (launches) (*launches)++;
+  return RQ_OK;
+}
+
+}  // namespace
+
+int gemm_tf32x3(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
+  if (p.M <= 0 || p.N <= 0) return RQ_OK;
+  if (p.K <= 0) {
+    if (p.beta == 1.0) return RQ_OK;
+    return set_error(RQ_EINTERNAL, "fp32 gemm: K == 0 with beta != 1 not supported");
+  }
+  RQ_TRY(encoder());
+  return p.a_mmajor ? launch<true>(p, st, launches) : launch<false>(p, st, launches);
+}
+
+}  // namespace rq

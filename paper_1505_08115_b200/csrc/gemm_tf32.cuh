@@ -1,0 +1,28 @@
+// FP32 GEMM on tcgen05 tensor cores (3xTF32 split products, TMEM accumulator, TMA staging);
+// see gemm_tf32.cu.  Same conventions as gemm_f64.cuh with fp32 operands:
+//   C[M x N] = alpha * op(A) * B + beta * C,  op(A) = A^T (A stored K x M) or A (A stored M x K),
+//   B stored K x N; views at element origins (r0, c0) of whole buffers (ld % 4 == 0, 16 B bases).
+#pragma once
+#include "common.cuh"
+
+namespace rq {
+
+struct GemmOperandF32 {
+  const float* base;
+  int64_t rows, cols, ld;
+  int64_t r0, c0;
+};
+
+struct GemmProblemF32 {
+  int64_t M, N, K;
+  GemmOperandF32 A;
+  bool a_mmajor;
+  GemmOperandF32 B;
+  float* C;
+  int64_t ldc;
+  double alpha, beta;
+};
+
+int gemm_tf32x3(const GemmProblemF32& p, cudaStream_t st, int64_t* launches);
+
+}  // namespace rq
