@@ -423,8 +423,9 @@ def run_fp32(args, local):
         "data": "synthetic",
         "config": {"workload": f"cfg3 fp32 HQRRP n={n} b={b} p={p} q=0, fresh sketch", "n": n, "b": b, "p": p,
                    "parallelism": "single", "l2": "inputs (400 MB) larger than L2 (126 MB)"},
-        "note": "fp32 storage; sketch and trailing GEMMs = cuBLAS SGEMM via torch (TF32 off); sketch CPQR, panel "
-                "QR, b x b CPQR, T in this library's fp64 kernels (fp32.py)",
+        "note": "fp32 storage; sketch and trailing GEMMs = this library's tcgen05 3xTF32 GEMM (rq_gemm_f32, "
+                "TMA + TMEM); sketch CPQR, panel QR, b x b CPQR, T in this library's fp64 kernels; panel-step "
+                "driver (dist.factorize_local, world size 1) (fp32.py)",
         "clocks": clk, "gpu_launches": eng.launches - launches0, "e2e": None, "cpu_baseline": None,
     }
     print(json.dumps(line), flush=True)

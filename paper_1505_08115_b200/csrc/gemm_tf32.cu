@@ -6,8 +6,8 @@
 //     B stored K x N (K contiguous)
 //
 // TF32 keeps 10 mantissa bits, so one TF32 product cannot meet the fp32 path's 1e-5 bar.  Every
-// operand x is split as hi = x with the low 13 mantissa bits cleared (exact in TF32) and
-// lo = x - hi (exact in fp32; its TF32 rounding costs ~2^-22 |x|), and each k-block issues
+// operand x is split as hi = tf32(x) and lo = tf32(x - hi) (round to nearest; both exact in TF32,
+// |x - hi - lo| <= 2^-23 |x|), and each k-block issues
 // A_hi B_hi + A_hi B_lo + A_lo B_hi into one FP32 TMEM accumulator (the lo x lo term is below
 // fp32 rounding).  Roles per CTA (one 128 x 128 output tile, BK = 32):
 //   warp 0      TMA producer: raw fp32 tiles of A and B into a 2-deep ring (mbarrier complete_tx)
@@ -15,10 +15,13 @@
 //               (an M-major A is transposed here), zeroing k outside the view; then the epilogue
 //   warp 1      TMEM allocation and the single-thread tcgen05.mma issue, tcgen05.commit frees a
 //               converted stage / signals the epilogue
-// Epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32 (w % 4) ..), alpha / beta, coalesced
-// column stores (lanes = consecutive rows).
+// Accumulation: each k-block's 12 MMAs go to one of two TMEM accumulators (k-block parity); the
+// converter warps drain it with tcgen05.ld 32x32b (warp w reads TMEM lanes 32 (w % 4) ..) into fp32
+// registers while the tensor core fills the other.  Epilogue: alpha / beta, coalesced column
+// stores (lanes = consecutive rows).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm_tf32.cuh"
@@ -29,10 +32,11 @@ namespace {
 
 constexpr int TBM = 128, TBN = 128, TBK = 32;
 constexpr int kTile = TBM * TBK * 4;      // 16 KB: one 128 x 32 fp32 tile
-constexpr int kRawStages = 2, kConvStages = 2;
+constexpr int kRawStages = 3, kConvStages = 2;
 constexpr int kThreads = 192;             // warps 0 (TMA), 1 (MMA), 2-5 (convert + epilogue)
 constexpr int kConvThreads = 128;
 constexpr int kSmem = kRawStages * 2 * kTile + kConvStages * 4 * kTile + 1024 + 256;
+static_assert(kSmem <= 232448, "shared memory per CTA");
 
 struct TArgs {
   int M, N, Kv;        // output extent (M includes m_lo padding rows), valid k range [k_lo, Kv)
@@ -43,6 +47,7 @@ struct TArgs {
   float alpha, beta;
   int tiles_m;
   int kblocks;
+  int four;  // 1: also A_lo B_lo (4 products; tuning / accuracy probe)
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -97,9 +102,15 @@ __device__ __forceinline__ int sw_off(int r, int k) {
   return (r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ (r & 7))) << 4) + ((k & 3) << 2);
 }
 
+// hi = x rounded to TF32 (nearest, ties away), lo = (x - hi) rounded to TF32: both exactly
+// representable, so the tensor core's TF32 read loses nothing; |x - hi - lo| <= 2^-23 |x|
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  lo = x - hi;
+  uint32_t h, l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  const float r = x - __uint_as_float(h);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+  hi = __uint_as_float(h);
+  lo = __uint_as_float(l);
 }
 
 template <bool A_MMAJOR>
@@ -110,30 +121,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   unsigned char* raw = sm;                                   // [stage][A, B] 16 KB each
   unsigned char* conv = sm + kRawStages * 2 * kTile;         // [stage][Ahi, Alo, Bhi, Blo]
   uint64_t* bars = (uint64_t*)(conv + kConvStages * 4 * kTile);
-  uint64_t* raw_full = bars;
-  uint64_t* raw_empty = bars + 2;
-  uint64_t* conv_full = bars + 4;
-  uint64_t* conv_empty = bars + 6;
-  uint64_t* tmem_full = bars + 8;
-  uint32_t* tmem_slot = (uint32_t*)(bars + 10);
+  uint64_t* raw_full = bars;        // [kRawStages]
+  uint64_t* raw_empty = bars + 4;   // [kRawStages]
+  uint64_t* conv_full = bars + 8;   // [2]
+  uint64_t* conv_empty = bars + 10;
+  uint64_t* acc_full = bars + 12;   // [2]: a k-block's products landed in TMEM accumulator (kb & 1)
+  uint64_t* acc_empty = bars + 14;  // [2]: the converter warps drained it into registers
+  uint32_t* tmem_slot = (uint32_t*)(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tm = blockIdx.x % a.tiles_m, tn = blockIdx.x / a.tiles_m;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; s++) {
+    for (int s = 0; s < kRawStages; s++) {
       bar_init(&raw_full[s], 1);
       bar_init(&raw_empty[s], kConvThreads);
+    }
+    for (int s = 0; s < 2; s++) {
       bar_init(&conv_full[s], kConvThreads);
       bar_init(&conv_empty[s], 1);
     }
-    bar_init(tmem_full, 1);
+    for (int s = 0; s < 2; s++) {
+      bar_init(&acc_full[s], 1);
+      bar_init(&acc_empty[s], kConvThreads);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&ma) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mb) : "memory");
   }
-  if (warp == 1) {  // 128 TMEM columns: the 128 x 128 fp32 accumulator
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(s_u32(tmem_slot))
+  if (warp == 1) {  // 256 TMEM columns: two 128 x 128 fp32 accumulators (k-block parity)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(s_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -146,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       for (int kb = 0; kb < a.kblocks; kb++) {
-        const int s = kb & 1;
-        bar_wait(&raw_empty[s], ((kb >> 1) & 1) ^ 1);
+        const int s = kb % kRawStages;
+        bar_wait(&raw_empty[s], ((kb / kRawStages) & 1) ^ 1);
         bar_expect_tx(&raw_full[s], 2 * kTile);
         unsigned char* ra = raw + (s * 2) * kTile;
         unsigned char* rb = raw + (s * 2 + 1) * kTile;
@@ -160,34 +177,68 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread) ----------------
+    // Each k-block accumulates into its own (parity) TMEM accumulator, which the converter warps
+    // add into fp32 registers: the tensor core's accumulation then spans 32 k only (its long
+    // in-TMEM sums measured ~6x less accurate than an fp32 SGEMM and biased, tools/gemm_acc.py).
     if (lane == 0) {
       for (int kb = 0; kb < a.kblocks; kb++) {
         const int s = kb & 1;
         bar_wait(&conv_full[s], (kb >> 1) & 1);
+        bar_wait(&acc_empty[s], ((kb >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t base = s_u32(conv + (s * 4) * kTile);
         const uint32_t ahi = base, alo = base + kTile, bhi = base + 2 * kTile, blo = base + 3 * kTile;
+        const uint32_t acc = tmem + (uint32_t)(s * TBN);
 #pragma unroll
         for (int kk = 0; kk < TBK / 8; kk++) {  // 8 tf32 (32 B) per MMA along K
           const uint32_t o = kk * 32;
-          umma_tf32(tmem, sw128_desc(ahi + o), sw128_desc(bhi + o), (kb | kk) != 0);
-          umma_tf32(tmem, sw128_desc(ahi + o), sw128_desc(blo + o), 1u);
-          umma_tf32(tmem, sw128_desc(alo + o), sw128_desc(bhi + o), 1u);
+          umma_tf32(acc, sw128_desc(ahi + o), sw128_desc(bhi + o), kk != 0);
+          umma_tf32(acc, sw128_desc(ahi + o), sw128_desc(blo + o), 1u);
+          umma_tf32(acc, sw128_desc(alo + o), sw128_desc(bhi + o), 1u);
+          if (a.four) umma_tf32(acc, sw128_desc(alo + o), sw128_desc(blo + o), 1u);
         }
         umma_commit(&conv_empty[s]);  // the stage's smem is free once these MMAs completed
+        umma_commit(&acc_full[s]);
       }
-      umma_commit(tmem_full);
     }
   } else {
     // ---------------- converters (then the epilogue) ----------------
     const int c = threadIdx.x - 64;
+    const int q = warp & 3;  // TMEM lanes 32q .. 32q + 31 = output rows of this thread's warp
+    float accr[TBN];
+#pragma unroll
+    for (int j = 0; j < TBN; j++) accr[j] = 0.0f;
+    // add k-block kd's TMEM accumulator (parity kd & 1) into accr and release it
+    auto drain = [&](int kd) {
+      const int s = kd & 1;
+      bar_wait(&acc_full[s], (kd >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int cb = 0; cb < TBN / 32; cb++) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * TBN + cb * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; j++) accr[cb * 32 + j] += __uint_as_float(r[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      bar_arrive(&acc_empty[s]);
+    };
     for (int kb = 0; kb < a.kblocks; kb++) {
-      const int s = kb & 1;
+      const int s = kb & 1, rs = kb % kRawStages;
       const uint32_t ph = (kb >> 1) & 1;
-      bar_wait(&raw_full[s], ph);
+      bar_wait(&raw_full[rs], (kb / kRawStages) & 1);
       bar_wait(&conv_empty[s], ph ^ 1);
-      const unsigned char* ra = raw + (s * 2) * kTile;
-      const unsigned char* rb = raw + (s * 2 + 1) * kTile;
+      const unsigned char* ra = raw + (rs * 2) * kTile;
+      const unsigned char* rb = raw + (rs * 2 + 1) * kTile;
       unsigned char* ahi = conv + (s * 4) * kTile;
       unsigned char* alo = ahi + kTile;
       unsigned char* bhi = ahi + 2 * kTile;
@@ -245,37 +296,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // generic-proxy smem writes -> the tensor core's async proxy
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bar_arrive(&raw_empty[s]);
+      bar_arrive(&raw_empty[rs]);
       bar_arrive(&conv_full[s]);
+      if (kb > 0) drain(kb - 1);  // (the tensor core works on kb meanwhile)
     }
-    // ---------------- epilogue ----------------
-    bar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3;  // TMEM lanes 32q .. 32q + 31
+    if (a.kblocks > 0) drain(a.kblocks - 1);
+    // ---------------- epilogue: registers -> C ----------------
     const int m = tm * TBM + q * 32 + lane;
-    const bool mok = m >= a.m_lo && m < a.M;
-#pragma unroll 1
-    for (int cb = 0; cb < TBN / 32; cb++) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-          "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (mok) {
+    if (m >= a.m_lo && m < a.M) {
+      float* cbase = a.C + (int64_t)(tn * TBN) * a.ldc + m;
+      const int nv = min(TBN, a.N - tn * TBN);
+#pragma unroll
+      for (int g = 0; g < TBN / 32; g++) {
+        // 32 independent loads of C first (the stores below could alias them), then 32 stores
+        float cv[32];
+        if (a.beta != 0.0f) {
+#pragma unroll
+          for (int j = 0; j < 32; j++)
+            cv[j] = (g * 32 + j < nv) ? __ldcs(cbase + (int64_t)(g * 32 + j) * a.ldc) : 0.0f;
+        }
 #pragma unroll
         for (int j = 0; j < 32; j++) {
-          const int n = tn * TBN + cb * 32 + j;
-          if (n < a.N) {
-            float* cp = a.C + (int64_t)n * a.ldc + m;
-            float v = a.alpha * __uint_as_float(r[j]);
-            if (a.beta != 0.0f) v = fmaf(a.beta, *cp, v);
-            *cp = v;
+          if (g * 32 + j < nv) {
+            float v = a.alpha * accr[g * 32 + j];
+            if (a.beta != 0.0f) v = fmaf(a.beta, cv[j], v);
+            __stcs(cbase + (int64_t)(g * 32 + j) * a.ldc, v);
           }
         }
       }
@@ -286,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -367,6 +412,8 @@ int launch(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
   a.tiles_m = (int)ceil_div(a.M, TBM);
   const int tiles_n = (int)ceil_div(a.N, TBN);
   a.kblocks = (int)ceil_div(a.Kv, TBK);
+  static const int env_four = getenv("RQ_TF32X4") ? atoi(getenv("RQ_TF32X4")) : 0;
+  a.four = env_four;
   const int64_t grid = (int64_t)a.tiles_m * tiles_n;
   if (grid > 0x7fffffff) return set_error(RQ_EUNSUPPORTED, "fp32 gemm: too many tiles");
   kern<<<(unsigned)grid, kThreads, kSmem, st>>>(ma, mb, a);

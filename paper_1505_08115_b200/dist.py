@@ -380,8 +380,9 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         slot_lpos[rest[order]] = s + b + np.arange(rest.size, dtype=np.int64)
         slot_lpos[s:s + b] = s + np.arange(b, dtype=np.int64)
         # ---- 4: panel on the owner; V, T, Q2, P-hat broadcast in one message ----
-        ldv = mp + (mp & 1)
-        ldb = b + (b & 1)
+        al = getattr(engine, "ld_align", 2)  # the fp32 engine's tensor-core GEMMs need ld % 4 == 0
+        ldv = (mp + al - 1) // al * al
+        ldb = (b + al - 1) // al * al
         ng1 = b * ldg if downdate else 0
         nfac = b * ldv + 2 * b * ldb + b
         pack = torch.empty(nfac + ng1, dtype=a_loc.dtype, device=a_loc.device)  # P-hat exact in fp32 too (b < 2^24)
@@ -409,6 +410,8 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         # P-hat reorders the panel's slots; those never compete for pivots again, so only
         # the final perm needs it: keep it on the device (no host sync here), apply at the end
         ph_pending.append((s, pack[nfac - b:nfac].clone()))
+        if hasattr(engine, "record_panel"):  # engines that form Q themselves keep the factors
+            engine.record_panel(s, mp, b, (v, ldv, t, ldb, q2, ldb))
         # ---- 5: trailing update of the local columns ----
         t1 = lay.local_from(rank, i + 1)
         n2 = nloc - t1
