@@ -492,7 +492,22 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
   CatGuard guard(cat, PROF_PANEL_GEMM);
   int wl_max = leaf_reg_width_for(mp);
   if (wl_max == 0) wl_max = leaf_width_for(mp);
-  if (wl_max == 0) return set_error(RQ_EUNSUPPORTED, "panel of %lld rows exceeds the leaf kernel", (long long)mp);
+  if (wl_max == 0) {
+    // A panel taller than one 16-CTA cluster holds (m' > 65536 rows): the grid-wide Householder
+    // sweep, unpivoted (householder_sweep(pivot=False), _kernels_numba.py:13-61), on the whole
+    // panel; columns stream through L2 each step.  Same reflector convention as the leaves.
+    RQ_TRY(la_flush());
+    SweepCall sc;
+    sc.a = A + s + s * lda;
+    sc.lda = lda;
+    sc.m = mp;
+    sc.n = b;
+    sc.steps = (int)std::min<int64_t>(mp, b);
+    sc.pivot = 0;
+    sc.v = V + vpad;
+    sc.ldv = ldv;
+    return sweep(sc);
+  }
   const int wl = std::min(wl_max, 32);
   // look-ahead: spread the pending tiles over the leaves in whole waves of the capped grid
   const int nleaves = (b + wl - 1) / wl;

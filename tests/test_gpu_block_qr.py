@@ -502,3 +502,46 @@ def test_space_sliced_lookahead_matches_plain_schedule(m, n, b, p):
     line = [ln for ln in res.stdout.splitlines() if ln.startswith("RESULT")][-1].split()
     assert line[1] == "1"
     assert float(line[2]) <= 1e-13
+
+
+@pytest.mark.parametrize("sketch", ["fresh", "downdate"])
+def test_tall_70000x2000_beyond_the_leaf_cluster(rq, sketch):
+    """m' > 65536 rows (more than one 16-CTA leaf cluster holds): the panels fall back to the
+    grid-wide unpivoted sweep.  70 000 x 2 000, b = 256, p = 16: random-probe residual and
+    orthogonality (||A[:, perm] x - Q (R x)|| <= 1e-13 ||A|| ||x||, ||Q^T Q y - y|| <= 1e-13 sqrt(n)),
+    R upper triangular, and the leading panel's pivots equal to the reference algorithm (oracle)."""
+    import ctypes
+
+    import torch
+
+    from oracle import randqr_oracle as O
+    from paper_1505_08115_b200 import _lib
+    from paper_1505_08115_b200.errors import check
+
+    m, n, b, p = 70000, 2000, 256, 16
+    eng = rq.Engine()
+    a0, ld = rq.gaussian_matrix_device(m, n, rq.RngState(11), engine=eng)
+    work = a0.clone()
+    perm = torch.empty(n, dtype=torch.int64, device=a0.device)
+    mode = _lib.RQ_SKETCH_FRESH if sketch == "fresh" else _lib.RQ_SKETCH_DOWNDATE
+    cfg = _lib.rq_config(b, p, 0, -1, _lib.RQ_PIVOT_PERMUTATION, 0, mode, 0)
+    ctr = ctypes.c_uint64(0)
+    check(eng.lib.rq_factorize(eng.handle, ctypes.byref(cfg), m, n, ctypes.c_void_p(work.data_ptr()), ld,
+                               ctypes.c_uint64(1), ctypes.byref(ctr), ctypes.c_void_p(perm.data_ptr())))
+    A = a0[:n, :m].T
+    R = work[:n, :m].T
+    assert torch.equal(torch.triu(R), R)
+    q, ldq = eng.alloc_matrix(m, n)
+    check(eng.lib.rq_form_q(eng.handle, n, ctypes.c_void_p(q.data_ptr()), ldq))
+    Q = q[:n, :m].T
+    g = torch.Generator(device=A.device).manual_seed(1)
+    x = torch.randn(n, 3, dtype=torch.float64, device=A.device, generator=g)
+    res = torch.linalg.norm(A[:, perm] @ x - Q @ (R[:n] @ x)) / (torch.linalg.norm(A) * torch.linalg.norm(x))
+    assert float(res) <= 1e-13, float(res)
+    y = torch.randn(n, 3, dtype=torch.float64, device=A.device, generator=g)
+    orth = torch.linalg.norm(Q.T @ (Q @ y) - y) / torch.linalg.norm(y)
+    assert float(orth) <= 1e-13 * np.sqrt(n), float(orth)
+    if sketch == "fresh":
+        ah = A.cpu().numpy()
+        fo = O.block_qr(np.asfortranarray(ah), O.BlockConfig(b, O.SketchConfig(b, p, 0)), O.RngState(1), max_panels=1)
+        assert np.array_equal(perm.cpu().numpy()[:b], fo.perm()[:b])
