@@ -397,7 +397,7 @@ def run_fp32(args, local):
     def step():
         with torch.cuda.stream(stream):
             work.copy_(a0)
-            rqd.factorize_local(work, lda, m, n, cfg, rq.RngState(1), engine=se)
+            rqd.factorize_local(work, lda, m, n, cfg, rq.RngState(1), engine=se, sketch=args.sketch)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -421,7 +421,8 @@ def run_fp32(args, local):
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (GEMMs) / f64 (serial kernels)",
         "data": "synthetic",
-        "config": {"workload": f"cfg3 fp32 HQRRP n={n} b={b} p={p} q=0, fresh sketch", "n": n, "b": b, "p": p,
+        "config": {"workload": f"cfg3 fp32 HQRRP n={n} b={b} p={p} q=0, {args.sketch} sketch", "n": n, "b": b, "p": p,
+                   "sketch": args.sketch,
                    "parallelism": "single", "l2": "inputs (400 MB) larger than L2 (126 MB)"},
         "note": "fp32 storage; sketch and trailing GEMMs = this library's tcgen05 3xTF32 GEMM (rq_gemm_f32, "
                 "TMA + TMEM); sketch CPQR, panel QR, b x b CPQR, T in this library's fp64 kernels; panel-step "
@@ -541,8 +542,10 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
+    h0 = time.perf_counter()
     for _ in range(args.steps):
         step()
+    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # enqueue time (rq_factorize is enqueue-only)
     ev1.record(stream)
     torch.cuda.synchronize()
     if dist is not None:
@@ -667,6 +670,9 @@ def main():
             "per_n": per_n,
             "clocks": clk,
             "gpu_launches": launches,
+            "host_enqueue_ms_per_step": host_ms,
+            "host_enqueue_note": "host time of the rq_factorize calls in the timed loop (they only enqueue; "
+                                 "below ms_per_step = the GPU never waits on the host)",
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

@@ -41,8 +41,39 @@ from .errors import DimensionError, check
 from .hqrrp import BlockConfig, Engine, RngState
 
 
-def _ptr(t):
-    return ctypes.c_void_p(t.data_ptr())
+def _ptr(t, off=0, esize=8):
+    return ctypes.c_void_p(t.data_ptr() + esize * off)
+
+
+class _Ready:
+    """Selection result already on the host (CPU engines)."""
+
+    def __init__(self, v):
+        self.v = v
+
+    def result(self):
+        return self.v
+
+
+class _PendingSelect:
+    """Pivots copied to pinned host memory behind an event: ``result()`` waits for the
+    selection only, not for the trailing update enqueued after it (look-ahead)."""
+
+    def __init__(self, host, event):
+        self.host, self.event = host, event
+
+    def result(self):
+        self.event.synchronize()
+        return self.host.numpy().astype(np.int64)
+
+
+def _host_index(torch, arr, device):
+    """int64 index tensor on `device` from host data, without synchronising the stream
+    (pinned staging + non-blocking copy; CPU devices get the tensor directly)."""
+    t = torch.from_numpy(np.ascontiguousarray(np.asarray(arr, dtype=np.int64)))
+    if device.type != "cuda":
+        return t
+    return t.pin_memory().to(device, non_blocking=True)
 
 
 class CudaStepEngine:
@@ -76,12 +107,22 @@ class CudaStepEngine:
                                    a_cols, r0, c0, _ptr(y), ldy, 1.0, 0.0))
         return y, ldy
 
-    def select(self, y, ldy, wdt, n, steps, init_pos):
+    def index(self, arr):
+        return _host_index(self.torch, arr, self.device)
+
+    def select_async(self, y, ldy, wdt, n, steps, init_pos):
         torch = self.torch
-        ip = torch.as_tensor(np.asarray(init_pos, dtype=np.int32), device=self.device)
+        ip = _host_index(torch, init_pos, self.device).to(torch.int32)
         ch = torch.empty(steps, dtype=torch.int32, device=self.device)
         check(self.lib.rq_sketch_select(self.h, _ptr(y), ldy, wdt, n, steps, _ptr(ip), _ptr(ch)))
-        return ch.cpu().numpy().astype(np.int64)
+        host = torch.empty(steps, dtype=torch.int32, pin_memory=True)
+        host.copy_(ch, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(self.eng.stream)
+        return _PendingSelect(host, ev)
+
+    def select(self, y, ldy, wdt, n, steps, init_pos):
+        return self.select_async(y, ldy, wdt, n, steps, init_pos).result()
 
     def panel_factor(self, p, ldp, mp, b):
         torch = self.torch
@@ -97,6 +138,30 @@ class CudaStepEngine:
         v, ldv, t, ldt, q2, ldq = fac
         check(self.lib.rq_panel_apply(self.h, _ptr(v), ldv, _ptr(t), ldt, _ptr(q2), ldq, mp, b, _ptr(a), lda,
                                       a_rows, a_cols, r0, c0, n2))
+
+    def panel_apply_top(self, fac, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
+        """The rows the next panel's pivots depend on (look-ahead): W = V^T A2, W2 = T^T W,
+        A2[0:b] -= V[0:b] W2, then Q2^T on those rows; returns W2 for panel_apply_rest."""
+        v, ldv, t, ldt, q2, ldq = fac
+        w, ldw = self.alloc(b, n2)
+        w2, _ = self.alloc(b, n2)
+        g = self.lib.rq_gemm
+        check(g(self.h, 0, b, n2, mp, _ptr(v), ldv, mp, b, 0, 0, _ptr(a), lda, a_rows, a_cols, r0, c0, _ptr(w), ldw,
+                1.0, 0.0))
+        check(g(self.h, 0, b, n2, b, _ptr(t), ldt, b, b, 0, 0, _ptr(w), ldw, b, n2, 0, 0, _ptr(w2), ldw, 1.0, 0.0))
+        c = _ptr(a, c0 * lda + r0)
+        check(g(self.h, 1, b, n2, b, _ptr(v), ldv, mp, b, 0, 0, _ptr(w2), ldw, b, n2, 0, 0, c, lda, -1.0, 1.0))
+        w[:n2, :b] = a[c0:c0 + n2, r0:r0 + b]
+        check(g(self.h, 0, b, n2, b, _ptr(q2), ldq, b, b, 0, 0, _ptr(w), ldw, b, n2, 0, 0, c, lda, 1.0, 0.0))
+        return w2, ldw
+
+    def panel_apply_rest(self, fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
+        """A2[b:] -= V[b:] W2 (the trailing update below the panel's rows)."""
+        v, ldv, t, ldt, q2, ldq = fac
+        w2, ldw = top
+        if mp > b:
+            check(self.lib.rq_gemm(self.h, 1, mp - b, n2, b, _ptr(v), ldv, mp, b, b, 0, _ptr(w2), ldw, b, n2, 0, 0,
+                                   _ptr(a, c0 * lda + r0 + b), lda, -1.0, 1.0))
 
     def downdate_g1(self, y, ldy, wdt, c0, ph, p, ldp, b, g1, ldg):
         """G1 = Y1 R11^{-1} (written into g1, wdt x b): Y1 = the panel's sketch columns c0.. of y
@@ -234,7 +299,7 @@ def _exchange_columns(a_loc, m, lay, rank, moves, d: _Dist, engine):
     bufs_out = {}
     for q, lst in send.items():
         if lst:
-            cols = torch.as_tensor([c for _, c in lst], dtype=torch.int64, device=a_loc.device)
+            cols = _host_index(torch, [c for _, c in lst], a_loc.device)
             bufs_out[q] = a_loc.index_select(0, cols).contiguous()
     bufs_in = {}
     for q, lst in recv.items():
@@ -254,7 +319,7 @@ def _exchange_columns(a_loc, m, lay, rank, moves, d: _Dist, engine):
             req.wait()
     for q, lst in recv.items():
         if lst:
-            cols = torch.as_tensor([c for _, c in lst], dtype=torch.int64, device=a_loc.device)
+            cols = _host_index(torch, [c for _, c in lst], a_loc.device)
             a_loc.index_copy_(0, cols, bufs_in[q])
 
 
@@ -316,6 +381,7 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
     if sketch not in ("fresh", "downdate"):
         raise ValueError(f"sketch must be 'fresh' or 'downdate', got {sketch!r}")
     downdate = sketch == "downdate" and n > b
+    al = getattr(engine, "ld_align", 2)  # the fp32 engine's tensor-core GEMMs need ld % 4 == 0
     slot_orig = np.arange(n, dtype=np.int64)
     slot_lpos = np.arange(n, dtype=np.int64)
     counts_cache = {}
@@ -327,18 +393,13 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         rng.counter += m * wdt
         y_loc, ldyl = engine.sketch(g_om, ldgo, a_loc, lda, m, nloc, 0, 0, m, nloc, wdt, nloc)
         del g_om
-        ldg = wdt + (wdt & 1)
-    for i in range(lay.nblk):
+        ldg = (wdt + al - 1) // al * al
+    def start_select(i):
+        """Steps 1-2 for panel i: the local sketch columns (fresh, or the downdated Y_loc), one
+        all-gather, and the identical pivot selection on every rank -- returned as a pending
+        host result (the trailing update enqueued after it keeps the GPU busy meanwhile)."""
         s = i * b
-        np_ = n - s
-        mp = m - s
-        o = lay.owner(i)
-        if np_ <= b:
-            _apply_pending_phat(slot_orig, ph_pending)
-            _final_block(a_loc, lda, m, n, s, i, lay, rank, slot_orig, slot_lpos, d, engine)
-            break
-        # ---- 1: sketch of the local trailing columns (same Omega on every rank), or the
-        #      downdated Y_loc (kept current by step 6) ----
+        np_, mp = n - s, m - s
         counts = counts_cache.get(i)
         if counts is None:
             counts = [lay.n_local(q) - lay.local_from(q, i) for q in range(d.world)]
@@ -354,19 +415,43 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
             rng.counter += mp * wdt
             y, ldy = engine.sketch(om, ldo, a_loc, lda, m, nloc, s, t0, mp, counts[rank], wdt, cmax)
             del om
-        # ---- 2: all-gather Y, identical pivot selection everywhere ----
         if d.world > 1:
             gathered = torch.empty((d.world * cmax, ldy), dtype=y.dtype, device=y.device)
             d.dist.all_gather_into_tensor(gathered, y[:cmax].contiguous(), group=d.group)
             idx = np.concatenate([np.arange(q * cmax, q * cmax + counts[q]) for q in range(d.world)])
-            y_all = gathered.index_select(0, torch.as_tensor(idx, device=y.device)).contiguous()
+            y_all = gathered.index_select(0, _host_index(torch, idx, y.device)).contiguous()
             del gathered
         else:
             y_all = y[:counts[0]].contiguous()
         ycol_slot = np.concatenate([lay.slots_from(q, i) for q in range(d.world)])
         init_pos = slot_lpos[ycol_slot] - s
-        chosen_y = engine.select(y_all, ldy, wdt, np_, b, init_pos)
-        del y, y_all
+        if hasattr(engine, "select_async"):
+            fut = engine.select_async(y_all, ldy, wdt, np_, b, init_pos)
+        else:
+            fut = _Ready(engine.select(y_all, ldy, wdt, np_, b, init_pos))
+        return fut, ycol_slot
+
+    # Look-ahead (downdated sketch): panel i+1's pivots depend only on the
+    # top b rows of panel i's trailing update (R12), so its selection is enqueued between those
+    # rows and the rest of the update; the host then waits for the pivots while the GPU runs
+    # the rest of the update.
+    lookahead = downdate and hasattr(engine, "panel_apply_top")
+    pending = None
+    for i in range(lay.nblk):
+        s = i * b
+        np_ = n - s
+        mp = m - s
+        o = lay.owner(i)
+        if np_ <= b:
+            _apply_pending_phat(slot_orig, ph_pending)
+            _final_block(a_loc, lda, m, n, s, i, lay, rank, slot_orig, slot_lpos, d, engine)
+            break
+        # ---- 1-2: sketch, all-gather, selection (started by the previous panel's look-ahead) ----
+        if pending is None:
+            pending = start_select(i)
+        fut, ycol_slot = pending
+        pending = None
+        chosen_y = fut.result()
         chosen = ycol_slot[chosen_y]
         # ---- 3: move the chosen columns into the panel slots ----
         moves = plan_moves(chosen, s, b)
@@ -380,11 +465,11 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         slot_lpos[rest[order]] = s + b + np.arange(rest.size, dtype=np.int64)
         slot_lpos[s:s + b] = s + np.arange(b, dtype=np.int64)
         # ---- 4: panel on the owner; V, T, Q2, P-hat broadcast in one message ----
-        al = getattr(engine, "ld_align", 2)  # the fp32 engine's tensor-core GEMMs need ld % 4 == 0
         ldv = (mp + al - 1) // al * al
         ldb = (b + al - 1) // al * al
+        nph = (b + al - 1) // al * al  # P-hat, padded so G1 after it stays 16-byte aligned
         ng1 = b * ldg if downdate else 0
-        nfac = b * ldv + 2 * b * ldb + b
+        nfac = b * ldv + 2 * b * ldb + nph
         pack = torch.empty(nfac + ng1, dtype=a_loc.dtype, device=a_loc.device)  # P-hat exact in fp32 too (b < 2^24)
         if rank == o:
             lo = lay.local_off(i)
@@ -401,7 +486,7 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
             pack[:b * ldv].copy_(v[:b, :ldv].reshape(-1))
             pack[b * ldv:b * ldv + b * ldb].copy_(t[:b, :ldb].reshape(-1))
             pack[b * ldv + b * ldb:b * ldv + 2 * b * ldb].copy_(q2[:b, :ldb].reshape(-1))
-            pack[nfac - b:nfac].copy_(ph.to(pack.dtype))
+            pack[nfac - nph:nfac - nph + b].copy_(ph.to(pack.dtype))
         if d.world > 1:
             d.dist.broadcast(pack, src=d.global_rank(o), group=d.group)
         v = pack[:b * ldv].view(b, ldv)
@@ -409,16 +494,28 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         q2 = pack[b * ldv + b * ldb:b * ldv + 2 * b * ldb].view(b, ldb)
         # P-hat reorders the panel's slots; those never compete for pivots again, so only
         # the final perm needs it: keep it on the device (no host sync here), apply at the end
-        ph_pending.append((s, pack[nfac - b:nfac].clone()))
+        ph_pending.append((s, pack[nfac - nph:nfac - nph + b].clone()))
         if hasattr(engine, "record_panel"):  # engines that form Q themselves keep the factors
             engine.record_panel(s, mp, b, (v, ldv, t, ldb, q2, ldb))
         # ---- 5: trailing update of the local columns ----
         t1 = lay.local_from(rank, i + 1)
         n2 = nloc - t1
-        if n2 > 0:
-            engine.panel_apply((v, ldv, t, ldb, q2, ldb), mp, b, a_loc, lda, m, nloc, s, t1, n2)
+        fac = (v, ldv, t, ldb, q2, ldb)
+        next_full = n - (s + b) > b
+        if lookahead:
+            top = engine.panel_apply_top(fac, mp, b, a_loc, lda, m, nloc, s, t1, n2) if n2 > 0 else None
+            if next_full:
+                # ---- 6: Y2_loc -= G1 R12_loc, then the next panel's selection (every rank) ----
+                if n2 > 0:
+                    engine.downdate_apply(pack[nfac:].view(b, ldg), ldg, wdt, b, a_loc, lda, m, nloc, s, t1, n2,
+                                          y_loc, ldyl)
+                pending = start_select(i + 1)
+            if n2 > 0:
+                engine.panel_apply_rest(fac, top, mp, b, a_loc, lda, m, nloc, s, t1, n2)
+        elif n2 > 0:
+            engine.panel_apply(fac, mp, b, a_loc, lda, m, nloc, s, t1, n2)
             # ---- 6 (downdate): Y2_loc -= G1 R12_loc on the local trailing columns ----
-            if downdate and n - (s + b) > b:
+            if downdate and next_full:
                 engine.downdate_apply(pack[nfac:].view(b, ldg), ldg, wdt, b, a_loc, lda, m, nloc, s, t1, n2,
                                       y_loc, ldyl)
         del pack

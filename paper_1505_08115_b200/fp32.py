@@ -90,10 +90,16 @@ class Fp32StepEngine:
                       0.0)
         return y, ldy
 
-    def select(self, y, ldy, wdt, n, steps, init_pos):
+    def index(self, arr):
+        return self.f64.index(arr)
+
+    def select_async(self, y, ldy, wdt, n, steps, init_pos):
         y64, ld64 = self.f64.alloc(wdt, n)
         y64[:n, :wdt] = y[:n, :wdt]
-        return self.f64.select(y64, ld64, wdt, n, steps, init_pos)
+        return self.f64.select_async(y64, ld64, wdt, n, steps, init_pos)
+
+    def select(self, y, ldy, wdt, n, steps, init_pos):
+        return self.select_async(y, ldy, wdt, n, steps, init_pos).result()
 
     def panel_factor(self, p, ldp, mp, b):
         p64, ldp64 = self.f64.alloc(mp, b)
@@ -121,6 +127,42 @@ class Fp32StepEngine:
         # top rows: Q2^T (TN) from a copy
         w[:n2, :b] = a[c0:c0 + n2, r0:r0 + b]
         self.gemm(0, b, n2, b, q2, ldq, b, b, 0, 0, w, ldw, b, n2, 0, 0, a, lda, c0 * lda + r0, 1.0, 0.0)
+
+    def panel_apply_top(self, fac, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
+        """Look-ahead split (dist.factorize_local): W, W2, the top b rows and Q2^T now."""
+        v, ldv, t, ldt, q2, ldq = fac
+        w, ldw = self.alloc(b, n2)
+        w2, _ = self.alloc(b, n2)
+        vs, ldvs, vo = self.shifted(v, ldv, mp, b, r0)
+        self.gemm(0, b, n2, mp, vs, ldvs, mp + vo, b, vo, 0, a, lda, a_rows, a_cols, r0, c0, w, ldw, 0, 1.0, 0.0)
+        self.gemm(0, b, n2, b, t, ldt, b, b, 0, 0, w, ldw, b, n2, 0, 0, w2, ldw, 0, 1.0, 0.0)
+        self.gemm(1, b, n2, b, v, ldv, mp, b, 0, 0, w2, ldw, b, n2, 0, 0, a, lda, c0 * lda + r0, -1.0, 1.0)
+        w[:n2, :b] = a[c0:c0 + n2, r0:r0 + b]
+        self.gemm(0, b, n2, b, q2, ldq, b, b, 0, 0, w, ldw, b, n2, 0, 0, a, lda, c0 * lda + r0, 1.0, 0.0)
+        return w2, ldw
+
+    def panel_apply_rest(self, fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
+        v, ldv, t, ldt, q2, ldq = fac
+        w2, ldw = top
+        if mp > b:
+            self.gemm(1, mp - b, n2, b, v, ldv, mp, b, b, 0, w2, ldw, b, n2, 0, 0, a, lda, c0 * lda + r0 + b, -1.0,
+                      1.0)
+
+    def downdate_g1(self, y, ldy, wdt, c0, ph, p, ldp, b, g1, ldg):
+        """G1 = Y1 R11^{-1} in fp64 (the serial kernels), rounded to fp32 for the downdate GEMM."""
+        y64, ldy64 = self.f64.alloc(wdt, b)
+        y64[:b, :wdt] = y[c0:c0 + b, :wdt]
+        p64, ldp64 = self.f64.alloc(b, b)
+        p64[:b, :b] = p[:b, :b]
+        g64, ldg64 = self.f64.alloc(wdt, b)
+        self.f64.downdate_g1(y64, ldy64, wdt, 0, ph, p64, ldp64, b, g64, ldg64)
+        g1[:b, :wdt] = g64[:b, :wdt]
+
+    def downdate_apply(self, g1, ldg, wdt, b, a, lda, a_rows, a_cols, s, t1, n2, y, ldy):
+        """Y2 <- Y2 - G1 R12 on the local columns t1 .. t1+n2 (fp32, NN)."""
+        if n2 <= 0:
+            return
+        self.gemm(1, wdt, n2, b, g1, ldg, wdt, b, 0, 0, a, lda, a_rows, a_cols, s, t1, y, ldy, t1 * ldy, -1.0, 1.0)
 
     def record_panel(self, s, mp, b, fac):
         if self.keep:
@@ -179,7 +221,7 @@ class Fp32Result:
     q: np.ndarray | None = None  # m x n float32 (economy Q) when requested
 
 
-def block_qr_fp32(a, cfg: BlockConfig, rng: RngState, *, engine=None, group=None, want_q=False):
+def block_qr_fp32(a, cfg: BlockConfig, rng: RngState, *, engine=None, group=None, want_q=False, sketch="fresh"):
     """block_qr (blocked.py:175) with A, its sketches and the trailing updates in fp32.
     ``rng.counter`` advances exactly as in the fp64 / reference run.  want_q (world size 1):
     also form the economy Q in fp32."""
@@ -190,7 +232,7 @@ def block_qr_fp32(a, cfg: BlockConfig, rng: RngState, *, engine=None, group=None
     m, n = a.shape
     buf, ld = eng.alloc(m, n)
     buf[:n, :m] = torch.from_numpy(np.ascontiguousarray(a.T)).to(eng.device)
-    res = factorize_local(buf, ld, m, n, cfg, rng, group=group, engine=eng)
+    res = factorize_local(buf, ld, m, n, cfg, rng, group=group, engine=eng, sketch=sketch)
     r_full = gather_r(res, eng, group)
     r = np.asfortranarray(r_full[:n, :m].cpu().numpy().T)
     q = None

@@ -101,6 +101,25 @@ class NumpyStepEngine:
         x[:b] = q2.T @ x[:b]
         self._put(a, x, r0, c0)
 
+    def panel_apply_top(self, fac, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
+        """Look-ahead split of panel_apply: the top b rows now (W2 returned), the rest later."""
+        vb, ldv, tb, ldt, qb, ldq = fac
+        v = self._get(vb, mp, b)
+        t = self._get(tb, b, b)
+        q2 = self._get(qb, b, b)
+        x = self._get(a, mp, n2, r0, c0)
+        w2 = t.T @ (v.T @ x)
+        top = x[:b] - v[:b] @ w2
+        self._put(a, q2.T @ top, r0, c0)
+        return w2
+
+    def panel_apply_rest(self, fac, w2, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
+        vb = fac[0]
+        v = self._get(vb, mp, b)
+        if mp > b:
+            x = self._get(a, mp - b, n2, r0 + b, c0)
+            self._put(a, x - v[b:] @ w2, r0 + b, c0)
+
     def downdate_g1(self, y, ldy, wdt, c0, ph, p, ldp, b, g1, ldg):
         y1 = self._get(y, wdt, b, 0, c0)[:, np.asarray(ph, dtype=np.int64)]
         r11 = np.triu(self._get(p, b, b))

@@ -21,16 +21,18 @@ def _bars(a, res):
     return resid, np.linalg.norm(g, 2), np.linalg.norm(g) / np.sqrt(n)
 
 
-@pytest.mark.parametrize("m,n,b,p", [(700, 600, 64, 8), (1024, 1000, 128, 16), (530, 500, 50, 6)])
-def test_fp32_q_based_residuals_and_counter(m, n, b, p):
+@pytest.mark.parametrize("m,n,b,p,sketch", [(700, 600, 64, 8, "fresh"), (1024, 1000, 128, 16, "fresh"),
+                                            (530, 500, 50, 6, "fresh"), (1024, 1000, 128, 16, "downdate"),
+                                            (530, 500, 50, 6, "downdate")])
+def test_fp32_q_based_residuals_and_counter(m, n, b, p, sketch):
     import paper_1505_08115_b200 as rq
     from paper_1505_08115_b200.fp32 import block_qr_fp32
 
     a = np.random.default_rng(m).standard_normal((m, n)).astype(np.float32)
     cfg = rq.BlockConfig(b, rq.SketchConfig(b, p, 0))
     rng32, rng64 = rq.RngState(1), rq.RngState(1)
-    res = block_qr_fp32(a, cfg, rng32, want_q=True)
-    f = rq.block_qr(a.astype(np.float64), cfg, rng64)
+    res = block_qr_fp32(a, cfg, rng32, want_q=True, sketch=sketch)
+    f = rq.block_qr(a.astype(np.float64), cfg, rng64, sketch=sketch)
     assert res.r.dtype == np.float32 and res.q.dtype == np.float32
     assert sorted(res.perm) == list(range(n))
     resid, orth2, orthf = _bars(a, res)
