@@ -75,6 +75,9 @@ int rq_ctx_create(rq_ctx** out, int32_t device, void* stream);
 int rq_ctx_destroy(rq_ctx* ctx);
 int rq_ctx_set_stream(rq_ctx* ctx, void* stream);
 int rq_ctx_set_inspect(rq_ctx* ctx, rq_panel_cb cb, void* user);
+/* Cap the grid of this context's GEMMs (rq_gemm, rq_gemm_f32, rq_panel_apply; 0 = whole GPU): a
+ * context whose GEMMs run beside a 16-CTA cluster kernel of another stream leaves it its SMs. */
+int rq_ctx_set_gemm_cap(rq_ctx* ctx, int32_t max_ctas);
 
 /* block_qr / block_rrqr (blocked.py:175-219 / :239-279) on device memory.
  * dA (m x n, lda >= m) is overwritten with R (exact zeros below the diagonal).

@@ -45,6 +45,7 @@ _SIGS = {
     "rq_ctx_destroy": (ctypes.c_int, [_vp]),
     "rq_ctx_set_stream": (ctypes.c_int, [_vp, _vp]),
     "rq_ctx_set_inspect": (ctypes.c_int, [_vp, PANEL_CB, _vp]),
+    "rq_ctx_set_gemm_cap": (ctypes.c_int, [_vp, _i32]),
     "rq_factorize": (ctypes.c_int, [_vp, ctypes.POINTER(rq_config), _i64, _i64, _vp, _i64, _u64,
                                     ctypes.POINTER(_u64), _vp]),
     "rq_factorize_host": (ctypes.c_int, [_vp, ctypes.POINTER(rq_config), _i64, _i64, _vp, _i64, _u64,

@@ -61,6 +61,13 @@ int rq_ctx_set_stream(rq_ctx* ctx, void* stream) {
   return RQ_OK;
 }
 
+int rq_ctx_set_gemm_cap(rq_ctx* ctx, int32_t max_ctas) {
+  CTX_CHECK(ctx);
+  if (max_ctas < 0) return rq::set_error(RQ_EVALUE, "max_ctas < 0");
+  ctx->c.gemm_cap = max_ctas;
+  return RQ_OK;
+}
+
 int rq_ctx_set_inspect(rq_ctx* ctx, rq_panel_cb cb, void* user) {
   CTX_CHECK(ctx);
   ctx->c.inspect_cb = cb;
@@ -457,6 +464,7 @@ int rq_gemm_f32(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, 
   p.ldc = ldc;
   p.alpha = alpha;
   p.beta = beta;
+  p.max_ctas = ctx->c.gemm_cap;
   return rq::gemm_tf32x3(p, ctx->c.stream, &ctx->c.launches);
 }
 

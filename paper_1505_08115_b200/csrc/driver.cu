@@ -279,7 +279,7 @@ int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_
   p.splitk = 0;  // automatic
   p.work = kwork;
   p.work_bytes = kwork ? kwork_bytes : 0;
-  p.max_ctas = gemm_max_ctas;
+  p.max_ctas = gemm_max_ctas > 0 ? gemm_max_ctas : gemm_cap;
   p.pdl = gemm_pdl;
   p.mid_event = gemm_mid;
   p.splitk_used = gemm_mid ? &gemm_splitk : nullptr;

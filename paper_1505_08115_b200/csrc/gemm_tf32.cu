@@ -9,9 +9,10 @@
 // operand x is split as hi = tf32(x) and lo = tf32(x - hi) (round to nearest; both exact in TF32,
 // |x - hi - lo| <= 2^-23 |x|), and each k-block issues
 // A_hi B_hi + A_hi B_lo + A_lo B_hi into one FP32 TMEM accumulator (the lo x lo term is below
-// fp32 rounding).  Roles per CTA (one 128 x 128 output tile, BK = 32):
+// fp32 rounding).  Persistent CTAs (<= one per SM, optionally capped) walk their 128 x 128 output
+// tiles as one stream of (tile, k-block) steps, BK = 32; roles per CTA:
 //   warp 0      TMA producer: raw fp32 tiles of A and B into a 2-deep ring (mbarrier complete_tx)
-//   warps 2-5   converters: raw -> hi / lo tiles in the canonical K-major SWIZZLE_128B layout
+//   warps 2-9   converters: raw -> hi / lo tiles in the canonical K-major SWIZZLE_128B layout
 //               (an M-major A is transposed here), zeroing k outside the view; then the epilogue
 //   warp 1      TMEM allocation and the single-thread tcgen05.mma issue, tcgen05.commit frees a
 //               converted stage / signals the epilogue
@@ -21,6 +22,7 @@
 // stores (lanes = consecutive rows).
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -33,8 +35,9 @@ namespace {
 constexpr int TBM = 128, TBN = 128, TBK = 32;
 constexpr int kTile = TBM * TBK * 4;      // 16 KB: one 128 x 32 fp32 tile
 constexpr int kRawStages = 3, kConvStages = 2;
-constexpr int kThreads = 192;             // warps 0 (TMA), 1 (MMA), 2-5 (convert + epilogue)
-constexpr int kConvThreads = 128;
+constexpr int kThreads = 320;             // warps 0 (TMA), 1 (MMA), 2-9 (convert + drain + epilogue)
+constexpr int kConvThreads = 256;
+constexpr int kHalf = TBN / 2;            // accumulator columns per converter thread
 constexpr int kSmem = kRawStages * 2 * kTile + kConvStages * 4 * kTile + 1024 + 256;
 static_assert(kSmem <= 232448, "shared memory per CTA");
 
@@ -45,7 +48,7 @@ struct TArgs {
   float* C;
   int64_t ldc;
   float alpha, beta;
-  int tiles_m;
+  int tiles_m, tiles;
   int kblocks;
   int four;  // 1: also A_lo B_lo (4 products; tuning / accuracy probe)
 };
@@ -125,12 +128,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* raw_empty = bars + 4;   // [kRawStages]
   uint64_t* conv_full = bars + 8;   // [2]
   uint64_t* conv_empty = bars + 10;
-  uint64_t* acc_full = bars + 12;   // [2]: a k-block's products landed in TMEM accumulator (kb & 1)
+  uint64_t* acc_full = bars + 12;   // [2]: a k-block's products landed in TMEM accumulator (g & 1)
   uint64_t* acc_empty = bars + 14;  // [2]: the converter warps drained it into registers
   uint32_t* tmem_slot = (uint32_t*)(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tm = blockIdx.x % a.tiles_m, tn = blockIdx.x / a.tiles_m;
+  // persistent: this CTA's tiles blockIdx.x, blockIdx.x + gridDim.x, ...; one stream of
+  // (tile, k-block) steps g = j * kblocks + kb through every pipeline
+  const int my_tiles = a.tiles > (int)blockIdx.x ? (a.tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int G = my_tiles * a.kblocks;
+  auto tile_of = [&](int g) { return (int)blockIdx.x + (g / a.kblocks) * (int)gridDim.x; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRawStages; s++) {
@@ -140,8 +147,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; s++) {
       bar_init(&conv_full[s], kConvThreads);
       bar_init(&conv_empty[s], 1);
-    }
-    for (int s = 0; s < 2; s++) {
       bar_init(&acc_full[s], 1);
       bar_init(&acc_empty[s], kConvThreads);
     }
@@ -149,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(&ma) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mb) : "memory");
   }
-  if (warp == 1) {  // 256 TMEM columns: two 128 x 128 fp32 accumulators (k-block parity)
+  if (warp == 1) {  // 256 TMEM columns: two 128 x 128 fp32 accumulators (step parity)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(s_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -162,9 +167,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
-      for (int kb = 0; kb < a.kblocks; kb++) {
-        const int s = kb % kRawStages;
-        bar_wait(&raw_empty[s], ((kb / kRawStages) & 1) ^ 1);
+      for (int g = 0; g < G; g++) {
+        const int t = tile_of(g), kb = g % a.kblocks;
+        const int tm = t % a.tiles_m, tn = t / a.tiles_m;
+        const int s = g % kRawStages;
+        bar_wait(&raw_empty[s], ((g / kRawStages) & 1) ^ 1);
         bar_expect_tx(&raw_full[s], 2 * kTile);
         unsigned char* ra = raw + (s * 2) * kTile;
         unsigned char* rb = raw + (s * 2 + 1) * kTile;
@@ -177,14 +184,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (one thread) ----------------
-    // Each k-block accumulates into its own (parity) TMEM accumulator, which the converter warps
+    // Each step accumulates into its own (parity) TMEM accumulator, which the converter warps
     // add into fp32 registers: the tensor core's accumulation then spans 32 k only (its long
-    // in-TMEM sums measured ~6x less accurate than an fp32 SGEMM and biased, tools/gemm_acc.py).
+    // in-TMEM sums measured ~6x less accurate than an fp32 SGEMM, tools/gemm_acc.py).
     if (lane == 0) {
-      for (int kb = 0; kb < a.kblocks; kb++) {
-        const int s = kb & 1;
-        bar_wait(&conv_full[s], (kb >> 1) & 1);
-        bar_wait(&acc_empty[s], ((kb >> 1) & 1) ^ 1);
+      for (int g = 0; g < G; g++) {
+        const int s = g & 1;
+        bar_wait(&conv_full[s], (g >> 1) & 1);
+        bar_wait(&acc_empty[s], ((g >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t base = s_u32(conv + (s * 4) * kTile);
         const uint32_t ahi = base, alo = base + kTile, bhi = base + 2 * kTile, blo = base + 3 * kTile;
@@ -202,21 +209,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- converters (then the epilogue) ----------------
+    // ---------------- converters, drains and epilogues ----------------
     const int c = threadIdx.x - 64;
-    const int q = warp & 3;  // TMEM lanes 32q .. 32q + 31 = output rows of this thread's warp
-    float accr[TBN];
+    const int q = warp & 3;            // TMEM lanes 32q .. 32q + 31 = output rows of this thread's warp
+    const int h0 = ((warp - 2) >> 2) * kHalf;  // this thread's accumulator columns h0 .. h0 + 63
+    float accr[kHalf];
 #pragma unroll
-    for (int j = 0; j < TBN; j++) accr[j] = 0.0f;
-    // add k-block kd's TMEM accumulator (parity kd & 1) into accr and release it
-    auto drain = [&](int kd) {
-      const int s = kd & 1;
-      bar_wait(&acc_full[s], (kd >> 1) & 1);
+    for (int j = 0; j < kHalf; j++) accr[j] = 0.0f;
+    // add step gd's TMEM accumulator (parity gd & 1) into accr and release it
+    auto drain = [&](int gd) {
+      const int s = gd & 1;
+      bar_wait(&acc_full[s], (gd >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int cb = 0; cb < TBN / 32; cb++) {
+      for (int cb = 0; cb < kHalf / 32; cb++) {
         uint32_t r[32];
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * TBN + cb * 32);
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * TBN + h0 + cb * 32);
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
             "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
@@ -232,10 +240,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       bar_arrive(&acc_empty[s]);
     };
-    for (int kb = 0; kb < a.kblocks; kb++) {
-      const int s = kb & 1, rs = kb % kRawStages;
-      const uint32_t ph = (kb >> 1) & 1;
-      bar_wait(&raw_full[rs], (kb / kRawStages) & 1);
+    // registers -> C for tile t (the tensor core already works on the next tile)
+    auto epilogue = [&](int t) {
+      const int tm = t % a.tiles_m, tn = t / a.tiles_m;
+      const int m = tm * TBM + q * 32 + lane;
+      if (m >= a.m_lo && m < a.M) {
+        float* cbase = a.C + (int64_t)(tn * TBN + h0) * a.ldc + m;
+        const int nv = min(kHalf, a.N - tn * TBN - h0);
+#pragma unroll
+        for (int gq = 0; gq < kHalf / 16; gq++) {
+          // 16 independent loads of C first (the stores below could alias them), then 16 stores
+          float cv[16];
+          if (a.beta != 0.0f) {
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+              cv[j] = (gq * 16 + j < nv) ? __ldcs(cbase + (int64_t)(gq * 16 + j) * a.ldc) : 0.0f;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; j++) {
+            if (gq * 16 + j < nv) {
+              float v = a.alpha * accr[gq * 16 + j];
+              if (a.beta != 0.0f) v = fmaf(a.beta, cv[j], v);
+              __stcs(cbase + (int64_t)(gq * 16 + j) * a.ldc, v);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kHalf; j++) accr[j] = 0.0f;
+    };
+    for (int g = 0; g < G; g++) {
+      const int s = g & 1, rs = g % kRawStages;
+      const uint32_t ph = (g >> 1) & 1;
+      bar_wait(&raw_full[rs], (g / kRawStages) & 1);
       bar_wait(&conv_empty[s], ph ^ 1);
       const unsigned char* ra = raw + (rs * 2) * kTile;
       const unsigned char* rb = raw + (rs * 2 + 1) * kTile;
@@ -243,10 +280,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       unsigned char* alo = ahi + kTile;
       unsigned char* bhi = ahi + 2 * kTile;
       unsigned char* blo = ahi + 3 * kTile;
-      const int kbase = kb * TBK;
-      // B (and a K-major A): the raw tile already has the target layout; split in place order
+      const int kbase = (g % a.kblocks) * TBK;
+      // B (and a K-major A): the raw tile already has the target layout
 #pragma unroll
-      for (int t = 0; t < 8; t++) {
+      for (int t = 0; t < 1024 / kConvThreads; t++) {
         const int v = c + kConvThreads * t;  // 16-byte vector index 0..1023
         const int r = v >> 3;
         const int k0 = (((v & 7) ^ (r & 7)) << 2);
@@ -277,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (A_MMAJOR) {
         // raw A: 32 k-rows of 128 contiguous m (no swizzle) -> K-major SWIZZLE_128B hi / lo
 #pragma unroll
-        for (int t = 0; t < 8; t++) {
+        for (int t = 0; t < 1024 / kConvThreads; t++) {
           const int v = c + kConvThreads * t;
           const int k = v >> 5, m0 = (v & 31) << 2;
           const float4 x = *reinterpret_cast<const float4*>(ra + v * 16);
@@ -298,32 +335,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar_arrive(&raw_empty[rs]);
       bar_arrive(&conv_full[s]);
-      if (kb > 0) drain(kb - 1);  // (the tensor core works on kb meanwhile)
-    }
-    if (a.kblocks > 0) drain(a.kblocks - 1);
-    // ---------------- epilogue: registers -> C ----------------
-    const int m = tm * TBM + q * 32 + lane;
-    if (m >= a.m_lo && m < a.M) {
-      float* cbase = a.C + (int64_t)(tn * TBN) * a.ldc + m;
-      const int nv = min(TBN, a.N - tn * TBN);
-#pragma unroll
-      for (int g = 0; g < TBN / 32; g++) {
-        // 32 independent loads of C first (the stores below could alias them), then 32 stores
-        float cv[32];
-        if (a.beta != 0.0f) {
-#pragma unroll
-          for (int j = 0; j < 32; j++)
-            cv[j] = (g * 32 + j < nv) ? __ldcs(cbase + (int64_t)(g * 32 + j) * a.ldc) : 0.0f;
-        }
-#pragma unroll
-        for (int j = 0; j < 32; j++) {
-          if (g * 32 + j < nv) {
-            float v = a.alpha * accr[g * 32 + j];
-            if (a.beta != 0.0f) v = fmaf(a.beta, cv[j], v);
-            __stcs(cbase + (int64_t)(g * 32 + j) * a.ldc, v);
-          }
-        }
+      if (g > 0) {  // (the tensor core works on step g meanwhile)
+        drain(g - 1);
+        if ((g - 1) % a.kblocks == a.kblocks - 1) epilogue(tile_of(g - 1));
       }
+    }
+    if (G > 0) {
+      drain(G - 1);
+      epilogue(tile_of(G - 1));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -414,9 +433,19 @@ int launch(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
   a.kblocks = (int)ceil_div(a.Kv, TBK);
   static const int env_four = getenv("RQ_TF32X4") ? atoi(getenv("RQ_TF32X4")) : 0;
   a.four = env_four;
-  const int64_t grid = (int64_t)a.tiles_m * tiles_n;
-  if (grid > 0x7fffffff) return set_error(RQ_EUNSUPPORTED, "fp32 gemm: too many tiles");
-  kern<<<(unsigned)grid, kThreads, kSmem, st>>>(ma, mb, a);
+  const int64_t tiles = (int64_t)a.tiles_m * tiles_n;
+  if (tiles > 0x7fffffff) return set_error(RQ_EUNSUPPORTED, "fp32 gemm: too many tiles");
+  a.tiles = (int)tiles;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = kSMs;
+  }
+  const int cap = p.max_ctas > 0 ? std::min(p.max_ctas, sms) : sms;  // persistent: <= one CTA per SM
+  const int grid = (int)std::min<int64_t>(tiles, cap);
+  kern<<<grid, kThreads, kSmem, st>>>(ma, mb, a);
   RQ_CUDA_TRY(cudaGetLastError());
   if (launches) (*launches)++;
   return RQ_OK;

@@ -21,6 +21,7 @@ struct GemmProblemF32 {
   float* C;
   int64_t ldc;
   double alpha, beta;
+  int max_ctas = 0;  // > 0: cap the persistent grid (leave SMs to a concurrent kernel)
 };
 
 int gemm_tf32x3(const GemmProblemF32& p, cudaStream_t st, int64_t* launches);

@@ -33,6 +33,7 @@ one GPU (hqrrp.block_qr / block_rrqr).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -79,6 +80,8 @@ def _host_index(torch, arr, device):
 class CudaStepEngine:
     """Panel steps on the GPU through the C ABI (rq_gemm, rq_sketch_select,
     rq_panel_factor, rq_panel_apply, rq_householder_sweep, rq_gaussian_matrix)."""
+
+    defer_rest = os.environ.get("RQ_DIST_DEFER", "0") == "1"
 
     def __init__(self, engine: Engine | None = None):
         import torch
@@ -155,13 +158,69 @@ class CudaStepEngine:
         check(g(self.h, 0, b, n2, b, _ptr(q2), ldq, b, b, 0, 0, _ptr(w), ldw, b, n2, 0, 0, c, lda, 1.0, 0.0))
         return w2, ldw
 
-    def panel_apply_rest(self, fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
-        """A2[b:] -= V[b:] W2 (the trailing update below the panel's rows)."""
+    def panel_apply_rest(self, fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2, w_off=0, h=None):
+        """A2[b:] -= V[b:] W2 (the trailing update below the panel's rows); W2's columns start at
+        w_off (a sub-range of the local trailing columns)."""
         v, ldv, t, ldt, q2, ldq = fac
         w2, ldw = top
-        if mp > b:
-            check(self.lib.rq_gemm(self.h, 1, mp - b, n2, b, _ptr(v), ldv, mp, b, b, 0, _ptr(w2), ldw, b, n2, 0, 0,
-                                   _ptr(a, c0 * lda + r0 + b), lda, -1.0, 1.0))
+        if mp > b and n2 > 0:
+            check(self.lib.rq_gemm(h or self.h, 1, mp - b, n2, b, _ptr(v), ldv, mp, b, b, 0, _ptr(w2), ldw, b,
+                                   w2.shape[0], 0, w_off, _ptr(a, c0 * lda + r0 + b), lda, -1.0, 1.0))
+
+    # ---- deferred rest of the update (look-ahead): the columns the next exchange / panel
+    #      needs first (gathered), then the bulk on a side stream beside the next panel ----
+    def panel_apply_rest_cols(self, fac, top, mp, b, a, lda, r0, t1, cols):
+        if mp <= b or len(cols) == 0:
+            return
+        torch = self.torch
+        w2, ldw = top
+        idx = self.index(cols)
+        widx = self.index(np.asarray(cols) - t1)
+        k = len(cols)
+        x, ldx = self.alloc(mp - b, k)
+        x[:k, :mp - b] = a.index_select(0, idx)[:, r0 + b:r0 + mp]
+        ws, ldws = self.alloc(b, k)
+        ws[:k, :b] = w2.index_select(0, widx)[:, :b]
+        v = fac[0]
+        check(self.lib.rq_gemm(self.h, 1, mp - b, k, b, _ptr(v), fac[1], mp, b, b, 0, _ptr(ws), ldws, b, k, 0, 0,
+                               _ptr(x), ldx, -1.0, 1.0))
+        rows = a.index_select(0, idx)
+        rows[:, r0 + b:r0 + mp] = x[:k, :mp - b]
+        a.index_copy_(0, idx, rows)
+        w2.index_fill_(0, widx, 0.0)
+
+    def zero_cols(self, top, cols):
+        if len(cols):
+            top[0].index_fill_(0, self.index(cols), 0.0)
+
+    def _side(self):
+        if getattr(self, "_side_eng", None) is None:
+            st = self.torch.cuda.Stream(device=self.device)
+            self._side_eng = Engine(self.device.index, stream=st)
+            # its GEMMs leave 16 SMs to the panel's cluster kernels on the main stream
+            check(self.lib.rq_ctx_set_gemm_cap(self._side_eng.handle, 148 - 16))
+        return self._side_eng
+
+    def rest_async(self, fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2, w_off, keep):
+        """panel_apply_rest on a side stream (its own library context); returns the event the
+        main stream waits for before the next panel's trailing update."""
+        torch = self.torch
+        se = self._side()
+        ev0 = torch.cuda.Event()
+        ev0.record(self.eng.stream)
+        se.stream.wait_event(ev0)
+        with torch.cuda.stream(se.stream):
+            self.panel_apply_rest(fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2, w_off, h=se.handle)
+            for t in keep:  # main-stream tensors the side stream reads: not reused before it is done
+                t.record_stream(se.stream)
+            top[0].record_stream(se.stream)
+        ev1 = torch.cuda.Event()
+        ev1.record(se.stream)
+        return ev1
+
+    def wait(self, ev):
+        if ev is not None:
+            self.eng.stream.wait_event(ev)
 
     def downdate_g1(self, y, ldy, wdt, c0, ph, p, ldp, b, g1, ldg):
         """G1 = Y1 R11^{-1} (written into g1, wdt x b): Y1 = the panel's sketch columns c0.. of y
@@ -436,13 +495,22 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
     # rows and the rest of the update; the host then waits for the pivots while the GPU runs
     # the rest of the update.
     lookahead = downdate and hasattr(engine, "panel_apply_top")
+    # Deferring the bulk of the update to a side stream beside the next panel's factorization
+    # (rest_async) measured slower with the CUDA engines -- rq_panel_factor's WY updates between
+    # leaves need the whole GPU (n = 10k, N = 1: 230 vs 199 ms) -- so they opt in (RQ_DIST_DEFER=1)
+    defer_rest = lookahead and hasattr(engine, "rest_async") and getattr(engine, "defer_rest", False)
     pending = None
+    deferred = None
+    rest_ev = None
     for i in range(lay.nblk):
         s = i * b
         np_ = n - s
         mp = m - s
         o = lay.owner(i)
         if np_ <= b:
+            if rest_ev is not None:
+                engine.wait(rest_ev)
+                rest_ev = None
             _apply_pending_phat(slot_orig, ph_pending)
             _final_block(a_loc, lda, m, n, s, i, lay, rank, slot_orig, slot_lpos, d, engine)
             break
@@ -455,7 +523,24 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         chosen = ycol_slot[chosen_y]
         # ---- 3: move the chosen columns into the panel slots ----
         moves = plan_moves(chosen, s, b)
-        _exchange_columns(a_loc, m, lay, rank, moves, d, engine)
+        if deferred is not None:
+            # the previous panel's update below its rows: first on the columns that move and on
+            # this panel's block (owner), then the bulk beside this panel's factorization
+            fac_d, top_d, mp_d, s_d, t1_d, n2_d, keep_d = deferred
+            deferred = None
+            sent = [lay.locate(src)[1] for src, _ in moves if lay.locate(src)[0] == rank]
+            recv = [lay.locate(dst)[1] for _, dst in moves if lay.locate(dst)[0] == rank]
+            own = rank == o
+            pre = set(sent) | (set(range(t1_d, t1_d + b)) if own else set())
+            pre = sorted(c for c in pre if t1_d <= c < t1_d + n2_d)
+            engine.panel_apply_rest_cols(fac_d, top_d, mp_d, b, a_loc, lda, s_d, t1_d, pre)
+            engine.zero_cols(top_d, [c - t1_d for c in recv if t1_d <= c < t1_d + n2_d])
+            _exchange_columns(a_loc, m, lay, rank, moves, d, engine)
+            c_lo = t1_d + (b if own else 0)
+            rest_ev = engine.rest_async(fac_d, top_d, mp_d, b, a_loc, lda, m, nloc, s_d, c_lo,
+                                        t1_d + n2_d - c_lo, c_lo - t1_d, keep_d)
+        else:
+            _exchange_columns(a_loc, m, lay, rank, moves, d, engine)
         if downdate:  # the sketch columns follow their matrix columns
             _exchange_columns(y_loc, wdt, lay, rank, moves, d, engine)
         _apply_moves_host(slot_orig, moves)
@@ -503,6 +588,8 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
         fac = (v, ldv, t, ldb, q2, ldb)
         next_full = n - (s + b) > b
         if lookahead:
+            engine.wait(rest_ev)  # the previous panel's bulk update (side stream)
+            rest_ev = None
             top = engine.panel_apply_top(fac, mp, b, a_loc, lda, m, nloc, s, t1, n2) if n2 > 0 else None
             if next_full:
                 # ---- 6: Y2_loc -= G1 R12_loc, then the next panel's selection (every rank) ----
@@ -511,7 +598,10 @@ def factorize_local(a_loc, lda, m, n, cfg: BlockConfig, rng: RngState, *, group=
                                           y_loc, ldyl)
                 pending = start_select(i + 1)
             if n2 > 0:
-                engine.panel_apply_rest(fac, top, mp, b, a_loc, lda, m, nloc, s, t1, n2)
+                if next_full and defer_rest:
+                    deferred = (fac, top, mp, s, t1, n2, [pack])
+                else:
+                    engine.panel_apply_rest(fac, top, mp, b, a_loc, lda, m, nloc, s, t1, n2)
         elif n2 > 0:
             engine.panel_apply(fac, mp, b, a_loc, lda, m, nloc, s, t1, n2)
             # ---- 6 (downdate): Y2_loc -= G1 R12_loc on the local trailing columns ----

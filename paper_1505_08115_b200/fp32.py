@@ -39,6 +39,7 @@ class Fp32StepEngine:
     """fp32 storage and tensor-core GEMMs; fp64 serial kernels on converted copies."""
 
     ld_align = 4  # rq_gemm_f32: ld % 4 == 0, 16-byte aligned operand bases
+    defer_rest = CudaStepEngine.defer_rest
 
     def __init__(self, engine: Engine | None = None, keep_factors: bool = False):
         import torch
@@ -58,12 +59,12 @@ class Fp32StepEngine:
         return torch.zeros((max(cols, 1), max(ld, 4)), dtype=torch.float32, device=self.device), ld
 
     def gemm(self, mmajor, M, N, K, a, lda, a_rows, a_cols, a_r0, a_c0, b, ldb, b_rows, b_cols, b_r0, b_c0, c, ldc,
-             c_off, alpha, beta):
+             c_off, alpha, beta, h=None):
         """rq_gemm_f32 on (cols, ld) storages; c_off = element offset of C's view."""
         if M <= 0 or N <= 0:
             return
-        check(self.lib.rq_gemm_f32(self.h, int(mmajor), M, N, K, _p(a), lda, a_rows, a_cols, a_r0, a_c0, _p(b), ldb,
-                                   b_rows, b_cols, b_r0, b_c0, _p(c, c_off), ldc, float(alpha), float(beta)))
+        check(self.lib.rq_gemm_f32(h or self.h, int(mmajor), M, N, K, _p(a), lda, a_rows, a_cols, a_r0, a_c0, _p(b),
+                                   ldb, b_rows, b_cols, b_r0, b_c0, _p(c, c_off), ldc, float(alpha), float(beta)))
 
     def shifted(self, x, ldx, rows, cols, r0):
         """x (rows x cols) re-based at row r0 % 4 of a new buffer: a TN product's two K origins must
@@ -141,12 +142,53 @@ class Fp32StepEngine:
         self.gemm(0, b, n2, b, q2, ldq, b, b, 0, 0, w, ldw, b, n2, 0, 0, a, lda, c0 * lda + r0, 1.0, 0.0)
         return w2, ldw
 
-    def panel_apply_rest(self, fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
+    def panel_apply_rest(self, fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2, w_off=0, h=None):
         v, ldv, t, ldt, q2, ldq = fac
         w2, ldw = top
-        if mp > b:
-            self.gemm(1, mp - b, n2, b, v, ldv, mp, b, b, 0, w2, ldw, b, n2, 0, 0, a, lda, c0 * lda + r0 + b, -1.0,
-                      1.0)
+        if mp > b and n2 > 0:
+            self.gemm(1, mp - b, n2, b, v, ldv, mp, b, b, 0, w2, ldw, b, w2.shape[0], 0, w_off, a, lda,
+                      c0 * lda + r0 + b, -1.0, 1.0, h=h)
+
+    def panel_apply_rest_cols(self, fac, top, mp, b, a, lda, r0, t1, cols):
+        """The deferred rest of the update on the listed local columns (gathered), then their
+        W2 columns zeroed (dist.factorize_local's look-ahead)."""
+        if mp <= b or len(cols) == 0:
+            return
+        w2, ldw = top
+        idx = self.index(cols)
+        widx = self.index(np.asarray(cols) - t1)
+        k = len(cols)
+        x, ldx = self.alloc(mp - b, k)
+        x[:k, :mp - b] = a.index_select(0, idx)[:, r0 + b:r0 + mp]
+        ws, ldws = self.alloc(b, k)
+        ws[:k, :b] = w2.index_select(0, widx)[:, :b]
+        v, ldv = fac[0], fac[1]
+        self.gemm(1, mp - b, k, b, v, ldv, mp, b, b, 0, ws, ldws, b, k, 0, 0, x, ldx, 0, -1.0, 1.0)
+        rows = a.index_select(0, idx)
+        rows[:, r0 + b:r0 + mp] = x[:k, :mp - b]
+        a.index_copy_(0, idx, rows)
+        w2.index_fill_(0, widx, 0.0)
+
+    def zero_cols(self, top, cols):
+        self.f64.zero_cols(top, cols)
+
+    def rest_async(self, fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2, w_off, keep):
+        torch = self.torch
+        se = self.f64._side()
+        ev0 = torch.cuda.Event()
+        ev0.record(self.f64.eng.stream)
+        se.stream.wait_event(ev0)
+        with torch.cuda.stream(se.stream):
+            self.panel_apply_rest(fac, top, mp, b, a, lda, a_rows, a_cols, r0, c0, n2, w_off, h=se.handle)
+            for t in keep:
+                t.record_stream(se.stream)
+            top[0].record_stream(se.stream)
+        ev1 = torch.cuda.Event()
+        ev1.record(se.stream)
+        return ev1
+
+    def wait(self, ev):
+        self.f64.wait(ev)
 
     def downdate_g1(self, y, ldy, wdt, c0, ph, p, ldp, b, g1, ldg):
         """G1 = Y1 R11^{-1} in fp64 (the serial kernels), rounded to fp32 for the downdate GEMM."""

@@ -32,6 +32,7 @@ def _tfac(v):
 
 class NumpyStepEngine:
     torch = torch
+    defer_rest = True  # exercise dist.factorize_local's deferred-update bookkeeping
 
     def __init__(self):
         self.device = torch.device("cpu")
@@ -113,12 +114,33 @@ class NumpyStepEngine:
         self._put(a, q2.T @ top, r0, c0)
         return w2
 
-    def panel_apply_rest(self, fac, w2, mp, b, a, lda, a_rows, a_cols, r0, c0, n2):
+    def panel_apply_rest(self, fac, w2, mp, b, a, lda, a_rows, a_cols, r0, c0, n2, w_off=0):
         vb = fac[0]
         v = self._get(vb, mp, b)
-        if mp > b:
+        if mp > b and n2 > 0:
             x = self._get(a, mp - b, n2, r0 + b, c0)
-            self._put(a, x - v[b:] @ w2, r0 + b, c0)
+            self._put(a, x - v[b:] @ w2[:, w_off:w_off + n2], r0 + b, c0)
+
+    # deferred-rest protocol of dist.factorize_local (synchronous here: exercises the
+    # column bookkeeping of the look-ahead on CPU)
+    def panel_apply_rest_cols(self, fac, w2, mp, b, a, lda, r0, t1, cols):
+        v = self._get(fac[0], mp, b)
+        for c in cols:
+            if mp > b:
+                x = self._get(a, mp - b, 1, r0 + b, c)
+                self._put(a, x - v[b:] @ w2[:, c - t1:c - t1 + 1], r0 + b, c)
+            w2[:, c - t1] = 0.0
+
+    def zero_cols(self, w2, cols):
+        for c in cols:
+            w2[:, c] = 0.0
+
+    def rest_async(self, fac, w2, mp, b, a, lda, a_rows, a_cols, r0, c0, n2, w_off, keep):
+        self.panel_apply_rest(fac, w2, mp, b, a, lda, a_rows, a_cols, r0, c0, n2, w_off)
+        return None
+
+    def wait(self, ev):
+        pass
 
     def downdate_g1(self, y, ldy, wdt, c0, ph, p, ldp, b, g1, ldg):
         y1 = self._get(y, wdt, b, 0, c0)[:, np.asarray(ph, dtype=np.int64)]
