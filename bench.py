@@ -517,6 +517,8 @@ def main():
             del u, v
         work, _ = eng.alloc_matrix(m, n)
         perm = torch.empty(n, dtype=torch.int64, device=eng.device)
+    if args.method != "m1":
+        args.sketch = "fresh"  # reflector pivots / block_rrqr: the reference's fresh sketches only
     mode = _lib.RQ_SKETCH_FRESH if args.sketch == "fresh" else _lib.RQ_SKETCH_DOWNDATE
     pk = _lib.RQ_PIVOT_PERMUTATION if args.method == "m1" else _lib.RQ_PIVOT_REFLECTORS
     cfg = _lib.rq_config(b, p, args.q, -1, pk, 1 if args.method == "m3" else 0, mode, 0)

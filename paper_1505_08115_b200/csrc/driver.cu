@@ -14,6 +14,7 @@
 //   9  tail <- Q2^T (tail - V T^T V^T tail)                       (blocked.py:210-211)
 // The final block (n - s <= b) is one pivoted sweep at full height (blocked.py:195-203).
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <vector>
 
@@ -313,6 +314,8 @@ void Ctx::phase(int id) {
   if (cudaEventCreate(&e) != cudaSuccess) return;
   cudaEventRecord(e, stream);
   phase_ev.emplace_back(id, e);
+  phase_host.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+                           .count());
 }
 
 void Ctx::side_phase(int id) {
@@ -345,6 +348,9 @@ void Ctx::phase_report() {
       cudaEventElapsedTime(&ms, phase_ev[k - 1].second, phase_ev[k].second);
       fprintf(stderr, " %d:%.4f", phase_ev[k].first, ms);
     }
+    fprintf(stderr, "\n[rq phase-host]");  // host enqueue time between the same phase calls
+    for (size_t k = 1; k < phase_host.size(); k++)
+      fprintf(stderr, " %d:%.4f", phase_ev[k].first, phase_host[k] - phase_host[k - 1]);
     fprintf(stderr, "\n");
   }
   fprintf(stderr, "[rq phases] total %.2f ms:", tot);
@@ -353,6 +359,7 @@ void Ctx::phase_report() {
   fprintf(stderr, "\n");
   for (auto& pe : phase_ev) cudaEventDestroy(pe.second);
   phase_ev.clear();
+  phase_host.clear();
   if (!side_ev.empty()) {
     // side stream: id 0 = CPQR done (start of W), 1 = capped W part, 2 = rest of W, 3 = T
     double sacc[4] = {0};

@@ -184,6 +184,7 @@ struct Ctx {
   // between a leaf and its look-ahead chunk); per-phase totals printed to stderr per call
   bool phases_on = false;
   std::vector<std::pair<int, cudaEvent_t>> phase_ev;
+  std::vector<double> phase_host;  // host clock (ms) at each phase() call
   std::vector<std::pair<int, cudaEvent_t>> side_ev;  // side stream: W GEMM parts and T
   void phase(int id);
   void side_phase(int id);

@@ -18,6 +18,7 @@ if os.environ.get("_RQ_CHILD") != "1":
         env = dict(os.environ, RQ_PHASES="2", _RQ_CHILD="1")
         r = subprocess.run([sys.executable, __file__, n], env=env, capture_output=True, text=True)
         lines = [ln for ln in r.stderr.splitlines() if ln.startswith("[rq phase-seq]")]
+        hlines = [ln for ln in r.stderr.splitlines() if ln.startswith("[rq phase-host]")]
         if not lines:
             print(r.stdout, r.stderr[-3000:])
             continue
@@ -39,6 +40,22 @@ if os.environ.get("_RQ_CHILD") != "1":
             if i < 6 or i % 8 == 0 or i >= len(panels) - 3:
                 print(f"{i:5d} " + " ".join(f"{p.get(c, 0.0):9.3f}" for c in cols) + f" {sum(p.values()):7.3f}")
         print("total " + " ".join(f"{tot[c]:9.2f}" for c in cols))
+        if hlines:  # host enqueue time per panel vs device time per panel
+            hseq = [(int(t.split(":")[0]), float(t.split(":")[1])) for t in hlines[-1].split()[2:]]
+            hp, cur = [], 0.0
+            first = True
+            for pid, ms in hseq:
+                if pid == 1 and not first:
+                    hp.append(cur)
+                    cur = 0.0
+                first = False
+                cur += ms
+            hp.append(cur)
+            print("host enqueue ms per panel (vs device):")
+            for i, (p, h) in enumerate(zip(panels, hp)):
+                if i < 4 or i % 8 == 0 or i >= len(panels) - 3:
+                    print(f"  panel {i:3d}: host {h:7.3f}  device {sum(p.values()):7.3f}")
+            print(f"  total host {sum(hp):.2f} ms, device {sum(ms for _, ms in seq):.2f} ms")
     sys.exit(0)
 
 sys.path.insert(0, os.getcwd())
