@@ -312,23 +312,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (A_MMAJOR) {
-        // raw A: 32 k-rows of 128 contiguous m (no swizzle) -> K-major SWIZZLE_128B hi / lo
+        // raw A: 32 k-rows of 128 contiguous m (no swizzle) -> K-major SWIZZLE_128B hi / lo.  Each
+        // thread builds one 16-byte target chunk (row r, k = 4 kc .. 4 kc + 3): lanes take
+        // consecutive rows, so the reads are consecutive words and the 16-byte stores of a
+        // quarter-warp land in 8 distinct swizzled chunks (no bank conflicts)
 #pragma unroll
         for (int t = 0; t < 1024 / kConvThreads; t++) {
           const int v = c + kConvThreads * t;
-          const int k = v >> 5, m0 = (v & 31) << 2;
-          const float4 x = *reinterpret_cast<const float4*>(ra + v * 16);
-          const float xs[4] = {x.x, x.y, x.z, x.w};
-          const int kg = kbase + k;
-          const bool ok = kg >= a.k_lo && kg < a.Kv;
+          const int r = v & (TBM - 1), kc = v >> 7;
+          const float* src = reinterpret_cast<const float*>(ra) + (kc * 4) * TBM + r;
+          float h[4], l[4];
 #pragma unroll
           for (int e = 0; e < 4; e++) {
-            float h, l;
-            split_tf32(ok ? xs[e] : 0.0f, h, l);
-            const int off = sw_off(m0 + e, k);
-            *reinterpret_cast<float*>(ahi + off) = h;
-            *reinterpret_cast<float*>(alo + off) = l;
+            const int kg = kbase + kc * 4 + e;
+            split_tf32((kg >= a.k_lo && kg < a.Kv) ? src[e * TBM] : 0.0f, h[e], l[e]);
           }
+          const int off = sw_off(r, kc * 4);
+          *reinterpret_cast<float4*>(ahi + off) = make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(alo + off) = make_float4(l[0], l[1], l[2], l[3]);
         }
       }
       // generic-proxy smem writes -> the tensor core's async proxy
