@@ -1,4 +1,5 @@
 // extern "C" entry points of librandqr_b200.so (declared in include/randqr_b200.h).
+#include <algorithm>
 #include <new>
 
 #include "driver.cuh"
@@ -465,6 +466,13 @@ int rq_gemm_f32(rq_ctx* ctx, int32_t a_mmajor, int64_t M, int64_t N, int64_t K, 
   p.alpha = alpha;
   p.beta = beta;
   p.max_ctas = ctx->c.gemm_cap;
+  // split-K slabs: up to 16 partial M x N products, from the context's step-API arena
+  const size_t kb = std::min<size_t>((size_t)16 * M * N * sizeof(float), (size_t)1 << 30);
+  if (K >= 4096 && rq::ceil_div(M, 128) * rq::ceil_div(N, 128) < 4 * rq::kSMs) {
+    RQ_TRY(ctx->c.sarena.reserve(kb));
+    p.work = static_cast<float*>(ctx->c.sarena.base);
+    p.work_bytes = kb;
+  }
   return rq::gemm_tf32x3(p, ctx->c.stream, &ctx->c.launches);
 }
 

@@ -49,8 +49,10 @@ struct TArgs {
   int64_t ldc;
   float alpha, beta;
   int tiles_m, tiles;
-  int kblocks;
-  int four;  // 1: also A_lo B_lo (4 products; tuning / accuracy probe)
+  int kblocks;  // k-blocks per unit (a split's range; the last split's tail reads zeros)
+  int splits;   // units = tiles * splits; > 1: partial sums into work slabs, then a reduce
+  float* work;  // splits x (M x N), ld = M
+  int four;     // 1: also A_lo B_lo (4 products; tuning / accuracy probe)
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -133,11 +135,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = (uint32_t*)(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // persistent: this CTA's tiles blockIdx.x, blockIdx.x + gridDim.x, ...; one stream of
-  // (tile, k-block) steps g = j * kblocks + kb through every pipeline
-  const int my_tiles = a.tiles > (int)blockIdx.x ? (a.tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
-  const int G = my_tiles * a.kblocks;
-  auto tile_of = [&](int g) { return (int)blockIdx.x + (g / a.kblocks) * (int)gridDim.x; };
+  // persistent: this CTA's units blockIdx.x, blockIdx.x + gridDim.x, ... (unit = tile x split);
+  // one stream of (unit, k-block) steps g = j * kblocks + kb through every pipeline
+  const int units = a.tiles * a.splits;
+  const int my_units = units > (int)blockIdx.x ? (units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  const int G = my_units * a.kblocks;
+  auto unit_of = [&](int g) { return (int)blockIdx.x + (g / a.kblocks) * (int)gridDim.x; };
+  auto tile_of = [&](int g) { return unit_of(g) / a.splits; };
+  auto kb_of = [&](int g) { return (unit_of(g) % a.splits) * a.kblocks + g % a.kblocks; };  // global k-block
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRawStages; s++) {
@@ -168,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       for (int g = 0; g < G; g++) {
-        const int t = tile_of(g), kb = g % a.kblocks;
+        const int t = tile_of(g), kb = kb_of(g);
         const int tm = t % a.tiles_m, tn = t / a.tiles_m;
         const int s = g % kRawStages;
         bar_wait(&raw_empty[s], ((g / kRawStages) & 1) ^ 1);
@@ -240,28 +245,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       bar_arrive(&acc_empty[s]);
     };
-    // registers -> C for tile t (the tensor core already works on the next tile)
-    auto epilogue = [&](int t) {
+    // registers -> C, or the unit's split-K slab (alpha = 1, beta = 0, ld = M), for unit u (the
+    // tensor core already works on the next unit)
+    auto epilogue = [&](int u) {
+      const int t = u / a.splits, sp = u % a.splits;
       const int tm = t % a.tiles_m, tn = t / a.tiles_m;
       const int m = tm * TBM + q * 32 + lane;
-      if (m >= a.m_lo && m < a.M) {
-        float* cbase = a.C + (int64_t)(tn * TBN + h0) * a.ldc + m;
+      const bool slab = a.splits > 1;
+      const int64_t ld = slab ? (int64_t)a.M : a.ldc;
+      const float alpha = slab ? 1.0f : a.alpha, beta = slab ? 0.0f : a.beta;
+      if (m >= (slab ? 0 : a.m_lo) && m < a.M) {
+        float* cbase = (slab ? a.work + (int64_t)sp * a.M * a.N : a.C) + (int64_t)(tn * TBN + h0) * ld + m;
         const int nv = min(kHalf, a.N - tn * TBN - h0);
 #pragma unroll
         for (int gq = 0; gq < kHalf / 16; gq++) {
           // 16 independent loads of C first (the stores below could alias them), then 16 stores
           float cv[16];
-          if (a.beta != 0.0f) {
+          if (beta != 0.0f) {
 #pragma unroll
             for (int j = 0; j < 16; j++)
-              cv[j] = (gq * 16 + j < nv) ? __ldcs(cbase + (int64_t)(gq * 16 + j) * a.ldc) : 0.0f;
+              cv[j] = (gq * 16 + j < nv) ? __ldcs(cbase + (int64_t)(gq * 16 + j) * ld) : 0.0f;
           }
 #pragma unroll
           for (int j = 0; j < 16; j++) {
             if (gq * 16 + j < nv) {
-              float v = a.alpha * accr[gq * 16 + j];
-              if (a.beta != 0.0f) v = fmaf(a.beta, cv[j], v);
-              __stcs(cbase + (int64_t)(gq * 16 + j) * a.ldc, v);
+              float v = alpha * accr[gq * 16 + j];
+              if (beta != 0.0f) v = fmaf(beta, cv[j], v);
+              __stcs(cbase + (int64_t)(gq * 16 + j) * ld, v);
             }
           }
         }
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       unsigned char* alo = ahi + kTile;
       unsigned char* bhi = ahi + 2 * kTile;
       unsigned char* blo = ahi + 3 * kTile;
-      const int kbase = (g % a.kblocks) * TBK;
+      const int kbase = kb_of(g) * TBK;
       // B (and a K-major A): the raw tile already has the target layout
 #pragma unroll
       for (int t = 0; t < 1024 / kConvThreads; t++) {
@@ -338,12 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       bar_arrive(&conv_full[s]);
       if (g > 0) {  // (the tensor core works on step g meanwhile)
         drain(g - 1);
-        if ((g - 1) % a.kblocks == a.kblocks - 1) epilogue(tile_of(g - 1));
+        if ((g - 1) % a.kblocks == a.kblocks - 1) epilogue(unit_of(g - 1));
       }
     }
     if (G > 0) {
       drain(G - 1);
-      epilogue(tile_of(G - 1));
+      epilogue(unit_of(G - 1));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -352,6 +362,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  }
+}
+
+// Deterministic split-K reduction: C = alpha * sum_s work_s + beta * C (fixed s order).
+__global__ void splitk_reduce_f32_kernel(const float* __restrict__ work, int splits, int M, int N, float* C,
+                                         int64_t ldc, float alpha, float beta, int m_lo) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(idx % M), n = (int)(idx / M);
+    if (m < m_lo) continue;
+    float s = 0.0f;
+    for (int k = 0; k < splits; k++) s += __ldcg(work + k * total + idx);
+    float* c = C + (int64_t)n * ldc + m;
+    float v = alpha * s;
+    if (beta != 0.0f) v = fmaf(beta, *c, v);
+    *c = v;
   }
 }
 
@@ -431,7 +458,7 @@ int launch(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
   a.beta = (float)p.beta;
   a.tiles_m = (int)ceil_div(a.M, TBM);
   const int tiles_n = (int)ceil_div(a.N, TBN);
-  a.kblocks = (int)ceil_div(a.Kv, TBK);
+  const int kb_total = (int)ceil_div(a.Kv, TBK);
   static const int env_four = getenv("RQ_TF32X4") ? atoi(getenv("RQ_TF32X4")) : 0;
   a.four = env_four;
   const int64_t tiles = (int64_t)a.tiles_m * tiles_n;
@@ -445,10 +472,36 @@ int launch(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
     if (sms <= 0) sms = kSMs;
   }
   const int cap = p.max_ctas > 0 ? std::min(p.max_ctas, sms) : sms;  // persistent: <= one CTA per SM
-  const int grid = (int)std::min<int64_t>(tiles, cap);
+  // split-K when the tiles fill the grid poorly (wave efficiency), K is long enough and the
+  // context's workspace holds the slabs
+  auto eff = [&](int64_t u) { return (double)u / (double)(ceil_div(u, cap) * cap); };
+  int splits = 1;
+  double best = eff(tiles);
+  if (p.work && best < 0.9 && tiles < 4 * cap) {
+    for (int sp = 2; sp <= 16; sp++) {
+      if (kb_total / sp < 4) break;
+      if ((size_t)sp * a.M * a.N * sizeof(float) > p.work_bytes) break;
+      const double e = eff(tiles * sp) * (1.0 - 0.02 * sp);
+      if (e > best + 0.03) {
+        best = e;
+        splits = sp;
+      }
+    }
+  }
+  a.splits = splits;
+  a.kblocks = (int)ceil_div(kb_total, splits);
+  a.work = p.work;
+  const int grid = (int)std::min<int64_t>(tiles * splits, cap);
   kern<<<grid, kThreads, kSmem, st>>>(ma, mb, a);
   RQ_CUDA_TRY(cudaGetLastError());
   if (launches) (*launches)++;
+  if (splits > 1) {
+    const int64_t total = (int64_t)a.M * a.N;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * sms);
+    splitk_reduce_f32_kernel<<<blocks, 256, 0, st>>>(a.work, splits, a.M, a.N, a.C, a.ldc, a.alpha, a.beta, a.m_lo);
+    RQ_CUDA_TRY(cudaGetLastError());
+    if (launches) (*launches)++;
+  }
   return RQ_OK;
 }
 

@@ -22,6 +22,8 @@ struct GemmProblemF32 {
   int64_t ldc;
   double alpha, beta;
   int max_ctas = 0;  // > 0: cap the persistent grid (leave SMs to a concurrent kernel)
+  float* work = nullptr;  // split-K slabs (deterministic reduction); null: no split-K
+  size_t work_bytes = 0;
 };
 
 int gemm_tf32x3(const GemmProblemF32& p, cudaStream_t st, int64_t* launches);
