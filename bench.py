@@ -47,6 +47,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 36.96  # measured DMMA m16n8k4 peak on this pool's B200 (profiles/probe_r01.jsonl)
+TF32X3_PEAK_TFLOPS = 1100.0 / 3  # nominal dense TF32 / 3 split products (B200_PROFILING.md; not measured)
 CATS = ["trailing_gemm", "other_gemm", "sketch_cpqr", "panel_leaf", "other", "small_cpqr", "sketch_gemm",
         "panel_gemm", "tfactor", "moves", "copy2d", "rng", "splitk_reduce"]
 BW_CATS = {"moves": 9, "copy2d": 10, "rng": 11, "splitk_reduce": 12}
@@ -205,7 +206,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def device_time_n(eng, lib, check, torch, stream, n, b, p, mode, pk, steps=None):
+def device_time_n(eng, lib, check, torch, stream, n, b, p, mode, pk, steps=None, flags=0):
     """One n x n factorization per step on the device (A resident, pristine copy per step)."""
     import paper_1505_08115_b200 as rq
     from paper_1505_08115_b200 import _lib
@@ -215,7 +216,7 @@ def device_time_n(eng, lib, check, torch, stream, n, b, p, mode, pk, steps=None)
         a0, ld = rq.gaussian_matrix_device(n, n, rq.RngState(0), engine=eng)
         work = torch.empty_like(a0)
         perm = torch.empty(n, dtype=torch.int64, device=eng.device)
-    cfg = _lib.rq_config(b, p, 0, -1, pk, 0, mode, 0)
+    cfg = _lib.rq_config(b, p, 0, -1, pk, 0, mode, flags)
 
     def step():
         with torch.cuda.stream(stream):
@@ -456,7 +457,10 @@ def main():
     ap.add_argument("--q", type=int, default=0, help="power iterations of the sketch")
     ap.add_argument("--dist", action="store_true", help="use the block-cyclic multi-GPU driver even at N = 1")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
-                    help="f32: cfg 3's fp32 variant (fp32 storage and GEMMs, fp64 serial kernels; fp32.py)")
+                    help="f32: cfg 3's fp32 variant -- the monolithic driver with the trailing-update GEMMs as "
+                         "tcgen05 3xTF32 products (RQ_FLAG_TF32_UPDATE); --f32-steps: fp32 storage through the "
+                         "panel-step driver (fp32.py)")
+    ap.add_argument("--f32-steps", action="store_true")
     ap.add_argument("--matrix", default="gauss", choices=["gauss", "cfg4"],
                     help="gauss: N(0,1) (cfg 3); cfg4: U diag(max(10^(-12j/2000),1e-15)) V^T")
     args = ap.parse_args()
@@ -468,7 +472,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if args.dtype == "f32":
+    if args.dtype == "f32" and args.f32_steps:
         run_fp32(args, local)
         return
 
@@ -521,7 +525,9 @@ def main():
         args.sketch = "fresh"  # reflector pivots / block_rrqr: the reference's fresh sketches only
     mode = _lib.RQ_SKETCH_FRESH if args.sketch == "fresh" else _lib.RQ_SKETCH_DOWNDATE
     pk = _lib.RQ_PIVOT_PERMUTATION if args.method == "m1" else _lib.RQ_PIVOT_REFLECTORS
-    cfg = _lib.rq_config(b, p, args.q, -1, pk, 1 if args.method == "m3" else 0, mode, 0)
+    f32 = args.dtype == "f32"
+    cfg = _lib.rq_config(b, p, args.q, -1, pk, 1 if args.method == "m3" else 0, mode,
+                         _lib.RQ_FLAG_TF32_UPDATE if f32 else 0)
     if args.method != "m1":
         args.no_variant = True  # the downdated sketch applies to permutation pivots only
 
@@ -592,7 +598,8 @@ def main():
     if args.per_n and args.method == "m1" and args.matrix == "gauss" and world == 1:
         per_n = {}
         for n_big in [int(x) for x in args.per_n.split(",") if x]:
-            per_n[str(n_big)] = device_time_n(eng, lib, check, torch, stream, n_big, b, p, mode, pk)
+            per_n[str(n_big)] = device_time_n(eng, lib, check, torch, stream, n_big, b, p, mode, pk,
+                                              flags=cfg.flags)
         torch.cuda.synchronize()
 
     # dominant kernel roofline: the trailing-update DMMA GEMMs
@@ -644,9 +651,13 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if not f32 else "fp32 TFLOP/s (4/3·n³ count) for HQRRP, cfg 3 fp32 variant",
+            "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if not f32 else "f32 (trailing-update GEMMs: tcgen05 3xTF32, fp32 accumulation; "
+                                          "panels / sketch / pivots fp64)",
+            "data": "synthetic",
             "config": {"workload": (f"cfg3 HQRRP fp64 n={n} b={b} p={p} q={args.q}, {args.sketch} sketch"
                                     + (" (reference semantics)" if args.sketch == "fresh" else " (HQRRP downdate)"))
                                    if args.method == "m1" else
@@ -656,15 +667,21 @@ def main():
                        "matrix": args.matrix,
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "inputs (800 MB) larger than L2 (126 MB)"},
-            "fraction_of_fp64_peak": value / FP64_PEAK_TFLOPS,
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
-                         # ncu --set full, one A2 -= V W2 launch (n = 10000, K = b = 256):
-                         # dram read + write vs 1.640e9 algorithmic bytes (profiles/ncu_gemm_nn_r01.txt)
-                         "traffic": 1.6466e9 if n == 10000 and b == 256 else None,
-                         "traffic_note": "bytes per launch of A2 -= V W2 at panel 1; algorithmic 1.640e9",
-                         "kernel": "gemm_f64_kernel (trailing update: V^T A2, T^T W, A2 -= V W2, Q2^T top)",
-                         "peak_source": "measured DMMA peak, profiles/probe_r01.jsonl"},
+            "fraction_of_fp64_peak": value / FP64_PEAK_TFLOPS if not f32 else None,
+            "roofline": ({"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                          "frac": (achieved / FP64_PEAK_TFLOPS) if achieved else None,
+                          # ncu --set full, one A2 -= V W2 launch (n = 10000, K = b = 256):
+                          # dram read + write vs 1.640e9 algorithmic bytes (profiles/ncu_gemm_nn_r01.txt)
+                          "traffic": 1.6466e9 if n == 10000 and b == 256 else None,
+                          "traffic_note": "bytes per launch of A2 -= V W2 at panel 1; algorithmic 1.640e9",
+                          "kernel": "gemm_f64_kernel (trailing update: V^T A2, T^T W, A2 -= V W2, Q2^T top)",
+                          "peak_source": "measured DMMA peak, profiles/probe_r01.jsonl"} if not f32 else
+                         {"bound": "tensor", "achieved": achieved, "peak": TF32X3_PEAK_TFLOPS, "unit": "TFLOP/s",
+                          "frac": (achieved / TF32X3_PEAK_TFLOPS) if achieved else None, "traffic": None,
+                          "kernel": "gemm_tf32x3_kernel<double> (trailing update on tcgen05, 3 TF32 products "
+                                    "per 2MNK flop)",
+                          "peak_source": "B200 nominal dense TF32 1.1 PFLOP/s (B200_PROFILING.md) / 3 products; "
+                                         "MEASURED_PEAKS.json has no TF32 entry"}),
             "breakdown_ms_per_step": cats,
             "breakdown_note": "one separate profiled step (CUDA events per launch); classes overlap in time "
                               "(W = V^T A2 and T run beside the b x b CPQR)",

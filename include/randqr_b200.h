@@ -61,6 +61,10 @@ typedef struct rq_config {
  * look-ahead (each panel's trailing update completes before the next panel's sketch
  * CPQR); results are identical, only the schedule differs. */
 #define RQ_FLAG_NO_LOOKAHEAD 1
+/* rq_config.flags: RQ_FLAG_TF32_UPDATE runs the trailing-update GEMMs (the dominant flops) at fp32
+ * accuracy on the tcgen05 tensor cores (3xTF32, fp32 accumulation) instead of FP64 DMMA; panels,
+ * sketches and pivot selection stay fp64.  The fp32 path of BASELINE cfg 3 (accuracy ~1e-6). */
+#define RQ_FLAG_TF32_UPDATE 2
 
 /* Called after each completed panel (the reference's `inspect` hook,
  * blocked.py:184-185, :215-216); the callee may call rq_snapshot(). */

@@ -19,6 +19,7 @@ RQ_OK, RQ_EDIM, RQ_EVALUE, RQ_ECONV, RQ_ECUDA, RQ_EINTERNAL, RQ_EUNSUPPORTED = r
 RQ_PIVOT_PERMUTATION, RQ_PIVOT_REFLECTORS = 0, 1
 RQ_SKETCH_FRESH, RQ_SKETCH_DOWNDATE = 0, 1
 RQ_FLAG_NO_LOOKAHEAD = 1
+RQ_FLAG_TF32_UPDATE = 2
 
 
 class rq_config(ctypes.Structure):

@@ -118,7 +118,10 @@ int rq_factorize(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, double
     return rq::set_error(RQ_EUNSUPPORTED, "the downdated sketch applies to permutation pivots");
   if (cfg->sketch_mode == RQ_SKETCH_DOWNDATE && cfg->power != 0)
     return rq::set_error(RQ_EUNSUPPORTED, "downdate sketch with power iterations");
-  return ctx->c.factorize_perm(*cfg, m, n, dA, lda, seed, counter, dperm);
+  ctx->c.tf32_update = (cfg->flags & RQ_FLAG_TF32_UPDATE) != 0;
+  const int rc = ctx->c.factorize_perm(*cfg, m, n, dA, lda, seed, counter, dperm);
+  ctx->c.tf32_update = false;
+  return rc;
 }
 
 int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, const double* hA, int64_t lda,

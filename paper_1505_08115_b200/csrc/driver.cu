@@ -20,6 +20,7 @@
 
 #include "driver.cuh"
 #include "gemm_f64.cuh"
+#include "gemm_tf32.cuh"
 #include "misc.cuh"
 #include "panel.cuh"
 
@@ -284,6 +285,7 @@ int Ctx::gemm_raw(int64_t M, int64_t N, int64_t K, const GemmOperand& A, bool a_
   p.pdl = gemm_pdl;
   p.mid_event = gemm_mid;
   p.splitk_used = gemm_mid ? &gemm_splitk : nullptr;
+  if (tf32_update && cat == PROF_TRAIL) return gemm_tf32x3_f64(p, stream, &launches);
   RQ_TRY(sched_for(stream, &p.sched, &p.sched_base));
   return gemm_f64(p, stream, &launches);
 }
@@ -400,7 +402,7 @@ int Ctx::la_chunk(int64_t upto, bool beside_leaf) {
     //  breakdown is taken from a separate step, never from the timed ones)
     cudaEvent_t e0;
     prof_begin(&e0);
-    const int rc = gemm_f64(p, stream, &launches);
+    const int rc = tf32_update ? gemm_tf32x3_f64(p, stream, &launches) : gemm_f64(p, stream, &launches);
     prof_end(e0, 2.0 * (double)p.M * (double)p.N * (double)p.K * (double)(upto - la.next) / (double)la.tiles);
     RQ_TRY(rc);
     la.next = upto;
@@ -1371,7 +1373,7 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
   g.ldc = lda;
   g.alpha = -1.0;
   g.beta = 1.0;
-  la.tiles = g.N > 0 ? gemm_f64_tiles(g) : 0;
+  la.tiles = g.N > 0 ? (tf32_update ? gemm_tf32x3_tiles(g.M, g.N, g.a_mmajor, g.A.r0) : gemm_f64_tiles(g)) : 0;
   la.next = 0;
   la.on = la.tiles > 0;
   return RQ_OK;

@@ -160,6 +160,7 @@ struct Ctx {
   // writes them (rq_factorize_host streams them to the host while later panels compute)
   std::function<void(int64_t, int64_t)> on_cols_final;
   int gemm_max_ctas = 0;
+  bool tf32_update = false;  // RQ_FLAG_TF32_UPDATE: trailing-update GEMMs on the tcgen05 3xTF32 kernel
   int gemm_cap = 0;  // rq_ctx_set_gemm_cap: default grid cap of this context's GEMMs (0 = none)
   bool gemm_pdl = false;
   cudaEvent_t gemm_mid = nullptr;  // profiling: split-K reduce boundary of the current GEMM

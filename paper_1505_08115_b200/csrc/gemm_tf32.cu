@@ -32,26 +32,43 @@ namespace rq {
 
 namespace {
 
-constexpr int TBM = 128, TBN = 128, TBK = 32;
-constexpr int kTile = TBM * TBK * 4;      // 16 KB: one 128 x 32 fp32 tile
+constexpr int TBM = 128, TBN = 128;
+constexpr int kRawTile = 16384;           // one raw operand tile: 128 rows x 128 B (TMA box)
 constexpr int kRawStages = 3, kConvStages = 2;
 constexpr int kThreads = 320;             // warps 0 (TMA), 1 (MMA), 2-9 (convert + drain + epilogue)
 constexpr int kConvThreads = 256;
 constexpr int kHalf = TBN / 2;            // accumulator columns per converter thread
-constexpr int kSmem = kRawStages * 2 * kTile + kConvStages * 4 * kTile + 1024 + 256;
-static_assert(kSmem <= 232448, "shared memory per CTA");
+
+// Per input type: k-block depth (one 128-byte TMA row of the raw operand), and the converted
+// tf32 tiles' K-major swizzle (rows of BK tf32: 128 B -> SWIZZLE_128B, 64 B -> SWIZZLE_64B).
+template <typename T>
+struct TfCfg;
+template <>
+struct TfCfg<float> {
+  static constexpr int BK = 32, ROWB = 128, LAYOUT = 2, SBO = 1024;
+};
+template <>
+struct TfCfg<double> {
+  static constexpr int BK = 16, ROWB = 64, LAYOUT = 4, SBO = 512;
+};
+template <typename T>
+constexpr int conv_tile() { return TBM * TfCfg<T>::BK * 4; }
+template <typename T>
+constexpr int smem_bytes() { return kRawStages * 2 * kRawTile + kConvStages * 4 * conv_tile<T>() + 1024 + 256; }
+static_assert(smem_bytes<float>() <= 232448 && smem_bytes<double>() <= 232448, "shared memory per CTA");
 
 struct TArgs {
   int M, N, Kv;        // output extent (M includes m_lo padding rows), valid k range [k_lo, Kv)
   int k_lo, m_lo;
   int a_c0, a_c1, b_c0, b_c1;
-  float* C;
+  void* C;             // fp32 or fp64 (the input type)
   int64_t ldc;
   float alpha, beta;
   int tiles_m, tiles;
   int kblocks;  // k-blocks per unit (a split's range; the last split's tail reads zeros)
   int splits;   // units = tiles * splits; > 1: partial sums into work slabs, then a reduce
   float* work;  // splits x (M x N), ld = M
+  int u0;       // first unit (a tile-range chunk of a larger GEMM: tiles u0 .. u0 + tiles - 1)
   int four;     // 1: also A_lo B_lo (4 products; tuning / accuracy probe)
 };
 
@@ -81,11 +98,12 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* m, uint64_t*
       : "memory");
 }
 
-// K-major SWIZZLE_128B shared-memory matrix descriptor (sm100 layout type 2, version 1): rows of
-// 128 B (32 fp32 along K), 8-row atoms 1024 B apart (stride byte offset).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+// K-major swizzled shared-memory matrix descriptor (sm100, version 1): SWIZZLE_128B (layout type 2,
+// 128-byte rows, 8-row atoms 1024 B apart) or SWIZZLE_64B (type 4, 64-byte rows, atoms 512 B apart)
+template <int LAYOUT, int SBO>
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(SBO >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)LAYOUT << 61);
 }
 // kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = 128
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
@@ -102,13 +120,27 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// byte offset of element (row r, k) in a 128-row x 32-k K-major SWIZZLE_128B tile
+// byte offset of tf32 element (row r, k) in a 128-row K-major swizzled tile: 16-byte chunk c of
+// row r sits at chunk c ^ (r & 7) (128-byte rows) or c ^ ((r >> 1) & 3) (64-byte rows)
+template <int ROWB>
 __device__ __forceinline__ int sw_off(int r, int k) {
-  return (r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ (r & 7))) << 4) + ((k & 3) << 2);
+  if constexpr (ROWB == 128)
+    return (r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ (r & 7))) << 4) + ((k & 3) << 2);
+  else
+    return (r >> 3) * 512 + (r & 7) * 64 + ((((k >> 2) ^ ((r >> 1) & 3))) << 4) + ((k & 3) << 2);
 }
 
 // hi = x rounded to TF32 (nearest, ties away), lo = (x - hi) rounded to TF32: both exactly
 // representable, so the tensor core's TF32 read loses nothing; |x - hi - lo| <= 2^-23 |x|
+__device__ __forceinline__ void split_tf32(double xd, float& hi, float& lo) {
+  const float x = (float)xd;  // fp32-level accuracy: the fp64 input rounded once
+  uint32_t h, l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  const float r = x - __uint_as_float(h);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+  hi = __uint_as_float(h);
+  lo = __uint_as_float(l);
+}
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   uint32_t h, l;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
@@ -118,14 +150,17 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   lo = __uint_as_float(l);
 }
 
-template <bool A_MMAJOR>
+template <typename T, bool A_MMAJOR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb, const TArgs a) {
+  using Cfg = TfCfg<T>;
+  constexpr int BK = Cfg::BK;
+  constexpr int kConv = conv_tile<T>();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* raw = sm;                                   // [stage][A, B] 16 KB each
-  unsigned char* conv = sm + kRawStages * 2 * kTile;         // [stage][Ahi, Alo, Bhi, Blo]
-  uint64_t* bars = (uint64_t*)(conv + kConvStages * 4 * kTile);
+  unsigned char* conv = sm + kRawStages * 2 * kRawTile;      // [stage][Ahi, Alo, Bhi, Blo]
+  uint64_t* bars = (uint64_t*)(conv + kConvStages * 4 * kConv);
   uint64_t* raw_full = bars;        // [kRawStages]
   uint64_t* raw_empty = bars + 4;   // [kRawStages]
   uint64_t* conv_full = bars + 8;   // [2]
@@ -137,10 +172,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // persistent: this CTA's units blockIdx.x, blockIdx.x + gridDim.x, ... (unit = tile x split);
   // one stream of (unit, k-block) steps g = j * kblocks + kb through every pipeline
-  const int units = a.tiles * a.splits;
+  const int units = a.tiles * a.splits;  // (relative to u0)
   const int my_units = units > (int)blockIdx.x ? (units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
   const int G = my_units * a.kblocks;
-  auto unit_of = [&](int g) { return (int)blockIdx.x + (g / a.kblocks) * (int)gridDim.x; };
+  auto unit_of = [&](int g) { return a.u0 + (int)blockIdx.x + (g / a.kblocks) * (int)gridDim.x; };
   auto tile_of = [&](int g) { return unit_of(g) / a.splits; };
   auto kb_of = [&](int g) { return (unit_of(g) % a.splits) * a.kblocks + g % a.kblocks; };  // global k-block
 
@@ -177,14 +212,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int tm = t % a.tiles_m, tn = t / a.tiles_m;
         const int s = g % kRawStages;
         bar_wait(&raw_empty[s], ((g / kRawStages) & 1) ^ 1);
-        bar_expect_tx(&raw_full[s], 2 * kTile);
-        unsigned char* ra = raw + (s * 2) * kTile;
-        unsigned char* rb = raw + (s * 2 + 1) * kTile;
+        bar_expect_tx(&raw_full[s], 2 * kRawTile);
+        unsigned char* ra = raw + (s * 2) * kRawTile;
+        unsigned char* rb = raw + (s * 2 + 1) * kRawTile;
         if (A_MMAJOR)
-          tma2d(ra, &ma, &raw_full[s], a.a_c0 + tm * TBM, a.a_c1 + kb * TBK);
+          tma2d(ra, &ma, &raw_full[s], a.a_c0 + tm * TBM, a.a_c1 + kb * BK);
         else
-          tma2d(ra, &ma, &raw_full[s], a.a_c0 + kb * TBK, a.a_c1 + tm * TBM);
-        tma2d(rb, &mb, &raw_full[s], a.b_c0 + kb * TBK, a.b_c1 + tn * TBN);
+          tma2d(ra, &ma, &raw_full[s], a.a_c0 + kb * BK, a.a_c1 + tm * TBM);
+        tma2d(rb, &mb, &raw_full[s], a.b_c0 + kb * BK, a.b_c1 + tn * TBN);
       }
     }
   } else if (warp == 1) {
@@ -198,16 +233,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         bar_wait(&conv_full[s], (g >> 1) & 1);
         bar_wait(&acc_empty[s], ((g >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t base = s_u32(conv + (s * 4) * kTile);
-        const uint32_t ahi = base, alo = base + kTile, bhi = base + 2 * kTile, blo = base + 3 * kTile;
+        const uint32_t base = s_u32(conv + (s * 4) * kConv);
+        const uint32_t ahi = base, alo = base + kConv, bhi = base + 2 * kConv, blo = base + 3 * kConv;
         const uint32_t acc = tmem + (uint32_t)(s * TBN);
+        constexpr int L = Cfg::LAYOUT, SB = Cfg::SBO;
 #pragma unroll
-        for (int kk = 0; kk < TBK / 8; kk++) {  // 8 tf32 (32 B) per MMA along K
+        for (int kk = 0; kk < BK / 8; kk++) {  // 8 tf32 (32 B) per MMA along K
           const uint32_t o = kk * 32;
-          umma_tf32(acc, sw128_desc(ahi + o), sw128_desc(bhi + o), kk != 0);
-          umma_tf32(acc, sw128_desc(ahi + o), sw128_desc(blo + o), 1u);
-          umma_tf32(acc, sw128_desc(alo + o), sw128_desc(bhi + o), 1u);
-          if (a.four) umma_tf32(acc, sw128_desc(alo + o), sw128_desc(blo + o), 1u);
+          umma_tf32(acc, sw_desc<L, SB>(ahi + o), sw_desc<L, SB>(bhi + o), kk != 0);
+          umma_tf32(acc, sw_desc<L, SB>(ahi + o), sw_desc<L, SB>(blo + o), 1u);
+          umma_tf32(acc, sw_desc<L, SB>(alo + o), sw_desc<L, SB>(bhi + o), 1u);
+          if (a.four) umma_tf32(acc, sw_desc<L, SB>(alo + o), sw_desc<L, SB>(blo + o), 1u);
         }
         umma_commit(&conv_empty[s]);  // the stage's smem is free once these MMAs completed
         umma_commit(&acc_full[s]);
@@ -245,33 +281,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       bar_arrive(&acc_empty[s]);
     };
-    // registers -> C, or the unit's split-K slab (alpha = 1, beta = 0, ld = M), for unit u (the
-    // tensor core already works on the next unit)
+    // registers -> C, or the unit's split-K slab (fp32, ld = M), for unit u (the tensor core
+    // already works on the next unit)
     auto epilogue = [&](int u) {
       const int t = u / a.splits, sp = u % a.splits;
       const int tm = t % a.tiles_m, tn = t / a.tiles_m;
       const int m = tm * TBM + q * 32 + lane;
-      const bool slab = a.splits > 1;
-      const int64_t ld = slab ? (int64_t)a.M : a.ldc;
-      const float alpha = slab ? 1.0f : a.alpha, beta = slab ? 0.0f : a.beta;
-      if (m >= (slab ? 0 : a.m_lo) && m < a.M) {
-        float* cbase = (slab ? a.work + (int64_t)sp * a.M * a.N : a.C) + (int64_t)(tn * TBN + h0) * ld + m;
-        const int nv = min(kHalf, a.N - tn * TBN - h0);
+      const int nv = min(kHalf, a.N - tn * TBN - h0);
+      if (a.splits > 1) {
+        if (m < a.M) {
+          float* w = a.work + (int64_t)sp * a.M * a.N + (int64_t)(tn * TBN + h0) * a.M + m;
 #pragma unroll
-        for (int gq = 0; gq < kHalf / 16; gq++) {
-          // 16 independent loads of C first (the stores below could alias them), then 16 stores
-          float cv[16];
-          if (beta != 0.0f) {
+          for (int j = 0; j < kHalf; j++)
+            if (j < nv) __stcg(w + (int64_t)j * a.M, accr[j]);
+        }
+      } else if (m >= a.m_lo && m < a.M) {
+        T* cbase = static_cast<T*>(a.C) + (int64_t)(tn * TBN + h0) * a.ldc + m;
 #pragma unroll
-            for (int j = 0; j < 16; j++)
-              cv[j] = (gq * 16 + j < nv) ? __ldcs(cbase + (int64_t)(gq * 16 + j) * ld) : 0.0f;
+        for (int gq = 0; gq < kHalf / 8; gq++) {
+          // 8 independent loads of C first (the stores below could alias them), then 8 stores
+          T cv[8];
+          if (a.beta != 0.0f) {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+              cv[j] = (gq * 8 + j < nv) ? __ldcs(cbase + (int64_t)(gq * 8 + j) * a.ldc) : T(0);
           }
 #pragma unroll
-          for (int j = 0; j < 16; j++) {
-            if (gq * 16 + j < nv) {
-              float v = alpha * accr[gq * 16 + j];
-              if (beta != 0.0f) v = fmaf(beta, cv[j], v);
-              __stcs(cbase + (int64_t)(gq * 16 + j) * ld, v);
+          for (int j = 0; j < 8; j++) {
+            if (gq * 8 + j < nv) {
+              T v = (T)a.alpha * (T)accr[gq * 8 + j];
+              if (a.beta != 0.0f) v = fma((T)a.beta, cv[j], v);
+              __stcs(cbase + (int64_t)(gq * 8 + j) * a.ldc, v);
             }
           }
         }
@@ -284,60 +324,73 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ph = (g >> 1) & 1;
       bar_wait(&raw_full[rs], (g / kRawStages) & 1);
       bar_wait(&conv_empty[s], ph ^ 1);
-      const unsigned char* ra = raw + (rs * 2) * kTile;
-      const unsigned char* rb = raw + (rs * 2 + 1) * kTile;
-      unsigned char* ahi = conv + (s * 4) * kTile;
-      unsigned char* alo = ahi + kTile;
-      unsigned char* bhi = ahi + 2 * kTile;
-      unsigned char* blo = ahi + 3 * kTile;
-      const int kbase = kb_of(g) * TBK;
-      // B (and a K-major A): the raw tile already has the target layout
+      const unsigned char* ra = raw + (rs * 2) * kRawTile;
+      const unsigned char* rb = raw + (rs * 2 + 1) * kRawTile;
+      unsigned char* ahi = conv + (s * 4) * kConv;
+      unsigned char* alo = ahi + kConv;
+      unsigned char* bhi = ahi + 2 * kConv;
+      unsigned char* blo = ahi + 3 * kConv;
+      const int kbase = kb_of(g) * BK;
+      // K-major raw tiles (B, and A when it is K-major) were written by TMA with SWIZZLE_128B:
+      // 16-byte vector v holds row r = v / 8, chunk (v % 8) ^ (r % 8) of the 128-byte row
 #pragma unroll
       for (int t = 0; t < 1024 / kConvThreads; t++) {
         const int v = c + kConvThreads * t;  // 16-byte vector index 0..1023
         const int r = v >> 3;
-        const int k0 = (((v & 7) ^ (r & 7)) << 2);
-        float4 x = *reinterpret_cast<const float4*>(rb + v * 16);
-        float xs[4] = {x.x, x.y, x.z, x.w};
-        float h[4], l[4];
+        const int ch = (v & 7) ^ (r & 7);
+        if constexpr (sizeof(T) == 4) {
+          const int k0 = ch << 2;
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-          const int kg = kbase + k0 + e;
-          const float val = (kg >= a.k_lo && kg < a.Kv) ? xs[e] : 0.0f;
-          split_tf32(val, h[e], l[e]);
-        }
-        *reinterpret_cast<float4*>(bhi + v * 16) = make_float4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<float4*>(blo + v * 16) = make_float4(l[0], l[1], l[2], l[3]);
-        if (!A_MMAJOR) {
-          x = *reinterpret_cast<const float4*>(ra + v * 16);
-          float ys[4] = {x.x, x.y, x.z, x.w};
+          for (int opnd = 0; opnd < (A_MMAJOR ? 1 : 2); opnd++) {
+            const unsigned char* src = opnd == 0 ? rb : ra;
+            unsigned char* dh = opnd == 0 ? bhi : ahi;
+            unsigned char* dl = opnd == 0 ? blo : alo;
+            const float4 x = *reinterpret_cast<const float4*>(src + v * 16);
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+            float h[4], l[4];
 #pragma unroll
-          for (int e = 0; e < 4; e++) {
-            const int kg = kbase + k0 + e;
-            const float val = (kg >= a.k_lo && kg < a.Kv) ? ys[e] : 0.0f;
-            split_tf32(val, h[e], l[e]);
+            for (int e = 0; e < 4; e++) {
+              const int kg = kbase + k0 + e;
+              split_tf32((kg >= a.k_lo && kg < a.Kv) ? xs[e] : 0.0f, h[e], l[e]);
+            }
+            *reinterpret_cast<float4*>(dh + v * 16) = make_float4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<float4*>(dl + v * 16) = make_float4(l[0], l[1], l[2], l[3]);
           }
-          *reinterpret_cast<float4*>(ahi + v * 16) = make_float4(h[0], h[1], h[2], h[3]);
-          *reinterpret_cast<float4*>(alo + v * 16) = make_float4(l[0], l[1], l[2], l[3]);
+        } else {
+          const int k0 = ch << 1;  // two doubles -> two tf32 of a 64-byte converted row
+          const int off = sw_off<Cfg::ROWB>(r, k0);
+#pragma unroll
+          for (int opnd = 0; opnd < (A_MMAJOR ? 1 : 2); opnd++) {
+            const unsigned char* src = opnd == 0 ? rb : ra;
+            unsigned char* dh = opnd == 0 ? bhi : ahi;
+            unsigned char* dl = opnd == 0 ? blo : alo;
+            const double2 x = *reinterpret_cast<const double2*>(src + v * 16);
+            float h0, l0, h1, l1;
+            const int kg = kbase + k0;
+            split_tf32((kg >= a.k_lo && kg < a.Kv) ? x.x : 0.0, h0, l0);
+            split_tf32((kg + 1 >= a.k_lo && kg + 1 < a.Kv) ? x.y : 0.0, h1, l1);
+            *reinterpret_cast<float2*>(dh + off) = make_float2(h0, h1);
+            *reinterpret_cast<float2*>(dl + off) = make_float2(l0, l1);
+          }
         }
       }
       if (A_MMAJOR) {
-        // raw A: 32 k-rows of 128 contiguous m (no swizzle) -> K-major SWIZZLE_128B hi / lo.  Each
+        // raw A: BK k-rows of 128 contiguous m (no swizzle) -> K-major swizzled hi / lo.  Each
         // thread builds one 16-byte target chunk (row r, k = 4 kc .. 4 kc + 3): lanes take
         // consecutive rows, so the reads are consecutive words and the 16-byte stores of a
-        // quarter-warp land in 8 distinct swizzled chunks (no bank conflicts)
+        // quarter-warp land in distinct swizzled chunks
 #pragma unroll
-        for (int t = 0; t < 1024 / kConvThreads; t++) {
+        for (int t = 0; t < (TBM * BK / 4) / kConvThreads; t++) {
           const int v = c + kConvThreads * t;
           const int r = v & (TBM - 1), kc = v >> 7;
-          const float* src = reinterpret_cast<const float*>(ra) + (kc * 4) * TBM + r;
+          const T* src = reinterpret_cast<const T*>(ra) + (kc * 4) * TBM + r;
           float h[4], l[4];
 #pragma unroll
           for (int e = 0; e < 4; e++) {
             const int kg = kbase + kc * 4 + e;
-            split_tf32((kg >= a.k_lo && kg < a.Kv) ? src[e * TBM] : 0.0f, h[e], l[e]);
+            split_tf32((kg >= a.k_lo && kg < a.Kv) ? src[e * TBM] : T(0), h[e], l[e]);
           }
-          const int off = sw_off(r, kc * 4);
+          const int off = sw_off<Cfg::ROWB>(r, kc * 4);
           *reinterpret_cast<float4*>(ahi + off) = make_float4(h[0], h[1], h[2], h[3]);
           *reinterpret_cast<float4*>(alo + off) = make_float4(l[0], l[1], l[2], l[3]);
         }
@@ -366,8 +419,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // Deterministic split-K reduction: C = alpha * sum_s work_s + beta * C (fixed s order).
-__global__ void splitk_reduce_f32_kernel(const float* __restrict__ work, int splits, int M, int N, float* C,
-                                         int64_t ldc, float alpha, float beta, int m_lo) {
+template <typename T>
+__global__ void splitk_reduce_tf_kernel(const float* __restrict__ work, int splits, int M, int N, T* C, int64_t ldc,
+                                        float alpha, float beta, int m_lo) {
   const int64_t total = (int64_t)M * N;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -375,9 +429,9 @@ __global__ void splitk_reduce_f32_kernel(const float* __restrict__ work, int spl
     if (m < m_lo) continue;
     float s = 0.0f;
     for (int k = 0; k < splits; k++) s += __ldcg(work + k * total + idx);
-    float* c = C + (int64_t)n * ldc + m;
-    float v = alpha * s;
-    if (beta != 0.0f) v = fmaf(beta, *c, v);
+    T* c = C + (int64_t)n * ldc + m;
+    T v = (T)alpha * (T)s;
+    if (beta != 0.0f) v = fma((T)beta, *c, v);
     *c = v;
   }
 }
@@ -399,71 +453,46 @@ int encoder() {
   return rc;
 }
 
-int map_f32(CUtensorMap* map, const GemmOperandF32& op, uint32_t box0, uint32_t box1, bool swizzle) {
-  if (((uintptr_t)op.base & 15) != 0 || (op.ld & 3) != 0)
-    return set_error(RQ_EVALUE, "fp32 GEMM operand needs a 16-byte aligned base and ld % 4 == 0 (ld %lld)",
-                     (long long)op.ld);
-  cuuint64_t dims[2] = {(cuuint64_t)op.rows, (cuuint64_t)op.cols};
-  cuuint64_t strides[1] = {(cuuint64_t)op.ld * 4};
+// Input-type-independent description of one product (pointers of the input type).
+struct TfProblem {
+  int64_t M, N, K;
+  const void* a_base;
+  int64_t a_rows, a_cols, a_ld, a_r0, a_c0;
+  bool a_mmajor;
+  const void* b_base;
+  int64_t b_rows, b_cols, b_ld, b_r0, b_c0;
+  void* C;
+  int64_t ldc;
+  double alpha, beta;
+  int max_ctas;
+  float* work;
+  size_t work_bytes;
+  int64_t tile_begin, tile_end;  // tile_end > 0: only output tiles [tile_begin, tile_end), no split-K
+  bool pdl;
+};
+
+template <typename T>
+int map_t(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, uint32_t box0, uint32_t box1,
+          bool swizzle) {
+  constexpr int per16 = 16 / (int)sizeof(T);
+  if (((uintptr_t)base & 15) != 0 || (ld % per16) != 0)
+    return set_error(RQ_EVALUE, "tf32 GEMM operand needs a 16-byte aligned base and 16-byte strides (ld %lld)",
+                     (long long)ld);
+  cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(T)};
   cuuint32_t box[2] = {box0, box1};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_enc32(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(op.base), dims, strides, box, estr,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+  CUresult r = g_enc32(map, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                       const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
-    return set_error(RQ_ECUDA, "cuTensorMapEncodeTiled (fp32) failed (%d): %llu x %llu ld %lld", (int)r,
-                     (unsigned long long)op.rows, (unsigned long long)op.cols, (long long)op.ld);
+    return set_error(RQ_ECUDA, "cuTensorMapEncodeTiled (tf32 GEMM) failed (%d): %llu x %llu ld %lld", (int)r,
+                     (unsigned long long)rows, (unsigned long long)cols, (long long)ld);
   return RQ_OK;
 }
 
-template <bool A_MMAJOR>
-int launch(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
-  auto kern = gemm_tf32x3_kernel<A_MMAJOR>;
-  static bool attr = false;
-  if (!attr) {
-    RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    attr = true;
-  }
-  // TMA origins along a contiguous dimension are rounded down to 16 bytes (4 fp32); the
-  // converters zero the padding k's, the epilogue skips the padding rows.
-  const int kshift = (int)(p.B.r0 & 3);
-  if (!A_MMAJOR && (int)(p.A.r0 & 3) != kshift)
-    return set_error(RQ_EINTERNAL, "fp32 gemm: K origins of A (%lld) and B (%lld) differ mod 4", (long long)p.A.r0,
-                     (long long)p.B.r0);
-  const int ashift = A_MMAJOR ? (int)(p.A.r0 & 3) : 0;  // M-major A: pad rows of the output
-  CUtensorMap ma, mb;
-  if (A_MMAJOR)
-    RQ_TRY(map_f32(&ma, p.A, TBM, TBK, false));
-  else
-    RQ_TRY(map_f32(&ma, p.A, TBK, TBM, true));
-  RQ_TRY(map_f32(&mb, p.B, TBK, TBN, true));
-  TArgs a;
-  a.M = (int)(p.M + ashift);
-  a.N = (int)p.N;
-  a.k_lo = kshift;
-  a.Kv = (int)(p.K + kshift);
-  a.m_lo = ashift;
-  if (A_MMAJOR) {
-    a.a_c0 = (int)(p.A.r0 - ashift);
-    a.a_c1 = (int)(p.A.c0 - kshift);  // the k coordinate is the outer dimension: shifted with B's k
-  } else {
-    a.a_c0 = (int)(p.A.r0 - kshift);
-    a.a_c1 = (int)p.A.c0;
-  }
-  a.b_c0 = (int)(p.B.r0 - kshift);
-  a.b_c1 = (int)p.B.c0;
-  a.C = p.C - ashift;
-  a.ldc = p.ldc;
-  a.alpha = (float)p.alpha;
-  a.beta = (float)p.beta;
-  a.tiles_m = (int)ceil_div(a.M, TBM);
-  const int tiles_n = (int)ceil_div(a.N, TBN);
-  const int kb_total = (int)ceil_div(a.Kv, TBK);
-  static const int env_four = getenv("RQ_TF32X4") ? atoi(getenv("RQ_TF32X4")) : 0;
-  a.four = env_four;
-  const int64_t tiles = (int64_t)a.tiles_m * tiles_n;
-  if (tiles > 0x7fffffff) return set_error(RQ_EUNSUPPORTED, "fp32 gemm: too many tiles");
-  a.tiles = (int)tiles;
+int num_sms32() {
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -471,13 +500,75 @@ int launch(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = kSMs;
   }
+  return sms;
+}
+
+template <typename T, bool A_MMAJOR>
+int launch(const TfProblem& p, cudaStream_t st, int64_t* launches) {
+  using Cfg = TfCfg<T>;
+  constexpr int BK = Cfg::BK;
+  constexpr int per16 = 16 / (int)sizeof(T);
+  auto kern = gemm_tf32x3_kernel<T, A_MMAJOR>;
+  static bool attr = false;
+  if (!attr) {
+    RQ_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<T>()));
+    attr = true;
+  }
+  // TMA origins along a contiguous dimension are rounded down to 16 bytes; the converters zero
+  // the padding k's, the epilogue skips the padding rows.
+  const int kshift = (int)(p.b_r0 % per16);
+  if (!A_MMAJOR && (int)(p.a_r0 % per16) != kshift)
+    return set_error(RQ_EINTERNAL, "tf32 gemm: K origins of A (%lld) and B (%lld) differ modulo 16 bytes",
+                     (long long)p.a_r0, (long long)p.b_r0);
+  const int ashift = A_MMAJOR ? (int)(p.a_r0 % per16) : 0;  // M-major A: pad rows of the output
+  CUtensorMap ma, mb;
+  if (A_MMAJOR)
+    RQ_TRY(map_t<T>(&ma, p.a_base, p.a_rows, p.a_cols, p.a_ld, TBM, BK, false));
+  else
+    RQ_TRY(map_t<T>(&ma, p.a_base, p.a_rows, p.a_cols, p.a_ld, BK, TBM, true));
+  RQ_TRY(map_t<T>(&mb, p.b_base, p.b_rows, p.b_cols, p.b_ld, BK, TBN, true));
+  TArgs a;
+  a.M = (int)(p.M + ashift);
+  a.N = (int)p.N;
+  a.k_lo = kshift;
+  a.Kv = (int)(p.K + kshift);
+  a.m_lo = ashift;
+  if (A_MMAJOR) {
+    a.a_c0 = (int)(p.a_r0 - ashift);
+    a.a_c1 = (int)(p.a_c0 - kshift);  // the k coordinate is the outer dimension: shifted with B's k
+  } else {
+    a.a_c0 = (int)(p.a_r0 - kshift);
+    a.a_c1 = (int)p.a_c0;
+  }
+  a.b_c0 = (int)(p.b_r0 - kshift);
+  a.b_c1 = (int)p.b_c0;
+  a.C = static_cast<T*>(p.C) - ashift;
+  a.ldc = p.ldc;
+  a.alpha = (float)p.alpha;
+  a.beta = (float)p.beta;
+  a.tiles_m = (int)ceil_div(a.M, TBM);
+  const int tiles_n = (int)ceil_div(a.N, TBN);
+  const int kb_total = (int)ceil_div(a.Kv, BK);
+  static const int env_four = getenv("RQ_TF32X4") ? atoi(getenv("RQ_TF32X4")) : 0;
+  a.four = env_four;
+  int64_t tiles = (int64_t)a.tiles_m * tiles_n;
+  if (tiles > 0x7fffffff) return set_error(RQ_EUNSUPPORTED, "tf32 gemm: too many tiles");
+  a.u0 = 0;
+  if (p.tile_end > 0) {  // a tile-range chunk of a larger product
+    const int64_t t1 = std::min<int64_t>(p.tile_end, tiles);
+    a.u0 = (int)std::min<int64_t>(p.tile_begin, t1);
+    tiles = t1 - a.u0;
+    if (tiles <= 0) return RQ_OK;
+  }
+  a.tiles = (int)tiles;
+  const int sms = num_sms32();
   const int cap = p.max_ctas > 0 ? std::min(p.max_ctas, sms) : sms;  // persistent: <= one CTA per SM
   // split-K when the tiles fill the grid poorly (wave efficiency), K is long enough and the
   // context's workspace holds the slabs
   auto eff = [&](int64_t u) { return (double)u / (double)(ceil_div(u, cap) * cap); };
   int splits = 1;
   double best = eff(tiles);
-  if (p.work && best < 0.9 && tiles < 4 * cap) {
+  if (p.work && p.tile_end <= 0 && best < 0.9 && tiles < 4 * cap) {
     for (int sp = 2; sp <= 16; sp++) {
       if (kb_total / sp < 4) break;
       if ((size_t)sp * a.M * a.N * sizeof(float) > p.work_bytes) break;
@@ -492,13 +583,30 @@ int launch(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
   a.kblocks = (int)ceil_div(kb_total, splits);
   a.work = p.work;
   const int grid = (int)std::min<int64_t>(tiles * splits, cap);
-  kern<<<grid, kThreads, kSmem, st>>>(ma, mb, a);
-  RQ_CUDA_TRY(cudaGetLastError());
+  if (p.pdl) {
+    // programmatic dependent launch behind the previous kernel of the stream (the look-ahead's
+    // chunks beside a leaf cluster): reads none of that kernel's outputs
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = smem_bytes<T>();
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    RQ_CUDA_TRY(cudaLaunchKernelEx(&lc, kern, ma, mb, a));
+  } else {
+    kern<<<grid, kThreads, smem_bytes<T>(), st>>>(ma, mb, a);
+    RQ_CUDA_TRY(cudaGetLastError());
+  }
   if (launches) (*launches)++;
   if (splits > 1) {
     const int64_t total = (int64_t)a.M * a.N;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 4 * sms);
-    splitk_reduce_f32_kernel<<<blocks, 256, 0, st>>>(a.work, splits, a.M, a.N, a.C, a.ldc, a.alpha, a.beta, a.m_lo);
+    splitk_reduce_tf_kernel<T><<<blocks, 256, 0, st>>>(a.work, splits, a.M, a.N, static_cast<T*>(a.C), a.ldc,
+                                                        a.alpha, a.beta, a.m_lo);
     RQ_CUDA_TRY(cudaGetLastError());
     if (launches) (*launches)++;
   }
@@ -514,7 +622,28 @@ int gemm_tf32x3(const GemmProblemF32& p, cudaStream_t st, int64_t* launches) {
     return set_error(RQ_EINTERNAL, "fp32 gemm: K == 0 with beta != 1 not supported");
   }
   RQ_TRY(encoder());
-  return p.a_mmajor ? launch<true>(p, st, launches) : launch<false>(p, st, launches);
+  TfProblem q{p.M, p.N, p.K, p.A.base, p.A.rows, p.A.cols, p.A.ld, p.A.r0, p.A.c0, p.a_mmajor, p.B.base, p.B.rows,
+              p.B.cols, p.B.ld, p.B.r0, p.B.c0, p.C, p.ldc, p.alpha, p.beta, p.max_ctas, p.work, p.work_bytes, 0, 0,
+              false};
+  return p.a_mmajor ? launch<float, true>(q, st, launches) : launch<float, false>(q, st, launches);
+}
+
+int gemm_tf32x3_f64(const GemmProblem& p, cudaStream_t st, int64_t* launches) {
+  if (p.M <= 0 || p.N <= 0) return RQ_OK;
+  if (p.K <= 0) {
+    if (p.beta == 1.0) return RQ_OK;
+    return set_error(RQ_EINTERNAL, "tf32 gemm (fp64 operands): K == 0 with beta != 1 not supported");
+  }
+  RQ_TRY(encoder());
+  TfProblem q{p.M, p.N, p.K, p.A.base, p.A.rows, p.A.cols, p.A.ld, p.A.r0, p.A.c0, p.a_mmajor, p.B.base, p.B.rows,
+              p.B.cols, p.B.ld, p.B.r0, p.B.c0, p.C, p.ldc, p.alpha, p.beta, p.max_ctas,
+              reinterpret_cast<float*>(p.work), p.work ? p.work_bytes : 0, p.tile_begin, p.tile_end, p.pdl};
+  return p.a_mmajor ? launch<double, true>(q, st, launches) : launch<double, false>(q, st, launches);
+}
+
+int64_t gemm_tf32x3_tiles(int64_t M, int64_t N, bool a_mmajor, int64_t a_r0) {
+  const int64_t ashift = a_mmajor ? (a_r0 & 1) : 0;
+  return ceil_div(M + ashift, TBM) * ceil_div(N, TBN);
 }
 
 }  // namespace rq

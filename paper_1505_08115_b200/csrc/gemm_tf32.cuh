@@ -4,6 +4,7 @@
 //   B stored K x N; views at element origins (r0, c0) of whole buffers (ld % 4 == 0, 16 B bases).
 #pragma once
 #include "common.cuh"
+#include "gemm_f64.cuh"
 
 namespace rq {
 
@@ -27,5 +28,11 @@ struct GemmProblemF32 {
 };
 
 int gemm_tf32x3(const GemmProblemF32& p, cudaStream_t st, int64_t* launches);
+// The same 3xTF32 tensor-core product on fp64 operands and C (fp32-level accuracy: the inputs are
+// rounded to fp32 once, partial sums accumulate in fp32): the trailing update of the fp32-accuracy
+// mode of the monolithic driver (RQ_FLAG_TF32_UPDATE).  Honours max_ctas, pdl, tile ranges and
+// split-K slabs (work, as fp32) like gemm_f64.
+int gemm_tf32x3_f64(const GemmProblem& p, cudaStream_t st, int64_t* launches);
+int64_t gemm_tf32x3_tiles(int64_t M, int64_t N, bool a_mmajor, int64_t a_r0);
 
 }  // namespace rq

@@ -416,12 +416,14 @@ class Factorization:
 # --------------------------------------------------------------------------
 # Entry points
 # --------------------------------------------------------------------------
-def _run(a, cfg, rng, inspect, rrqr, engine, sketch="fresh"):
+def _run(a, cfg, rng, inspect, rrqr, engine, sketch="fresh", tf32_update=False):
     torch = _torch()
     a = _check_input(a)
     eng = engine if engine is not None else Engine()
     buf, ld, m, n = eng.upload(a)
     c = _make_config(cfg, rrqr, sketch)
+    if tf32_update:
+        c.flags |= _lib.RQ_FLAG_TF32_UPDATE
     eng._release_factors()
     counter = ctypes.c_uint64(int(rng.counter))
     perm = None if (rrqr or cfg.pivot_kind == "reflectors") else torch.empty(max(n, 1), dtype=torch.int64,
@@ -449,7 +451,7 @@ def _run(a, cfg, rng, inspect, rrqr, engine, sketch="fresh"):
     return Factorization(eng, m, n, cfg.block, method, buf, ld, perm)
 
 
-def block_qr(a, cfg, rng, inspect=None, *, engine=None, sketch="fresh"):
+def block_qr(a, cfg, rng, inspect=None, *, engine=None, sketch="fresh", tf32_update=False):
     """Blocked QR with randomized block pivoting (blocked.py:175-219), on the B200.
 
     The input is not modified; ``rng.counter`` advances by the draws consumed.
@@ -457,8 +459,11 @@ def block_qr(a, cfg, rng, inspect=None, *, engine=None, sketch="fresh"):
     ``sketch="downdate"`` is HQRRP proper: G is drawn once (counter += m(b+p)),
     Y = G A is downdated after every panel (Y2 <- Y2 - G1 R12); its pivots
     legitimately differ from the reference's.
+    ``tf32_update=True`` is the fp32-accuracy path (BASELINE cfg 3 fp32): the trailing-update
+    GEMMs run as 3xTF32 products on the tcgen05 tensor cores (fp32 accumulation) instead of FP64
+    DMMA; panels, sketches and pivot selection stay fp64 (RQ_FLAG_TF32_UPDATE).
     """
-    return _run(a, cfg, rng, inspect, False, engine, sketch)
+    return _run(a, cfg, rng, inspect, False, engine, sketch, tf32_update)
 
 
 def block_rrqr(a, cfg, rng, inspect=None, *, engine=None):

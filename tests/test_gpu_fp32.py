@@ -94,3 +94,26 @@ def test_fp32_leading_pivots_on_graded_spectrum():
     assert np.array_equal(res.perm[:k], f.perm[:k])
     d32, d64 = np.abs(np.diag(res.r))[:k], np.abs(np.diag(f.r))[:k]
     assert np.all(np.abs(d32 - d64) <= 1e-4 * d64 + 1e-6)
+
+
+@pytest.mark.parametrize("m,n,b,p,sketch", [(700, 600, 64, 8, "fresh"), (1024, 1000, 128, 16, "downdate"),
+                                            (530, 500, 50, 6, "downdate"), (3000, 3000, 256, 16, "downdate")])
+def test_tf32_update_mode_fp32_bars(m, n, b, p, sketch):
+    """The monolithic driver's fp32 path (RQ_FLAG_TF32_UPDATE: trailing-update GEMMs as 3xTF32
+    tcgen05 products, fp64 panels): Q-based bars at the north star's fp32 level (1e-5), the same
+    RNG counter as fp64, and pivots equal to fp64's on the leading panel."""
+    import paper_1505_08115_b200 as rq
+
+    a = np.random.default_rng(m + 1).standard_normal((m, n))
+    cfg = rq.BlockConfig(b, rq.SketchConfig(b, p, 0))
+    r1, r2 = rq.RngState(1), rq.RngState(1)
+    f = rq.block_qr(a, cfg, r1, sketch=sketch, tf32_update=True)
+    f64 = rq.block_qr(a, cfg, r2, sketch=sketch)
+    assert r1.counter == r2.counter
+    q = f.expand_q()
+    resid = np.linalg.norm(a[:, f.perm] - q @ f.r[:n]) / np.linalg.norm(a)
+    orth = np.linalg.norm(q.T @ q - np.eye(n), 2)
+    assert resid <= 1e-5 and orth <= 1e-5, (resid, orth)
+    assert resid >= 1e-9  # the update really ran at fp32 accuracy (fp64 gives ~1e-15)
+    assert np.array_equal(f.perm[:b], f64.perm[:b])
+    assert not np.tril(f.r, -1).any()
