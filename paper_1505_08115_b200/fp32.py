@@ -1,5 +1,10 @@
 """fp32 path (BASELINE cfg 3 "fp32 and fp64").
 
+Two drivers: ``block_qr_fp32(..., driver="monolithic")`` (default on one GPU) runs the C++
+driver with RQ_FLAG_TF32_UPDATE -- the trailing-update GEMMs, the dominant flops, as 3xTF32
+products on the tcgen05 tensor cores, panels / sketches / pivots in fp64; the panel-step engine
+below keeps A itself in fp32 (half the bytes; process groups).
+
 The reference is fp64-only (blocked.py:161 converts its input), so this is an
 extension with its own accuracy bar (north star: ||AP - QR|| / ||A|| and
 ||Q^T Q - I|| <= 1e-5) and with the pivots compared against the fp64 path where the
@@ -263,12 +268,24 @@ class Fp32Result:
     q: np.ndarray | None = None  # m x n float32 (economy Q) when requested
 
 
-def block_qr_fp32(a, cfg: BlockConfig, rng: RngState, *, engine=None, group=None, want_q=False, sketch="fresh"):
-    """block_qr (blocked.py:175) with A, its sketches and the trailing updates in fp32.
-    ``rng.counter`` advances exactly as in the fp64 / reference run.  want_q (world size 1):
-    also form the economy Q in fp32."""
+def block_qr_fp32(a, cfg: BlockConfig, rng: RngState, *, engine=None, group=None, want_q=False, sketch="fresh",
+                  driver=None):
+    """block_qr (blocked.py:175) at fp32 accuracy.  ``rng.counter`` advances exactly as in the
+    fp64 / reference run.  want_q: also form the economy Q (fp32).
+
+    driver="monolithic" (default on one GPU): the C++ driver with RQ_FLAG_TF32_UPDATE -- the
+    trailing-update GEMMs on the tcgen05 tensor cores (3xTF32), everything else fp64;
+    driver="steps" (default with a process group): fp32 storage through the panel-step driver."""
     import torch
 
+    if driver is None:
+        driver = "steps" if group is not None else "monolithic"
+    if driver == "monolithic":
+        from .hqrrp import block_qr
+
+        f = block_qr(np.asarray(a, dtype=np.float64), cfg, rng, engine=engine, sketch=sketch, tf32_update=True)
+        q = f.expand_q().astype(np.float32) if want_q else None
+        return Fp32Result(np.asfortranarray(f.r.astype(np.float32)), f.perm, q)
     eng = Fp32StepEngine(engine, keep_factors=want_q)
     a = np.asarray(a, dtype=np.float32)
     m, n = a.shape

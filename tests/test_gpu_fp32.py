@@ -31,7 +31,7 @@ def test_fp32_q_based_residuals_and_counter(m, n, b, p, sketch):
     a = np.random.default_rng(m).standard_normal((m, n)).astype(np.float32)
     cfg = rq.BlockConfig(b, rq.SketchConfig(b, p, 0))
     rng32, rng64 = rq.RngState(1), rq.RngState(1)
-    res = block_qr_fp32(a, cfg, rng32, want_q=True, sketch=sketch)
+    res = block_qr_fp32(a, cfg, rng32, want_q=True, sketch=sketch, driver="steps")
     f = rq.block_qr(a.astype(np.float64), cfg, rng64, sketch=sketch)
     assert res.r.dtype == np.float32 and res.q.dtype == np.float32
     assert sorted(res.perm) == list(range(n))
@@ -88,10 +88,12 @@ def test_fp32_leading_pivots_on_graded_spectrum():
     s = 0.93 ** np.arange(n)  # well-separated down to ~1e-16: compare where fp32 resolves it
     a64 = (u * s) @ v.T
     cfg = rq.BlockConfig(b, rq.SketchConfig(b, p, 0))
-    res = block_qr_fp32(a64.astype(np.float32), cfg, rq.RngState(1))
+    res = block_qr_fp32(a64.astype(np.float32), cfg, rq.RngState(1), driver="steps")
+    mono = block_qr_fp32(a64.astype(np.float32), cfg, rq.RngState(1))  # the monolithic tf32-update driver
     f = rq.block_qr(a64, cfg, rq.RngState(1))
     k = 96  # s_k ~ 1e-3: sketch norms far above fp32 rounding
     assert np.array_equal(res.perm[:k], f.perm[:k])
+    assert np.array_equal(mono.perm[:k], f.perm[:k])
     d32, d64 = np.abs(np.diag(res.r))[:k], np.abs(np.diag(f.r))[:k]
     assert np.all(np.abs(d32 - d64) <= 1e-4 * d64 + 1e-6)
 
