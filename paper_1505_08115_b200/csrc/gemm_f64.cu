@@ -387,15 +387,26 @@ __global__ void __launch_bounds__(GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, ST
 }
 
 // Deterministic split-K reduction: C = alpha * sum_s W_s + beta * C (fixed s order).
-__global__ void splitk_reduce_kernel(const double* __restrict__ work, int splitk, int64_t M, int64_t N,
-                                     double* C, int64_t ldc, double alpha, double beta, int m_lo) {
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const double* __restrict__ work, int splitk, int64_t M,
+                                                            int64_t N, double* C, int64_t ldc, double alpha,
+                                                            double beta, int m_lo) {
+  // 2-D grid (row blocks x columns): no 64-bit division per element, every slab load of a thread
+  // issued before the (fixed-order) sum
   const int64_t total = M * N;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M || m < m_lo) return;
+  for (int64_t n = blockIdx.y; n < N; n += gridDim.y) {
+    const double* w = work + n * M + m;
+    double part[8];
     double s = 0.0;
-    for (int k = 0; k < splitk; k++) s += work[k * total + idx];
-    const int64_t m = idx % M, n = idx / M;
-    if (m < m_lo) continue;
+    int k = 0;
+    for (; k + 8 <= splitk; k += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) part[q] = __ldcs(w + (int64_t)(k + q) * total);
+#pragma unroll
+      for (int q = 0; q < 8; q++) s += part[q];
+    }
+    for (; k < splitk; k++) s += __ldcs(w + (int64_t)k * total);
     double* c = C + n * ldc + m;
     double v = alpha * s;
     if (beta != 0.0) v = fma(beta, *c, v);
@@ -553,11 +564,9 @@ static int launch_cfg(const GemmProblem& p, cudaStream_t stream, int64_t* launch
   if (p.splitk_used) *p.splitk_used = a.splitk > 1 ? a.splitk : 1;
   if (a.splitk > 1) {
     if (p.mid_event) cudaEventRecord(p.mid_event, stream);
-    const int64_t total = a.M * a.N;
-    int blocks = (int)ceil_div(total, 256);
-    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
-    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(p.work, a.splitk, a.M, a.N, a.C, p.ldc, p.alpha, p.beta,
-                                                     a.m_lo);
+    const dim3 rgrid((unsigned)ceil_div(a.M, 256), (unsigned)std::min<int64_t>(a.N, 65535));
+    splitk_reduce_kernel<<<rgrid, 256, 0, stream>>>(p.work, a.splitk, a.M, a.N, a.C, p.ldc, p.alpha, p.beta,
+                                                    a.m_lo);
     RQ_CUDA_TRY(cudaGetLastError());
     if (launches) (*launches)++;
   }
