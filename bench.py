@@ -240,7 +240,8 @@ def device_time_n(eng, lib, check, torch, stream, n, b, p, mode, pk, steps=None,
     tf = 4.0 / 3.0 * n ** 3 / (ms * 1e-3) / 1e12
     del a0, work, perm
     torch.cuda.empty_cache()
-    return {"ms_per_step": ms, "value": tf, "unit": "TFLOP/s", "fraction_of_fp64_peak": tf / FP64_PEAK_TFLOPS,
+    return {"ms_per_step": ms, "value": tf, "unit": "TFLOP/s",
+            "fraction_of_fp64_peak": tf / FP64_PEAK_TFLOPS if not flags else None,
             "steps": steps, "warmup": 1, "sm_mhz": clk.get("sm_mhz"), "reasons": clk.get("reasons")}
 
 
