@@ -533,8 +533,10 @@ int Ctx::panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64
   }();
   bool space = false, t_on_aux = false;
   if (la.on && env_space != 0 && nleaves > 1) {
+    // (the tcgen05 3xTF32 update of the fp32 mode runs ~2x the in-situ DMMA rate)
+    const double nn_rate = tf32_update ? 48e12 : 24e12;
     const double nn_s = 2.0 * (double)la.g.M * (double)la.g.N * (double)la.g.K *
-                        ((double)(la.tiles - la.next) / (double)la.tiles) / 24e12;
+                        ((double)(la.tiles - la.next) / (double)la.tiles) / nn_rate;
     double rest_cols = 0.0;
     for (int k0 = wl; k0 < b; k0 += wl) rest_cols += (double)(b - k0);
     // leaves ~3.6 us per column plus the cluster WY updates at a nominal 110 GB/s per SM (they
