@@ -460,6 +460,18 @@ int Ctx::sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, c
   cudaEvent_t e0;
   const int saved = cat;
   cat = PROF_SWEEP;
+  if (sketch_batched(m, n, steps, sketch_gmax)) {
+    if (!sb_ws) {
+      RQ_CUDA_TRY(cudaMalloc(&sb_ws, sketch_batch_workspace_bytes()));
+      RQ_CUDA_TRY(cudaMemsetAsync(sb_ws, 0, sketch_batch_workspace_bytes(), stream));
+    }
+    prof_begin(&e0);
+    const int rc = sketch_batch_launch(yt, ldy, m, n, steps, init_pos, chosen, sb_ws, sb_stamp_base, stream, &launches,
+                                       sketch_gmax);
+    prof_end(e0, 0.0);
+    cat = saved;
+    if (rc >= 0) return rc;
+  }
   prof_begin(&e0);
   SweepWork w;
   w.scratch = sweep_ws;
@@ -473,6 +485,17 @@ int Ctx::sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, c
   prof_end(e0, 0.0);
   cat = saved;
   return rc;
+}
+
+// RQ_SK_BATCH=1: the batched sketch CPQR (sketch_batch.cu) where the shape fits.  Same pivots as
+// the per-step kernel; measured at parity with it (n' = 10k: 4.9 vs 4.5 us/step, 20k: 7.8 vs 7.8,
+// its solver step costs as much as the exchanges it saves), so it stays opt-in.
+bool Ctx::sketch_batched(int m, int n, int steps, int gmax) const {
+  static const int env_sb = [] {
+    const char* e = getenv("RQ_SK_BATCH");
+    return e ? atoi(e) : 0;
+  }();
+  return env_sb != 0 && m <= 288 && sketch_batch_fits(m, n, steps, gmax);
 }
 
 int Ctx::sweep_raw(SweepCall c) {
@@ -1339,7 +1362,8 @@ int Ctx::lookahead_tail(const rq_config& cfg, double* A, int64_t lda, int64_t m,
   const int64_t s2 = s + b;
   sketch_gmax = cpqr_off ? kSkMinGrid : 0;  // leave the b x b CPQR's cluster its 16 SMs
   int rc;
-  if (sketch_cpqr_preserves_input(wdt, (int)np2, sketch_gmax)) {  // (the register tiers only read Y)
+  if (sketch_batched(wdt, (int)np2, b, sketch_gmax) ||
+      sketch_cpqr_preserves_input(wdt, (int)np2, sketch_gmax)) {  // (these kernels only read Y)
     rc = sketch_select(L.yt + s2 * L.ldy, L.ldy, wdt, (int)np2, b, rank, L.cap);
   } else {
     rc = copy2d_p(L.yt + s2 * L.ldy, L.ldy, L.ybuf, L.ldy, wdt, np2, 0, stream, &launches);
@@ -1925,6 +1949,7 @@ int Ctx::step_panel_apply(const double* V, int64_t ldv, const double* T, int64_t
 
 Ctx::~Ctx() {
   if (sk_counter) cudaFree(sk_counter);
+  if (sb_ws) cudaFree(sb_ws);
   if (gsched) cudaFree(gsched);
   for (auto e : ev_pool) cudaEventDestroy(e);
   arena.release();

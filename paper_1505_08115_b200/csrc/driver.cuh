@@ -229,6 +229,9 @@ struct Ctx {
   int finish_top(double* A, int64_t lda, int64_t s, int b, int64_t n2, const double* Q2, int64_t ldt, Layout& L);
   unsigned long long* sk_counter = nullptr;  // device: monotone arrival counter of the sketch CPQR
   unsigned long long sk_counter_base = 0;    // host mirror of its value
+  void* sb_ws = nullptr;                     // device: exchange words of the batched sketch CPQR (sketch_batch.cu)
+  unsigned long long sb_stamp_base = 0;      // its monotone event stamps
+  bool sketch_batched(int m, int n, int steps, int gmax) const;  // sketch_select takes the batched kernel
   int sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, const int* init_pos, int* chosen);
   int panel_qr(double* A, int64_t lda, int64_t m, int64_t n, int64_t s, int64_t mp, int b, double* V, int64_t ldv,
                int vpad, double* tleaf, double* w1, double* w2, double* T = nullptr, int64_t ldt = 0,

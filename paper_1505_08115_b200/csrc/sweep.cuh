@@ -60,4 +60,13 @@ int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, con
                        SweepWork& w, unsigned long long* counter, unsigned long long& counter_base, cudaStream_t st,
                        int64_t* launches, int gmax = 0);
 
+
+// Batched sketch CPQR (sketch_batch.cu): the same greedy pivots with one grid-wide exchange per
+// batch of provable pivots.  y is only read.  ws: sketch_batch_workspace_bytes(), zero at
+// allocation, private to the context.  Returns -1 when the shape does not fit.
+size_t sketch_batch_workspace_bytes();
+bool sketch_batch_fits(int m, int n, int steps, int gmax = 0);
+int sketch_batch_launch(const double* y, int64_t ld, int m, int n, int steps, const int* init_pos, int* chosen,
+                        void* ws, unsigned long long& stamp_base, cudaStream_t st, int64_t* launches, int gmax = 0);
+
 }  // namespace rq

@@ -257,3 +257,62 @@ def test_exchange_kernels_repeatable_under_stress():
                 assert np.array_equal(got, first)
         r_ref = O.qr_unpivoted(a0).r[:w, :]
         assert np.abs(np.triu(first.T[:w, :]) - r_ref).max() <= 1e-12 * np.linalg.norm(a0)
+
+
+def test_batched_sketch_cpqr_opt_in_picks_the_same_pivots():
+    """RQ_SK_BATCH=1 (sketch_batch.cu: one grid exchange per provable batch of pivots, opt-in because it
+    measured at parity with the per-step kernel) returns the per-step kernel's pivots bit for bit -- also
+    on duplicated columns, zero columns and beyond the numerical rank -- and the oracle's where those are
+    well determined.  The switch is read once per process, hence the subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import ctypes, sys
+import numpy as np, torch
+import paper_1505_08115_b200 as rq
+from paper_1505_08115_b200.errors import check
+eng = rq.Engine()
+rng = np.random.default_rng(11)
+cases = []
+cases.append(("gauss", rng.standard_normal((272, 3000)), 256))
+y = rng.standard_normal((272, 3000)); y[:, 100] = y[:, 2500]; y[:, 1500:1510] = y[:, 20:21]
+cases.append(("dups", y, 256))
+cases.append(("rank40", rng.standard_normal((272, 40)) @ rng.standard_normal((40, 2500)), 100))
+y = rng.standard_normal((80, 500)); y[:, 50:] = 0.0
+cases.append(("zeros", y, 70))
+cases.append(("small", rng.standard_normal((74, 1200)), 64))
+cases.append(("wide", rng.standard_normal((272, 14000)), 128))
+out = {}
+for name, y, steps in cases:
+    m, n = y.shape
+    buf, ld = eng.alloc_matrix(m, n)
+    buf[:n, :m].copy_(torch.from_numpy(np.ascontiguousarray(y.T)))
+    before = buf.clone()
+    ch = torch.full((steps,), -1, dtype=torch.int32, device=eng.device)
+    check(eng.lib.rq_test_sketch_cpqr(eng.handle, ctypes.c_void_p(buf.data_ptr()), ld, m, n, steps,
+                                      ctypes.c_void_p(ch.data_ptr())))
+    torch.cuda.synchronize()
+    assert torch.equal(buf, before), name
+    out[name] = ch.cpu().numpy()
+np.savez(sys.argv[1], **out)
+"""
+    import tempfile
+
+    from oracle import randqr_oracle as O
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    with tempfile.TemporaryDirectory() as d:
+        for flag in ("0", "1"):
+            path = os.path.join(d, f"p{flag}.npz")
+            env = dict(os.environ, RQ_SK_BATCH=flag, PYTHONPATH=root)
+            r = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            res[flag] = dict(np.load(path))
+    for name in res["0"]:
+        assert np.array_equal(res["0"][name], res["1"][name]), name
+    rng = np.random.default_rng(11)
+    y = rng.standard_normal((272, 3000))
+    assert np.array_equal(res["1"]["gauss"].astype(np.int64), O.qr_column_pivoted(y, steps=256).perm[:256])
