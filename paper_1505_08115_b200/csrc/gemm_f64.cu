@@ -607,6 +607,39 @@ static int choose_splitk(const GemmProblem& p, int BM, int BN) {
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, bool A_MMAJOR, int STAGES>
 static int launch_auto(GemmProblem p, cudaStream_t stream, int64_t* launches) {
+  // Long-K products whose tile count is a little over a whole number of waves (W = V^T A2 at
+  // n2 > 9.4k: 2 x 79 tiles on 148 SMs): whole waves of unsplit tiles first, then the remaining
+  // tile columns alone with split-K -- the last wave costs 1/s of a tile instead of a whole one,
+  // and only the remainder's slabs go through the reduction.  RQ_GEMM_WAVES=0 restores the
+  // single launch with one split factor for all tiles.
+  static const int env_waves = [] {
+    const char* e = getenv("RQ_GEMM_WAVES");
+    return e ? atoi(e) : 1;
+  }();
+  if (env_waves != 0 && p.splitk == 0 && p.work && p.tile_end == 0 && !p.sched) {
+    using Cfg = GemmCfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>;
+    const int sms = p.max_ctas > 0 ? std::min(num_sms(), p.max_ctas) : num_sms();
+    const int64_t slots = (int64_t)sms * (Cfg::kThreads <= 128 ? 2 : 1);
+    const int mshift = A_MMAJOR ? (int)(p.A.r0 & 1) : 0, kshift = (int)(p.B.r0 & 1);
+    const int64_t tiles_m = ceil_div(p.M + mshift, BM), tiles_n = ceil_div(p.N, BN);
+    const int64_t tiles = tiles_m * tiles_n, kch = ceil_div(p.K + kshift, BK);
+    const int64_t whole_cols = (tiles / slots) * slots / tiles_m;  // tile columns in whole waves
+    const double eff = (double)tiles / (double)(ceil_div(tiles, slots) * slots);
+    if (tiles > slots && tiles < 8 * slots && eff < 0.93 && kch >= 128 && whole_cols > 0 && whole_cols < tiles_n) {
+      GemmProblem p1 = p;
+      p1.N = whole_cols * BN;
+      p1.splitk = 1;
+      p1.mid_event = nullptr;
+      p1.splitk_used = nullptr;
+      RQ_TRY((launch_cfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(p1, stream, launches)));
+      GemmProblem p2 = p;
+      p2.N = p.N - p1.N;
+      p2.B.c0 += p1.N;
+      p2.C += p1.N * p.ldc;
+      p2.splitk = choose_splitk(p2, BM, BN);
+      return launch_cfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(p2, stream, launches);
+    }
+  }
   p.splitk = choose_splitk(p, BM, BN);
   return launch_cfg<BM, BN, WARPS_M, WARPS_N, A_MMAJOR, STAGES>(p, stream, launches);
 }

@@ -123,7 +123,7 @@ if "skstamps" in which:
         print(f"  {nm:20s} {int(np.median(d[:, k])):6d}")
     print("  step total          ", int(np.median(h[6:60, 0] - h[5:59, 0])))
 
-if "gemm" in which:
+if "gemm" in which or "gemm_tn" in which:
     def gemm_case(mm, M, N, K, label):
         A = torch.randn((K, M) if not mm else (M, K), dtype=torch.float64, device=eng.device)
         B = torch.randn((K, N), dtype=torch.float64, device=eng.device)
@@ -142,12 +142,16 @@ if "gemm" in which:
                                    ctypes.c_void_p(cbuf.data_ptr()), ldc, -1.0, 1.0))
         ms = timeit(run, reps=5)
         print(f"gemm {label:28s} M={M} N={N} K={K}: {ms*1e3:8.0f} us  {2*M*N*K/ms/1e9:6.2f} TF/s")
+if "gemm" in which:
     gemm_case(1, 10000, 10000, 256, "NN  A2 -= V W2")
     gemm_case(0, 256, 10000, 10000, "TN  W = V^T A2")
     gemm_case(0, 272, 10000, 10000, "TN  Yt = Om^T X (sketch)")
     gemm_case(0, 256, 256, 10000, "TN  Gram V^T V")
     gemm_case(1, 5000, 5000, 256, "NN  half size")
     gemm_case(0, 4096, 4096, 4096, "TN  square 4096")
+if "gemm_tn" in which:
+    for nn in (9600, 12000, 16000, 20000, 30000):
+        gemm_case(0, 256, nn, nn, "TN  W = V^T A2")
 if "gemm_nn" in which:
     M, N, K = 10000, 10000, 256
     abuf, lda = eng.alloc_matrix(M, K)
