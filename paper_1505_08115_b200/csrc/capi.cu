@@ -143,8 +143,42 @@ int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, c
   double* dA = static_cast<double*>(c.harena.base);
   int64_t* dp = reinterpret_cast<int64_t*>(static_cast<char*>(c.harena.base) + abytes);
   int rc = RQ_OK;
-  cudaError_t e = cudaMemcpy2DAsync(dA, ldd * 8, hA, lda * 8, m * 8, n, cudaMemcpyHostToDevice, c.stream);
-  if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "H2D: %s", cudaGetErrorString(e));
+  cudaError_t e = cudaSuccess;
+  // HQRRP's downdated sketch needs Y = G A before anything else: A arrives in column chunks on
+  // its own stream and every chunk's Y columns are formed while the next chunk is on the wire,
+  // so only the last chunk's product is exposed (RQ_H2D_CHUNKS: chunk count, 0/1 = one copy;
+  // default 8 from 64 MB up).
+  static const int env_chunks = getenv("RQ_H2D_CHUNKS") ? atoi(getenv("RQ_H2D_CHUNKS")) : -1;
+  int chunks = env_chunks >= 0 ? env_chunks : ((size_t)m * n * 8 >= ((size_t)64 << 20) ? 8 : 1);
+  const bool chunked = chunks > 1 && !cfg->rrqr && cfg->pivot_kind == RQ_PIVOT_PERMUTATION &&
+                       cfg->sketch_mode == RQ_SKETCH_DOWNDATE && cfg->power == 0 && n > cfg->block &&
+                       !c.inspect_cb;
+  if (chunked) {
+    chunks = (int)std::min<int64_t>(chunks, n);
+    if (!c.h2d_stream && cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking) != cudaSuccess)
+      rc = rq::set_error(RQ_ECUDA, "h2d stream");
+    while (rc == RQ_OK && (int)c.h2d_ev.size() < chunks) {
+      cudaEvent_t ev;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "event");
+      else c.h2d_ev.push_back(ev);
+    }
+    if (rc == RQ_OK) rc = c.presketch_begin(*cfg, m, n, seed, *counter);
+    const int64_t per = (n + chunks - 1) / chunks;
+    for (int k = 0; rc == RQ_OK && k < chunks; k++) {
+      const int64_t c0 = (int64_t)k * per, c1 = std::min<int64_t>(n, c0 + per);
+      if (c1 <= c0) break;
+      e = cudaMemcpy2DAsync(dA + c0 * ldd, ldd * 8, hA + c0 * lda, lda * 8, m * 8, c1 - c0, cudaMemcpyHostToDevice,
+                            c.h2d_stream);
+      if (e == cudaSuccess) e = cudaEventRecord(c.h2d_ev[k], c.h2d_stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(c.stream, c.h2d_ev[k], 0);
+      if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "H2D chunk: %s", cudaGetErrorString(e));
+      if (rc == RQ_OK) rc = c.presketch_cols(*cfg, m, n, dA, ldd, c0, c1);
+    }
+    c.presketched = rc == RQ_OK;
+  } else {
+    e = cudaMemcpy2DAsync(dA, ldd * 8, hA, lda * 8, m * 8, n, cudaMemcpyHostToDevice, c.stream);
+    if (e != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "H2D: %s", cudaGetErrorString(e));
+  }
   // R streams back panel by panel on the context's copy stream (created on its device) while
   // later panels compute
   if (rc == RQ_OK && hR && !c.copy_stream) {
@@ -173,6 +207,7 @@ int rq_factorize_host(rq_ctx* ctx, const rq_config* cfg, int64_t m, int64_t n, c
   }
   if (rc == RQ_OK) rc = rq_factorize(ctx, cfg, m, n, dA, ldd, seed, counter, dp);
   c.on_cols_final = nullptr;
+  c.presketched = false;
   if (rc == RQ_OK && cb_err != cudaSuccess) rc = rq::set_error(RQ_ECUDA, "D2H (streamed R): %s", cudaGetErrorString(cb_err));
   if (rc == RQ_OK && hR && copied < n) {
     e = cudaMemcpy2DAsync(hR + copied * ldr, ldr * 8, dA + copied * ldd, ldd * 8, m * 8, n - copied,

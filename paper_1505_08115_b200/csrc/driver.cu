@@ -778,10 +778,14 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
   phase(0);
   if (downdate && n > b) {
     // HQRRP: G = Omega^T drawn once (m(b+p) normals), Y = G A; downdated per panel
-    RQ_TRY(gaussian_fill_p(L.omega, m, wdt, L.ldo, seed, *counter, stream, &launches));
+    // (rq_factorize_host forms both while A's column chunks arrive: presketch_begin / _cols)
+    if (!presketched) {
+      RQ_TRY(gaussian_fill_p(L.omega, m, wdt, L.ldo, seed, *counter, stream, &launches));
+      RQ_TRY(gemm(wdt, n, m, op(L.omega, m, wdt, L.ldo), false, op(A, m, n, lda, 0, 0), L.yt, L.ldy, 1.0, 0.0));
+    }
     *counter += (uint64_t)m * (uint64_t)wdt;
-    RQ_TRY(gemm(wdt, n, m, op(L.omega, m, wdt, L.ldo), false, op(A, m, n, lda, 0, 0), L.yt, L.ldy, 1.0, 0.0));
   }
+  presketched = false;
   int panel = 0;
   for (int64_t s = 0; s < n; s += b) {
     panel++;
@@ -1199,6 +1203,25 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
   phase_report();
   have_factors = true;
   return RQ_OK;
+}
+
+// The downdated sketch's G and Y = G A ahead of factorize_perm (same arena layout), so that the
+// host entry can form Y chunk by chunk while the rest of A is still on its way to the device.
+int Ctx::presketch_begin(const rq_config& cfg, int64_t m, int64_t n, uint64_t seed, uint64_t counter) {
+  const int b = cfg.block, p = cfg.oversample, wdt = b + p;
+  RQ_TRY(arena.reserve(plan_layout(nullptr, m, n, b, p, cfg.power).total));
+  Layout L = plan_layout(arena.base, m, n, b, p, cfg.power);
+  return gaussian_fill_p(L.omega, m, wdt, L.ldo, seed, counter, stream, &launches);
+}
+
+int Ctx::presketch_cols(const rq_config& cfg, int64_t m, int64_t n, const double* A, int64_t lda, int64_t c0,
+                        int64_t c1) {
+  const int b = cfg.block, p = cfg.oversample, wdt = b + p;
+  Layout L = plan_layout(arena.base, m, n, b, p, cfg.power);
+  kwork = L.kwork;
+  kwork_bytes = L.kwork_bytes;
+  return gemm(wdt, c1 - c0, m, op(L.omega, m, wdt, L.ldo), false, op(A, m, n, lda, 0, c0), L.yt + c0 * L.ldy, L.ldy,
+              1.0, 0.0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1962,6 +1985,8 @@ Ctx::~Ctx() {
   if (ev_g1) cudaEventDestroy(ev_g1);
   if (ev_hipdone) cudaEventDestroy(ev_hipdone);
   if (copy_ev) cudaEventDestroy(copy_ev);
+  if (h2d_stream) cudaStreamDestroy(h2d_stream);
+  for (cudaEvent_t e : h2d_ev) cudaEventDestroy(e);
   if (ev_v) cudaEventDestroy(ev_v);
   if (ev_side) cudaEventDestroy(ev_side);
   if (ev_hi) cudaEventDestroy(ev_hi);

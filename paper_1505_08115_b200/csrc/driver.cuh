@@ -140,6 +140,12 @@ struct Ctx {
   Arena harena;                 // rq_factorize_host: device copy of A and the permutation
   cudaStream_t copy_stream = nullptr;  // rq_factorize_host: R streams to the host on this stream
   cudaEvent_t copy_ev = nullptr;
+  cudaStream_t h2d_stream = nullptr;   // rq_factorize_host: A arrives in column chunks on this stream
+  std::vector<cudaEvent_t> h2d_ev;     // one per chunk
+  bool presketched = false;            // the next factorize_perm finds G drawn and Y = G A formed (presketch_*)
+  int presketch_begin(const rq_config& cfg, int64_t m, int64_t n, uint64_t seed, uint64_t counter);
+  int presketch_cols(const rq_config& cfg, int64_t m, int64_t n, const double* A, int64_t lda, int64_t c0,
+                     int64_t c1);
   unsigned int* barriers = nullptr;
   int nbarriers = 0;
   int next_barrier = 0;

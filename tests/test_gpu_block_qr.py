@@ -363,6 +363,46 @@ def test_host_entry_streams_r_identically(rq, m, n, b, p, kind):
         assert np.array_equal(hp, f.perm)
 
 
+_CHUNK_SCRIPT = r"""
+import ctypes, sys
+import numpy as np
+import paper_1505_08115_b200 as rq
+from paper_1505_08115_b200 import _lib
+from paper_1505_08115_b200.errors import check
+m, n, b, p = (int(x) for x in sys.argv[1:5])
+a = np.asfortranarray(np.random.default_rng(m + n).standard_normal((m, n)))
+f = rq.block_qr(a, rq.BlockConfig(b, rq.SketchConfig(b, p, 0)), rq.RngState(3), sketch="downdate")
+eng = rq.Engine()
+cfg = _lib.rq_config(b, p, 0, -1, _lib.RQ_PIVOT_PERMUTATION, 0, _lib.RQ_SKETCH_DOWNDATE, 0)
+hr = np.zeros((m, n), order="F")
+hp = np.zeros(n, dtype=np.int64)
+ctr = ctypes.c_uint64(0)
+for _ in range(2):  # twice: the context's chunk stream, events and buffers are reused
+    ctr = ctypes.c_uint64(0)
+    check(eng.lib.rq_factorize_host(eng.handle, ctypes.byref(cfg), m, n, a.ctypes.data_as(ctypes.c_void_p), m,
+                                    ctypes.c_uint64(3), ctypes.byref(ctr), hr.ctypes.data_as(ctypes.c_void_p), m,
+                                    hp.ctypes.data_as(ctypes.c_void_p)))
+    ok = np.array_equal(np.triu(hr), f.r) and np.array_equal(hp, f.perm) and ctr.value == m * (b + p)
+    print("RESULT", int(ok))
+"""
+
+
+@pytest.mark.parametrize("m,n,b,p,chunks", [(3000, 3000, 256, 16, 5), (700, 650, 64, 8, 3), (1000, 896, 128, 8, 64)])
+def test_host_entry_chunked_upload_forms_the_sketch_on_arrival(m, n, b, p, chunks):
+    """rq_factorize_host with the downdated sketch uploads A in column chunks and forms Y = G A chunk by
+    chunk while the next one is on the wire (default from 64 MB; forced here with RQ_H2D_CHUNKS): R, the
+    permutation and the RNG counter equal the device path's."""
+    import subprocess
+
+    env = dict(os.environ, RQ_H2D_CHUNKS=str(chunks))
+    root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
+    res = subprocess.run([sys.executable, "-c", _CHUNK_SCRIPT, str(m), str(n), str(b), str(p)], env=env, cwd=root,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("RESULT")]
+    assert lines == ["RESULT 1", "RESULT 1"], res.stdout[-500:]
+
+
 def test_cfg2_full_size_vs_reference_algorithm(rq):
     """BASELINE cfg 2 at its full size: A = U diag(s) V^T, U, V = haar_orthonormal(4000,
     RngState(0)) (built on the device with this library's QR), s_j = 10^(-8 j / n); m1 with
