@@ -954,6 +954,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     ss.col_at_pos = L.cap;
     ss.r_out = L.rfin;
     ss.ldr = L.lds_small;
+    bool t_early = false;
     if (overlap) {
       // env_overlap 1: CPQR then the W GEMM in one stream, the GEMM a programmatic dependent launch
       //   (it starts once every CPQR CTA is resident, so the cluster never waits behind it), with a
@@ -989,6 +990,21 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
         rc = cudaEventRecord(ev_hi, cpqr_stream) == cudaSuccess ? RQ_OK : set_error(RQ_ECUDA, "event");
       double* kw = kwork;
       const size_t kwb = kwork_bytes;
+      // off-chain panels: the main stream idles until W and T are there, so T (Gram + triangular
+      // inverse, independent of W) runs beside W on the aux stream with the main stream's split-K
+      // slabs and Gram scratch instead of behind W on the side stream (RQ_T_OFF_AUX=0: behind W)
+      static const int env_toff = [] {
+        const char* e = getenv("RQ_T_OFF_AUX");
+        return e ? atoi(e) : 1;
+      }();
+      if (rc == RQ_OK && cpqr_off && !t_done && env_toff != 0 && !t_on_hip) {
+        if (cudaStreamWaitEvent(aux, ev_v, 0) != cudaSuccess) rc = set_error(RQ_ECUDA, "wait");
+        stream = aux;
+        if (rc == RQ_OK) rc = tfactor(V, mp, b, ldv, vpad, T, ldt, L.gram);
+        if (rc == RQ_OK && cudaEventRecord(ev_t, aux) != cudaSuccess) rc = set_error(RQ_ECUDA, "event");
+        t_done = true;
+        t_early = rc == RQ_OK;
+      }
       if (rc == RQ_OK) {
         stream = side;
         kwork = L.kwork2;
@@ -1105,6 +1121,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
       phase(12);
       RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_g1, 0));    // G1' (the downdate)
       RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_side, 0));  // W and T
+      if (t_early) RQ_CUDA_TRY(cudaStreamWaitEvent(stream, ev_t, 0));  // (T from the aux stream)
       phase(3);
       RQ_TRY(lookahead_tail(cfg, A, lda, m, n, s, mp, b, n2, V, ldv, vpad, T, ldt, Q2, L, L.wside, lorder, lorder_n,
                             rank, rank_n));
