@@ -931,7 +931,8 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
     }();
     // Only where the CPQR outlasts W = V^T A2 (the late panels): the capped sketch grid costs
     // ~25 % per step at n' ~ 10k, and early panels hide the CPQR behind W anyway.
-    static const double env_off_tf = getenv("RQ_CPQR_OFF_TF") ? atof(getenv("RQ_CPQR_OFF_TF")) : 20.0;
+    // (threshold re-tuned with T on the aux stream: 20 -> 30 TF/s, n = 10k 131.3 -> 130.8 ms)
+    static const double env_off_tf = getenv("RQ_CPQR_OFF_TF") ? atof(getenv("RQ_CPQR_OFF_TF")) : 30.0;
     const double w_s = 2.0 * b * (double)mp * (double)n2 / (env_off_tf * 1e12);
     const double cpqr_s = b * 2.2e-6;
     cpqr_off = la_mode && overlap && env_off != 0 && b <= 256 && !w2_side && !t_on_hip &&
@@ -1018,7 +1019,7 @@ int Ctx::factorize_perm(const rq_config& cfg, int64_t m, int64_t n, double* A, i
           // measured b x b CPQR step (2.26 us at b = 256) and capped DMMA rate; RQ_CPQR_US /
           // RQ_CAPPED_TF override them (tuning)
           static const double env_us = getenv("RQ_CPQR_US") ? atof(getenv("RQ_CPQR_US")) : 2.7;
-          static const double env_tf = getenv("RQ_CAPPED_TF") ? atof(getenv("RQ_CAPPED_TF")) : 24.0;
+          static const double env_tf = getenv("RQ_CAPPED_TF") ? atof(getenv("RQ_CAPPED_TF")) : 30.0;
           const double cpqr_s = (double)b * env_us * 1e-6, rate = env_tf * 1e12;
           int64_t n_a = (int64_t)(cpqr_s * rate / (2.0 * b * (double)mp));
           n_a = std::max<int64_t>(128, (n_a + 127) / 128 * 128);
