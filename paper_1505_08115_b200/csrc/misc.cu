@@ -87,6 +87,14 @@ __global__ void __launch_bounds__(128) trinv_upper_kernel(const double* __restri
                                                           double* __restrict__ X, int64_t ldx) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int TR_DEPTH = TrDepth<RPL>::value;
+  // reciprocals of the diagonal once per block: the substitution's serial step is then a
+  // multiply instead of an fp64 division (0 for an exactly-zero pivot)
+  __shared__ double rdiag[32 * RPL];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const double d = __ldg(R + (int64_t)i * ldr + i);
+    rdiag[i] = d != 0.0 ? 1.0 / d : 0.0;
+  }
+  __syncthreads();
   const int j = blockIdx.x * (blockDim.x >> 5) + warp;
   if (j >= k) return;
   double acc[RPL], xv[RPL];
@@ -109,17 +117,13 @@ __global__ void __launch_bounds__(128) trinv_upper_kernel(const double* __restri
     for (int d = 0; d < TR_DEPTH; d++) {
       const int kk = kb - d;
       if (kk < 0) break;
-      double sa = 0.0, sd = 0.0;
+      double sa = 0.0;
       const int rk = kk >> 5;
 #pragma unroll
-      for (int r = 0; r < RPL; r++) {
-        sa = (r == rk) ? acc[r] : sa;
-        sd = (r == rk) ? ring[d][r] : sd;  // diagonal R_kk sits in column kk at row kk
-      }
+      for (int r = 0; r < RPL; r++) sa = (r == rk) ? acc[r] : sa;
       const double a = __shfl_sync(0xffffffffu, sa, kk & 31);
-      const double dg = __shfl_sync(0xffffffffu, sd, kk & 31);
       const double rhs = ((kk == j) ? 1.0 : 0.0) - a;
-      const double xk = (dg != 0.0) ? rhs / dg : 0.0;
+      const double xk = rhs * rdiag[kk];
       const int kn = kk - TR_DEPTH;
 #pragma unroll
       for (int r = 0; r < RPL; r++) {
