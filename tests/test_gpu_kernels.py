@@ -80,6 +80,24 @@ def test_dmma_gemm_vs_fp64_reference(eng, M, N, K, mmajor):
     assert np.abs(out - ref).max() <= tol
 
 
+@pytest.mark.parametrize("M,N,K,org", [(256, 9700, 2100, (0, 0)), (272, 9650, 2049, (1, 3)), (256, 19000, 2064, (0, 0))])
+def test_dmma_gemm_whole_waves_plus_split_remainder(eng, M, N, K, org):
+    """TN products with a little more than a whole number of tile waves (152 / 152 / 298 tiles on 148
+    SMs, K >= 2048) run as whole waves of unsplit tiles plus the remaining tile columns with split-K
+    (launch_auto, gemm_f64.cu): same result as one product, also from an offset view."""
+    rng = np.random.default_rng(M + N + K)
+    r0, c0 = org
+    A = rng.standard_normal((K + r0, M + 5))
+    B = rng.standard_normal((K + r0, N + c0))
+    C = rng.standard_normal((M, N))
+    out = _gemm(eng, False, M, N, K, A, B, C, -1.0, 1.0, a_org=(r0, 2), b_org=(r0, c0))
+    opA = A[r0:r0 + K, 2:2 + M].T
+    Bv = B[r0:r0 + K, c0:c0 + N]
+    ref = C - opA @ Bv
+    tol = 1e-13 * np.sqrt(K) * (np.abs(opA) @ np.abs(Bv)).max()
+    assert np.abs(out - ref).max() <= tol
+
+
 def test_dmma_gemm_views_and_ktail(eng):
     # views at odd origins, K not a multiple of 16, buffers larger than the views
     rng = np.random.default_rng(5)
