@@ -117,6 +117,24 @@ class Clocks:
                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+        self.wait_ready()
+
+    def wait_ready(self, timeout=8.0):
+        """Block until the sampler has written its first line: nvidia-smi's start-up (NVML init,
+        device enumeration) perturbs a running GPU for tens of ms, so it must be over before the
+        timed region starts; the steady 200 ms polling that follows is what the recipe asks for."""
+        if self.proc is None:
+            return
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < timeout:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    return
+            except OSError:
+                pass
+            if self.proc.poll() is not None:
+                return
+            time.sleep(0.05)
 
     def stop(self):
         if self.proc is None:

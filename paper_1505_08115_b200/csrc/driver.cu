@@ -457,6 +457,7 @@ int Ctx::sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, c
     sc.col_at_pos = chosen;
     return sweep(sc);
   }
+  RQ_TRY(place_sketch_words(m, n, steps));
   cudaEvent_t e0;
   const int saved = cat;
   cat = PROF_SWEEP;
@@ -476,14 +477,93 @@ int Ctx::sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, c
   SweepWork w;
   w.scratch = sweep_ws;
   w.scratch_bytes = sweep_ws_bytes;
-  if (!sk_counter) {  // counter (offset 0) + two winner records (offset 64)
-    RQ_CUDA_TRY(cudaMalloc(&sk_counter, 256));
-    RQ_CUDA_TRY(cudaMemsetAsync(sk_counter, 0, 256, stream));
-  }
   const int rc = sketch_cpqr_launch(yt, ldy, m, n, steps, init_pos, chosen, w, sk_counter, sk_counter_base, stream,
                                     &launches, sketch_gmax);
   prof_end(e0, 0.0);
   cat = saved;
+  return rc;
+}
+
+// The sketch CPQR's winner record -- one line written by the reducer CTA and polled by every
+// other CTA each step -- costs ~0.8 us more per step at some addresses than at others (B200,
+// n' = 10k: 4.55 vs 5.4 us per step; e.g. fast at offsets 0, 64 KB, 3 MB of a block and slow at
+// 4 KB, 128 KB, 1 MB, 2 MB: the line's L2 slice / die relative to the reducer).  cudaMalloc gives
+// no control over that, and the address a 256-byte allocation gets shifts with whatever the
+// process allocated before (a context created after PyTorch's stream pool landed on a slow line:
+// 136.9 instead of 129.1 ms per n = 10k factorization).  So the context allocates a block once,
+// times a short sketch CPQR with the record at 16 offsets of it and keeps the fastest
+// (RQ_SK_PLACE_CAL=0: offset 0; 2: print the timings).
+int Ctx::place_sketch_words(int m, int n, int steps) {
+  static const int env_cal = [] {
+    const char* e = getenv("RQ_SK_PLACE_CAL");
+    return e ? atoi(e) : 1;
+  }();
+  constexpr int kCand = 16;
+  constexpr size_t kStride = 4096;
+  if (!sk_block) {
+    RQ_CUDA_TRY(cudaMalloc(&sk_block, kCand * kStride));
+    RQ_CUDA_TRY(cudaMemsetAsync(sk_block, 0, kCand * kStride, stream));
+    sk_counter = reinterpret_cast<unsigned long long*>(sk_block);
+  }
+  char* blk = sk_block;
+  // (small problems never repay the one-off ~6 ms: calibrate at the first sizeable sketch)
+  if (sk_placed || env_cal == 0 || m > 288 || n < 2048 || steps < 32) return RQ_OK;
+  sk_placed = true;
+  const int cn = 2048, csteps = 32;
+  const size_t ws = sketch_workspace_bytes(m, cn) + 4096;
+  const int64_t ldc = even(m);
+  double* ycal = nullptr;
+  void* wcal = nullptr;
+  int* ccal = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  auto cleanup = [&] {
+    if (ycal) cudaFree(ycal);
+    if (wcal) cudaFree(wcal);
+    if (ccal) cudaFree(ccal);
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+  };
+  if (cudaMalloc(&ycal, (size_t)ldc * cn * 8) != cudaSuccess || cudaMalloc(&wcal, ws) != cudaSuccess ||
+      cudaMalloc(&ccal, 1024) != cudaSuccess || cudaEventCreate(&t0) != cudaSuccess ||
+      cudaEventCreate(&t1) != cudaSuccess) {
+    cleanup();
+    cudaGetLastError();
+    return RQ_OK;  // no calibration: offset 0
+  }
+  cudaMemsetAsync(wcal, 0, ws, stream);
+  int rc = gaussian_fill(ycal, m, cn, ldc, 0x5eedULL, 0, stream, nullptr);
+  SweepWork w;
+  w.scratch = wcal;
+  w.scratch_bytes = ws;
+  float tms[kCand];
+  int best = 0;
+  for (int i = 0; i < kCand && rc == RQ_OK; i++) {
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(blk + i * kStride);
+    tms[i] = 1e30f;
+    for (int rep = 0; rep < 3 && rc == RQ_OK; rep++) {
+      cudaEventRecord(t0, stream);
+      rc = sketch_cpqr_launch(ycal, ldc, m, cn, csteps, nullptr, ccal, w, ctr, sk_counter_base, stream, nullptr, 0);
+      cudaEventRecord(t1, stream);
+      if (rc == RQ_OK && cudaStreamSynchronize(stream) != cudaSuccess) rc = set_error(RQ_ECUDA, "calibration run");
+      float ms = 0.0f;
+      if (rc == RQ_OK && rep > 0 && cudaEventElapsedTime(&ms, t0, t1) == cudaSuccess) tms[i] = std::min(tms[i], ms);
+    }
+    if (tms[i] < tms[best]) best = i;
+  }
+  if (rc == RQ_OK) {
+    sk_counter = reinterpret_cast<unsigned long long*>(blk + best * kStride);
+    // every candidate's arrival counter saw its own launches only: set the chosen one to the
+    // host mirror (the stamps keep growing: records and slots written so far stay in the past)
+    if (cudaMemcpyAsync(sk_counter, &sk_counter_base, 8, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+        cudaStreamSynchronize(stream) != cudaSuccess)
+      rc = set_error(RQ_ECUDA, "sketch counter");
+    if (env_cal == 2) {
+      fprintf(stderr, "[rq] sketch CPQR winner-record placement (us/step at 4 KB offsets):");
+      for (int i = 0; i < kCand; i++) fprintf(stderr, " %.2f", tms[i] * 1e3f / csteps);
+      fprintf(stderr, " -> offset %d KB\n", best * 4);
+    }
+  }
+  cleanup();
   return rc;
 }
 
@@ -1989,7 +2069,7 @@ int Ctx::step_panel_apply(const double* V, int64_t ldv, const double* T, int64_t
 }
 
 Ctx::~Ctx() {
-  if (sk_counter) cudaFree(sk_counter);
+  if (sk_block) cudaFree(sk_block);
   if (sb_ws) cudaFree(sb_ws);
   if (gsched) cudaFree(gsched);
   for (auto e : ev_pool) cudaEventDestroy(e);

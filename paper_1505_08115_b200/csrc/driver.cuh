@@ -233,8 +233,11 @@ struct Ctx {
   int sketch_gmax = 0;
   cudaEvent_t ev_g1 = nullptr, ev_hipdone = nullptr;
   int finish_top(double* A, int64_t lda, int64_t s, int b, int64_t n2, const double* Q2, int64_t ldt, Layout& L);
-  unsigned long long* sk_counter = nullptr;  // device: monotone arrival counter of the sketch CPQR
+  unsigned long long* sk_counter = nullptr;  // device: monotone arrival counter of the sketch CPQR + its winner records
   unsigned long long sk_counter_base = 0;    // host mirror of its value
+  char* sk_block = nullptr;  // the allocation sk_counter points into (place_sketch_words)
+  bool sk_placed = false;    // its offset was calibrated
+  int place_sketch_words(int m, int n, int steps);
   void* sb_ws = nullptr;                     // device: exchange words of the batched sketch CPQR (sketch_batch.cu)
   unsigned long long sb_stamp_base = 0;      // its monotone event stamps
   bool sketch_batched(int m, int n, int steps, int gmax) const;  // sketch_select takes the batched kernel

@@ -67,7 +67,9 @@ from paper_1505_08115_b200.errors import check  # noqa: E402
 
 n = int(sys.argv[1])
 b, p = 256, 16
-eng = rq.Engine()
+# RQ_NEWSTREAM=1: the library's main stream is a created (non-default) stream, as in bench.py
+eng = rq.Engine(0, stream=torch.cuda.Stream()) if os.environ.get("RQ_NEWSTREAM") == "1" else rq.Engine()
+torch.cuda.set_stream(eng.stream)
 a0, ld = rq.gaussian_matrix_device(n, n, rq.RngState(0), engine=eng)
 work = torch.empty_like(a0)
 perm = torch.empty(n, dtype=torch.int64, device=a0.device)
