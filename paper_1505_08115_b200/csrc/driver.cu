@@ -477,6 +477,7 @@ int Ctx::sketch_select(const double* yt, int64_t ldy, int m, int n, int steps, c
   SweepWork w;
   w.scratch = sweep_ws;
   w.scratch_bytes = sweep_ws_bytes;
+  w.ll = sk_ll;
   const int rc = sketch_cpqr_launch(yt, ldy, m, n, steps, init_pos, chosen, w, sk_counter, sk_counter_base, stream,
                                     &launches, sketch_gmax);
   prof_end(e0, 0.0);
@@ -501,11 +502,15 @@ int Ctx::place_sketch_words(int m, int n, int steps) {
   constexpr int kCand = 16;
   constexpr size_t kStride = 4096;
   if (!sk_block) {
-    RQ_CUDA_TRY(cudaMalloc(&sk_block, kCand * kStride));
-    RQ_CUDA_TRY(cudaMemsetAsync(sk_block, 0, kCand * kStride, stream));
+    // [16 candidate winner records][slots + LL columns (b + p <= 288) + 16 candidate offsets]
+    const size_t llb = sketch_ll_bytes(288) + kCand * kStride;
+    RQ_CUDA_TRY(cudaMalloc(&sk_block, kCand * kStride + llb));
+    RQ_CUDA_TRY(cudaMemsetAsync(sk_block, 0, kCand * kStride + llb, stream));
     sk_counter = reinterpret_cast<unsigned long long*>(sk_block);
+    sk_ll = sk_block + kCand * kStride;
   }
   char* blk = sk_block;
+  char* ll0 = sk_block + kCand * kStride;
   // (small problems never repay the one-off ~6 ms: calibrate at the first sizeable sketch)
   if (sk_placed || env_cal == 0 || m > 288 || n < 2048 || steps < 32) return RQ_OK;
   sk_placed = true;
@@ -535,22 +540,36 @@ int Ctx::place_sketch_words(int m, int n, int steps) {
   SweepWork w;
   w.scratch = wcal;
   w.scratch_bytes = ws;
-  float tms[kCand];
-  int best = 0;
-  for (int i = 0; i < kCand && rc == RQ_OK; i++) {
-    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(blk + i * kStride);
-    tms[i] = 1e30f;
+  w.ll = ll0;
+  float tms[kCand], tll[kCand];
+  int best = 0, best_ll = 0;
+  auto time_one = [&](unsigned long long* ctr, int ncols) {
+    float best_ms = 1e30f;
     for (int rep = 0; rep < 3 && rc == RQ_OK; rep++) {
       cudaEventRecord(t0, stream);
-      rc = sketch_cpqr_launch(ycal, ldc, m, cn, csteps, nullptr, ccal, w, ctr, sk_counter_base, stream, nullptr, 0);
+      rc = sketch_cpqr_launch(ycal, ldc, m, ncols, csteps, nullptr, ccal, w, ctr, sk_counter_base, stream, nullptr, 0);
       cudaEventRecord(t1, stream);
       if (rc == RQ_OK && cudaStreamSynchronize(stream) != cudaSuccess) rc = set_error(RQ_ECUDA, "calibration run");
       float ms = 0.0f;
-      if (rc == RQ_OK && rep > 0 && cudaEventElapsedTime(&ms, t0, t1) == cudaSuccess) tms[i] = std::min(tms[i], ms);
+      if (rc == RQ_OK && rep > 0 && cudaEventElapsedTime(&ms, t0, t1) == cudaSuccess) best_ms = std::min(best_ms, ms);
     }
+    return best_ms;
+  };
+  // two grid sizes (128 and 63 CTAs: the slots span two 4 KB chunks or one), mean of both
+  auto time_run = [&](unsigned long long* ctr, float* out) { *out = 0.5f * (time_one(ctr, cn) + time_one(ctr, 1008)); };
+  // (1) the winner record's offset, (2) with it, the offset of the slots + LL columns (the reducer
+  // polls every CTA's slot each step; 4.39-4.67 us per step at n' = 10k, 3.06-3.62 at n' = 1k)
+  for (int i = 0; i < kCand && rc == RQ_OK; i++) {
+    time_run(reinterpret_cast<unsigned long long*>(blk + i * kStride), &tms[i]);
     if (tms[i] < tms[best]) best = i;
   }
+  for (int i = 0; i < kCand && rc == RQ_OK; i++) {
+    w.ll = ll0 + i * kStride;
+    time_run(reinterpret_cast<unsigned long long*>(blk + best * kStride), &tll[i]);
+    if (tll[i] < tll[best_ll]) best_ll = i;
+  }
   if (rc == RQ_OK) {
+    sk_ll = ll0 + best_ll * kStride;
     sk_counter = reinterpret_cast<unsigned long long*>(blk + best * kStride);
     // every candidate's arrival counter saw its own launches only: set the chosen one to the
     // host mirror (the stamps keep growing: records and slots written so far stay in the past)
@@ -560,7 +579,9 @@ int Ctx::place_sketch_words(int m, int n, int steps) {
     if (env_cal == 2) {
       fprintf(stderr, "[rq] sketch CPQR winner-record placement (us/step at 4 KB offsets):");
       for (int i = 0; i < kCand; i++) fprintf(stderr, " %.2f", tms[i] * 1e3f / csteps);
-      fprintf(stderr, " -> offset %d KB\n", best * 4);
+      fprintf(stderr, " -> offset %d KB; slots + LL columns:", best * 4);
+      for (int i = 0; i < kCand; i++) fprintf(stderr, " %.2f", tll[i] * 1e3f / csteps);
+      fprintf(stderr, " -> offset %d KB\n", best_ll * 4);
     }
   }
   cleanup();

@@ -237,6 +237,7 @@ struct Ctx {
   unsigned long long sk_counter_base = 0;    // host mirror of its value
   char* sk_block = nullptr;  // the allocation sk_counter points into (place_sketch_words)
   bool sk_placed = false;    // its offset was calibrated
+  char* sk_ll = nullptr;     // the sketch CPQR's slots + LL columns (inside sk_block, offset calibrated)
   int place_sketch_words(int m, int n, int steps);
   void* sb_ws = nullptr;                     // device: exchange words of the batched sketch CPQR (sketch_batch.cu)
   unsigned long long sb_stamp_base = 0;      // its monotone event stamps

@@ -1821,6 +1821,7 @@ size_t sketch_glob_bytes(int m, int n) {
   return (size_t)kSMs * W * (spw - 7) * 9 * 32 * sizeof(double);
 }
 
+size_t sketch_ll_bytes(int m) { return ((2 * (size_t)kSMs * 64 + 255) & ~size_t(255)) + 256 + sketch_ll_column_bytes(m); }
 static size_t sketch_base_bytes(int m) {
   return ((2 * (size_t)kSMs * 64 + 255) & ~size_t(255)) + 256 + sketch_ll_column_bytes(m);
 }
@@ -1846,14 +1847,16 @@ int sketch_cpqr_launch(const double* y, int64_t ld, int m, int n, int steps, con
     a.steps = steps;
     a.init_pos = init_pos;
     a.chosen = chosen;
-    SkSlot2* slots = reinterpret_cast<SkSlot2*>(w.scratch);  // [2][G] slots of 8 LL words
+    // slots + LL columns: in the caller's scratch, or in the context's placed block (w.ll)
+    char* llb = w.ll ? reinterpret_cast<char*>(w.ll) : reinterpret_cast<char*>(w.scratch);
+    SkSlot2* slots = reinterpret_cast<SkSlot2*>(llb);  // [2][G] slots of 8 LL words
     const size_t slot_bytes = ((2 * (size_t)kSMs * 64 + 255) & ~size_t(255));
     // dedicated, zero-initialised winner records (2 x 10 LL words) next to the counter
     SkWin* wins = reinterpret_cast<SkWin*>(reinterpret_cast<char*>(counter) + 64);
-    a.slotdata = reinterpret_cast<double*>(reinterpret_cast<char*>(w.scratch) + slot_bytes + 256);  // LL columns
+    a.slotdata = reinterpret_cast<double*>(llb + slot_bytes + 256);  // LL columns
     a.counter = counter;
     a.counter_base = counter_base;
-    const size_t need = slot_bytes + 256 + sketch_ll_column_bytes(m);
+    const size_t need = w.ll ? 0 : slot_bytes + 256 + sketch_ll_column_bytes(m);
     const size_t gbytes = sketch_glob_bytes(m, n);
     a.gcols = (gbytes > 0 && w.scratch_bytes >= need + gbytes)
                   ? reinterpret_cast<double*>(reinterpret_cast<char*>(w.scratch) + need)

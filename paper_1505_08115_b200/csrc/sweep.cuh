@@ -12,6 +12,7 @@ namespace rq {
 struct SweepWork {
   void* scratch = nullptr;
   size_t scratch_bytes = 0;
+  void* ll = nullptr;  // sketch CPQR: its slots + LL columns live here (sketch_ll_bytes(m)) instead of in scratch
   unsigned int* barriers = nullptr;  // ring, zeroed by the owner
   int nbarriers = 0;
   int next = 0;
@@ -45,6 +46,7 @@ struct SweepCall {
 
 size_t sweep_workspace_bytes(int64_t m, int total_cols, int grid);
 size_t sketch_ll_column_bytes(int m);
+size_t sketch_ll_bytes(int m);  // slots + LL columns of the register sketch CPQR
 size_t sketch_workspace_bytes(int m, int n);  // register-resident sketch CPQR (LL exchange) of n columns
 // Smallest grid a sketch CPQR launch is given (the overlapped schedule leaves 16 SMs to the b x b
 // CPQR's cluster); workspace sizes cover it.
