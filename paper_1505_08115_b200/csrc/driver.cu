@@ -546,6 +546,12 @@ int Ctx::place_sketch_words(int m, int n, int steps) {
   auto time_one = [&](unsigned long long* ctr, int ncols) {
     float best_ms = 1e30f;
     for (int rep = 0; rep < 3 && rc == RQ_OK; rep++) {
+      // (the arrival counter of RQ_SK_FIXED_REDUCER=0 must equal the host mirror at launch)
+      if (cudaMemcpyAsync(ctr, &sk_counter_base, 8, cudaMemcpyHostToDevice, stream) != cudaSuccess ||
+          cudaStreamSynchronize(stream) != cudaSuccess) {
+        rc = set_error(RQ_ECUDA, "sketch counter");
+        break;
+      }
       cudaEventRecord(t0, stream);
       rc = sketch_cpqr_launch(ycal, ldc, m, ncols, csteps, nullptr, ccal, w, ctr, sk_counter_base, stream, nullptr, 0);
       cudaEventRecord(t1, stream);

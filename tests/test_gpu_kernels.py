@@ -334,3 +334,39 @@ np.savez(sys.argv[1], **out)
     rng = np.random.default_rng(11)
     y = rng.standard_normal((272, 3000))
     assert np.array_equal(res["1"]["gauss"].astype(np.int64), O.qr_column_pivoted(y, steps=256).perm[:256])
+
+
+@pytest.mark.parametrize("reducer", ["0", "1", "2"])
+def test_sketch_cpqr_placement_calibration_with_every_reducer_mode(reducer):
+    """The one-off placement calibration of the sketch CPQR's exchange words (driver.cu place_sketch_words,
+    triggered by the first sketch with >= 2048 columns) runs the kernel on 16 candidate records: with the
+    arrival-counter reducer (RQ_SK_FIXED_REDUCER=0) every candidate's device counter must match the host
+    mirror or the launch never ends -- run each mode in a subprocess under a timeout and check the pivots."""
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import ctypes, sys
+import numpy as np, torch
+import paper_1505_08115_b200 as rq
+from oracle import randqr_oracle as O
+from paper_1505_08115_b200.errors import check
+eng = rq.Engine()
+rng = np.random.default_rng(3)
+for (m, n, steps) in [(272, 2600, 128), (272, 900, 64), (74, 2100, 48)]:
+    y = rng.standard_normal((m, n))
+    buf, ld = eng.alloc_matrix(m, n)
+    buf[:n, :m].copy_(torch.from_numpy(np.ascontiguousarray(y.T)))
+    ch = torch.full((steps,), -1, dtype=torch.int32, device=eng.device)
+    for _ in range(2):
+        check(eng.lib.rq_test_sketch_cpqr(eng.handle, ctypes.c_void_p(buf.data_ptr()), ld, m, n, steps,
+                                          ctypes.c_void_p(ch.data_ptr())))
+        torch.cuda.synchronize()
+        assert np.array_equal(ch.cpu().numpy().astype(np.int64), O.qr_column_pivoted(y, steps=steps).perm[:steps])
+print("OK")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RQ_SK_FIXED_REDUCER=reducer, PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=180)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-2000:]
